@@ -1,0 +1,203 @@
+/* cgvk — B200-native preconditioned CG variants (arXiv 1905.01549), C ABI.
+ *
+ * This is the drop-in boundary for the reference's hot path. The reference
+ * (/root/reference/proj) is a C++20 static library with no FFI; each entry
+ * point below replaces one reference interface (file:line cited), with plain
+ * pointers and sizes, host buffers in and out, and status codes that map 1:1
+ * onto the reference's exception types:
+ *
+ *   CGVK_EINVAL  <-> std::invalid_argument  (dimension / config / CSR errors)
+ *   CGVK_ESTATE  <-> std::logic_error       ("step() on a terminated solver")
+ *   CGVK_ECUDA / CGVK_ENCCL / CGVK_ENOMEM   <-> std::runtime_error
+ *
+ * Numerical breakdown is NOT an error: it is reported through
+ * cgvk_solver_status(), exactly as SolveStatus (inc/variants.hpp:62-86).
+ * The C++ shim paper_1905_01549_b200/cpp/cgvariants/*.hpp rethrows these codes
+ * so that cgv:: callers see the reference semantics.
+ *
+ * Threading: a matrix handle is immutable after creation and may be shared by
+ * solvers on the same device (the reference borrows A read-only,
+ * inc/variants.hpp:103-104). A solver handle is single-owner
+ * (inc/variants.hpp:95-97) and owns its stream, graphs and device buffers.
+ */
+#ifndef CGVK_H
+#define CGVK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CGVK_VERSION 1
+
+enum {
+    CGVK_OK = 0,
+    CGVK_EINVAL = -1,
+    CGVK_ESTATE = -2,
+    CGVK_ECUDA = -3,
+    CGVK_ENCCL = -4,
+    CGVK_ENOMEM = -5,
+};
+
+/* inc/variants.hpp:17-25 (same order) */
+enum {
+    CGVK_HS = 0,
+    CGVK_CG_CG = 1,
+    CGVK_M = 2,
+    CGVK_PR = 3,
+    CGVK_GV = 4,
+    CGVK_PIPE_PR_M = 5,
+    CGVK_PIPE_PR = 6,
+};
+
+/* inc/variants.hpp:28-32 (same order) */
+enum { CGVK_NU_EXPANDED = 0, CGVK_NU_SIMPLIFIED = 1, CGVK_NU_MEURANT = 2 };
+
+/* inc/preconditioner.hpp:13-14 */
+enum { CGVK_PRECOND_IDENTITY = 0, CGVK_PRECOND_JACOBI = 1 };
+
+/* SolveStatus::State, BreakdownReason, ConvergedBy (inc/variants.hpp:62-86).
+ * CGVK_CONVERGED_BY_TOLERANCE is the relative-residual stop rule applied by
+ * cgvk_solver_set_tolerance (the reference applies it in its harness, after
+ * step()). */
+enum { CGVK_RUNNING = 0, CGVK_BREAKDOWN = 1, CGVK_MAX_ITERATIONS = 2, CGVK_CONVERGED = 3 };
+enum {
+    CGVK_BREAKDOWN_NONE = 0,
+    CGVK_BREAKDOWN_NU_PRIME_NONPOSITIVE = 1,
+    CGVK_BREAKDOWN_NU_NONPOSITIVE = 2,
+    CGVK_BREAKDOWN_MU_NONPOSITIVE = 3,
+    CGVK_BREAKDOWN_NON_FINITE = 4,
+};
+enum {
+    CGVK_CONVERGED_BY_ZERO_RESIDUAL = 0,
+    CGVK_CONVERGED_BY_ERROR_THRESHOLD = 1,
+    CGVK_CONVERGED_BY_STAGNATION = 2,
+    CGVK_CONVERGED_BY_TOLERANCE = 3,
+};
+
+/* Working-vector ids for cgvk_solver_get_vector (SolverState fields,
+ * inc/variants.hpp:108-111). */
+enum {
+    CGVK_VEC_X = 0, CGVK_VEC_R, CGVK_VEC_P, CGVK_VEC_S, CGVK_VEC_W, CGVK_VEC_U, CGVK_VEC_T,
+    CGVK_VEC_R_TILDE, CGVK_VEC_S_TILDE, CGVK_VEC_W_TILDE, CGVK_VEC_U_TILDE,
+};
+
+/* Matrix creation flags. */
+enum {
+    CGVK_MATRIX_CHECK_SYMMETRIC = 1, /* is_symmetric (src/sparse_matrix.cpp:84-107) */
+};
+
+/* POD mirror of VariantConfig (inc/variants.hpp:34-57). */
+typedef struct cgvk_variant_config {
+    int variant;
+    int nu_expression;
+    int recompute_nu;
+    int recompute_w;
+    int unsimplified_mu;
+    int track_delta;
+} cgvk_variant_config;
+
+typedef struct cgvk_solve_status {
+    int state;     /* CGVK_RUNNING ... */
+    int breakdown; /* CGVK_BREAKDOWN_* */
+    int criterion; /* CGVK_CONVERGED_BY_* */
+    int k;         /* SolverState::k */
+    int allocated_vectors; /* SolverState::allocated_vectors() */
+} cgvk_solve_status;
+
+/* SolverState scalars (inc/variants.hpp:122-130) plus the last <r,r>. */
+typedef struct cgvk_scalars {
+    double alpha, beta, nu, nu_prime, mu, delta, delta_hat, gamma, eta;
+    double rr;
+} cgvk_scalars;
+
+/* SolverStats (inc/variants.hpp:88-93). */
+typedef struct cgvk_stats {
+    uint64_t spmv_calls, block_spmv_calls, precond_applies, reductions;
+} cgvk_stats;
+
+typedef struct cgvk_matrix_s* cgvk_matrix;
+typedef struct cgvk_solver_s* cgvk_solver;
+
+/* Thread-local message for the last non-OK return on this thread. */
+const char* cgvk_last_error(void);
+int cgvk_device_count(int* count);
+
+/* VariantConfig::make / validate (src/variants.cpp:10-47). */
+cgvk_variant_config cgvk_variant_config_make(int variant);
+int cgvk_variant_config_validate(const cgvk_variant_config* cfg);
+
+/* SparseMatrix upload (inc/sparse_matrix.hpp:16-23) with validate_csr
+ * (src/sparse_matrix.cpp:64-82) run on the device; CGVK_EINVAL on any
+ * violated invariant. Host arrays are the reference's int64/fp64 layout and
+ * may be pageable or pinned. Device layout: int32 row_ptr/col_idx + fp64
+ * values (12 B/nnz), requires nnz < 2^31. */
+int cgvk_matrix_create_csr(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                           const double* values, int device, int flags, cgvk_matrix* out);
+int cgvk_matrix_destroy(cgvk_matrix a);
+int cgvk_matrix_info(cgvk_matrix a, int64_t* n, int64_t* nnz, int* device);
+
+/* spmv (inc/sparse_matrix.hpp:41-42, src/sparse_matrix.cpp:109-118): y = A*x,
+ * per-row left-to-right, no FMA — bit-identical to the reference. */
+int cgvk_spmv(cgvk_matrix a, const double* x, double* y);
+/* block_spmv (inc/sparse_matrix.hpp:46-47, src/sparse_matrix.cpp:126-143). */
+int cgvk_block_spmv(cgvk_matrix a, const double* x1, const double* x2, double* y1,
+                    double* y2);
+/* Preconditioner::jacobi (src/preconditioner.cpp:12-31): inv_diag = 1/a_ii;
+ * CGVK_EINVAL when a diagonal entry is missing or <= 0. */
+int cgvk_jacobi(cgvk_matrix a, double* inv_diag);
+/* Preconditioner::apply (src/preconditioner.cpp:33-42). */
+int cgvk_precond_apply(cgvk_matrix a, int kind, const double* in, double* out);
+/* dot (inc/vector_ops.hpp:20-25) in the device's canonical reduction order
+ * (reproduced bit-for-bit by oracle/cgv_oracle.c ORC_DOT_TREE). */
+int cgvk_dot(cgvk_matrix a, const double* x, const double* y, double* out);
+/* The reduction-tree parameters the oracle needs: rows per tile (= threads
+ * per CTA) and the CTA cap G. */
+int cgvk_reduction_config(cgvk_matrix a, int* block, int* gmax);
+
+/* initialize() (inc/variants.hpp:149-150, src/variants.cpp:354-444). The
+ * status may already be terminal (zero initial residual, nu0/mu0 <= 0). */
+int cgvk_solver_create(cgvk_matrix a, const cgvk_variant_config* cfg, int precond,
+                       const double* b, const double* x0, cgvk_solver* out);
+int cgvk_solver_destroy(cgvk_solver s);
+/* Relative-residual stop: terminate with CGVK_CONVERGED_BY_TOLERANCE after the
+ * first step whose sqrt(<r,r>) <= rel_tol*||b||. rel_tol <= 0 disables it. */
+int cgvk_solver_set_tolerance(cgvk_solver s, double rel_tol);
+/* Enqueue up to n_iters step() calls (inc/variants.hpp:153) on the solver's
+ * stream as CUDA-graph replays; returns immediately. Iterations after a
+ * terminal status are device-side no-ops. CGVK_ESTATE if the status last
+ * observed by the host is already terminal. */
+int cgvk_solver_step(cgvk_solver s, int n_iters);
+/* Wait for enqueued work and refresh the host mirror of the status. */
+int cgvk_solver_sync(cgvk_solver s);
+int cgvk_solver_status(cgvk_solver s, cgvk_solve_status* st, cgvk_scalars* sc,
+                       cgvk_stats* stats);
+/* Copy a working vector to the host in the reference's state (tilde vectors
+ * that the fused schedule recomputes on the fly are materialised);
+ * CGVK_EINVAL when the variant does not allocate it. Synchronises. */
+int cgvk_solver_get_vector(cgvk_solver s, int which, double* out);
+/* ||b - A x_k|| with a fresh device spmv (diagnostics.cpp:19-24). */
+int cgvk_solver_true_residual(cgvk_solver s, double* out);
+/* sqrt(<r_j,r_j>) for j = 0..k as recorded on the device each iteration. */
+int cgvk_solver_history(cgvk_solver s, double* out, int cap, int* len);
+/* The stream the solver enqueues on (cudaStream_t), for event timing. */
+void* cgvk_solver_stream(cgvk_solver s);
+/* Number of kernel launches one iteration makes (graph nodes / iteration). */
+int cgvk_solver_launches_per_iter(cgvk_solver s);
+
+/* run() (inc/runner.hpp:47-49) with StopRule::fixed(max_iter) and probes
+ * off, plus an optional relative-residual tolerance: initialize, step until
+ * terminal or max_iter, copy x back. Fills status/scalars when non-NULL. */
+int cgvk_solve(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, const double* b,
+               const double* x0, int max_iter, double rel_tol, double* x_out,
+               cgvk_solve_status* st, cgvk_scalars* sc);
+
+/* Page-lock / unlock a host buffer (cudaHostRegister) for the e2e path. */
+int cgvk_host_register(void* ptr, uint64_t bytes);
+int cgvk_host_unregister(void* ptr);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CGVK_H */

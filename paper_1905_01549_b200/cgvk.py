@@ -1,0 +1,472 @@
+"""ctypes binding of the cgvk C ABI (include/cgvk.h).
+
+Python-side mirror of the reference's solver interface
+(/root/reference/proj/include/cgvariants/{variants,runner,sparse_matrix,
+preconditioner}.hpp): the same names, argument meaning and error behaviour, so
+the parity tests read like the reference's own tests. There is no CPU fallback:
+importing this module without the built CUDA library raises.
+
+Error mapping (include/cgvk.h): CGVK_EINVAL -> InvalidArgument (a ValueError,
+like std::invalid_argument), CGVK_ESTATE -> LogicError (std::logic_error),
+CUDA/NCCL/OOM -> CgvkError (std::runtime_error).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcgvk.so")
+
+
+class CgvkError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"cgvk error {code}: {msg}")
+        self.code = code
+
+
+class InvalidArgument(CgvkError, ValueError):
+    pass
+
+
+class LogicError(CgvkError):
+    pass
+
+
+class Variant(enum.IntEnum):  # inc/variants.hpp:17-25
+    HS = 0
+    CG_CG = 1
+    M = 2
+    PR = 3
+    GV = 4
+    PIPE_PR_M = 5
+    PIPE_PR = 6
+
+
+VARIANT_NAMES = {  # src/variants.cpp:49-60
+    Variant.HS: "hs", Variant.CG_CG: "cg", Variant.M: "m", Variant.PR: "pr",
+    Variant.GV: "gv", Variant.PIPE_PR_M: "pipe-pr-m", Variant.PIPE_PR: "pipe-pr",
+}
+
+
+def variant_from_name(name: str) -> Variant | None:  # src/variants.cpp:62-71
+    alias = {"hs": Variant.HS, "cg": Variant.CG_CG, "cg-cg": Variant.CG_CG, "m": Variant.M,
+             "pr": Variant.PR, "gv": Variant.GV, "pipe-pr-m": Variant.PIPE_PR_M,
+             "pprm": Variant.PIPE_PR_M, "pipe-pr": Variant.PIPE_PR, "ppr": Variant.PIPE_PR}
+    return alias.get(name)
+
+
+class NuExpression(enum.IntEnum):  # inc/variants.hpp:28-32
+    EXPANDED = 0
+    SIMPLIFIED = 1
+    MEURANT = 2
+
+
+class Precond(enum.IntEnum):  # inc/preconditioner.hpp:13-14
+    IDENTITY = 0
+    JACOBI = 1
+
+
+class State(enum.IntEnum):  # SolveStatus::State
+    RUNNING = 0
+    BREAKDOWN = 1
+    MAX_ITERATIONS = 2
+    CONVERGED = 3
+
+
+class Breakdown(enum.IntEnum):
+    NONE = 0
+    NU_PRIME_NONPOSITIVE = 1
+    NU_NONPOSITIVE = 2
+    MU_NONPOSITIVE = 3
+    NON_FINITE = 4
+
+
+class ConvergedBy(enum.IntEnum):
+    ZERO_RESIDUAL = 0
+    ERROR_THRESHOLD = 1
+    STAGNATION = 2
+    TOLERANCE = 3
+
+
+class Vec(enum.IntEnum):  # SolverState fields
+    X = 0
+    R = 1
+    P = 2
+    S = 3
+    W = 4
+    U = 5
+    T = 6
+    R_TILDE = 7
+    S_TILDE = 8
+    W_TILDE = 9
+    U_TILDE = 10
+
+
+class _Config(C.Structure):
+    _fields_ = [(f, C.c_int) for f in ("variant", "nu_expression", "recompute_nu", "recompute_w",
+                                       "unsimplified_mu", "track_delta")]
+
+
+class _Status(C.Structure):
+    _fields_ = [(f, C.c_int) for f in ("state", "breakdown", "criterion", "k",
+                                       "allocated_vectors")]
+
+
+class _Scalars(C.Structure):
+    _fields_ = [(f, C.c_double) for f in ("alpha", "beta", "nu", "nu_prime", "mu", "delta",
+                                          "delta_hat", "gamma", "eta", "rr")]
+
+
+class _Stats(C.Structure):
+    _fields_ = [(f, C.c_uint64) for f in ("spmv_calls", "block_spmv_calls", "precond_applies",
+                                          "reductions")]
+
+
+def _load() -> C.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"cgvk CUDA library not built: {LIB_PATH} (run __graft_entry__.build())")
+    lib = C.CDLL(LIB_PATH)
+    P, I, I64, D = C.c_void_p, C.c_int, C.c_int64, C.c_double
+    pp = C.POINTER(C.c_void_p)
+    sig = {
+        "cgvk_last_error": (C.c_char_p, []),
+        "cgvk_device_count": (I, [C.POINTER(I)]),
+        "cgvk_variant_config_make": (_Config, [I]),
+        "cgvk_variant_config_validate": (I, [C.POINTER(_Config)]),
+        "cgvk_matrix_create_csr": (I, [I64, P, P, P, I, I, pp]),
+        "cgvk_matrix_destroy": (I, [P]),
+        "cgvk_matrix_info": (I, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(I)]),
+        "cgvk_spmv": (I, [P, P, P]),
+        "cgvk_block_spmv": (I, [P, P, P, P, P]),
+        "cgvk_jacobi": (I, [P, P]),
+        "cgvk_precond_apply": (I, [P, I, P, P]),
+        "cgvk_dot": (I, [P, P, P, C.POINTER(D)]),
+        "cgvk_reduction_config": (I, [P, C.POINTER(I), C.POINTER(I)]),
+        "cgvk_solver_create": (I, [P, C.POINTER(_Config), I, P, P, pp]),
+        "cgvk_solver_destroy": (I, [P]),
+        "cgvk_solver_set_tolerance": (I, [P, D]),
+        "cgvk_solver_step": (I, [P, I]),
+        "cgvk_solver_sync": (I, [P]),
+        "cgvk_solver_status": (I, [P, C.POINTER(_Status), C.POINTER(_Scalars),
+                                   C.POINTER(_Stats)]),
+        "cgvk_solver_get_vector": (I, [P, I, P]),
+        "cgvk_solver_true_residual": (I, [P, C.POINTER(D)]),
+        "cgvk_solver_history": (I, [P, P, I, C.POINTER(I)]),
+        "cgvk_solver_stream": (P, [P]),
+        "cgvk_solver_launches_per_iter": (I, [P]),
+        "cgvk_solve": (I, [P, C.POINTER(_Config), I, P, P, I, D, P, C.POINTER(_Status),
+                           C.POINTER(_Scalars)]),
+        "cgvk_host_register": (I, [P, C.c_uint64]),
+        "cgvk_host_unregister": (I, [P]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+_lib = _load()
+
+# every symbol include/cgvk.h declares (checked by tests/test_abi.py)
+EXPORTED = sorted(n for n in dir(_lib) if n.startswith("cgvk_"))
+
+
+def lib() -> C.CDLL:
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = (_lib.cgvk_last_error() or b"").decode()
+    if rc == -1:
+        raise InvalidArgument(rc, msg)
+    if rc == -2:
+        raise LogicError(rc, msg)
+    raise CgvkError(rc, msg)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _i64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    _check(_lib.cgvk_device_count(C.byref(n)))
+    return n.value
+
+
+@dataclass
+class VariantConfig:
+    """POD mirror of VariantConfig (inc/variants.hpp:34-57)."""
+
+    variant: Variant = Variant.HS
+    recompute_nu: bool = True
+    recompute_w: bool = True
+    nu_expression: NuExpression = NuExpression.SIMPLIFIED
+    unsimplified_mu: bool = False
+    track_delta: bool = False
+
+    @staticmethod
+    def make(v: Variant) -> "VariantConfig":  # src/variants.cpp:10-23
+        c = _lib.cgvk_variant_config_make(int(v))
+        return VariantConfig._from_c(c)
+
+    @staticmethod
+    def _from_c(c: _Config) -> "VariantConfig":
+        return VariantConfig(Variant(c.variant), bool(c.recompute_nu), bool(c.recompute_w),
+                             NuExpression(c.nu_expression), bool(c.unsimplified_mu),
+                             bool(c.track_delta))
+
+    def _to_c(self) -> _Config:
+        return _Config(int(self.variant), int(self.nu_expression), int(self.recompute_nu),
+                       int(self.recompute_w), int(self.unsimplified_mu), int(self.track_delta))
+
+    def validate(self) -> None:  # src/variants.cpp:35-47
+        c = self._to_c()
+        _check(_lib.cgvk_variant_config_validate(C.byref(c)))
+
+    def is_predictor(self) -> bool:
+        return self.variant in (Variant.M, Variant.PR, Variant.PIPE_PR_M, Variant.PIPE_PR)
+
+    def is_pipelined(self) -> bool:
+        return self.variant in (Variant.GV, Variant.PIPE_PR_M, Variant.PIPE_PR)
+
+
+class DeviceMatrix:
+    """SparseMatrix resident on one GPU (int32 CSR + fp64 values)."""
+
+    def __init__(self, n: int, row_ptr, col_idx, values, device: int = 0,
+                 check_symmetric: bool = False):
+        rp, ci, va = _i64(row_ptr), _i64(col_idx), _f64(values)
+        if rp.shape[0] != n + 1:
+            raise InvalidArgument(-1, "row_ptr length must be n+1")
+        if ci.shape[0] != va.shape[0] or int(rp[-1]) != ci.shape[0]:
+            raise InvalidArgument(-1, "row_ptr[n] must equal number of stored entries")
+        h = C.c_void_p()
+        _check(_lib.cgvk_matrix_create_csr(n, _ptr(rp), _ptr(ci) if ci.size else None,
+                                           _ptr(va) if va.size else None, device,
+                                           1 if check_symmetric else 0, C.byref(h)))
+        self._h = h
+        self.n = int(n)
+        self.nnz = int(ci.shape[0])
+        self.device = device
+
+    @classmethod
+    def from_csr(cls, csr, device: int = 0, check_symmetric: bool = False) -> "DeviceMatrix":
+        return cls(csr.n, csr.row_ptr, csr.col_idx, csr.values, device, check_symmetric)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _lib.cgvk_matrix_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def _vec(self, v) -> np.ndarray:
+        a = _f64(v)
+        if a.shape != (self.n,):
+            raise InvalidArgument(-1, "vector dimension mismatch")
+        return a
+
+    def spmv(self, x) -> np.ndarray:
+        x = self._vec(x)
+        y = np.empty(self.n)
+        _check(_lib.cgvk_spmv(self._h, _ptr(x), _ptr(y)))
+        return y
+
+    def block_spmv(self, x1, x2) -> tuple[np.ndarray, np.ndarray]:
+        x1, x2 = self._vec(x1), self._vec(x2)
+        y1, y2 = np.empty(self.n), np.empty(self.n)
+        _check(_lib.cgvk_block_spmv(self._h, _ptr(x1), _ptr(x2), _ptr(y1), _ptr(y2)))
+        return y1, y2
+
+    def jacobi(self) -> np.ndarray:
+        d = np.empty(self.n)
+        _check(_lib.cgvk_jacobi(self._h, _ptr(d)))
+        return d
+
+    def precond_apply(self, kind: Precond, v) -> np.ndarray:
+        v = self._vec(v)
+        out = np.empty(self.n)
+        _check(_lib.cgvk_precond_apply(self._h, int(kind), _ptr(v), _ptr(out)))
+        return out
+
+    def dot(self, x, y) -> float:
+        x, y = self._vec(x), self._vec(y)
+        out = C.c_double()
+        _check(_lib.cgvk_dot(self._h, _ptr(x), _ptr(y), C.byref(out)))
+        return out.value
+
+    def reduction_config(self) -> tuple[int, int]:
+        b, g = C.c_int(), C.c_int()
+        _check(_lib.cgvk_reduction_config(self._h, C.byref(b), C.byref(g)))
+        return b.value, g.value
+
+
+@dataclass
+class SolveStatus:
+    state: State
+    breakdown: Breakdown
+    criterion: ConvergedBy
+
+    def running(self) -> bool:
+        return self.state == State.RUNNING
+
+
+SCALAR_NAMES = ("alpha", "beta", "nu", "nu_prime", "mu", "delta", "delta_hat", "gamma", "eta")
+
+
+class Solver:
+    """A device SolverState (inc/variants.hpp:101-143) created by initialize()."""
+
+    def __init__(self, config: VariantConfig, A: DeviceMatrix, precond: Precond, b, x0):
+        self.A = A  # borrowed, kept alive
+        self.config = config
+        self.precond = Precond(precond)
+        b, x0 = _f64(b), _f64(x0)
+        if b.shape != (A.n,) or x0.shape != (A.n,):
+            raise InvalidArgument(-1, "right-hand side or initial guess dimension mismatch")
+        c = config._to_c()
+        h = C.c_void_p()
+        _check(_lib.cgvk_solver_create(A.handle, C.byref(c), int(precond), _ptr(b), _ptr(x0),
+                                       C.byref(h)))
+        self._h = h
+        self.n = A.n
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _lib.cgvk_solver_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_tolerance(self, rel_tol: float) -> None:
+        _check(_lib.cgvk_solver_set_tolerance(self._h, float(rel_tol)))
+
+    def step(self, n_iters: int = 1) -> None:
+        """step() n times (src/variants.cpp:446-458), enqueued asynchronously."""
+        _check(_lib.cgvk_solver_step(self._h, int(n_iters)))
+
+    def sync(self) -> None:
+        _check(_lib.cgvk_solver_sync(self._h))
+
+    def _status(self):
+        st, sc, stats = _Status(), _Scalars(), _Stats()
+        _check(_lib.cgvk_solver_status(self._h, C.byref(st), C.byref(sc), C.byref(stats)))
+        return st, sc, stats
+
+    @property
+    def status(self) -> SolveStatus:
+        st, _, _ = self._status()
+        return SolveStatus(State(st.state), Breakdown(st.breakdown), ConvergedBy(st.criterion))
+
+    @property
+    def k(self) -> int:
+        return self._status()[0].k
+
+    def allocated_vectors(self) -> int:
+        return self._status()[0].allocated_vectors
+
+    def scalars(self) -> dict:
+        _, sc, _ = self._status()
+        out = {f: getattr(sc, f) for f in SCALAR_NAMES}
+        out["rr"] = sc.rr
+        return out
+
+    def stats(self) -> dict:
+        _, _, s = self._status()
+        return {f: getattr(s, f) for f in ("spmv_calls", "block_spmv_calls", "precond_applies",
+                                           "reductions")}
+
+    def vector(self, which: Vec) -> np.ndarray:
+        out = np.empty(self.n)
+        _check(_lib.cgvk_solver_get_vector(self._h, int(which), _ptr(out) if self.n else None))
+        return out
+
+    def has_vector(self, which: Vec) -> bool:
+        try:
+            self.vector(which)
+            return True
+        except InvalidArgument:
+            return False
+
+    def true_residual(self) -> float:
+        out = C.c_double()
+        _check(_lib.cgvk_solver_true_residual(self._h, C.byref(out)))
+        return out.value
+
+    def history(self) -> np.ndarray:
+        ln = C.c_int()
+        _check(_lib.cgvk_solver_history(self._h, None, 0, C.byref(ln)))
+        out = np.empty(max(ln.value, 1))
+        _check(_lib.cgvk_solver_history(self._h, _ptr(out), ln.value, C.byref(ln)))
+        return out[: ln.value]
+
+    def stream(self) -> int:
+        return _lib.cgvk_solver_stream(self._h) or 0
+
+    def launches_per_iter(self) -> int:
+        return _lib.cgvk_solver_launches_per_iter(self._h)
+
+    # reference-named accessors
+    @property
+    def x(self):
+        return self.vector(Vec.X)
+
+    @property
+    def r(self):
+        return self.vector(Vec.R)
+
+
+def initialize(config: VariantConfig, A: DeviceMatrix, precond: Precond, b, x0) -> Solver:
+    """initialize() (inc/variants.hpp:149-150)."""
+    return Solver(config, A, precond, b, x0)
+
+
+def step(state: Solver) -> None:
+    """step() (inc/variants.hpp:153): exactly one iteration, synchronised."""
+    state.step(1)
+    state.sync()
+
+
+def solve(A: DeviceMatrix, config: VariantConfig, precond: Precond, b, x0, max_iter: int,
+          rel_tol: float = 0.0):
+    """run() with StopRule::fixed and probes off (+ optional ||r||/||b|| stop)."""
+    b, x0 = _f64(b), _f64(x0)
+    x = np.empty(A.n)
+    st, sc = _Status(), _Scalars()
+    c = config._to_c()
+    _check(_lib.cgvk_solve(A.handle, C.byref(c), int(precond), _ptr(b), _ptr(x0), int(max_iter),
+                           float(rel_tol), _ptr(x), C.byref(st), C.byref(sc)))
+    return x, SolveStatus(State(st.state), Breakdown(st.breakdown), ConvergedBy(st.criterion)), st.k
+
+
+def host_register(arr: np.ndarray) -> None:
+    _check(_lib.cgvk_host_register(_ptr(arr), arr.nbytes))
+
+
+def host_unregister(arr: np.ndarray) -> None:
+    _check(_lib.cgvk_host_unregister(_ptr(arr)))

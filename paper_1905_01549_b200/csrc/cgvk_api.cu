@@ -1,0 +1,944 @@
+// cgvk C-ABI implementation: device matrix, solver runtime (streams, CUDA
+// graphs of whole iterations, host mirror of the device control block) and
+// the reference-facing entry points declared in include/cgvk.h.
+#include "cgvk.h"
+#include "cgvk_generic.cuh"
+#include "cgvk_variants.cuh"
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+using namespace cgvk;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return set_err(CGVK_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_),    \
+                           __FILE__, __LINE__);                                           \
+    } while (0)
+
+#define TRY(expr)                  \
+    do {                           \
+        int rc_ = (expr);          \
+        if (rc_ != CGVK_OK) return rc_; \
+    } while (0)
+
+int grid_elem(int64_t n) {
+    int64_t g = (n + 255) / 256;
+    if (g > 148 * 16) g = 148 * 16;
+    return g < 1 ? 1 : (int)g;
+}
+
+template <class T>
+int dalloc(T** p, size_t count) {
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc((void**)p, sizeof(T) * count);
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        return set_err(CGVK_ENOMEM, "cudaMalloc(%zu bytes): %s", sizeof(T) * count,
+                       cudaGetErrorString(e));
+    }
+    return CGVK_OK;
+}
+
+}  // namespace
+
+// ===================================================================== matrix
+
+struct cgvk_matrix_s {
+    int device = 0;
+    int64_t n = 0, nnz = 0;
+    int ntiles = 0, gmax = 0, G = 1;
+    int* rp = nullptr;
+    int* ci = nullptr;
+    double* va = nullptr;
+    double* inv_diag = nullptr;  // built on first use
+    int jacobi_state = 0;        // 0 not built, 1 ok, -1 missing/non-positive diagonal
+    cudaStream_t stream = nullptr;
+    // L1-op scratch (guarded by mu: the matrix may be shared across threads)
+    std::mutex mu;
+    double* part = nullptr;
+    unsigned int* counter = nullptr;
+    double* out = nullptr;
+    int* flags = nullptr;
+    double* tmp[4] = {nullptr, nullptr, nullptr, nullptr};
+
+    Params base() const {
+        Params P{};
+        P.n = (int)n;
+        P.ntiles = ntiles;
+        P.rp = rp;
+        P.ci = ci;
+        P.va = va;
+        P.d = inv_diag;
+        return P;
+    }
+};
+
+namespace {
+
+int ensure_jacobi(cgvk_matrix a) {
+    if (a->jacobi_state == 1) return CGVK_OK;
+    if (a->jacobi_state == -1)
+        return set_err(CGVK_EINVAL, "Jacobi preconditioner needs a positive diagonal");
+    if (!a->inv_diag) TRY(dalloc(&a->inv_diag, a->n));
+    CK(cudaMemsetAsync(a->flags, 0, sizeof(int), a->stream));
+    if (a->n > 0)
+        k_jacobi<<<grid_elem(a->n), 256, 0, a->stream>>>((int)a->n, a->rp, a->ci, a->va, a->inv_diag,
+                                                          a->flags);
+    int flags = 0;
+    CK(cudaMemcpyAsync(&flags, a->flags, sizeof(int), cudaMemcpyDeviceToHost, a->stream));
+    CK(cudaStreamSynchronize(a->stream));
+    a->jacobi_state = flags ? -1 : 1;
+    if (flags) return set_err(CGVK_EINVAL, "Jacobi preconditioner needs a positive diagonal");
+    return CGVK_OK;
+}
+
+// canonical dots of (x_q, y_q) with optional d∘x_q, results to host
+int run_dots(cgvk_matrix a, cudaStream_t stream, double* part, unsigned int* counter, double* dout,
+             int nd, const double* const* xs, const double* const* ys, const int* dxs,
+             double* host_out) {
+    if (a->n == 0) {
+        for (int q = 0; q < nd; ++q) host_out[q] = 0.0;
+        return CGVK_OK;
+    }
+    DotArgs A{};
+    A.n = (int)a->n;
+    A.ntiles = a->ntiles;
+    for (int q = 0; q < nd; ++q) {
+        A.x[q] = xs[q];
+        A.y[q] = ys[q];
+        A.dx[q] = dxs ? dxs[q] : 0;
+    }
+    A.d = a->inv_diag;
+    A.part = part;
+    A.counter = counter;
+    A.out = dout;
+    switch (nd) {
+        case 1: k_dots<1><<<a->G, kBlock, 0, stream>>>(A); break;
+        case 2: k_dots<2><<<a->G, kBlock, 0, stream>>>(A); break;
+        case 3: k_dots<3><<<a->G, kBlock, 0, stream>>>(A); break;
+        default: k_dots<4><<<a->G, kBlock, 0, stream>>>(A); break;
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(host_out, dout, sizeof(double) * nd, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    return CGVK_OK;
+}
+
+int ensure_tmp(cgvk_matrix a, int count) {
+    for (int q = 0; q < count; ++q)
+        if (!a->tmp[q]) TRY(dalloc(&a->tmp[q], a->n));
+    return CGVK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cgvk_last_error(void) { return g_err.c_str(); }
+
+int cgvk_device_count(int* count) {
+    CK(cudaGetDeviceCount(count));
+    return CGVK_OK;
+}
+
+cgvk_variant_config cgvk_variant_config_make(int variant) {
+    cgvk_variant_config c{};
+    c.variant = variant;
+    c.nu_expression = (variant == CGVK_M || variant == CGVK_PIPE_PR_M) ? CGVK_NU_MEURANT
+                                                                       : CGVK_NU_SIMPLIFIED;
+    c.recompute_nu = 1;
+    c.recompute_w = 1;
+    c.unsimplified_mu = 0;
+    c.track_delta = 0;
+    return c;
+}
+
+// src/variants.cpp:35-47
+int cgvk_variant_config_validate(const cgvk_variant_config* c) {
+    if (!c) return set_err(CGVK_EINVAL, "null config");
+    const int v = c->variant;
+    if (v < CGVK_HS || v > CGVK_PIPE_PR) return set_err(CGVK_EINVAL, "unknown variant %d", v);
+    if (c->nu_expression < 0 || c->nu_expression > 2)
+        return set_err(CGVK_EINVAL, "unknown nu expression %d", c->nu_expression);
+    const bool pipe_pr = v == CGVK_PIPE_PR || v == CGVK_PIPE_PR_M;
+    const bool predictor = v == CGVK_M || v == CGVK_PR || pipe_pr;
+    if (!c->recompute_w && !pipe_pr)
+        return set_err(CGVK_EINVAL, "recompute_w only applies to the pipelined PR variants");
+    if (!c->recompute_nu && !predictor)
+        return set_err(CGVK_EINVAL, "recompute_nu only applies to predictor variants");
+    if (!predictor && c->nu_expression != CGVK_NU_SIMPLIFIED)
+        return set_err(CGVK_EINVAL, "nu_expression only applies to predictor variants");
+    if (c->unsimplified_mu && v != CGVK_CG_CG && v != CGVK_GV)
+        return set_err(CGVK_EINVAL, "unsimplified_mu only applies to CG_CG and GV");
+    if (c->track_delta && !predictor)
+        return set_err(CGVK_EINVAL, "track_delta only applies to predictor variants");
+    return CGVK_OK;
+}
+
+int cgvk_matrix_create_csr(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                           const double* values, int device, int flags, cgvk_matrix* out) {
+    if (!out) return set_err(CGVK_EINVAL, "null output handle");
+    *out = nullptr;
+    if (n < 0) return set_err(CGVK_EINVAL, "negative dimension");
+    if (!row_ptr) return set_err(CGVK_EINVAL, "row_ptr length must be n+1");
+    const int64_t nnz = row_ptr[n];
+    if (nnz < 0) return set_err(CGVK_EINVAL, "row_ptr[n] must equal number of stored entries");
+    if (n >= (int64_t(1) << 31) - 256 || nnz >= (int64_t(1) << 31))
+        return set_err(CGVK_EINVAL, "device CSR uses int32 indices: n and nnz must be < 2^31");
+    if (nnz > 0 && (!col_idx || !values)) return set_err(CGVK_EINVAL, "null CSR arrays");
+    CK(cudaSetDevice(device));
+    auto* a = new cgvk_matrix_s;
+    a->device = device;
+    a->n = n;
+    a->nnz = nnz;
+    a->ntiles = (int)((n + kBlock - 1) / kBlock);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    a->gmax = sms * kMinBlocksPerSM;
+    a->G = a->ntiles < a->gmax ? a->ntiles : a->gmax;
+    if (a->G < 1) a->G = 1;
+    auto bail = [&](int rc) {
+        cgvk_matrix_destroy(a);
+        return rc;
+    };
+    int rc;
+    if ((rc = dalloc(&a->rp, n + 1)) || (rc = dalloc(&a->ci, nnz)) || (rc = dalloc(&a->va, nnz)) ||
+        (rc = dalloc(&a->part, kMaxDots * (size_t)a->gmax)) || (rc = dalloc(&a->counter, 4)) ||
+        (rc = dalloc(&a->out, 8)) || (rc = dalloc(&a->flags, 1)))
+        return bail(rc);
+    if (cudaStreamCreateWithFlags(&a->stream, cudaStreamNonBlocking) != cudaSuccess)
+        return bail(set_err(CGVK_ECUDA, "stream create failed"));
+    cudaMemsetAsync(a->counter, 0, 4 * sizeof(unsigned int), a->stream);
+    cudaMemsetAsync(a->flags, 0, sizeof(int), a->stream);
+    // stage the int64 arrays on the device and narrow/validate there
+    int64_t *rp64 = nullptr, *ci64 = nullptr;
+    if ((rc = dalloc(&rp64, n + 1)) || (rc = dalloc(&ci64, nnz))) {
+        cudaFree(rp64);
+        return bail(rc);
+    }
+    cudaError_t e = cudaMemcpyAsync(rp64, row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice,
+                                    a->stream);
+    if (e == cudaSuccess && nnz)
+        e = cudaMemcpyAsync(ci64, col_idx, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, a->stream);
+    if (e == cudaSuccess && nnz)
+        e = cudaMemcpyAsync(a->va, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, a->stream);
+    if (e == cudaSuccess) {
+        k_convert_csr<<<grid_elem(nnz > n ? nnz : n + 1), 256, 0, a->stream>>>(n, nnz, rp64, ci64, a->rp,
+                                                                              a->ci, a->flags);
+        e = cudaGetLastError();
+    }
+    int hflags = 0;
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(&hflags, a->flags, sizeof(int), cudaMemcpyDeviceToHost, a->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(a->stream);
+    cudaFree(rp64);
+    cudaFree(ci64);
+    if (e != cudaSuccess) return bail(set_err(CGVK_ECUDA, "matrix upload: %s", cudaGetErrorString(e)));
+    if (hflags & 1) return bail(set_err(CGVK_EINVAL, "row_ptr not monotone or wrong end points"));
+    if (hflags & 2) return bail(set_err(CGVK_EINVAL, "column index out of range"));
+    if (n > 0) {
+        k_check_sorted<<<grid_elem(n), 256, 0, a->stream>>>((int)n, a->rp, a->ci, a->flags);
+        if (flags & CGVK_MATRIX_CHECK_SYMMETRIC)
+            k_check_symmetric<<<grid_elem(n), 256, 0, a->stream>>>((int)n, a->rp, a->ci, a->va,
+                                                                   a->flags);
+        e = cudaMemcpyAsync(&hflags, a->flags, sizeof(int), cudaMemcpyDeviceToHost, a->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(a->stream);
+        if (e != cudaSuccess)
+            return bail(set_err(CGVK_ECUDA, "matrix validate: %s", cudaGetErrorString(e)));
+        if (hflags & 4) return bail(set_err(CGVK_EINVAL, "column indices not strictly increasing"));
+        if (hflags & 8) return bail(set_err(CGVK_EINVAL, "matrix is not bitwise symmetric"));
+    }
+    *out = a;
+    return CGVK_OK;
+}
+
+int cgvk_matrix_destroy(cgvk_matrix a) {
+    if (!a) return CGVK_OK;
+    cudaSetDevice(a->device);
+    if (a->stream) cudaStreamSynchronize(a->stream);
+    cudaFree(a->rp);
+    cudaFree(a->ci);
+    cudaFree(a->va);
+    cudaFree(a->inv_diag);
+    cudaFree(a->part);
+    cudaFree(a->counter);
+    cudaFree(a->out);
+    cudaFree(a->flags);
+    for (double* t : a->tmp) cudaFree(t);
+    if (a->stream) cudaStreamDestroy(a->stream);
+    delete a;
+    return CGVK_OK;
+}
+
+int cgvk_matrix_info(cgvk_matrix a, int64_t* n, int64_t* nnz, int* device) {
+    if (!a) return set_err(CGVK_EINVAL, "null matrix");
+    if (n) *n = a->n;
+    if (nnz) *nnz = a->nnz;
+    if (device) *device = a->device;
+    return CGVK_OK;
+}
+
+int cgvk_reduction_config(cgvk_matrix a, int* block, int* gmax) {
+    if (!a) return set_err(CGVK_EINVAL, "null matrix");
+    *block = kBlock;
+    *gmax = a->gmax;
+    return CGVK_OK;
+}
+
+int cgvk_spmv(cgvk_matrix a, const double* x, double* y) {
+    if (!a || !x || !y) return set_err(CGVK_EINVAL, "spmv dimension mismatch");
+    std::lock_guard<std::mutex> lock(a->mu);
+    CK(cudaSetDevice(a->device));
+    if (a->n == 0) return CGVK_OK;
+    TRY(ensure_tmp(a, 2));
+    CK(cudaMemcpyAsync(a->tmp[0], x, 8 * a->n, cudaMemcpyHostToDevice, a->stream));
+    k_spmv<<<a->G, kBlock, 0, a->stream>>>(a->base(), a->tmp[0], nullptr, a->tmp[1], 0);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(y, a->tmp[1], 8 * a->n, cudaMemcpyDeviceToHost, a->stream));
+    CK(cudaStreamSynchronize(a->stream));
+    return CGVK_OK;
+}
+
+int cgvk_block_spmv(cgvk_matrix a, const double* x1, const double* x2, double* y1, double* y2) {
+    if (!a || !x1 || !x2 || !y1 || !y2) return set_err(CGVK_EINVAL, "block_spmv dimension mismatch");
+    std::lock_guard<std::mutex> lock(a->mu);
+    CK(cudaSetDevice(a->device));
+    if (a->n == 0) return CGVK_OK;
+    TRY(ensure_tmp(a, 4));
+    CK(cudaMemcpyAsync(a->tmp[0], x1, 8 * a->n, cudaMemcpyHostToDevice, a->stream));
+    CK(cudaMemcpyAsync(a->tmp[1], x2, 8 * a->n, cudaMemcpyHostToDevice, a->stream));
+    k_block_spmv<<<a->G, kBlock, 0, a->stream>>>(a->base(), a->tmp[0], a->tmp[1], a->tmp[2], a->tmp[3]);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(y1, a->tmp[2], 8 * a->n, cudaMemcpyDeviceToHost, a->stream));
+    CK(cudaMemcpyAsync(y2, a->tmp[3], 8 * a->n, cudaMemcpyDeviceToHost, a->stream));
+    CK(cudaStreamSynchronize(a->stream));
+    return CGVK_OK;
+}
+
+int cgvk_jacobi(cgvk_matrix a, double* inv_diag) {
+    if (!a) return set_err(CGVK_EINVAL, "null matrix");
+    std::lock_guard<std::mutex> lock(a->mu);
+    CK(cudaSetDevice(a->device));
+    TRY(ensure_jacobi(a));
+    if (inv_diag && a->n)
+        CK(cudaMemcpy(inv_diag, a->inv_diag, 8 * a->n, cudaMemcpyDeviceToHost));
+    return CGVK_OK;
+}
+
+int cgvk_precond_apply(cgvk_matrix a, int kind, const double* in, double* out) {
+    if (!a || !in || !out) return set_err(CGVK_EINVAL, "preconditioner dimension mismatch");
+    if (kind != CGVK_PRECOND_IDENTITY && kind != CGVK_PRECOND_JACOBI)
+        return set_err(CGVK_EINVAL, "unknown preconditioner kind %d", kind);
+    std::lock_guard<std::mutex> lock(a->mu);
+    CK(cudaSetDevice(a->device));
+    if (kind == CGVK_PRECOND_JACOBI) TRY(ensure_jacobi(a));
+    if (a->n == 0) return CGVK_OK;
+    TRY(ensure_tmp(a, 2));
+    CK(cudaMemcpyAsync(a->tmp[0], in, 8 * a->n, cudaMemcpyHostToDevice, a->stream));
+    k_scale<<<grid_elem(a->n), 256, 0, a->stream>>>((int)a->n, kind ? a->inv_diag : nullptr, a->tmp[0],
+                                                     a->tmp[1]);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, a->tmp[1], 8 * a->n, cudaMemcpyDeviceToHost, a->stream));
+    CK(cudaStreamSynchronize(a->stream));
+    return CGVK_OK;
+}
+
+int cgvk_dot(cgvk_matrix a, const double* x, const double* y, double* out) {
+    if (!a || !x || !y || !out) return set_err(CGVK_EINVAL, "vector dimension mismatch");
+    std::lock_guard<std::mutex> lock(a->mu);
+    CK(cudaSetDevice(a->device));
+    if (a->n == 0) {
+        *out = 0.0;
+        return CGVK_OK;
+    }
+    TRY(ensure_tmp(a, 2));
+    CK(cudaMemcpyAsync(a->tmp[0], x, 8 * a->n, cudaMemcpyHostToDevice, a->stream));
+    CK(cudaMemcpyAsync(a->tmp[1], y, 8 * a->n, cudaMemcpyHostToDevice, a->stream));
+    const double* xs[1] = {a->tmp[0]};
+    const double* ys[1] = {a->tmp[1]};
+    return run_dots(a, a->stream, a->part, a->counter, a->out, 1, xs, ys, nullptr, out);
+}
+
+int cgvk_host_register(void* ptr, uint64_t bytes) {
+    CK(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault));
+    return CGVK_OK;
+}
+
+int cgvk_host_unregister(void* ptr) {
+    CK(cudaHostUnregister(ptr));
+    return CGVK_OK;
+}
+
+}  // extern "C"
+
+// ===================================================================== solver
+
+using KernelFn = void (*)(Params);
+
+struct cgvk_solver_s {
+    cgvk_matrix a = nullptr;
+    cgvk_variant_config cfg{};
+    int prec = 0;
+    int64_t n = 0;
+    cudaStream_t stream = nullptr;
+    double *x = nullptr, *r = nullptr, *p0 = nullptr, *p1 = nullptr, *s = nullptr, *w = nullptr,
+           *u = nullptr, *t = nullptr, *rt = nullptr, *st = nullptr, *wt = nullptr, *b = nullptr,
+           *tmp = nullptr;
+    double *part = nullptr, *hist = nullptr, *dout = nullptr;
+    unsigned int* counter = nullptr;
+    int hist_cap = 0;
+    Ctrl* ctrl = nullptr;
+    Ctrl mirror{};
+    bool mirror_fresh = true;
+    int k_target = 0;
+    KernelFn k1 = nullptr, k2 = nullptr;
+    cudaGraphExec_t g1 = nullptr, g8 = nullptr;
+    Params P{};
+    int allocated = 0;
+};
+
+namespace {
+
+template <bool PREC>
+void pick_kernels(int v, KernelFn* k1, KernelFn* k2) {
+    switch (v) {
+        case CGVK_HS: *k1 = hs_k1<PREC>; *k2 = hs_k2<PREC>; break;
+        case CGVK_CG_CG: *k1 = cg_k1<PREC>; *k2 = cg_k2<PREC>; break;
+        case CGVK_M:
+        case CGVK_PR: *k1 = pr_k1<PREC>; *k2 = pr_k2<PREC>; break;
+        case CGVK_GV: *k1 = gv_k1<PREC>; *k2 = gv_k2<PREC>; break;
+        default: *k1 = ppr_k1<PREC>; *k2 = ppr_k2<PREC>; break;
+    }
+}
+
+// the reference's allocated_vectors() (src/variants.cpp:97-103) for the
+// vectors initialize() resizes (src/variants.cpp:354-444)
+int ref_allocated(int v, bool prec) {
+    int c = 4;  // x r p s
+    if (prec) c += 1;  // r~
+    const bool needs_st = prec && v != CGVK_HS && v != CGVK_CG_CG;
+    if (needs_st) c += 1;
+    switch (v) {
+        case CGVK_CG_CG: c += 1; break;                          // w
+        case CGVK_GV: c += 3 + (prec ? 1 : 0); break;            // w u t (+w~)
+        case CGVK_PIPE_PR:
+        case CGVK_PIPE_PR_M: c += 2 + (prec ? 2 : 0); break;     // w u (+w~ u~)
+        default: break;
+    }
+    return c;
+}
+
+void launch_iter(cgvk_solver s) {
+    const int G = s->a->G;
+    s->k1<<<G, kBlock, 0, s->stream>>>(s->P);
+    s->k2<<<G, kBlock, 0, s->stream>>>(s->P);
+}
+
+int capture(cgvk_solver s, int iters, cudaGraphExec_t* exec) {
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < iters; ++i) launch_iter(s);
+    CK(cudaStreamEndCapture(s->stream, &g));
+    CK(cudaGraphInstantiate(exec, g, 0));
+    CK(cudaGraphDestroy(g));
+    return CGVK_OK;
+}
+
+int refresh_mirror(cgvk_solver s) {
+    CK(cudaMemcpyAsync(&s->mirror, s->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    s->mirror_fresh = true;
+    return CGVK_OK;
+}
+
+bool host_settle_nonpositive(Ctrl& c, double value, int reason, double rr) {
+    if (!std::isfinite(value)) {
+        c.state = ST_BREAKDOWN;
+        c.reason = BR_NONFINITE;
+        return true;
+    }
+    if (value > 0.0) return false;
+    if (value == 0.0 && rr == 0.0) {
+        c.state = ST_CONVERGED;
+        c.criterion = CB_ZERO;
+    } else {
+        c.state = ST_BREAKDOWN;
+        c.reason = reason;
+    }
+    return true;
+}
+
+bool host_settle_mu(Ctrl& c) {
+    if (!std::isfinite(c.sc[SMU])) {
+        c.state = ST_BREAKDOWN;
+        c.reason = BR_NONFINITE;
+        return true;
+    }
+    if (c.sc[SMU] <= 0.0) {
+        c.state = ST_BREAKDOWN;
+        c.reason = BR_MU;
+        return true;
+    }
+    return false;
+}
+
+// initialize(): src/variants.cpp:354-444, assembled from generic kernels with
+// host-side scalar logic (runs once per solve).
+int solver_init(cgvk_solver s, const double* b, const double* x0) {
+    cgvk_matrix a = s->a;
+    const int64_t n = s->n;
+    const int v = s->cfg.variant;
+    const bool prec = s->prec;
+    const bool stores_rt = prec && (v == CGVK_M || v == CGVK_PR || v == CGVK_GV ||
+                                    v == CGVK_PIPE_PR || v == CGVK_PIPE_PR_M);
+    const bool needs_st = prec && v != CGVK_HS && v != CGVK_CG_CG;
+    const bool pipe = v == CGVK_PIPE_PR || v == CGVK_PIPE_PR_M;
+    Ctrl c{};
+    c.state = ST_RUNNING;
+    c.hist_cap = s->hist_cap;
+    unsigned long long spmv = 0, prec_ap = 0, red = 0;
+    cudaStream_t st = s->stream;
+    Params P = a->base();
+    const int G = a->G;
+    const int eg = grid_elem(n);
+    const double* d = a->inv_diag;
+
+    CK(cudaMemcpyAsync(s->b, b, 8 * n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(s->x, x0, 8 * n, cudaMemcpyHostToDevice, st));
+    // r0 = b - A x0
+    k_spmv<<<G, kBlock, 0, st>>>(P, s->x, s->b, s->r, 0);
+    spmv++;
+    if (prec) {
+        prec_ap++;
+        if (stores_rt) k_scale<<<eg, 256, 0, st>>>((int)n, d, s->r, s->rt);
+    }
+    const double* rtv = stores_rt ? s->rt : s->r;
+    const int rt_fly = prec && !stores_rt;  // r~ = d∘r recomputed
+    double h[4];
+    {
+        const double* xs[3] = {rtv, s->r, s->b};
+        const double* ys[3] = {s->r, s->r, s->b};
+        const int dx[3] = {rt_fly, 0, 0};
+        TRY(run_dots(a, st, s->part, s->counter, s->dout, 3, xs, ys, dx, h));
+    }
+    red++;
+    const double nu0 = h[0], rr0 = h[1];
+    c.rr = rr0;
+    c.bnorm = std::sqrt(h[2]);
+    CK(cudaMemcpyAsync(s->hist, &rr0, 8, cudaMemcpyHostToDevice, st));
+    c.sc[SNU] = nu0;
+    auto finish = [&]() -> int {
+        c.stats[STAT_SPMV] = spmv;
+        c.stats[STAT_PREC] = prec_ap;
+        c.stats[STAT_RED] = red;
+        CK(cudaMemcpyAsync(s->ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+        s->mirror = c;
+        s->mirror_fresh = true;
+        return CGVK_OK;
+    };
+    if (host_settle_nonpositive(c, nu0, BR_NU, rr0)) return finish();
+    // p0 = r~0; s0 = A p0; mu0; alpha0
+    k_scale<<<eg, 256, 0, st>>>((int)n, rt_fly ? d : nullptr, rtv, s->p0);
+    k_spmv<<<G, kBlock, 0, st>>>(P, s->p0, nullptr, s->s, 0);
+    spmv++;
+    {
+        const double* xs[1] = {s->p0};
+        const double* ys[1] = {s->s};
+        TRY(run_dots(a, st, s->part, s->counter, s->dout, 1, xs, ys, nullptr, h));
+    }
+    red++;
+    c.sc[SMU] = h[0];
+    if (host_settle_mu(c)) return finish();
+    c.sc[SA] = c.sc[SNU] / c.sc[SMU];
+    if (needs_st) {
+        prec_ap++;
+        if (v == CGVK_GV || pipe) k_scale<<<eg, 256, 0, st>>>((int)n, d, s->s, s->st);
+    }
+    const double* stv = needs_st && (v == CGVK_GV || pipe) ? s->st : s->s;
+    const int st_fly = needs_st && !(v == CGVK_GV || pipe);  // PR/M: s~ = d∘s
+    const int expr = s->cfg.nu_expression;
+    auto scalar_dots = [&](bool want_delta) -> int {
+        const bool want_dhat = expr == CGVK_NU_EXPANDED;
+        const double* xs[3];
+        const double* ys[3];
+        int dx[3], slot[3], nd = 0;
+        if (want_delta) { xs[nd] = rtv; ys[nd] = s->s; dx[nd] = 0; slot[nd++] = SDEL; }
+        if (want_dhat) { xs[nd] = stv; ys[nd] = s->r; dx[nd] = st_fly; slot[nd++] = SDELH; }
+        xs[nd] = stv; ys[nd] = s->s; dx[nd] = st_fly; slot[nd++] = SGAM;
+        TRY(run_dots(a, st, s->part, s->counter, s->dout, nd, xs, ys, dx, h));
+        for (int q = 0; q < nd; ++q) c.sc[slot[q]] = h[q];
+        red += nd;
+        return CGVK_OK;
+    };
+    switch (v) {
+        case CGVK_HS:
+        case CGVK_CG_CG: break;
+        case CGVK_M:
+        case CGVK_PR:
+            TRY(scalar_dots(v == CGVK_PR || expr != CGVK_NU_MEURANT || s->cfg.track_delta));
+            break;
+        case CGVK_GV:
+            k_spmv<<<G, kBlock, 0, st>>>(P, rtv, nullptr, s->w, 0);
+            k_spmv<<<G, kBlock, 0, st>>>(P, stv, nullptr, s->u, 0);
+            spmv += 2;
+            break;
+        default:  // pipelined PR
+            k_spmv<<<G, kBlock, 0, st>>>(P, rtv, nullptr, s->w, 0);
+            spmv++;
+            if (prec) {
+                prec_ap++;
+                if (!s->cfg.recompute_w) k_scale<<<eg, 256, 0, st>>>((int)n, d, s->w, s->wt);
+            }
+            k_spmv<<<G, kBlock, 0, st>>>(P, stv, nullptr, s->u, 0);
+            spmv++;
+            if (prec) prec_ap++;
+            TRY(scalar_dots(expr != CGVK_NU_MEURANT || s->cfg.track_delta));
+            break;
+    }
+    CK(cudaGetLastError());
+    return finish();
+}
+
+void free_solver(cgvk_solver s) {
+    if (!s) return;
+    if (s->a) cudaSetDevice(s->a->device);
+    if (s->stream) cudaStreamSynchronize(s->stream);
+    if (s->g1) cudaGraphExecDestroy(s->g1);
+    if (s->g8) cudaGraphExecDestroy(s->g8);
+    for (double* p : {s->x, s->r, s->p0, s->p1, s->s, s->w, s->u, s->t, s->rt, s->st, s->wt, s->b,
+                      s->tmp, s->part, s->hist, s->dout})
+        cudaFree(p);
+    cudaFree(s->counter);
+    cudaFree(s->ctrl);
+    if (s->stream) cudaStreamDestroy(s->stream);
+    delete s;
+}
+
+int materialize(cgvk_solver s) {
+    TRY(refresh_mirror(s));
+    if (!s->mirror.form_pending) return CGVK_OK;
+    k_set_limit<<<1, 1, 0, s->stream>>>(s->ctrl, s->mirror.k);
+    s->k1<<<s->a->G, kBlock, 0, s->stream>>>(s->P);
+    k_set_limit<<<1, 1, 0, s->stream>>>(s->ctrl, s->k_target);
+    CK(cudaGetLastError());
+    return refresh_mirror(s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int cgvk_solver_create(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, const double* b,
+                       const double* x0, cgvk_solver* out) {
+    if (!out) return set_err(CGVK_EINVAL, "null output handle");
+    *out = nullptr;
+    if (!a) return set_err(CGVK_EINVAL, "null matrix");
+    TRY(cgvk_variant_config_validate(cfg));
+    if (!b || !x0) return set_err(CGVK_EINVAL, "right-hand side or initial guess dimension mismatch");
+    if (precond != CGVK_PRECOND_IDENTITY && precond != CGVK_PRECOND_JACOBI)
+        return set_err(CGVK_EINVAL, "unknown preconditioner kind %d", precond);
+    CK(cudaSetDevice(a->device));
+    if (precond == CGVK_PRECOND_JACOBI) {
+        std::lock_guard<std::mutex> lock(a->mu);
+        TRY(ensure_jacobi(a));
+    }
+    auto* s = new cgvk_solver_s;
+    s->a = a;
+    s->cfg = *cfg;
+    s->prec = precond == CGVK_PRECOND_JACOBI;
+    s->n = a->n;
+    const int v = cfg->variant;
+    const bool pipe = v == CGVK_PIPE_PR || v == CGVK_PIPE_PR_M;
+    const int64_t n = a->n;
+    int rc;
+    auto bail = [&](int code) {
+        free_solver(s);
+        return code;
+    };
+    s->hist_cap = 1 << 17;
+    if ((rc = dalloc(&s->x, n)) || (rc = dalloc(&s->r, n)) || (rc = dalloc(&s->p0, n)) ||
+        (rc = dalloc(&s->s, n)) || (rc = dalloc(&s->b, n)) || (rc = dalloc(&s->tmp, n)) ||
+        (rc = dalloc(&s->part, kMaxDots * (size_t)a->gmax)) || (rc = dalloc(&s->hist, s->hist_cap)) ||
+        (rc = dalloc(&s->dout, 8)) || (rc = dalloc(&s->counter, 4)) || (rc = dalloc(&s->ctrl, 1)))
+        return bail(rc);
+    if (v == CGVK_HS && (rc = dalloc(&s->p1, n))) return bail(rc);
+    if ((v == CGVK_CG_CG || v == CGVK_GV || pipe) && (rc = dalloc(&s->w, n))) return bail(rc);
+    if ((v == CGVK_GV || pipe) && (rc = dalloc(&s->u, n))) return bail(rc);
+    if (v == CGVK_GV && (rc = dalloc(&s->t, n))) return bail(rc);
+    if (s->prec && (v == CGVK_M || v == CGVK_PR || v == CGVK_GV || pipe) && (rc = dalloc(&s->rt, n)))
+        return bail(rc);
+    if (s->prec && (v == CGVK_GV || pipe) && (rc = dalloc(&s->st, n))) return bail(rc);
+    if (s->prec && pipe && (rc = dalloc(&s->wt, n))) return bail(rc);
+    if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess)
+        return bail(set_err(CGVK_ECUDA, "stream create failed"));
+    for (double* p : {s->x, s->r, s->p0, s->p1, s->s, s->w, s->u, s->t, s->rt, s->st, s->wt, s->tmp})
+        if (p && cudaMemsetAsync(p, 0, 8 * (n ? n : 1), s->stream) != cudaSuccess)
+            return bail(set_err(CGVK_ECUDA, "memset failed"));
+    if (cudaMemsetAsync(s->counter, 0, 4 * sizeof(unsigned int), s->stream) != cudaSuccess)
+        return bail(set_err(CGVK_ECUDA, "memset failed"));
+    s->allocated = ref_allocated(v, s->prec);
+
+    Params& P = s->P;
+    P = a->base();
+    P.d = s->prec ? a->inv_diag : nullptr;
+    P.x = s->x;
+    P.r = s->r;
+    P.p0 = s->p0;
+    P.p1 = s->p1;
+    P.s = s->s;
+    P.w = s->w;
+    P.u = s->u;
+    P.t = s->t;
+    P.rt = s->rt;
+    P.st = s->st;
+    P.wt = s->wt;
+    P.part = s->part;
+    P.hist = s->hist;
+    P.ctrl = s->ctrl;
+    P.nu_expr = cfg->nu_expression;
+    P.recompute_nu = cfg->recompute_nu;
+    P.recompute_w = cfg->recompute_w;
+    P.unsimplified_mu = cfg->unsimplified_mu;
+    P.track_delta = cfg->track_delta;
+    if (s->prec) pick_kernels<true>(v, &s->k1, &s->k2);
+    else pick_kernels<false>(v, &s->k1, &s->k2);
+
+    if (n == 0) {  // r0 is empty: nu0 = 0 = <r,r> -> Converged(ZeroResidual)
+        Ctrl c{};
+        c.state = ST_CONVERGED;
+        c.criterion = CB_ZERO;
+        c.stats[STAT_SPMV] = 1;
+        c.stats[STAT_PREC] = s->prec;
+        c.stats[STAT_RED] = 1;
+        c.hist_cap = 0;
+        s->mirror = c;
+        if (cudaMemcpy(s->ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice) != cudaSuccess)
+            return bail(set_err(CGVK_ECUDA, "ctrl upload failed"));
+        *out = s;
+        return CGVK_OK;
+    }
+    if ((rc = solver_init(s, b, x0)) != CGVK_OK) return bail(rc);
+    if ((rc = capture(s, 1, &s->g1)) != CGVK_OK || (rc = capture(s, 8, &s->g8)) != CGVK_OK)
+        return bail(rc);
+    *out = s;
+    return CGVK_OK;
+}
+
+int cgvk_solver_destroy(cgvk_solver s) {
+    free_solver(s);
+    return CGVK_OK;
+}
+
+int cgvk_solver_set_tolerance(cgvk_solver s, double rel_tol) {
+    if (!s) return set_err(CGVK_EINVAL, "null solver");
+    CK(cudaSetDevice(s->a->device));
+    CK(cudaStreamSynchronize(s->stream));
+    CK(cudaMemcpy(&s->ctrl->tol, &rel_tol, sizeof(double), cudaMemcpyHostToDevice));
+    s->mirror.tol = rel_tol;
+    return CGVK_OK;
+}
+
+int cgvk_solver_step(cgvk_solver s, int n_iters) {
+    if (!s) return set_err(CGVK_EINVAL, "null solver");
+    if (n_iters < 0) return set_err(CGVK_EINVAL, "n_iters must be >= 0");
+    if (s->mirror_fresh && s->mirror.state != ST_RUNNING)
+        return set_err(CGVK_ESTATE, "step() on a terminated solver");
+    if (n_iters == 0 || s->n == 0) return CGVK_OK;
+    CK(cudaSetDevice(s->a->device));
+    s->k_target += n_iters;
+    k_set_limit<<<1, 1, 0, s->stream>>>(s->ctrl, s->k_target);
+    for (int i = 0; i < n_iters / 8; ++i) CK(cudaGraphLaunch(s->g8, s->stream));
+    for (int i = 0; i < n_iters % 8; ++i) CK(cudaGraphLaunch(s->g1, s->stream));
+    CK(cudaGetLastError());
+    s->mirror_fresh = false;
+    return CGVK_OK;
+}
+
+int cgvk_solver_sync(cgvk_solver s) {
+    if (!s) return set_err(CGVK_EINVAL, "null solver");
+    CK(cudaSetDevice(s->a->device));
+    if (s->n == 0) return CGVK_OK;
+    return refresh_mirror(s);
+}
+
+int cgvk_solver_status(cgvk_solver s, cgvk_solve_status* st, cgvk_scalars* sc, cgvk_stats* stats) {
+    if (!s) return set_err(CGVK_EINVAL, "null solver");
+    if (!s->mirror_fresh) TRY(cgvk_solver_sync(s));
+    const Ctrl& c = s->mirror;
+    if (st) {
+        st->state = c.state;
+        st->breakdown = c.reason;
+        st->criterion = c.criterion;
+        st->k = c.k;
+        st->allocated_vectors = s->allocated;
+    }
+    if (sc) {
+        sc->alpha = c.sc[SA];
+        sc->beta = c.sc[SB];
+        sc->nu = c.sc[SNU];
+        sc->nu_prime = c.sc[SNUP];
+        sc->mu = c.sc[SMU];
+        sc->delta = c.sc[SDEL];
+        sc->delta_hat = c.sc[SDELH];
+        sc->gamma = c.sc[SGAM];
+        sc->eta = c.sc[SETA];
+        sc->rr = c.rr;
+    }
+    if (stats) {
+        stats->spmv_calls = c.stats[STAT_SPMV];
+        stats->block_spmv_calls = c.stats[STAT_BLOCK];
+        stats->precond_applies = c.stats[STAT_PREC];
+        stats->reductions = c.stats[STAT_RED];
+    }
+    return CGVK_OK;
+}
+
+int cgvk_solver_get_vector(cgvk_solver s, int which, double* out) {
+    if (!s || !out) return set_err(CGVK_EINVAL, "null argument");
+    const int v = s->cfg.variant;
+    const bool pipe = v == CGVK_PIPE_PR || v == CGVK_PIPE_PR_M;
+    const bool prec = s->prec;
+    const double* src = nullptr;
+    const double* scale_src = nullptr;  // out = d∘scale_src
+    bool zeros = false;
+    CK(cudaSetDevice(s->a->device));
+    if (s->n == 0) {
+        if (which == CGVK_VEC_X || which == CGVK_VEC_R || which == CGVK_VEC_P || which == CGVK_VEC_S)
+            return CGVK_OK;
+    }
+    TRY(materialize(s));
+    const Ctrl& c = s->mirror;
+    switch (which) {
+        case CGVK_VEC_X: src = s->x; break;
+        case CGVK_VEC_R: src = s->r; break;
+        case CGVK_VEC_P: src = (v == CGVK_HS && c.pcur) ? s->p1 : s->p0; break;
+        case CGVK_VEC_S: src = s->s; break;
+        case CGVK_VEC_W: src = s->w; break;
+        case CGVK_VEC_U: src = s->u; break;
+        case CGVK_VEC_T: src = s->t; break;
+        case CGVK_VEC_R_TILDE:
+            if (!prec) break;
+            if (s->rt) src = s->rt;
+            else scale_src = s->r;
+            break;
+        case CGVK_VEC_S_TILDE:
+            if (!prec || v == CGVK_HS || v == CGVK_CG_CG) break;
+            if (s->st) src = s->st;
+            else scale_src = s->s;
+            break;
+        case CGVK_VEC_W_TILDE:
+            if (!prec || !(v == CGVK_GV || pipe)) break;
+            if (v == CGVK_GV) {
+                if (c.k == 0) zeros = true;  // resized, never applied before step 1
+                else scale_src = s->w;
+            } else if (!s->cfg.recompute_w || c.wt_stored) {
+                src = s->wt;
+            } else {
+                scale_src = s->w;
+            }
+            break;
+        case CGVK_VEC_U_TILDE:
+            if (!prec || !pipe) break;
+            scale_src = s->u;
+            break;
+        default: break;
+    }
+    if (!src && !scale_src && !zeros) return set_err(CGVK_EINVAL, "vector %d is not allocated by this variant", which);
+    if (zeros) {
+        memset(out, 0, 8 * s->n);
+        return CGVK_OK;
+    }
+    if (scale_src) {
+        k_scale<<<grid_elem(s->n), 256, 0, s->stream>>>((int)s->n, s->a->inv_diag, scale_src, s->tmp);
+        CK(cudaGetLastError());
+        src = s->tmp;
+    }
+    CK(cudaMemcpyAsync(out, src, 8 * s->n, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    return CGVK_OK;
+}
+
+int cgvk_solver_true_residual(cgvk_solver s, double* out) {
+    if (!s || !out) return set_err(CGVK_EINVAL, "null argument");
+    CK(cudaSetDevice(s->a->device));
+    if (s->n == 0) {
+        *out = 0.0;
+        return CGVK_OK;
+    }
+    Params P = s->a->base();
+    k_spmv<<<s->a->G, kBlock, 0, s->stream>>>(P, s->x, s->b, s->tmp, 0);
+    CK(cudaGetLastError());
+    const double* xs[1] = {s->tmp};
+    double h[1];
+    TRY(run_dots(s->a, s->stream, s->part, s->counter, s->dout, 1, xs, xs, nullptr, h));
+    *out = std::sqrt(h[0]);
+    return CGVK_OK;
+}
+
+int cgvk_solver_history(cgvk_solver s, double* out, int cap, int* len) {
+    if (!s || !len) return set_err(CGVK_EINVAL, "null argument");
+    TRY(cgvk_solver_sync(s));
+    int m = s->mirror.k + 1;
+    if (m > s->hist_cap) m = s->hist_cap;
+    if (s->n == 0) m = 0;
+    if (out && cap > 0) {
+        const int c = m < cap ? m : cap;
+        std::vector<double> h(c);
+        if (c) CK(cudaMemcpy(h.data(), s->hist, 8 * c, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < c; ++i) out[i] = std::sqrt(h[i]);
+    }
+    *len = m;
+    return CGVK_OK;
+}
+
+void* cgvk_solver_stream(cgvk_solver s) { return s ? (void*)s->stream : nullptr; }
+
+int cgvk_solver_launches_per_iter(cgvk_solver s) { return s ? 2 : 0; }
+
+int cgvk_solve(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, const double* b,
+               const double* x0, int max_iter, double rel_tol, double* x_out, cgvk_solve_status* st,
+               cgvk_scalars* sc) {
+    if (max_iter < 0) return set_err(CGVK_EINVAL, "max_iter must be >= 0");
+    cgvk_solver s = nullptr;
+    TRY(cgvk_solver_create(a, cfg, precond, b, x0, &s));
+    int rc = CGVK_OK;
+    if (rel_tol > 0.0) rc = cgvk_solver_set_tolerance(s, rel_tol);
+    if (rc == CGVK_OK && s->mirror.state == ST_RUNNING) rc = cgvk_solver_step(s, max_iter);
+    if (rc == CGVK_OK) rc = cgvk_solver_sync(s);
+    if (rc == CGVK_OK && x_out) rc = cgvk_solver_get_vector(s, CGVK_VEC_X, x_out);
+    cgvk_solve_status tmp{};
+    if (rc == CGVK_OK) rc = cgvk_solver_status(s, &tmp, sc, nullptr);
+    // run(): a budget exhausted while running reports MaxIterations
+    // (src/runner.cpp:138)
+    if (rc == CGVK_OK && tmp.state == CGVK_RUNNING) tmp.state = CGVK_MAX_ITERATIONS;
+    if (st) *st = tmp;
+    cgvk_solver_destroy(s);
+    return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,245 @@
+// Device-side building blocks shared by every cgvk kernel (sm_100a).
+//
+//  * Ctrl: the device-resident solver control block — SolverState's scalars
+//    (inc/variants.hpp:122-130), status (:62-86), stats (:88-93) and the
+//    fused-schedule bookkeeping. Written only by the single "last CTA" of a
+//    reducing kernel; read by every CTA at kernel entry.
+//  * The canonical reduction tree: one row per thread, per-
+//    thread sequential sums over the tiles b, b+G, ..., a shfl_down warp tree,
+//    a cross-warp tree, and a last-arriving-CTA final pass over the G CTA
+//    partials. oracle/cgv_oracle.c (ORC_DOT_TREE) restates it bit-for-bit.
+//  * Rounded arithmetic helpers: every multiply and add is rounded separately
+//    (no FMA), as the reference is built with -ffp-contract=off
+//    (proj/CMakeLists.txt:12-14). The whole library is also compiled with
+//    --fmad=false.
+#pragma once
+
+#include <cstdint>
+
+namespace cgvk {
+
+constexpr int kBlock = 256;       // rows per tile == threads per CTA
+constexpr int kWarps = kBlock / 32;
+constexpr int kMinBlocksPerSM = 4;  // __launch_bounds__ minimum -> G = SMs * 4
+constexpr int kMaxDots = 6;
+
+// SolverState scalar slots
+enum { SA = 0, SB, SNU, SNUP, SMU, SDEL, SDELH, SGAM, SETA, NSCAL };
+// status (inc/variants.hpp:62-86 order)
+enum { ST_RUNNING = 0, ST_BREAKDOWN = 1, ST_MAXITER = 2, ST_CONVERGED = 3 };
+enum { BR_NONE = 0, BR_NUPRIME, BR_NU, BR_MU, BR_NONFINITE };
+enum { CB_ZERO = 0, CB_ERROR, CB_STAGNATION, CB_TOL };
+// second-kernel modes
+enum { MODE_SKIP = 0, MODE_FULL = 1, MODE_X_ONLY = 2 };
+// stats slots
+enum { STAT_SPMV = 0, STAT_BLOCK, STAT_PREC, STAT_RED };
+
+struct __align__(16) Ctrl {
+    double sc[NSCAL];
+    double rr;     // <r,r> of the current r (canonical order)
+    double tol;    // relative-residual stop (<= 0: off)
+    double bnorm;  // ||b|| (canonical order)
+    unsigned long long stats[4];
+    int k;         // SolverState::k
+    int k_limit;   // iterations run while k < k_limit
+    int state, reason, criterion;
+    int mode2;        // what the second kernel of the iteration must do
+    int form_pending; // CG-CG / GV: the beta-recurrences of the last step are owed
+    int pcur;         // HS: which p buffer is current
+    int wt_stored;    // pipe-PR: w~ lives in its buffer (nu'-terminal step)
+    int hist_cap;
+    unsigned int count[2];  // last-CTA arrival counters
+    int pad[2];
+};
+
+struct Params {
+    int n, ntiles;
+    const int* __restrict__ rp;
+    const int* __restrict__ ci;
+    const double* __restrict__ va;
+    const double* __restrict__ d;  // Jacobi inv_diag (PREC) or null
+    double* x;
+    double* r;
+    double* p0;
+    double* p1;
+    double* s;
+    double* w;
+    double* u;
+    double* t;
+    double* rt;
+    double* st;
+    double* wt;
+    double* part;  // [kMaxDots][G] CTA partials
+    double* hist;  // rr per iteration
+    Ctrl* ctrl;
+    int nu_expr, recompute_nu, recompute_w, unsimplified_mu, track_delta;
+};
+
+__device__ __forceinline__ double MUL(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ADD(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double SUB(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double DIV(double a, double b) { return __ddiv_rn(a, b); }
+
+// Canonical CTA tree over ND per-thread values; the totals end up in thread 0.
+template <int ND>
+__device__ __forceinline__ void cta_tree(double (&v)[ND], double* sm /* ND*32 */) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1)
+            v[d] = ADD(v[d], __shfl_down_sync(0xffffffffu, v[d], off));
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int d = 0; d < ND; ++d) sm[d * 32 + warp] = v[d];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int d = 0; d < ND; ++d) {
+            double y = lane < kWarps ? sm[d * 32 + lane] : 0.0;
+#pragma unroll
+            for (int off = kWarps / 2; off >= 1; off >>= 1)
+                y = ADD(y, __shfl_down_sync(0xffffffffu, y, off));
+            v[d] = y;
+        }
+    }
+    __syncthreads();
+}
+
+// Arrive on `counter`; true in every thread of the last CTA to arrive.
+__device__ __forceinline__ bool arrive_last(unsigned int* counter) {
+    __shared__ int last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned int prev = atomicAdd(counter, 1u);
+        last = prev == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) __threadfence();
+    return last != 0;
+}
+
+// Write this CTA's ND partials, arrive, and (last CTA only) fold all G
+// partials into tot[] (valid in thread 0). Returns true in the last CTA.
+template <int ND>
+__device__ __forceinline__ bool reduce_grid(double (&acc)[ND], double* part, unsigned int* counter,
+                                            double (&tot)[ND]) {
+    __shared__ double sm[ND * 32];
+    cta_tree<ND>(acc, sm);
+    const int G = gridDim.x;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int d = 0; d < ND; ++d) part[d * G + blockIdx.x] = acc[d];
+    }
+    if (!arrive_last(counter)) return false;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) tot[d] = 0.0;
+    for (int j = threadIdx.x; j < G; j += kBlock) {
+#pragma unroll
+        for (int d = 0; d < ND; ++d) tot[d] = ADD(tot[d], __ldcg(part + d * G + j));
+    }
+    cta_tree<ND>(tot, sm);
+    if (threadIdx.x == 0) *counter = 0u;
+    return true;
+}
+
+// ------------------------------------------------ status helpers (thread 0)
+// src/variants.cpp:128-173
+
+__device__ __forceinline__ void fail(Ctrl* c, int reason) {
+    c->state = ST_BREAKDOWN;
+    c->reason = reason;
+}
+
+// settle_nonpositive; rr = <r,r> of the current r (an exact-zero test, so the
+// summation order cannot change the outcome)
+__device__ __forceinline__ bool settle_nonpositive(Ctrl* c, double value, int reason, double rr) {
+    if (!isfinite(value)) {
+        fail(c, BR_NONFINITE);
+        return true;
+    }
+    if (value > 0.0) return false;
+    if (value == 0.0 && rr == 0.0) {
+        c->state = ST_CONVERGED;
+        c->criterion = CB_ZERO;
+    } else {
+        fail(c, reason);
+    }
+    return true;
+}
+
+__device__ __forceinline__ bool settle_mu(Ctrl* c) {
+    const double mu = c->sc[SMU];
+    if (!isfinite(mu)) {
+        fail(c, BR_NONFINITE);
+        return true;
+    }
+    if (mu <= 0.0) {
+        fail(c, BR_MU);
+        return true;
+    }
+    return false;
+}
+
+__device__ __forceinline__ bool finalize_alpha(Ctrl* c) {
+    c->sc[SA] = DIV(c->sc[SNU], c->sc[SMU]);
+    if (!isfinite(c->sc[SA]) || !isfinite(c->sc[SB])) {
+        fail(c, BR_NONFINITE);
+        return true;
+    }
+    return false;
+}
+
+// predicted_nu, src/variants.cpp:175-187; operands are the k-1 values
+__device__ __forceinline__ double predicted_nu(int expr, const double* sc) {
+    const double a = sc[SA];
+    const double a2g = MUL(MUL(a, a), sc[SGAM]);
+    if (expr == 1) return ADD(SUB(sc[SNU], MUL(MUL(2.0, a), sc[SDEL])), a2g);   // Simplified
+    if (expr == 2) return ADD(-sc[SNU], a2g);                                  // Meurant
+    return ADD(SUB(sc[SNU], MUL(a, ADD(sc[SDEL], sc[SDELH]))), a2g);           // Expanded
+}
+
+// Harness stop rule ||r_k|| <= tol*||b||, checked after a step.
+__device__ __forceinline__ void check_tolerance(Ctrl* c) {
+    if (c->state == ST_RUNNING && c->tol > 0.0 && sqrt(c->rr) <= MUL(c->tol, c->bnorm)) {
+        c->state = ST_CONVERGED;
+        c->criterion = CB_TOL;
+    }
+}
+
+__device__ __forceinline__ void record_rr(const Params& P, Ctrl* c, double rr) {
+    c->rr = rr;
+    if (c->k < c->hist_cap) P.hist[c->k] = rr;
+}
+
+// CSR row product, left-to-right, each term rounded (sparse_matrix.cpp:112-117).
+template <class XF>
+__device__ __forceinline__ double row_sum(const Params& P, int row, XF xf) {
+    const int k0 = __ldg(P.rp + row), k1 = __ldg(P.rp + row + 1);
+    double sum = 0.0;
+#pragma unroll 4
+    for (int k = k0; k < k1; ++k) sum = ADD(sum, MUL(__ldg(P.va + k), xf(__ldg(P.ci + k))));
+    return sum;
+}
+
+// two right-hand sides in one traversal (sparse_matrix.cpp:131-142)
+template <class XF1, class XF2>
+__device__ __forceinline__ void row_sum2(const Params& P, int row, XF1 xf1, XF2 xf2, double& y1,
+                                         double& y2) {
+    const int k0 = __ldg(P.rp + row), k1 = __ldg(P.rp + row + 1);
+    double s1 = 0.0, s2 = 0.0;
+#pragma unroll 4
+    for (int k = k0; k < k1; ++k) {
+        const double v = __ldg(P.va + k);
+        const int c = __ldg(P.ci + k);
+        s1 = ADD(s1, MUL(v, xf1(c)));
+        s2 = ADD(s2, MUL(v, xf2(c)));
+    }
+    y1 = s1;
+    y2 = s2;
+}
+
+}  // namespace cgvk
