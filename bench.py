@@ -1,0 +1,422 @@
+#!/usr/bin/env python3
+"""Benchmark: CG iterations/s and effective HBM GB/s per variant (BASELINE.json
+metric) on the BASELINE.json configs[1] workload — 3D Poisson 7-point 128^3
+(n=2,097,152, nnz=14,581,760), fp64 CSR, Jacobi, b = A x*, x* ~ U(-1,1) seeded,
+x0 = 0 — for the six variants HS, CG-CG, M, PR, GV, pipe-PR.
+
+A "step" is one CG iteration of each of the six variants (six solvers share
+the matrix), so `value` = 6*K / (sum of the six device-timed K-iteration
+runs) is the aggregate CG iterations/s; per-variant it/s, GB/s and roofline
+fractions are in `per_variant`. Timing: CUDA events on each solver's stream
+around K graph-replayed iterations (inputs resident in HBM; the per-iteration
+working set, 368-536 MB, exceeds the 126 MB L2, so no flush is needed).
+
+`e2e` goes through the public C ABI with pinned host buffers: matrix upload
+(int64 CSR, validated and narrowed on the device), then per variant
+cgvk_solve(K iterations) including the b/x0 upload and the x download.
+
+--impl reference times the reference's own CPU solver (oracle/_ref, the
+unchanged reference sources; the C restatement if that library is absent) on
+the host cores: the six variants in six threads, K steps each.
+
+Multi-GPU (torchrun, N>1): row-block (z-slab) strong scaling is not wired
+into this bench yet; each rank runs an independent replica of the workload
+("scaling": "weak", "mode": "replicas") and rank 0 reports the max-over-ranks
+time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+VARIANTS = ["hs", "cg", "m", "pr", "gv", "pipe-pr"]
+# App. A vector traffic per kernel launch (n-length fp64 vectors), Jacobi /
+# none: (update kernel K1, SpMV kernel K2). K2 additionally streams A once.
+KERNEL_VECTORS = {
+    "hs": {True: (4, 7), False: (3, 6)},
+    "cg": {True: (10, 3), False: (8, 3)},
+    "m": {True: (10, 5), False: (6, 4)},
+    "pr": {True: (10, 5), False: (6, 4)},
+    "gv": {True: (18, 3), False: (13, 2)},
+    "pipe-pr": {True: (15, 4), False: (11, 3)},
+    "pipe-pr-m": {True: (15, 4), False: (11, 3)},
+}
+KERNEL_NAMES = {"hs": ("hs_k1", "hs_k2"), "cg": ("cg_k1", "cg_k2"), "m": ("pr_k1", "pr_k2"),
+                "pr": ("pr_k1", "pr_k2"), "gv": ("gv_k1", "gv_k2"),
+                "pipe-pr": ("ppr_k1", "ppr_k2"), "pipe-pr-m": ("ppr_k1", "ppr_k2")}
+
+
+def a_bytes(n: int, nnz: int) -> int:
+    return 12 * nnz + 4 * (n + 1)
+
+
+def iter_bytes(v: str, n: int, nnz: int, prec: bool) -> int:
+    k1, k2 = KERNEL_VECTORS[v][prec]
+    return a_bytes(n, nnz) + 8 * n * (k1 + k2)
+
+
+def peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def wait_first(self, timeout: float = 5.0) -> None:
+        t0 = time.perf_counter()
+        while self.proc and not self.lines and time.perf_counter() - t0 < timeout:
+            time.sleep(0.01)
+
+    def mark(self, name: str) -> None:
+        setattr(self, name, time.perf_counter())
+
+    def stop(self) -> dict | None:
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        t0, t1 = getattr(self, "t_start", None), getattr(self, "t_end", None)
+        lines = [ln for ts, ln in self.lines if t0 is None or t0 <= ts <= t1 + 0.025]
+        in_region = len(lines)
+        if not lines:  # region shorter than the sampling period: nearest samples
+            lines = [ln for _, ln in self.lines[-3:]]
+        for ln in lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, f[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm), "samples_in_timed_region": in_region}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+        return rank, local, world, dist
+    return rank, local, world, None
+
+
+def max_over_ranks(dist, value: float) -> float:
+    if dist is None:
+        return value
+    import torch
+
+    t = torch.tensor([value], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ CPU arms
+
+def cpu_sweep(P, variants, steps: int, warmup: int, kind: str):
+    """The six variants in six threads (the reference's jobs>1 model,
+    src/experiment.cpp:317-322); each thread runs `steps` step() calls."""
+    from oracle import oracle as O
+    from paper_1905_01549_b200.cgvk import variant_from_name
+
+    solvers = []
+    for v in variants:
+        vid = int(variant_from_name(v))
+        if kind == "reference":
+            solvers.append(O.Reference(P.A, vid, 1, P.b, P.x0))
+        else:
+            solvers.append(O.Restatement(P.A, vid, 1, P.b, P.x0))
+    if warmup:
+        ths = [threading.Thread(target=s.time_steps, args=(warmup,)) for s in solvers]
+        [t.start() for t in ths]
+        [t.join() for t in ths]
+    res = [None] * len(solvers)
+
+    def work(i):
+        res[i] = solvers[i].time_steps(steps)
+
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(len(solvers))]
+    t0 = time.perf_counter()
+    [t.start() for t in ths]
+    [t.join() for t in ths]
+    wall = time.perf_counter() - t0
+    iters = sum(r[1] for r in res)
+    per = {v: {"it_per_s": r[1] / r[0] if r[0] > 0 else None, "ms_per_iter": 1e3 * r[0] / max(r[1], 1)}
+           for v, r in zip(variants, res)}
+    return iters, wall, per
+
+
+def run_reference_arm(args, rank, world, dist):
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    from paper_1905_01549_b200 import problems as pb
+
+    kind = "reference" if O.reference_available() else "port"
+    P = pb.config_problem(args.config)
+    iters, wall, per = cpu_sweep(P, VARIANTS, args.steps, args.warmup, kind)
+    value = iters / wall
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "iterations/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, P),
+        "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": len(VARIANTS),
+                         "kind": kind,
+                         "sample": f"{args.steps} step() calls of each of the six variants on "
+                                   f"{args.config}, one thread per variant"},
+        "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "per_variant": per,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+METRIC = "CG iterations/s (six-variant sweep) and effective HBM GB/s per variant"
+
+
+def workload_config(args, P) -> dict:
+    return {"workload": f"{args.config} ({P.A.n} rows, {P.A.nnz} nnz) fp64 CSR, Jacobi, "
+                        f"six variants, K fixed iterations each",
+            "variants": VARIANTS, "n": P.A.n, "nnz": P.A.nnz, "precond": "jacobi",
+            "l2": "working set > L2 (126 MB); no flush", "parallelism": "replicas" if
+            int(os.environ.get("WORLD_SIZE", "1")) > 1 else "single-gpu"}
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def load_traffic() -> dict:
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+def run_gpu_arm(args, rank, local, world, dist):
+    from paper_1905_01549_b200 import cgvk, problems as pb
+    from paper_1905_01549_b200.cgvk import Precond, VariantConfig, variant_from_name
+
+    device = local
+    P = pb.config_problem(args.config)
+    n, nnz = P.A.n, P.A.nnz
+    pk = peaks()
+    A = cgvk.DeviceMatrix.from_csr(P.A, device=device)
+    solvers = {}
+    for v in VARIANTS:
+        s = cgvk.initialize(VariantConfig.make(variant_from_name(v)), A, Precond.JACOBI, P.b, P.x0)
+        solvers[v] = s
+    # warm-up: W iterations per variant (graphs, clocks, caches)
+    for v, s in solvers.items():
+        s.time_steps(args.warmup)
+
+    clocks = ClockSampler(device) if not args.no_clocks else None
+    if clocks:
+        clocks.start()
+        clocks.wait_first()
+    barrier(dist)
+    if clocks:
+        clocks.mark("t_start")
+    per = {}
+    total_ms, total_iters = 0.0, 0
+    for v, s in solvers.items():
+        ms, it = s.time_steps(args.steps)
+        per[v] = {"ms": ms, "iters": it}
+        total_ms += ms
+        total_iters += it
+    if clocks:
+        clocks.mark("t_end")
+        time.sleep(0.05)
+    clk = clocks.stop() if clocks else None
+    barrier(dist)
+    total_ms = max_over_ranks(dist, total_ms)
+
+    # per-kernel device times (events around each launch, same stream)
+    prof_iters = min(args.steps, 20)
+    kernels = []
+    for v in VARIANTS:
+        s = cgvk.initialize(VariantConfig.make(variant_from_name(v)), A, Precond.JACOBI, P.b, P.x0)
+        s.time_steps(2)
+        k1, k2, it = s.profile(prof_iters)
+        names = KERNEL_NAMES[v]
+        vec = KERNEL_VECTORS[v][True]
+        b1 = 8 * n * vec[0]
+        b2 = a_bytes(n, nnz) + 8 * n * vec[1]
+        kernels.append({"variant": v, "kernel": names[0], "ms_per_launch": k1 / it,
+                        "bytes_per_launch": b1, "gbs": b1 / (k1 / it * 1e-3) / 1e9})
+        kernels.append({"variant": v, "kernel": names[1], "ms_per_launch": k2 / it,
+                        "bytes_per_launch": b2, "gbs": b2 / (k2 / it * 1e-3) / 1e9})
+        s.close()
+    top = max(kernels, key=lambda k: k["ms_per_launch"])
+    traffic = load_traffic().get(top["kernel"])
+
+    for v in VARIANTS:
+        d = per[v]
+        t_iter = d["ms"] / max(d["iters"], 1) * 1e-3
+        bi = iter_bytes(v, n, nnz, True)
+        per[v].update({"it_per_s": d["iters"] / (d["ms"] * 1e-3), "us_per_iter": t_iter * 1e6,
+                       "bytes_per_iter": bi, "gbs": bi / t_iter / 1e9,
+                       "roofline_frac": bi / t_iter / 1e9 / pk["hbm_gbs"],
+                       "roofline_frac_nominal_8tbs": bi / t_iter / 1e9 / 8000.0})
+
+    # e2e through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        rp, ci, va = P.A.row_ptr.copy(), P.A.col_idx.copy(), P.A.values.copy()
+        b, x0 = P.b.copy(), P.x0.copy()
+        xout = np.empty(n)
+        pinned = [rp, ci, va, b, x0, xout]
+        for arr in pinned:
+            cgvk.host_register(arr)
+        try:
+            barrier(dist)
+            t0 = time.perf_counter()
+            A2 = cgvk.DeviceMatrix(n, rp, ci, va, device=device)
+            e2e_iters = 0
+            for v in VARIANTS:
+                x, st, k = cgvk.solve(A2, VariantConfig.make(variant_from_name(v)), Precond.JACOBI,
+                                      b, x0, args.steps)
+                e2e_iters += k
+            A2.close()
+            t1 = time.perf_counter()
+            barrier(dist)
+            wall = max_over_ranks(dist, t1 - t0)
+        finally:
+            for arr in pinned:
+                cgvk.host_unregister(arr)
+        h2d = rp.nbytes + ci.nbytes + va.nbytes + len(VARIANTS) * (b.nbytes + x0.nbytes)
+        d2h = len(VARIANTS) * xout.nbytes
+        e2e = {"value": world * e2e_iters / wall, "unit": "iterations/s",
+               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+               "note": "per solve sweep: int64 CSR + b,x0 per variant up, x per variant down; "
+                       "bytes_per_step = sweep bytes / K"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import oracle as O
+
+        kind = "reference" if O.reference_available() else "port"
+        cpu_steps = args.cpu_steps
+        iters, wall, cper = cpu_sweep(P, VARIANTS, cpu_steps, 1, kind)
+        cpu = {"value": iters / wall, "unit": "iterations/s", "cores": len(VARIANTS), "kind": kind,
+               "sample": f"{cpu_steps} step() calls of each of the six variants on {args.config} "
+                         f"(one thread per variant, -O2 -ffp-contract=off build)",
+               "per_variant": cper}
+
+    value = world * total_iters / (total_ms * 1e-3)
+    if rank == 0:
+        launches = sum(1 + 2 * per[v]["iters"] for v in VARIANTS)
+        line = {
+            "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (App. B generator: Dirichlet 7-point Laplacian, x* from "
+                    "mt19937_64(1))",
+            "config": workload_config(args, P),
+            "roofline": {"bound": "hbm", "kernel": top["kernel"], "variant": top["variant"],
+                         "achieved": top["gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": top["gbs"] / pk["hbm_gbs"], "peak_source": pk["source"],
+                         "traffic": traffic,
+                         "bytes_per_launch": top["bytes_per_launch"],
+                         "ms_per_launch": top["ms_per_launch"]},
+            "kernels": kernels,
+            "per_variant": per,
+            "gpu_launches": launches,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    for s in solvers.values():
+        s.close()
+    A.close()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="p128", choices=["p2d", "p64", "p128", "v256", "r4m"])
+    ap.add_argument("--cpu-steps", type=int, default=10)
+    ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: at least 3 warm-up steps
+    rank, local, world, dist = dist_init()
+    try:
+        if args.impl == "reference":
+            return run_reference_arm(args, rank, world, dist)
+        return run_gpu_arm(args, rank, local, world, dist)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

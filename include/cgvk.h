@@ -185,6 +185,14 @@ int cgvk_solver_history(cgvk_solver s, double* out, int cap, int* len);
 void* cgvk_solver_stream(cgvk_solver s);
 /* Number of kernel launches one iteration makes (graph nodes / iteration). */
 int cgvk_solver_launches_per_iter(cgvk_solver s);
+/* Device-timed step(): CUDA events on the solver's stream around the enqueue
+ * of n_iters graph-replayed iterations; synchronises. *iters = iterations
+ * actually executed (fewer if the solver terminated). */
+int cgvk_solver_time_steps(cgvk_solver s, int n_iters, double* ms, int* iters);
+/* Per-kernel device times: n_iters iterations launched kernel by kernel (no
+ * graph) with CUDA events around each launch on the solver's stream; returns
+ * the summed milliseconds of the first (update) and second (SpMV) kernel. */
+int cgvk_solver_profile(cgvk_solver s, int n_iters, double* k1_ms, double* k2_ms, int* iters);
 
 /* run() (inc/runner.hpp:47-49) with StopRule::fixed(max_iter) and probes
  * off, plus an optional relative-residual tolerance: initialize, step until

@@ -159,6 +159,8 @@ def _load() -> C.CDLL:
         "cgvk_solver_history": (I, [P, P, I, C.POINTER(I)]),
         "cgvk_solver_stream": (P, [P]),
         "cgvk_solver_launches_per_iter": (I, [P]),
+        "cgvk_solver_time_steps": (I, [P, I, C.POINTER(D), C.POINTER(I)]),
+        "cgvk_solver_profile": (I, [P, I, C.POINTER(D), C.POINTER(D), C.POINTER(I)]),
         "cgvk_solve": (I, [P, C.POINTER(_Config), I, P, P, I, D, P, C.POINTER(_Status),
                            C.POINTER(_Scalars)]),
         "cgvk_host_register": (I, [P, C.c_uint64]),
@@ -430,6 +432,19 @@ class Solver:
 
     def launches_per_iter(self) -> int:
         return _lib.cgvk_solver_launches_per_iter(self._h)
+
+    def time_steps(self, n_iters: int) -> tuple[float, int]:
+        """Device time (ms) of n_iters graph-replayed iterations, and how many ran."""
+        ms, it = C.c_double(), C.c_int()
+        _check(_lib.cgvk_solver_time_steps(self._h, int(n_iters), C.byref(ms), C.byref(it)))
+        return ms.value, it.value
+
+    def profile(self, n_iters: int) -> tuple[float, float, int]:
+        """Summed device ms of the update kernel and the SpMV kernel over n_iters."""
+        a, b, it = C.c_double(), C.c_double(), C.c_int()
+        _check(_lib.cgvk_solver_profile(self._h, int(n_iters), C.byref(a), C.byref(b),
+                                        C.byref(it)))
+        return a.value, b.value, it.value
 
     # reference-named accessors
     @property

@@ -45,6 +45,8 @@ int set_err(int code, const char* fmt, ...) {
         if (rc_ != CGVK_OK) return rc_; \
     } while (0)
 
+constexpr int kMaxStageCap = 12288;  // CSR entries per stage (tiles above: direct loads)
+
 int grid_elem(int64_t n) {
     int64_t g = (n + 255) / 256;
     if (g > 148 * 16) g = 148 * 16;
@@ -70,7 +72,8 @@ int dalloc(T** p, size_t count) {
 struct cgvk_matrix_s {
     int device = 0;
     int64_t n = 0, nnz = 0;
-    int ntiles = 0, gmax = 0, G = 1;
+    int ntiles = 0, gmax = 0, G = 1, sms = 0;
+    int cap = 4;  // CSR entries a pipeline stage holds (max over tiles, capped)
     int* rp = nullptr;
     int* ci = nullptr;
     double* va = nullptr;
@@ -103,7 +106,7 @@ int ensure_jacobi(cgvk_matrix a) {
     if (a->jacobi_state == 1) return CGVK_OK;
     if (a->jacobi_state == -1)
         return set_err(CGVK_EINVAL, "Jacobi preconditioner needs a positive diagonal");
-    if (!a->inv_diag) TRY(dalloc(&a->inv_diag, a->n));
+    if (!a->inv_diag) TRY(dalloc(&a->inv_diag, a->n + 32));
     CK(cudaMemsetAsync(a->flags, 0, sizeof(int), a->stream));
     if (a->n > 0)
         k_jacobi<<<grid_elem(a->n), 256, 0, a->stream>>>((int)a->n, a->rp, a->ci, a->va, a->inv_diag,
@@ -218,7 +221,18 @@ int cgvk_matrix_create_csr(int64_t n, const int64_t* row_ptr, const int64_t* col
     a->ntiles = (int)((n + kBlock - 1) / kBlock);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    a->sms = sms;
     a->gmax = sms * kMinBlocksPerSM;
+    {   // stage capacity: the largest tile's CSR span (+ alignment slack)
+        int64_t mx = 0;
+        for (int64_t r0 = 0; r0 < n; r0 += kBlock) {
+            const int64_t r1 = r0 + kBlock < n ? r0 + kBlock : n;
+            const int64_t span = row_ptr[r1] - (row_ptr[r0] & ~int64_t(3)) + 8;
+            if (span > mx) mx = span;
+        }
+        mx = (mx + 3) & ~int64_t(3);
+        a->cap = (int)(mx < kMaxStageCap ? mx : kMaxStageCap);
+    }
     a->G = a->ntiles < a->gmax ? a->ntiles : a->gmax;
     if (a->G < 1) a->G = 1;
     auto bail = [&](int rc) {
@@ -226,7 +240,9 @@ int cgvk_matrix_create_csr(int64_t n, const int64_t* row_ptr, const int64_t* col
         return rc;
     };
     int rc;
-    if ((rc = dalloc(&a->rp, n + 1)) || (rc = dalloc(&a->ci, nnz)) || (rc = dalloc(&a->va, nnz)) ||
+    // +padding: bulk copies round their sizes up to 16 bytes
+    if ((rc = dalloc(&a->rp, n + 1 + 16)) || (rc = dalloc(&a->ci, nnz + 16)) ||
+        (rc = dalloc(&a->va, nnz + 16)) ||
         (rc = dalloc(&a->part, kMaxDots * (size_t)a->gmax)) || (rc = dalloc(&a->counter, 4)) ||
         (rc = dalloc(&a->out, 8)) || (rc = dalloc(&a->flags, 1)))
         return bail(rc);
@@ -397,7 +413,15 @@ int cgvk_host_unregister(void* ptr) {
 
 // ===================================================================== solver
 
-using KernelFn = void (*)(Params);
+using StreamFn = void (*)(Params, StageCfg);
+
+// One pipelined kernel: function, stage configuration, grid, dynamic smem.
+struct KLaunch {
+    StreamFn fn = nullptr;
+    StageCfg S{};
+    int grid = 1;
+    size_t smem = 0;
+};
 
 struct cgvk_solver_s {
     cgvk_matrix a = nullptr;
@@ -415,7 +439,7 @@ struct cgvk_solver_s {
     Ctrl mirror{};
     bool mirror_fresh = true;
     int k_target = 0;
-    KernelFn k1 = nullptr, k2 = nullptr;
+    KLaunch k1, k2;
     cudaGraphExec_t g1 = nullptr, g8 = nullptr;
     Params P{};
     int allocated = 0;
@@ -423,17 +447,59 @@ struct cgvk_solver_s {
 
 namespace {
 
+constexpr int kSmemPerSM = 227 * 1024;
+
+// Configure k_stream<Op> for matrix `a`: ring depth chosen so two CTAs fit
+// per SM when the stages allow it, physical grid = resident CTAs (<= Gv).
+template <class Op>
+int make_launch(cgvk_matrix a, KLaunch* L) {
+    L->fn = k_stream<Op>;
+    StageCfg S{};
+    S.nvec = Op::NV;
+    S.cap = Op::CSR ? a->cap : 0;
+    S.stage_bytes = (stage_bytes_for(S.cap, S.nvec, Op::CSR) + 127) & ~127;
+    S.gvirt = a->G;
+    const int header = ((int)sizeof(PipeHeader) + 127) & ~127;
+    const int budget2 = kSmemPerSM / 2 - 2048;  // two CTAs per SM
+    int ns = (budget2 - header) / S.stage_bytes;
+    if (ns < 2) ns = 2;
+    if (ns > 6) ns = 6;
+    S.nstage = ns;
+    L->smem = (size_t)header + (size_t)ns * S.stage_bytes;
+    if (L->smem > (size_t)kSmemPerSM - 1024)
+        return set_err(CGVK_EINVAL, "pipeline stage (%d bytes) exceeds shared memory", S.stage_bytes);
+    CK(cudaFuncSetAttribute(L->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L->smem));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L->fn, kThreads, L->smem));
+    if (occ < 1) return set_err(CGVK_ECUDA, "pipeline kernel does not fit on an SM");
+    L->grid = occ * a->sms < a->G ? occ * a->sms : a->G;
+    L->S = S;
+    return CGVK_OK;
+}
+
 template <bool PREC>
-void pick_kernels(int v, KernelFn* k1, KernelFn* k2) {
+int pick_kernels(cgvk_matrix a, int v, KLaunch* k1, KLaunch* k2) {
     switch (v) {
-        case CGVK_HS: *k1 = hs_k1<PREC>; *k2 = hs_k2<PREC>; break;
-        case CGVK_CG_CG: *k1 = cg_k1<PREC>; *k2 = cg_k2<PREC>; break;
+        case CGVK_HS:
+            TRY(make_launch<HsK1<PREC>>(a, k1));
+            return make_launch<HsK2<PREC>>(a, k2);
+        case CGVK_CG_CG:
+            TRY(make_launch<CgK1<PREC>>(a, k1));
+            return make_launch<CgK2<PREC>>(a, k2);
         case CGVK_M:
-        case CGVK_PR: *k1 = pr_k1<PREC>; *k2 = pr_k2<PREC>; break;
-        case CGVK_GV: *k1 = gv_k1<PREC>; *k2 = gv_k2<PREC>; break;
-        default: *k1 = ppr_k1<PREC>; *k2 = ppr_k2<PREC>; break;
+        case CGVK_PR:
+            TRY(make_launch<PrK1<PREC>>(a, k1));
+            return make_launch<PrK2<PREC>>(a, k2);
+        case CGVK_GV:
+            TRY(make_launch<GvK1<PREC>>(a, k1));
+            return make_launch<GvK2<PREC>>(a, k2);
+        default:
+            TRY(make_launch<PprK1<PREC>>(a, k1));
+            return make_launch<PprK2<PREC>>(a, k2);
     }
 }
+
+void launch(cgvk_solver s, const KLaunch& L);
 
 // the reference's allocated_vectors() (src/variants.cpp:97-103) for the
 // vectors initialize() resizes (src/variants.cpp:354-444)
@@ -452,10 +518,13 @@ int ref_allocated(int v, bool prec) {
     return c;
 }
 
+void launch(cgvk_solver s, const KLaunch& L) {
+    L.fn<<<L.grid, kThreads, L.smem, s->stream>>>(s->P, L.S);
+}
+
 void launch_iter(cgvk_solver s) {
-    const int G = s->a->G;
-    s->k1<<<G, kBlock, 0, s->stream>>>(s->P);
-    s->k2<<<G, kBlock, 0, s->stream>>>(s->P);
+    launch(s, s->k1);
+    launch(s, s->k2);
 }
 
 int capture(cgvk_solver s, int iters, cudaGraphExec_t* exec) {
@@ -643,7 +712,7 @@ int materialize(cgvk_solver s) {
     TRY(refresh_mirror(s));
     if (!s->mirror.form_pending) return CGVK_OK;
     k_set_limit<<<1, 1, 0, s->stream>>>(s->ctrl, s->mirror.k);
-    s->k1<<<s->a->G, kBlock, 0, s->stream>>>(s->P);
+    launch(s, s->k1);
     k_set_limit<<<1, 1, 0, s->stream>>>(s->ctrl, s->k_target);
     CK(cudaGetLastError());
     return refresh_mirror(s);
@@ -681,19 +750,20 @@ int cgvk_solver_create(cgvk_matrix a, const cgvk_variant_config* cfg, int precon
         return code;
     };
     s->hist_cap = 1 << 17;
-    if ((rc = dalloc(&s->x, n)) || (rc = dalloc(&s->r, n)) || (rc = dalloc(&s->p0, n)) ||
-        (rc = dalloc(&s->s, n)) || (rc = dalloc(&s->b, n)) || (rc = dalloc(&s->tmp, n)) ||
+    const int64_t nv = n + 32;  // bulk copies of the last tile round up to 16 bytes
+    if ((rc = dalloc(&s->x, nv)) || (rc = dalloc(&s->r, nv)) || (rc = dalloc(&s->p0, nv)) ||
+        (rc = dalloc(&s->s, nv)) || (rc = dalloc(&s->b, nv)) || (rc = dalloc(&s->tmp, nv)) ||
         (rc = dalloc(&s->part, kMaxDots * (size_t)a->gmax)) || (rc = dalloc(&s->hist, s->hist_cap)) ||
         (rc = dalloc(&s->dout, 8)) || (rc = dalloc(&s->counter, 4)) || (rc = dalloc(&s->ctrl, 1)))
         return bail(rc);
-    if (v == CGVK_HS && (rc = dalloc(&s->p1, n))) return bail(rc);
-    if ((v == CGVK_CG_CG || v == CGVK_GV || pipe) && (rc = dalloc(&s->w, n))) return bail(rc);
-    if ((v == CGVK_GV || pipe) && (rc = dalloc(&s->u, n))) return bail(rc);
-    if (v == CGVK_GV && (rc = dalloc(&s->t, n))) return bail(rc);
-    if (s->prec && (v == CGVK_M || v == CGVK_PR || v == CGVK_GV || pipe) && (rc = dalloc(&s->rt, n)))
+    if (v == CGVK_HS && (rc = dalloc(&s->p1, nv))) return bail(rc);
+    if ((v == CGVK_CG_CG || v == CGVK_GV || pipe) && (rc = dalloc(&s->w, nv))) return bail(rc);
+    if ((v == CGVK_GV || pipe) && (rc = dalloc(&s->u, nv))) return bail(rc);
+    if (v == CGVK_GV && (rc = dalloc(&s->t, nv))) return bail(rc);
+    if (s->prec && (v == CGVK_M || v == CGVK_PR || v == CGVK_GV || pipe) && (rc = dalloc(&s->rt, nv)))
         return bail(rc);
-    if (s->prec && (v == CGVK_GV || pipe) && (rc = dalloc(&s->st, n))) return bail(rc);
-    if (s->prec && pipe && (rc = dalloc(&s->wt, n))) return bail(rc);
+    if (s->prec && (v == CGVK_GV || pipe) && (rc = dalloc(&s->st, nv))) return bail(rc);
+    if (s->prec && pipe && (rc = dalloc(&s->wt, nv))) return bail(rc);
     if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess)
         return bail(set_err(CGVK_ECUDA, "stream create failed"));
     for (double* p : {s->x, s->r, s->p0, s->p1, s->s, s->w, s->u, s->t, s->rt, s->st, s->wt, s->tmp})
@@ -725,8 +795,9 @@ int cgvk_solver_create(cgvk_matrix a, const cgvk_variant_config* cfg, int precon
     P.recompute_w = cfg->recompute_w;
     P.unsimplified_mu = cfg->unsimplified_mu;
     P.track_delta = cfg->track_delta;
-    if (s->prec) pick_kernels<true>(v, &s->k1, &s->k2);
-    else pick_kernels<false>(v, &s->k1, &s->k2);
+    if ((rc = s->prec ? pick_kernels<true>(a, v, &s->k1, &s->k2)
+                      : pick_kernels<false>(a, v, &s->k1, &s->k2)) != CGVK_OK)
+        return bail(rc);
 
     if (n == 0) {  // r0 is empty: nu0 = 0 = <r,r> -> Converged(ZeroResidual)
         Ctrl c{};
@@ -919,6 +990,64 @@ int cgvk_solver_history(cgvk_solver s, double* out, int cap, int* len) {
 void* cgvk_solver_stream(cgvk_solver s) { return s ? (void*)s->stream : nullptr; }
 
 int cgvk_solver_launches_per_iter(cgvk_solver s) { return s ? 2 : 0; }
+
+int cgvk_solver_time_steps(cgvk_solver s, int n_iters, double* ms, int* iters) {
+    if (!s || !ms || !iters) return set_err(CGVK_EINVAL, "null argument");
+    CK(cudaSetDevice(s->a->device));
+    TRY(refresh_mirror(s));
+    const int k0 = s->mirror.k;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, s->stream));
+    const int rc = cgvk_solver_step(s, n_iters);
+    CK(cudaEventRecord(e1, s->stream));
+    CK(cudaEventSynchronize(e1));
+    float f = 0.f;
+    CK(cudaEventElapsedTime(&f, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    TRY(rc);
+    TRY(refresh_mirror(s));
+    *ms = f;
+    *iters = s->mirror.k - k0;
+    return CGVK_OK;
+}
+
+int cgvk_solver_profile(cgvk_solver s, int n_iters, double* k1_ms, double* k2_ms, int* iters) {
+    if (!s || !k1_ms || !k2_ms || !iters) return set_err(CGVK_EINVAL, "null argument");
+    CK(cudaSetDevice(s->a->device));
+    TRY(refresh_mirror(s));
+    if (s->mirror.state != ST_RUNNING) return set_err(CGVK_ESTATE, "step() on a terminated solver");
+    const int k0 = s->mirror.k;
+    s->k_target += n_iters;
+    k_set_limit<<<1, 1, 0, s->stream>>>(s->ctrl, s->k_target);
+    std::vector<cudaEvent_t> ev(3 * (size_t)n_iters);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    for (int i = 0; i < n_iters; ++i) {
+        CK(cudaEventRecord(ev[3 * i], s->stream));
+        launch(s, s->k1);
+        CK(cudaEventRecord(ev[3 * i + 1], s->stream));
+        launch(s, s->k2);
+        CK(cudaEventRecord(ev[3 * i + 2], s->stream));
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s->stream));
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < n_iters; ++i) {
+        float f1 = 0.f, f2 = 0.f;
+        CK(cudaEventElapsedTime(&f1, ev[3 * i], ev[3 * i + 1]));
+        CK(cudaEventElapsedTime(&f2, ev[3 * i + 1], ev[3 * i + 2]));
+        a += f1;
+        b += f2;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    TRY(refresh_mirror(s));
+    *k1_ms = a;
+    *k2_ms = b;
+    *iters = s->mirror.k - k0;
+    return CGVK_OK;
+}
 
 int cgvk_solve(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, const double* b,
                const double* x0, int max_iter, double rel_tol, double* x_out, cgvk_solve_status* st,

@@ -1,0 +1,331 @@
+// The TMA-staged tile pipeline every hot kernel runs on (sm_100a).
+//
+// A CTA = 8 consumer warps (one row per thread, kBlock = 256 rows per tile)
+// + 1 producer warp. The producer streams, per tile, the row_ptr slice, the
+// CSR values and column indices of the tile's rows, and each per-row input
+// vector the kernel needs, into a ring of shared-memory stages with 1D bulk
+// async copies (cp.async.bulk ... mbarrier::complete_tx, "UBLKCP" in SASS),
+// NSTAGE tiles ahead. Consumers wait on the stage's full barrier, compute
+// their row (the SpMV row product from shared memory, the x gathers through
+// L1/L2), store outputs straight to global, fold the dot products, and
+// release the stage on its empty barrier. Only the gathered SpMV operand is
+// read with ordinary loads.
+//
+// Reduction order is the canonical one of cgvk_device.cuh, expressed on
+// "virtual CTAs": virtual CTA vb (0 <= vb < Gv = min(gmax, ntiles)) owns
+// tiles vb, vb+Gv, ...; a physical CTA p runs virtual CTAs p, p+Gp, ... one
+// after the other (Gp = resident CTAs), so the result bits do not depend on
+// how many CTAs fit on the chip.
+#pragma once
+
+#include "cgvk_device.cuh"
+
+namespace cgvk {
+
+constexpr int kConsumers = kBlock;           // 8 warps, one row each
+constexpr int kThreads = kBlock + 32;        // + producer warp
+constexpr int kMaxStages = 8;
+constexpr int kRpInts = kBlock + 4;          // row_ptr slice (257 used), padded to 16 B
+constexpr int kMaxVec = 12;
+
+struct StageCfg {
+    int nstage;     // ring depth
+    int cap;        // CSR entries per stage (multiple of 4)
+    int nvec;       // staged vectors
+    int stage_bytes;
+    int gvirt;      // Gv
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// 1D bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0,
+// both addresses 16-byte aligned). Streams are read once: evict-first in L2.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
+
+// Canonical CTA tree over the 256 consumer threads (same order as cta_tree).
+template <int ND>
+__device__ __forceinline__ void cta_tree_c(double (&v)[ND], double* sm) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) v[d] = ADD(v[d], __shfl_down_sync(0xffffffffu, v[d], off));
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int d = 0; d < ND; ++d) sm[d * 32 + warp] = v[d];
+    }
+    consumer_sync();
+    if (warp == 0) {
+#pragma unroll
+        for (int d = 0; d < ND; ++d) {
+            double y = lane < kWarps ? sm[d * 32 + lane] : 0.0;
+#pragma unroll
+            for (int off = kWarps / 2; off >= 1; off >>= 1) y = ADD(y, __shfl_down_sync(0xffffffffu, y, off));
+            v[d] = y;
+        }
+    }
+    consumer_sync();
+}
+
+__device__ __forceinline__ bool arrive_last_c(unsigned int* counter, int* flag) {
+    consumer_sync();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned int prev = atomicAdd(counter, 1u);
+        *flag = prev == gridDim.x - 1;
+    }
+    consumer_sync();
+    const bool last = *flag != 0;
+    if (last) __threadfence();
+    return last;
+}
+
+// A CSR row as seen by a consumer: entries [b, e) of the global arrays, read
+// from the stage when staged.
+struct RowRef {
+    const double* va;  // already offset so that va[k] is entry k
+    const int* ci;
+    int b, e;
+};
+
+template <class XF>
+__device__ __forceinline__ double row_dot(const RowRef& R, XF xf) {
+    double sum = 0.0;
+#pragma unroll 4
+    for (int k = R.b; k < R.e; ++k) sum = ADD(sum, MUL(R.va[k], xf(R.ci[k])));
+    return sum;
+}
+
+template <class XF1, class XF2>
+__device__ __forceinline__ void row_dot2(const RowRef& R, XF1 xf1, XF2 xf2, double& y1, double& y2) {
+    double s1 = 0.0, s2 = 0.0;
+#pragma unroll 4
+    for (int k = R.b; k < R.e; ++k) {
+        const double v = R.va[k];
+        const int c = R.ci[k];
+        s1 = ADD(s1, MUL(v, xf1(c)));
+        s2 = ADD(s2, MUL(v, xf2(c)));
+    }
+    y1 = s1;
+    y2 = s2;
+}
+
+// Per-stage shared-memory layout.
+struct StageView {
+    int* rp;      // kRpInts
+    double* va;   // cap
+    int* ci;      // cap
+    double* vec;  // nvec * kBlock
+};
+
+__device__ __forceinline__ StageView stage_view(unsigned char* base, const StageCfg& S, int slot) {
+    unsigned char* p = base + (size_t)slot * S.stage_bytes;
+    StageView v;
+    v.rp = reinterpret_cast<int*>(p);
+    p += kRpInts * 4;
+    v.va = reinterpret_cast<double*>(p);
+    p += (size_t)S.cap * 8;
+    v.ci = reinterpret_cast<int*>(p);
+    p += (size_t)S.cap * 4;
+    v.vec = reinterpret_cast<double*>(p);
+    return v;
+}
+
+__host__ __device__ inline int stage_bytes_for(int cap, int nvec, bool csr) {
+    return kRpInts * 4 + (csr ? cap * 12 : 0) + nvec * kBlock * 8;
+}
+
+// Header in dynamic shared memory: barriers + per-slot metadata.
+struct PipeHeader {
+    uint64_t full[kMaxStages];
+    uint64_t empty[kMaxStages];
+    int k0a[kMaxStages];   // first staged value index (even)
+    int k0c[kMaxStages];   // first staged column index (multiple of 4)
+    int direct[kMaxStages];
+    int last_flag;
+    int pad[3];
+    double red[kMaxDots * 32];
+};
+
+// ---------------------------------------------------------------- driver
+//
+// Op contract (all device members):
+//   static constexpr int NV, ND; static constexpr bool CSR;
+//   bool enter(const Params&)            uniform: false -> nothing to do
+//   const double* vec(const Params&, int v)   stream v (nullptr: not staged)
+//   int sync()                           0: none, 1: arrive only, 2: reduce ND dots
+//   void row(const Params&, int i, const double* sv, const RowRef&, double* acc)
+//        sv[v * kBlock] = staged value of vector v at row i
+//   void finish(const Params&, Ctrl*, const double* tot)   thread 0, last CTA
+template <class Op>
+__global__ void __launch_bounds__(kThreads, 1) k_stream(Params P, StageCfg S) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    PipeHeader* H = reinterpret_cast<PipeHeader*>(smem_raw);
+    unsigned char* stages = smem_raw + ((sizeof(PipeHeader) + 127) / 128) * 128;
+    Op op;
+    if (!op.enter(P)) return;  // uniform over the grid
+    const int Gv = S.gvirt, Gp = gridDim.x, ntiles = P.ntiles, NS = S.nstage;
+    const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&H->full[s], 1);
+            mbar_init(&H->empty[s], kWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == kWarps) {  // ------------------------------ producer warp
+        if ((threadIdx.x & 31) != 0) return;
+        const uint64_t pol = evict_first_policy();
+        const double* vp[kMaxVec];
+#pragma unroll
+        for (int v = 0; v < Op::NV; ++v) vp[v] = op.vec(P, v);
+        int j = 0;
+        for (int vb = blockIdx.x; vb < Gv; vb += Gp) {
+            for (int tile = vb; tile < ntiles; tile += Gv, ++j) {
+                const int slot = j % NS;
+                if (j >= NS) mbar_wait(&H->empty[slot], ((j / NS) - 1) & 1);
+                StageView V = stage_view(stages, S, slot);
+                const int r0 = tile * kBlock;
+                const int rows = min(kBlock, P.n - r0);
+                uint32_t bytes = 0;
+                const uint32_t rp_bytes = ((rows + 1) * 4 + 15) & ~15;
+                int k0a = 0, k0c = 0, direct = 1;
+                uint32_t va_bytes = 0, ci_bytes = 0;
+                if (Op::CSR) {
+                    bytes += rp_bytes;
+                    const int k0 = __ldg(P.rp + r0), k1 = __ldg(P.rp + r0 + rows);
+                    k0a = k0 & ~1;
+                    k0c = k0 & ~3;
+                    if (k1 - k0c + 4 <= S.cap) {
+                        direct = 0;
+                        va_bytes = ((k1 - k0a) * 8 + 15) & ~15;
+                        ci_bytes = ((k1 - k0c) * 4 + 15) & ~15;
+                        bytes += va_bytes + ci_bytes;
+                    }
+                }
+                const uint32_t vec_bytes = (rows * 8 + 15) & ~15;
+#pragma unroll
+                for (int v = 0; v < Op::NV; ++v)
+                    if (vp[v]) bytes += vec_bytes;
+                H->k0a[slot] = k0a;
+                H->k0c[slot] = k0c;
+                H->direct[slot] = direct;
+                mbar_expect_tx(&H->full[slot], bytes);
+                if (Op::CSR) {
+                    bulk_g2s(V.rp, P.rp + r0, rp_bytes, &H->full[slot], pol);
+                    if (!direct) {
+                        bulk_g2s(V.va, P.va + k0a, va_bytes, &H->full[slot], pol);
+                        bulk_g2s(V.ci, P.ci + k0c, ci_bytes, &H->full[slot], pol);
+                    }
+                }
+#pragma unroll
+                for (int v = 0; v < Op::NV; ++v)
+                    if (vp[v]) bulk_g2s(V.vec + v * kBlock, vp[v] + r0, vec_bytes, &H->full[slot], pol);
+            }
+        }
+        return;
+    }
+
+    // ------------------------------------------------------ consumer warps
+    const int t = threadIdx.x;
+    double acc[Op::ND > 0 ? Op::ND : 1];
+    int j = 0;
+    for (int vb = blockIdx.x; vb < Gv; vb += Gp) {
+#pragma unroll
+        for (int d = 0; d < Op::ND; ++d) acc[d] = 0.0;
+        for (int tile = vb; tile < ntiles; tile += Gv, ++j) {
+            const int slot = j % NS;
+            mbar_wait(&H->full[slot], (j / NS) & 1);
+            StageView V = stage_view(stages, S, slot);
+            const int i = tile * kBlock + t;
+            if (i < P.n) {
+                RowRef R;
+                if (Op::CSR) {
+                    R.b = V.rp[t];
+                    R.e = V.rp[t + 1];
+                    if (H->direct[slot]) {
+                        R.va = P.va;
+                        R.ci = P.ci;
+                    } else {
+                        R.va = V.va - H->k0a[slot];
+                        R.ci = V.ci - H->k0c[slot];
+                    }
+                }
+                op.row(P, i, V.vec + t, R, acc);
+            }
+            __syncwarp();
+            if ((t & 31) == 0) mbar_arrive(&H->empty[slot]);
+        }
+        if constexpr (Op::ND > 0) {
+            if (op.sync() != 2) continue;
+            cta_tree_c<Op::ND>(acc, H->red);
+            if (t == 0) {
+#pragma unroll
+                for (int d = 0; d < Op::ND; ++d) P.part[d * Gv + vb] = acc[d];
+            }
+        }
+    }
+    const int mode = op.sync();
+    if (mode == 0) return;
+    unsigned int* counter = op.counter(P);
+    if (!arrive_last_c(counter, &H->last_flag)) return;
+    double tot[Op::ND > 0 ? Op::ND : 1];
+#pragma unroll
+    for (int d = 0; d < Op::ND; ++d) tot[d] = 0.0;
+    if (mode == 2) {
+        for (int q = t; q < Gv; q += kConsumers) {
+#pragma unroll
+            for (int d = 0; d < Op::ND; ++d) tot[d] = ADD(tot[d], __ldcg(P.part + d * Gv + q));
+        }
+        if constexpr (Op::ND > 0) cta_tree_c<Op::ND>(tot, H->red);
+    }
+    if (t == 0) {
+        *counter = 0u;
+        op.finish(P, P.ctrl, tot);
+    }
+}
+
+}  // namespace cgvk

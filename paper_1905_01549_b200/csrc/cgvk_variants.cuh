@@ -1,5 +1,7 @@
-// The per-iteration kernels of the six CG variants (+ pipe-PR-M, M via the
-// nu' expression), as fused two-kernel schedules.
+// The per-iteration kernels of the six CG variants (+ pipe-PR-M; M-CG is the
+// PR stepper with the Meurant nu'), as fused two-kernel schedules (SURVEY.md
+// Appendix A), each an "Op" run by the TMA-staged pipeline of
+// cgvk_stream.cuh.
 //
 // Each iteration is exactly two launches, K1 then K2, captured in a CUDA
 // graph. Global reductions are folded by the last-arriving CTA of the kernel
@@ -15,15 +17,18 @@
 // defer into the next K1 (`form_pending`); the host materialises them (a K1
 // launch with k_limit = k) before reading vectors. Terminal steps keep the
 // reference's partial-update semantics through `mode2` / `form_pending`.
+//
+// Staged per-row vectors are read as sv[v * kBlock]; SpMV operands are
+// gathered from global memory (L1/L2) by column index.
 #pragma once
 
-#include "cgvk_device.cuh"
+#include "cgvk_stream.cuh"
 
 namespace cgvk {
 
 template <bool PREC>
-__device__ __forceinline__ double M_(const Params& P, int i, double v) {
-    if constexpr (PREC) return MUL(__ldg(P.d + i), v);
+__device__ __forceinline__ double Mg(const Params& P, int j, double v) {  // gathered d_j * v
+    if constexpr (PREC) return MUL(__ldg(P.d + j), v);
     return v;
 }
 
@@ -31,280 +36,384 @@ __device__ __forceinline__ bool step_wanted(const Ctrl* c) {
     return c->state == ST_RUNNING && c->k < c->k_limit;
 }
 
-#define TILE_LOOP(P)                                                                   \
-    for (int tile = blockIdx.x; tile < (P).ntiles; tile += gridDim.x)                  \
-        if (const int i = tile * kBlock + threadIdx.x; i < (P).n)
+#define SV(v) sv[(v) * kBlock]
 
 // =====================================================================  HS
 // src/variants.cpp:189-205, paper Alg. 1. V = 3+1 (K1) + 4+3 (K2) vectors.
 
-// K1: r -= alpha*s; nu = <M r, r>, <r,r>
+// K1: r -= alpha*s; nu = <M r, r>, <r,r>.   streams: r s [d]
 template <bool PREC>
-__global__ void __launch_bounds__(kBlock, kMinBlocksPerSM) hs_k1(Params P) {
-    Ctrl* c = P.ctrl;
-    if (!step_wanted(c)) return;
-    const double alpha = c->sc[SA];
-    double acc[2] = {0.0, 0.0}, tot[2];
-    TILE_LOOP(P) {
-        const double r = SUB(P.r[i], MUL(alpha, P.s[i]));
+struct HsK1 {
+    static constexpr int NV = PREC ? 3 : 2, ND = 2;
+    static constexpr bool CSR = false;
+    double alpha;
+    __device__ bool enter(const Params& P) {
+        if (!step_wanted(P.ctrl)) return false;
+        alpha = P.ctrl->sc[SA];
+        return true;
+    }
+    __device__ const double* vec(const Params& P, int v) const { return v == 0 ? P.r : v == 1 ? P.s : P.d; }
+    __device__ int sync() const { return 2; }
+    __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[0]; }
+    __device__ void row(const Params& P, int i, const double* sv, const RowRef&, double* acc) const {
+        const double r = SUB(SV(0), MUL(alpha, SV(1)));
         P.r[i] = r;
-        acc[0] = ADD(acc[0], MUL(M_<PREC>(P, i, r), r));
+        const double rt = PREC ? MUL(SV(2), r) : r;
+        acc[0] = ADD(acc[0], MUL(rt, r));
         acc[1] = ADD(acc[1], MUL(r, r));
     }
-    if (!reduce_grid<2>(acc, P.part, &c->count[0], tot)) return;
-    if (threadIdx.x != 0) return;
-    c->k += 1;
-    c->stats[STAT_PREC] += PREC;
-    c->stats[STAT_RED] += 1;
-    record_rr(P, c, tot[1]);
-    const double nu_next = tot[0];
-    if (settle_nonpositive(c, nu_next, BR_NU, tot[1])) {
+    __device__ void finish(const Params& P, Ctrl* c, const double* tot) const {
+        c->k += 1;
+        c->stats[STAT_PREC] += PREC;
+        c->stats[STAT_RED] += 1;
+        record_rr(P, c, tot[1]);
+        const double nu_next = tot[0];
+        if (settle_nonpositive(c, nu_next, BR_NU, tot[1])) {
+            c->sc[SNU] = nu_next;
+            c->mode2 = MODE_X_ONLY;  // x_k = x_{k-1} + alpha p_{k-1} still owed
+            return;
+        }
+        c->sc[SB] = DIV(nu_next, c->sc[SNU]);
         c->sc[SNU] = nu_next;
-        c->mode2 = MODE_X_ONLY;  // x_k = x_{k-1} + alpha p_{k-1} still owed
-        return;
+        c->mode2 = MODE_FULL;
     }
-    c->sc[SB] = DIV(nu_next, c->sc[SNU]);
-    c->sc[SNU] = nu_next;
-    c->mode2 = MODE_FULL;
-}
+};
 
 // K2: x += alpha*p_old; p = M r + beta p_old (on the fly for every gathered
-// column); s = A p; mu = <p,s>
+// column); s = A p; mu = <p,s>.   streams: A, p_old r x [d]
 template <bool PREC>
-__global__ void __launch_bounds__(kBlock, kMinBlocksPerSM) hs_k2(Params P) {
-    Ctrl* c = P.ctrl;
-    const int mode = c->mode2;
-    if (mode == MODE_SKIP) return;
-    const int pc = c->pcur;
-    const double* __restrict__ pold = pc ? P.p1 : P.p0;
-    double* pnew = pc ? P.p0 : P.p1;
-    const double alpha = c->sc[SA], beta = c->sc[SB];
-    const double* __restrict__ r = P.r;
-    double acc[1] = {0.0}, tot[1];
-    TILE_LOOP(P) {
-        const double po = pold[i];
-        P.x[i] = ADD(P.x[i], MUL(alpha, po));
-        if (mode == MODE_FULL) {
-            const double sum = row_sum(P, i, [&](int j) {
-                return ADD(M_<PREC>(P, j, __ldg(r + j)), MUL(beta, __ldg(pold + j)));
-            });
-            const double pi = ADD(M_<PREC>(P, i, r[i]), MUL(beta, po));
-            pnew[i] = pi;
-            P.s[i] = sum;
-            acc[0] = ADD(acc[0], MUL(pi, sum));
-        }
+struct HsK2 {
+    static constexpr int NV = PREC ? 4 : 3, ND = 1;
+    static constexpr bool CSR = true;
+    int mode;
+    const double* pold;
+    double* pnew;
+    double alpha, beta;
+    __device__ bool enter(const Params& P) {
+        const Ctrl* c = P.ctrl;
+        mode = c->mode2;
+        if (mode == MODE_SKIP) return false;
+        const int pc = c->pcur;
+        pold = pc ? P.p1 : P.p0;
+        pnew = pc ? P.p0 : P.p1;
+        alpha = c->sc[SA];
+        beta = c->sc[SB];
+        return true;
     }
-    if (!reduce_grid<1>(acc, P.part, &c->count[1], tot)) return;
-    if (threadIdx.x != 0) return;
-    c->mode2 = MODE_SKIP;
-    if (mode != MODE_FULL) return;
-    c->pcur = pc ^ 1;
-    c->stats[STAT_SPMV] += 1;
-    c->stats[STAT_RED] += 1;
-    c->sc[SMU] = tot[0];
-    if (settle_mu(c)) return;
-    if (finalize_alpha(c)) return;
-    check_tolerance(c);
-}
+    __device__ const double* vec(const Params& P, int v) const {
+        return v == 0 ? pold : v == 1 ? P.r : v == 2 ? P.x : P.d;
+    }
+    __device__ int sync() const { return mode == MODE_FULL ? 2 : 1; }
+    __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
+    __device__ void row(const Params& P, int i, const double* sv, const RowRef& R, double* acc) const {
+        const double po = SV(0);
+        P.x[i] = ADD(SV(2), MUL(alpha, po));
+        if (mode != MODE_FULL) return;
+        const double* __restrict__ r = P.r;
+        const double* __restrict__ pg = pold;
+        const double b = beta;
+        const double sum =
+            row_dot(R, [&](int j) { return ADD(Mg<PREC>(P, j, __ldg(r + j)), MUL(b, __ldg(pg + j))); });
+        const double pi = ADD(PREC ? MUL(SV(3), SV(1)) : SV(1), MUL(b, po));
+        pnew[i] = pi;
+        P.s[i] = sum;
+        acc[0] = ADD(acc[0], MUL(pi, sum));
+    }
+    __device__ void finish(const Params& P, Ctrl* c, const double* tot) const {
+        c->mode2 = MODE_SKIP;
+        if (mode != MODE_FULL) return;
+        c->pcur ^= 1;
+        c->stats[STAT_SPMV] += 1;
+        c->stats[STAT_RED] += 1;
+        c->sc[SMU] = tot[0];
+        if (settle_mu(c)) return;
+        if (finalize_alpha(c)) return;
+        check_tolerance(c);
+    }
+};
 
 // ==================================================================  CG-CG
 // src/variants.cpp:207-234. K1 = tail of step k-1 (p, s recurrences) + head
 // of step k (x, r); K2 = w = A M r with nu, eta (+ unsimplified dots).
 
+// streams: p s x r w [d]
 template <bool PREC>
-__global__ void __launch_bounds__(kBlock, kMinBlocksPerSM) cg_k1(Params P) {
-    Ctrl* c = P.ctrl;
-    const bool F = c->form_pending != 0, S = step_wanted(c);
-    if (!F && !S) return;
-    const double alpha = c->sc[SA], beta = c->sc[SB];
-    TILE_LOOP(P) {
-        double p = P.p0[i], s = P.s[i];
+struct CgK1 {
+    static constexpr int NV = PREC ? 6 : 5, ND = 0;
+    static constexpr bool CSR = false;
+    bool F, S;
+    double alpha, beta;
+    __device__ bool enter(const Params& P) {
+        const Ctrl* c = P.ctrl;
+        F = c->form_pending != 0;
+        S = step_wanted(c);
+        alpha = c->sc[SA];
+        beta = c->sc[SB];
+        return F || S;
+    }
+    __device__ const double* vec(const Params& P, int v) const {
+        switch (v) {
+            case 0: return P.p0;
+            case 1: return P.s;
+            case 2: return S ? P.x : nullptr;
+            case 3: return P.r;
+            case 4: return F ? P.w : nullptr;
+            default: return F ? P.d : nullptr;
+        }
+    }
+    __device__ int sync() const { return (F && !S) ? 1 : 0; }
+    __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[0]; }
+    __device__ void row(const Params& P, int i, const double* sv, const RowRef&, double*) const {
+        double p = SV(0), s = SV(1);
+        const double r = SV(3);
         if (F) {
-            p = ADD(M_<PREC>(P, i, P.r[i]), MUL(beta, p));
-            s = ADD(P.w[i], MUL(beta, s));
+            p = ADD(PREC ? MUL(SV(5), r) : r, MUL(beta, p));
+            s = ADD(SV(4), MUL(beta, s));
             P.p0[i] = p;
             P.s[i] = s;
         }
         if (S) {
-            P.x[i] = ADD(P.x[i], MUL(alpha, p));
-            P.r[i] = SUB(P.r[i], MUL(alpha, s));
+            P.x[i] = ADD(SV(2), MUL(alpha, p));
+            P.r[i] = SUB(r, MUL(alpha, s));
         }
     }
-    if (F && !S) {  // materialisation only: clear the debt
-        if (arrive_last(&c->count[0]) && threadIdx.x == 0) {
-            c->form_pending = 0;
-            c->count[0] = 0u;
-        }
-    }
-}
+    __device__ void finish(const Params&, Ctrl* c, const double*) const { c->form_pending = 0; }
+};
 
+// streams: A, r [d] [s p (unsimplified)]
 template <bool PREC>
-__global__ void __launch_bounds__(kBlock, kMinBlocksPerSM) cg_k2(Params P) {
-    Ctrl* c = P.ctrl;
-    if (!step_wanted(c)) return;
-    const bool unsimp = P.unsimplified_mu != 0;
-    const double* __restrict__ r = P.r;
-    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0}, tot[5];
-    TILE_LOOP(P) {
-        const double w = row_sum(P, i, [&](int j) { return M_<PREC>(P, j, __ldg(r + j)); });
+struct CgK2 {
+    static constexpr int NV = 4, ND = 5;
+    static constexpr bool CSR = true;
+    bool unsimp;
+    __device__ bool enter(const Params& P) {
+        unsimp = P.unsimplified_mu != 0;
+        return step_wanted(P.ctrl);
+    }
+    __device__ const double* vec(const Params& P, int v) const {
+        switch (v) {
+            case 0: return P.r;
+            case 1: return PREC ? P.d : nullptr;
+            case 2: return unsimp ? P.s : nullptr;
+            default: return unsimp ? P.p0 : nullptr;
+        }
+    }
+    __device__ int sync() const { return 2; }
+    __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
+    __device__ void row(const Params& P, int i, const double* sv, const RowRef& R, double* acc) const {
+        const double* __restrict__ r = P.r;
+        const double w = row_dot(R, [&](int j) { return Mg<PREC>(P, j, __ldg(r + j)); });
         P.w[i] = w;
-        const double ri = r[i], rti = M_<PREC>(P, i, ri);
+        const double ri = SV(0), rti = PREC ? MUL(SV(1), ri) : ri;
         acc[0] = ADD(acc[0], MUL(rti, ri));
         acc[1] = ADD(acc[1], MUL(rti, w));
         acc[2] = ADD(acc[2], MUL(ri, ri));
         if (unsimp) {
-            acc[3] = ADD(acc[3], MUL(rti, P.s[i]));   // <r~_k, s_{k-1}>
-            acc[4] = ADD(acc[4], MUL(P.p0[i], w));     // <p_{k-1}, w_k>
+            acc[3] = ADD(acc[3], MUL(rti, SV(2)));  // <r~_k, s_{k-1}>
+            acc[4] = ADD(acc[4], MUL(SV(3), w));    // <p_{k-1}, w_k>
         }
     }
-    if (!reduce_grid<5>(acc, P.part, &c->count[1], tot)) return;
-    if (threadIdx.x != 0) return;
-    c->k += 1;
-    c->stats[STAT_SPMV] += 1;
-    c->stats[STAT_PREC] += PREC;
-    c->stats[STAT_RED] += 2;
-    record_rr(P, c, tot[2]);
-    const double nu_next = tot[0];
-    c->sc[SETA] = tot[1];
-    c->form_pending = 0;
-    if (settle_nonpositive(c, nu_next, BR_NU, tot[2])) {
+    __device__ void finish(const Params& P, Ctrl* c, const double* tot) const {
+        c->k += 1;
+        c->stats[STAT_SPMV] += 1;
+        c->stats[STAT_PREC] += PREC;
+        c->stats[STAT_RED] += 2;
+        record_rr(P, c, tot[2]);
+        const double nu_next = tot[0];
+        c->sc[SETA] = tot[1];
+        c->form_pending = 0;
+        if (settle_nonpositive(c, nu_next, BR_NU, tot[2])) {
+            c->sc[SNU] = nu_next;
+            return;
+        }
+        const double beta = DIV(nu_next, c->sc[SNU]);
+        c->sc[SB] = beta;
+        if (unsimp) c->stats[STAT_RED] += 2;
+        const double mu_prev = c->sc[SMU];
         c->sc[SNU] = nu_next;
-        return;
+        c->form_pending = 1;  // p_k = M r_k + beta p, s_k = w_k + beta s (next K1)
+        c->sc[SMU] = unsimp ? ADD(ADD(tot[1], MUL(beta, ADD(tot[3], tot[4]))), MUL(MUL(beta, beta), mu_prev))
+                            : SUB(tot[1], MUL(DIV(beta, c->sc[SA]), nu_next));
+        if (settle_mu(c)) return;
+        if (finalize_alpha(c)) return;
+        check_tolerance(c);
     }
-    const double beta = DIV(nu_next, c->sc[SNU]);
-    c->sc[SB] = beta;
-    if (unsimp) c->stats[STAT_RED] += 2;
-    const double mu_prev = c->sc[SMU];
-    c->sc[SNU] = nu_next;
-    c->form_pending = 1;  // p_k = M r_k + beta p, s_k = w_k + beta s (next K1)
-    c->sc[SMU] = unsimp ? ADD(ADD(tot[1], MUL(beta, ADD(tot[3], tot[4]))), MUL(MUL(beta, beta), mu_prev))
-                        : SUB(tot[1], MUL(DIV(beta, c->sc[SA]), nu_next));
-    if (settle_mu(c)) return;
-    if (finalize_alpha(c)) return;
-    check_tolerance(c);
-}
+};
 
 // ===============================================================  PR / M
 // src/variants.cpp:237-265, paper Alg. 2 (M-CG with the Meurant nu').
 // K1: x, r, r~ (s~ = M s on the fly) and p; K2: s = A p with mu, delta,
 // delta-hat, gamma (s~ on the fly), nu, <r,r>.
 
+// streams: x p r s [r~ d]
 template <bool PREC>
-__global__ void __launch_bounds__(kBlock, kMinBlocksPerSM) pr_k1(Params P) {
-    Ctrl* c = P.ctrl;
-    if (!step_wanted(c)) return;
-    const double alpha = c->sc[SA];
-    const double nup = predicted_nu(P.nu_expr, c->sc);
-    const bool valid = isfinite(nup) && nup > 0.0;
-    const double beta = DIV(nup, c->sc[SNU]);
-    double acc[1] = {0.0}, tot[1];
-    TILE_LOOP(P) {
-        const double s = P.s[i];
-        P.x[i] = ADD(P.x[i], MUL(alpha, P.p0[i]));
-        const double r = SUB(P.r[i], MUL(alpha, s));
+struct PrK1 {
+    static constexpr int NV = PREC ? 6 : 4, ND = 1;
+    static constexpr bool CSR = false;
+    double alpha, beta, nup;
+    bool valid;
+    __device__ bool enter(const Params& P) {
+        const Ctrl* c = P.ctrl;
+        if (!step_wanted(c)) return false;
+        alpha = c->sc[SA];
+        nup = predicted_nu(P.nu_expr, c->sc);
+        valid = isfinite(nup) && nup > 0.0;
+        beta = DIV(nup, c->sc[SNU]);
+        return true;
+    }
+    __device__ const double* vec(const Params& P, int v) const {
+        switch (v) {
+            case 0: return P.x;
+            case 1: return P.p0;
+            case 2: return P.r;
+            case 3: return P.s;
+            case 4: return P.rt;
+            default: return P.d;
+        }
+    }
+    __device__ int sync() const { return valid ? 0 : 2; }
+    __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[0]; }
+    __device__ void row(const Params& P, int i, const double* sv, const RowRef&, double* acc) const {
+        const double s = SV(3), p = SV(1);
+        P.x[i] = ADD(SV(0), MUL(alpha, p));
+        const double r = SUB(SV(2), MUL(alpha, s));
         P.r[i] = r;
         double rt = r;
         if constexpr (PREC) {
-            rt = SUB(P.rt[i], MUL(alpha, M_<PREC>(P, i, s)));
+            rt = SUB(SV(4), MUL(alpha, MUL(SV(5), s)));
             P.rt[i] = rt;
         }
         if (valid)
-            P.p0[i] = ADD(rt, MUL(beta, P.p0[i]));
+            P.p0[i] = ADD(rt, MUL(beta, p));
         else
             acc[0] = ADD(acc[0], MUL(r, r));
     }
-    if (valid) return;  // K2 finishes the step
-    if (!reduce_grid<1>(acc, P.part, &c->count[0], tot)) return;
-    if (threadIdx.x != 0) return;
-    c->k += 1;
-    c->sc[SNUP] = nup;
-    record_rr(P, c, tot[0]);
-    settle_nonpositive(c, nup, BR_NUPRIME, tot[0]);
-}
+    __device__ void finish(const Params& P, Ctrl* c, const double* tot) const {
+        c->k += 1;
+        c->sc[SNUP] = nup;
+        record_rr(P, c, tot[0]);
+        settle_nonpositive(c, nup, BR_NUPRIME, tot[0]);
+    }
+};
 
+// streams: A, p r [r~ d]
 template <bool PREC>
-__global__ void __launch_bounds__(kBlock, kMinBlocksPerSM) pr_k2(Params P) {
-    Ctrl* c = P.ctrl;
-    if (!step_wanted(c)) return;
-    const double nup = predicted_nu(P.nu_expr, c->sc);
-    if (!(isfinite(nup) && nup > 0.0)) return;
-    const bool want_delta = P.nu_expr != 2 || P.track_delta;
-    const bool want_dhat = P.nu_expr == 0;
-    const double* __restrict__ p = P.p0;
-    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, tot[6];
-    TILE_LOOP(P) {
-        const double s = row_sum(P, i, [&](int j) { return __ldg(p + j); });
+struct PrK2 {
+    static constexpr int NV = PREC ? 4 : 2, ND = 6;
+    static constexpr bool CSR = true;
+    double nup;
+    bool want_delta, want_dhat;
+    __device__ bool enter(const Params& P) {
+        const Ctrl* c = P.ctrl;
+        if (!step_wanted(c)) return false;
+        nup = predicted_nu(P.nu_expr, c->sc);
+        want_delta = P.nu_expr != 2 || P.track_delta;
+        want_dhat = P.nu_expr == 0;
+        return isfinite(nup) && nup > 0.0;
+    }
+    __device__ const double* vec(const Params& P, int v) const {
+        return v == 0 ? P.p0 : v == 1 ? P.r : v == 2 ? P.rt : P.d;
+    }
+    __device__ int sync() const { return 2; }
+    __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
+    __device__ void row(const Params& P, int i, const double* sv, const RowRef& R, double* acc) const {
+        const double* __restrict__ p = P.p0;
+        const double s = row_dot(R, [&](int j) { return __ldg(p + j); });
         P.s[i] = s;
-        const double st = M_<PREC>(P, i, s);
-        const double r = P.r[i];
-        const double rt = PREC ? P.rt[i] : r;
-        acc[0] = ADD(acc[0], MUL(p[i], s));
+        const double st = PREC ? MUL(SV(3), s) : s;
+        const double r = SV(1);
+        const double rt = PREC ? SV(2) : r;
+        acc[0] = ADD(acc[0], MUL(SV(0), s));
         if (want_delta) acc[1] = ADD(acc[1], MUL(rt, s));
         if (want_dhat) acc[2] = ADD(acc[2], MUL(st, r));
         acc[3] = ADD(acc[3], MUL(st, s));
         acc[4] = ADD(acc[4], MUL(rt, r));
         acc[5] = ADD(acc[5], MUL(r, r));
     }
-    if (!reduce_grid<6>(acc, P.part, &c->count[1], tot)) return;
-    if (threadIdx.x != 0) return;
-    c->k += 1;
-    c->sc[SNUP] = nup;
-    c->sc[SB] = DIV(nup, c->sc[SNU]);
-    c->stats[STAT_SPMV] += 1;
-    c->stats[STAT_PREC] += PREC;
-    c->stats[STAT_RED] += 2 + want_delta + want_dhat;
-    record_rr(P, c, tot[5]);
-    c->sc[SMU] = tot[0];
-    if (want_delta) c->sc[SDEL] = tot[1];
-    if (want_dhat) c->sc[SDELH] = tot[2];
-    c->sc[SGAM] = tot[3];
-    if (settle_mu(c)) return;
-    if (P.recompute_nu) {
-        c->stats[STAT_RED] += 1;
-        const double nu_next = tot[4];
-        if (settle_nonpositive(c, nu_next, BR_NU, tot[5])) {
+    __device__ void finish(const Params& P, Ctrl* c, const double* tot) const {
+        c->k += 1;
+        c->sc[SNUP] = nup;
+        c->sc[SB] = DIV(nup, c->sc[SNU]);
+        c->stats[STAT_SPMV] += 1;
+        c->stats[STAT_PREC] += PREC;
+        c->stats[STAT_RED] += 2 + want_delta + want_dhat;
+        record_rr(P, c, tot[5]);
+        c->sc[SMU] = tot[0];
+        if (want_delta) c->sc[SDEL] = tot[1];
+        if (want_dhat) c->sc[SDELH] = tot[2];
+        c->sc[SGAM] = tot[3];
+        if (settle_mu(c)) return;
+        if (P.recompute_nu) {
+            c->stats[STAT_RED] += 1;
+            const double nu_next = tot[4];
+            if (settle_nonpositive(c, nu_next, BR_NU, tot[5])) {
+                c->sc[SNU] = nu_next;
+                return;
+            }
             c->sc[SNU] = nu_next;
-            return;
+        } else {
+            c->sc[SNU] = nup;
         }
-        c->sc[SNU] = nu_next;
-    } else {
-        c->sc[SNU] = nup;
+        if (finalize_alpha(c)) return;
+        check_tolerance(c);
     }
-    if (finalize_alpha(c)) return;
-    check_tolerance(c);
-}
+};
 
 // ====================================================================  GV
 // src/variants.cpp:267-298. K1 = beta-recurrences of step k-1 (p, s, s~, u)
-// + step k updates (x, r, r~, w) with nu, eta; the reduction is folded at
-// the end of K1, so on multi-GPU it overlaps K2 = t = A M w.
+// + step k updates (x, r, r~, w) with nu, eta; the reduction is folded at the
+// end of K1, so on multi-GPU it overlaps K2 = t = A M w.
 
+// streams: p s u w t x r [s~ r~ d]
 template <bool PREC>
-__global__ void __launch_bounds__(kBlock, kMinBlocksPerSM) gv_k1(Params P) {
-    Ctrl* c = P.ctrl;
-    const bool F = c->form_pending != 0, S = step_wanted(c);
-    if (!F && !S) return;
-    const double alpha = c->sc[SA], beta = c->sc[SB];
-    const bool unsimp = P.unsimplified_mu != 0;
-    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0}, tot[5];
-    TILE_LOOP(P) {
-        double p = P.p0[i], s = P.s[i], u = P.u[i], w = P.w[i];
-        double st = PREC ? P.st[i] : s;
-        double rt = PREC ? P.rt[i] : P.r[i];
+struct GvK1 {
+    static constexpr int NV = PREC ? 10 : 7, ND = 5;
+    static constexpr bool CSR = false;
+    bool F, S, unsimp;
+    double alpha, beta;
+    __device__ bool enter(const Params& P) {
+        const Ctrl* c = P.ctrl;
+        F = c->form_pending != 0;
+        S = step_wanted(c);
+        alpha = c->sc[SA];
+        beta = c->sc[SB];
+        unsimp = P.unsimplified_mu != 0;
+        return F || S;
+    }
+    __device__ const double* vec(const Params& P, int v) const {
+        switch (v) {
+            case 0: return P.p0;
+            case 1: return P.s;
+            case 2: return P.u;
+            case 3: return P.w;
+            case 4: return F ? P.t : nullptr;
+            case 5: return S ? P.x : nullptr;
+            case 6: return P.r;
+            case 7: return P.st;
+            case 8: return P.rt;
+            default: return P.d;
+        }
+    }
+    __device__ int sync() const { return S ? 2 : 1; }
+    __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[0]; }
+    __device__ void row(const Params& P, int i, const double* sv, const RowRef&, double* acc) const {
+        double p = SV(0), s = SV(1), u = SV(2), w = SV(3);
+        double st = PREC ? SV(7) : s;
+        double rt = PREC ? SV(8) : SV(6);
         if (F) {
             p = ADD(rt, MUL(beta, p));
             s = ADD(w, MUL(beta, s));
-            if constexpr (PREC) st = ADD(M_<PREC>(P, i, w), MUL(beta, st));
+            if constexpr (PREC) st = ADD(MUL(SV(9), w), MUL(beta, st));
             else st = s;
-            u = ADD(P.t[i], MUL(beta, u));
+            u = ADD(SV(4), MUL(beta, u));
             P.p0[i] = p;
             P.s[i] = s;
             if constexpr (PREC) P.st[i] = st;
             P.u[i] = u;
         }
         if (S) {
-            P.x[i] = ADD(P.x[i], MUL(alpha, p));
-            const double r = SUB(P.r[i], MUL(alpha, s));
+            P.x[i] = ADD(SV(5), MUL(alpha, p));
+            const double r = SUB(SV(6), MUL(alpha, s));
             P.r[i] = r;
             if constexpr (PREC) {
                 rt = SUB(rt, MUL(alpha, st));
@@ -323,54 +432,53 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSM) gv_k1(Params P) {
             }
         }
     }
-    if (!S) {  // materialisation only
-        if (arrive_last(&c->count[0]) && threadIdx.x == 0) {
+    __device__ void finish(const Params& P, Ctrl* c, const double* tot) const {
+        if (!S) {  // materialisation only
             c->form_pending = 0;
-            c->count[0] = 0u;
+            return;
         }
-        return;
-    }
-    if (!reduce_grid<5>(acc, P.part, &c->count[0], tot)) return;
-    if (threadIdx.x != 0) return;
-    c->k += 1;
-    c->mode2 = MODE_FULL;  // t = A w~ precedes the checks in the reference
-    c->stats[STAT_SPMV] += 1;
-    c->stats[STAT_PREC] += PREC;
-    c->stats[STAT_RED] += 2;
-    record_rr(P, c, tot[2]);
-    const double nu_next = tot[0];
-    c->sc[SETA] = tot[1];
-    c->form_pending = 0;
-    if (settle_nonpositive(c, nu_next, BR_NU, tot[2])) {
+        c->k += 1;
+        c->mode2 = MODE_FULL;  // t = A w~ precedes the checks in the reference
+        c->stats[STAT_SPMV] += 1;
+        c->stats[STAT_PREC] += PREC;
+        c->stats[STAT_RED] += 2;
+        record_rr(P, c, tot[2]);
+        const double nu_next = tot[0];
+        c->sc[SETA] = tot[1];
+        c->form_pending = 0;
+        if (settle_nonpositive(c, nu_next, BR_NU, tot[2])) {
+            c->sc[SNU] = nu_next;
+            return;
+        }
+        const double beta_k = DIV(nu_next, c->sc[SNU]);
+        c->sc[SB] = beta_k;
+        if (unsimp) c->stats[STAT_RED] += 2;
+        const double mu_prev = c->sc[SMU];
         c->sc[SNU] = nu_next;
-        return;
+        c->form_pending = 1;
+        c->sc[SMU] = unsimp ? ADD(ADD(tot[1], MUL(beta_k, ADD(tot[3], tot[4]))), MUL(MUL(beta_k, beta_k), mu_prev))
+                            : SUB(tot[1], MUL(DIV(beta_k, c->sc[SA]), nu_next));
+        if (settle_mu(c)) return;
+        if (finalize_alpha(c)) return;
+        check_tolerance(c);
     }
-    const double beta_k = DIV(nu_next, c->sc[SNU]);
-    c->sc[SB] = beta_k;
-    if (unsimp) c->stats[STAT_RED] += 2;
-    const double mu_prev = c->sc[SMU];
-    c->sc[SNU] = nu_next;
-    c->form_pending = 1;
-    c->sc[SMU] = unsimp ? ADD(ADD(tot[1], MUL(beta_k, ADD(tot[3], tot[4]))), MUL(MUL(beta_k, beta_k), mu_prev))
-                        : SUB(tot[1], MUL(DIV(beta_k, c->sc[SA]), nu_next));
-    if (settle_mu(c)) return;
-    if (finalize_alpha(c)) return;
-    check_tolerance(c);
-}
+};
 
+// t = A M w (streams: A only)
 template <bool PREC>
-__global__ void __launch_bounds__(kBlock, kMinBlocksPerSM) gv_k2(Params P) {
-    Ctrl* c = P.ctrl;
-    if (c->mode2 == MODE_SKIP) return;
-    const double* __restrict__ w = P.w;
-    TILE_LOOP(P) {
-        P.t[i] = row_sum(P, i, [&](int j) { return M_<PREC>(P, j, __ldg(w + j)); });
+struct GvK2 {
+    static constexpr int NV = 0, ND = 0;
+    static constexpr bool CSR = true;
+    __device__ bool enter(const Params& P) { return P.ctrl->mode2 != MODE_SKIP; }
+    __device__ const double* vec(const Params&, int) const { return nullptr; }
+    __device__ int sync() const { return 1; }
+    __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
+    __device__ void row(const Params& P, int i, const double*, const RowRef& R, double*) const {
+        const double* __restrict__ w = P.w;
+        P.t[i] = row_dot(R, [&](int j) { return Mg<PREC>(P, j, __ldg(w + j)); });
     }
-    if (arrive_last(&c->count[1]) && threadIdx.x == 0) {
-        c->mode2 = MODE_SKIP;
-        c->count[1] = 0u;
-    }
-}
+    __device__ void finish(const Params&, Ctrl* c, const double*) const { c->mode2 = MODE_SKIP; }
+};
 
 // ===============================================================  pipe-PR
 // src/variants.cpp:303-350, paper Alg. 3 and the §2.2.1 schedule
@@ -379,38 +487,61 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSM) gv_k2(Params P) {
 // SpMV K2 = (u, w) = A (s~, r~). w~ = M w and u~ = M u are recomputed on the
 // fly (recompute_w); with recompute_w off, w and w~ are stored recurrences.
 
+// streams: x p r s w u [s~ r~ d w~]
 template <bool PREC>
-__global__ void __launch_bounds__(kBlock, kMinBlocksPerSM) ppr_k1(Params P) {
-    Ctrl* c = P.ctrl;
-    if (!step_wanted(c)) return;
-    const double alpha = c->sc[SA];
-    const double nup = predicted_nu(P.nu_expr, c->sc);
-    const bool valid = isfinite(nup) && nup > 0.0;
-    const double beta = DIV(nup, c->sc[SNU]);
-    const bool want_delta = P.nu_expr != 2 || P.track_delta;
-    const bool want_dhat = P.nu_expr == 0;
-    const bool recw = P.recompute_w != 0;
-    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, tot[6];
-    TILE_LOOP(P) {
-        P.x[i] = ADD(P.x[i], MUL(alpha, P.p0[i]));
-        const double s_old = P.s[i];
-        const double r = SUB(P.r[i], MUL(alpha, s_old));
+struct PprK1 {
+    static constexpr int NV = PREC ? 10 : 6, ND = 6;
+    static constexpr bool CSR = false;
+    double alpha, beta, nup;
+    bool valid, want_delta, want_dhat, recw;
+    __device__ bool enter(const Params& P) {
+        const Ctrl* c = P.ctrl;
+        if (!step_wanted(c)) return false;
+        alpha = c->sc[SA];
+        nup = predicted_nu(P.nu_expr, c->sc);
+        valid = isfinite(nup) && nup > 0.0;
+        beta = DIV(nup, c->sc[SNU]);
+        want_delta = P.nu_expr != 2 || P.track_delta;
+        want_dhat = P.nu_expr == 0;
+        recw = P.recompute_w != 0;
+        return true;
+    }
+    __device__ const double* vec(const Params& P, int v) const {
+        switch (v) {
+            case 0: return P.x;
+            case 1: return P.p0;
+            case 2: return P.r;
+            case 3: return P.s;
+            case 4: return P.w;
+            case 5: return P.u;
+            case 6: return P.st;
+            case 7: return P.rt;
+            case 8: return P.d;
+            default: return recw ? nullptr : P.wt;
+        }
+    }
+    __device__ int sync() const { return 2; }
+    __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[0]; }
+    __device__ void row(const Params& P, int i, const double* sv, const RowRef&, double* acc) const {
+        const double p_old = SV(1), s_old = SV(3), w_old = SV(4), u = SV(5);
+        P.x[i] = ADD(SV(0), MUL(alpha, p_old));
+        const double r = SUB(SV(2), MUL(alpha, s_old));
         P.r[i] = r;
         double rt = r, st_old = s_old;
         if constexpr (PREC) {
-            st_old = P.st[i];
-            rt = SUB(P.rt[i], MUL(alpha, st_old));
+            st_old = SV(6);
+            rt = SUB(SV(7), MUL(alpha, st_old));
             P.rt[i] = rt;
         }
-        const double u = P.u[i];
-        const double wn = SUB(P.w[i], MUL(alpha, u));  // w'_k
+        const double wn = SUB(w_old, MUL(alpha, u));  // w'_k
         double wtn = wn;
         if constexpr (PREC) {
-            const double wt_old = recw ? M_<PREC>(P, i, P.w[i]) : P.wt[i];
-            wtn = SUB(wt_old, MUL(alpha, M_<PREC>(P, i, u)));
+            const double d = SV(8);
+            const double wt_old = recw ? MUL(d, w_old) : SV(9);
+            wtn = SUB(wt_old, MUL(alpha, MUL(d, u)));
         }
         if (valid) {
-            const double p = ADD(rt, MUL(beta, P.p0[i]));
+            const double p = ADD(rt, MUL(beta, p_old));
             const double s = ADD(wn, MUL(beta, s_old));
             double st = s;
             if constexpr (PREC) {
@@ -434,69 +565,71 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSM) ppr_k1(Params P) {
         }
         acc[5] = ADD(acc[5], MUL(r, r));
     }
-    if (!reduce_grid<6>(acc, P.part, &c->count[0], tot)) return;
-    if (threadIdx.x != 0) return;
-    c->k += 1;
-    c->sc[SNUP] = nup;
-    record_rr(P, c, tot[5]);
-    if (!valid) {
-        c->wt_stored = PREC;
-        settle_nonpositive(c, nup, BR_NUPRIME, tot[5]);
-        return;
-    }
-    c->sc[SB] = beta;
-    c->mode2 = MODE_FULL;  // the block SpMV precedes the checks in the reference
-    if (recw) {
-        c->stats[STAT_BLOCK] += 1;
-        c->stats[STAT_PREC] += 2 * PREC;
-    } else {
-        c->stats[STAT_SPMV] += 1;
-        c->stats[STAT_PREC] += PREC;
-    }
-    c->stats[STAT_RED] += 2 + want_delta + want_dhat;
-    c->sc[SMU] = tot[0];
-    if (want_delta) c->sc[SDEL] = tot[1];
-    if (want_dhat) c->sc[SDELH] = tot[2];
-    c->sc[SGAM] = tot[3];
-    if (settle_mu(c)) return;
-    if (P.recompute_nu) {
-        c->stats[STAT_RED] += 1;
-        const double nu_next = tot[4];
-        if (settle_nonpositive(c, nu_next, BR_NU, tot[5])) {
-            c->sc[SNU] = nu_next;
+    __device__ void finish(const Params& P, Ctrl* c, const double* tot) const {
+        c->k += 1;
+        c->sc[SNUP] = nup;
+        record_rr(P, c, tot[5]);
+        if (!valid) {
+            c->wt_stored = PREC;
+            settle_nonpositive(c, nup, BR_NUPRIME, tot[5]);
             return;
         }
-        c->sc[SNU] = nu_next;
-    } else {
-        c->sc[SNU] = nup;
+        c->sc[SB] = beta;
+        c->mode2 = MODE_FULL;  // the block SpMV precedes the checks in the reference
+        if (recw) {
+            c->stats[STAT_BLOCK] += 1;
+            c->stats[STAT_PREC] += 2 * PREC;
+        } else {
+            c->stats[STAT_SPMV] += 1;
+            c->stats[STAT_PREC] += PREC;
+        }
+        c->stats[STAT_RED] += 2 + want_delta + want_dhat;
+        c->sc[SMU] = tot[0];
+        if (want_delta) c->sc[SDEL] = tot[1];
+        if (want_dhat) c->sc[SDELH] = tot[2];
+        c->sc[SGAM] = tot[3];
+        if (settle_mu(c)) return;
+        if (P.recompute_nu) {
+            c->stats[STAT_RED] += 1;
+            const double nu_next = tot[4];
+            if (settle_nonpositive(c, nu_next, BR_NU, tot[5])) {
+                c->sc[SNU] = nu_next;
+                return;
+            }
+            c->sc[SNU] = nu_next;
+        } else {
+            c->sc[SNU] = nup;
+        }
+        if (finalize_alpha(c)) return;
+        check_tolerance(c);
     }
-    if (finalize_alpha(c)) return;
-    check_tolerance(c);
-}
+};
 
+// (u, w) = A (s~, r~) in one traversal, or u = A s~ with recompute_w off
+// (streams: A only)
 template <bool PREC>
-__global__ void __launch_bounds__(kBlock, kMinBlocksPerSM) ppr_k2(Params P) {
-    Ctrl* c = P.ctrl;
-    if (c->mode2 == MODE_SKIP) return;
-    const double* __restrict__ sv = PREC ? P.st : P.s;
-    const double* __restrict__ rv = PREC ? P.rt : P.r;
-    if (P.recompute_w) {
-        TILE_LOOP(P) {
+struct PprK2 {
+    static constexpr int NV = 0, ND = 0;
+    static constexpr bool CSR = true;
+    __device__ bool enter(const Params& P) { return P.ctrl->mode2 != MODE_SKIP; }
+    __device__ const double* vec(const Params&, int) const { return nullptr; }
+    __device__ int sync() const { return 1; }
+    __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
+    __device__ void row(const Params& P, int i, const double*, const RowRef& R, double*) const {
+        const double* __restrict__ sv_ = PREC ? P.st : P.s;
+        const double* __restrict__ rv = PREC ? P.rt : P.r;
+        if (P.recompute_w) {
             double u, w;
-            row_sum2(P, i, [&](int j) { return __ldg(sv + j); }, [&](int j) { return __ldg(rv + j); },
-                     u, w);
+            row_dot2(R, [&](int j) { return __ldg(sv_ + j); }, [&](int j) { return __ldg(rv + j); }, u, w);
             P.u[i] = u;
             P.w[i] = w;
+        } else {
+            P.u[i] = row_dot(R, [&](int j) { return __ldg(sv_ + j); });
         }
-    } else {
-        TILE_LOOP(P) { P.u[i] = row_sum(P, i, [&](int j) { return __ldg(sv + j); }); }
     }
-    if (arrive_last(&c->count[1]) && threadIdx.x == 0) {
-        c->mode2 = MODE_SKIP;
-        c->count[1] = 0u;
-    }
-}
+    __device__ void finish(const Params&, Ctrl* c, const double*) const { c->mode2 = MODE_SKIP; }
+};
 
-#undef TILE_LOOP
+#undef SV
 
 }  // namespace cgvk
