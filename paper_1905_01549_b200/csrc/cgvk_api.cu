@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -77,6 +78,10 @@ struct cgvk_matrix_s {
     int* rp = nullptr;
     int* ci = nullptr;
     double* va = nullptr;
+    int* sell_ptr = nullptr;  // SELL-32 copy of A for the SpMV kernels
+    int* sell_ci = nullptr;
+    double* sell_va = nullptr;
+    int64_t sell_entries = 0;
     double* inv_diag = nullptr;  // built on first use
     int jacobi_state = 0;        // 0 not built, 1 ok, -1 missing/non-positive diagonal
     cudaStream_t stream = nullptr;
@@ -96,6 +101,9 @@ struct cgvk_matrix_s {
         P.ci = ci;
         P.va = va;
         P.d = inv_diag;
+        P.sell_ptr = sell_ptr;
+        P.sell_va = sell_va;
+        P.sell_ci = sell_ci;
         return P;
     }
 };
@@ -154,6 +162,54 @@ int run_dots(cgvk_matrix a, cudaStream_t stream, double* part, unsigned int* cou
 int ensure_tmp(cgvk_matrix a, int count) {
     for (int q = 0; q < count; ++q)
         if (!a->tmp[q]) TRY(dalloc(&a->tmp[q], a->n));
+    return CGVK_OK;
+}
+
+// SELL-32 (sliced ELLPACK, slice = one warp's 32 consecutive rows, sigma = 1:
+// rows keep their order): entry j of row 32s+l at sell_ptr[s] + 32 j + l,
+// slice width = its longest row, padding marked by column -1. Offsets are
+// computed on the host from the reference-layout row_ptr; the fill runs on
+// the device from the validated int32 CSR.
+__global__ void k_fill_sell(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                            const double* __restrict__ va, const int* __restrict__ sp, int* sci,
+                            double* sva) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int base = sp[i >> 5] + (i & 31);
+        for (int k = rp[i], j = 0; k < rp[i + 1]; ++k, ++j) {
+            sci[base + 32 * j] = ci[k];
+            sva[base + 32 * j] = va[k];
+        }
+    }
+}
+
+int build_sell(cgvk_matrix a, const int64_t* row_ptr) {
+    const int64_t n = a->n;
+    const int64_t nslots = (int64_t)a->ntiles * kWarps + 1;  // whole tiles, padded
+    std::vector<int> sp(nslots > 0 ? nslots : 1, 0);
+    int64_t off = 0;
+    for (int64_t s = 0; s + 1 < nslots; ++s) {
+        sp[s] = (int)off;
+        int64_t w = 0;
+        for (int64_t i = 32 * s; i < 32 * s + 32 && i < n; ++i) {
+            const int64_t len = row_ptr[i + 1] - row_ptr[i];
+            if (len > w) w = len;
+        }
+        off += 32 * w;
+        if (off >= (int64_t(1) << 31)) return set_err(CGVK_EINVAL, "SELL layout exceeds 2^31 entries");
+    }
+    sp[nslots - 1] = (int)off;
+    a->sell_entries = off;
+    TRY(dalloc(&a->sell_ptr, nslots));
+    TRY(dalloc(&a->sell_ci, off + 32));
+    TRY(dalloc(&a->sell_va, off + 32));
+    CK(cudaMemcpyAsync(a->sell_ptr, sp.data(), sizeof(int) * nslots, cudaMemcpyHostToDevice, a->stream));
+    CK(cudaMemsetAsync(a->sell_ci, 0xff, sizeof(int) * (off + 32), a->stream));
+    CK(cudaMemsetAsync(a->sell_va, 0, sizeof(double) * (off + 32), a->stream));
+    if (n > 0)
+        k_fill_sell<<<grid_elem(n), 256, 0, a->stream>>>((int)n, a->rp, a->ci, a->va, a->sell_ptr,
+                                                          a->sell_ci, a->sell_va);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(a->stream));
     return CGVK_OK;
 }
 
@@ -222,7 +278,7 @@ int cgvk_matrix_create_csr(int64_t n, const int64_t* row_ptr, const int64_t* col
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     a->sms = sms;
-    a->gmax = sms * kMinBlocksPerSM;
+    a->gmax = sms * kVirtualPerSM;
     {   // stage capacity: the largest tile's CSR span (+ alignment slack)
         int64_t mx = 0;
         for (int64_t r0 = 0; r0 < n; r0 += kBlock) {
@@ -288,6 +344,7 @@ int cgvk_matrix_create_csr(int64_t n, const int64_t* row_ptr, const int64_t* col
         if (hflags & 4) return bail(set_err(CGVK_EINVAL, "column indices not strictly increasing"));
         if (hflags & 8) return bail(set_err(CGVK_EINVAL, "matrix is not bitwise symmetric"));
     }
+    if ((rc = build_sell(a, row_ptr)) != CGVK_OK) return bail(rc);
     *out = a;
     return CGVK_OK;
 }
@@ -299,6 +356,9 @@ int cgvk_matrix_destroy(cgvk_matrix a) {
     cudaFree(a->rp);
     cudaFree(a->ci);
     cudaFree(a->va);
+    cudaFree(a->sell_ptr);
+    cudaFree(a->sell_ci);
+    cudaFree(a->sell_va);
     cudaFree(a->inv_diag);
     cudaFree(a->part);
     cudaFree(a->counter);
@@ -420,6 +480,7 @@ struct KLaunch {
     StreamFn fn = nullptr;
     StageCfg S{};
     int grid = 1;
+    int threads = kThreads;
     size_t smem = 0;
 };
 
@@ -449,21 +510,59 @@ namespace {
 
 constexpr int kSmemPerSM = 227 * 1024;
 
+// Physical CTAs for Gv virtual CTAs with `cap` resident: every physical CTA
+// runs the same number of virtual CTAs (when Gv allows it).
+int balanced_grid(int Gv, int cap) {
+    if (cap >= Gv) return Gv;
+    const int per = (Gv + cap - 1) / cap;
+    return (Gv + per - 1) / per;
+}
+
 // Configure k_stream<Op> for matrix `a`: ring depth chosen so two CTAs fit
 // per SM when the stages allow it, physical grid = resident CTAs (<= Gv).
+// Tuning knobs (read once per solver; for experiments): CGVK_SPMV_ENGINE =
+// staged (default) | sell, CGVK_NSTAGE = ring depth, CGVK_SMEM_CTAS = CTAs per
+// SM the stage budget targets.
+int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+
+bool spmv_sell() {
+    const char* v = getenv("CGVK_SPMV_ENGINE");
+    return v && strcmp(v, "sell") == 0;
+}
+
 template <class Op>
 int make_launch(cgvk_matrix a, KLaunch* L) {
+    if (Op::CSR && spmv_sell()) {  // SpMV kernels: direct engine over SELL-32
+        L->fn = k_direct<Op>;
+        StageCfg S{};
+        S.gvirt = a->G;
+        L->smem = 0;
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L->fn, kBlock, 0));
+        if (occ < 1) return set_err(CGVK_ECUDA, "SpMV kernel does not fit on an SM");
+        L->grid = balanced_grid(a->G, occ * a->sms);
+        L->threads = kBlock;
+        L->S = S;
+        return CGVK_OK;
+    }
     L->fn = k_stream<Op>;
+    L->threads = kThreads;
     StageCfg S{};
     S.nvec = Op::NV;
     S.cap = Op::CSR ? a->cap : 0;
     S.stage_bytes = (stage_bytes_for(S.cap, S.nvec, Op::CSR) + 127) & ~127;
     S.gvirt = a->G;
     const int header = ((int)sizeof(PipeHeader) + 127) & ~127;
-    const int budget2 = kSmemPerSM / 2 - 2048;  // two CTAs per SM
-    int ns = (budget2 - header) / S.stage_bytes;
+    const int ctas = env_int("CGVK_SMEM_CTAS", 2);
+    const int budget = kSmemPerSM / ctas - 2048;
+    int ns = (budget - header) / S.stage_bytes;
     if (ns < 2) ns = 2;
     if (ns > 6) ns = 6;
+    const int forced = env_int(Op::CSR ? "CGVK_NSTAGE_SPMV" : "CGVK_NSTAGE", 0);
+    if (forced >= 2 && forced <= kMaxStages) ns = forced;
     S.nstage = ns;
     L->smem = (size_t)header + (size_t)ns * S.stage_bytes;
     if (L->smem > (size_t)kSmemPerSM - 1024)
@@ -472,7 +571,7 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L->fn, kThreads, L->smem));
     if (occ < 1) return set_err(CGVK_ECUDA, "pipeline kernel does not fit on an SM");
-    L->grid = occ * a->sms < a->G ? occ * a->sms : a->G;
+    L->grid = balanced_grid(a->G, occ * a->sms);
     L->S = S;
     return CGVK_OK;
 }
@@ -519,7 +618,7 @@ int ref_allocated(int v, bool prec) {
 }
 
 void launch(cgvk_solver s, const KLaunch& L) {
-    L.fn<<<L.grid, kThreads, L.smem, s->stream>>>(s->P, L.S);
+    L.fn<<<L.grid, L.threads, L.smem, s->stream>>>(s->P, L.S);
 }
 
 void launch_iter(cgvk_solver s) {

@@ -20,7 +20,8 @@ namespace cgvk {
 
 constexpr int kBlock = 256;       // rows per tile == threads per CTA
 constexpr int kWarps = kBlock / 32;
-constexpr int kMinBlocksPerSM = 4;  // __launch_bounds__ minimum -> G = SMs * 4
+constexpr int kMinBlocksPerSM = 4;  // generic kernels: __launch_bounds__ minimum
+constexpr int kVirtualPerSM = 12;   // canonical G cap = SMs * 12 (divisible by 2, 3, 4, 6 CTAs/SM)
 constexpr int kMaxDots = 6;
 
 // SolverState scalar slots
@@ -69,6 +70,9 @@ struct Params {
     double* rt;
     double* st;
     double* wt;
+    const int* __restrict__ sell_ptr;   // SELL-32: slice offsets (entries), nslices+1
+    const double* __restrict__ sell_va;
+    const int* __restrict__ sell_ci;    // -1 marks padding
     double* part;  // [kMaxDots][G] CTA partials
     double* hist;  // rr per iteration
     Ctrl* ctrl;

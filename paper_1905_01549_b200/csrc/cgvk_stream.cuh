@@ -121,35 +121,85 @@ __device__ __forceinline__ bool arrive_last_c(unsigned int* counter, int* flag) 
     return last;
 }
 
-// A CSR row as seen by a consumer: entries [b, e) of the global arrays, read
-// from the stage when staged.
+// A sparse row as seen by a thread: `len` entries at va[k*stride], ci[k*stride].
+// CSR (staged or global): stride 1, exactly the row's entries. SELL-32: stride
+// 32 (one warp = one slice), len = slice width, padding marked by ci < 0 (a
+// row-length predicate, never a padded multiply). Either way a row is summed
+// left to right in CSR column order (src/sparse_matrix.cpp:112-117).
 struct RowRef {
-    const double* va;  // already offset so that va[k] is entry k
+    const double* va;
     const int* ci;
-    int b, e;
+    int len, stride;
 };
+
+// The row is consumed in chunks of 8 entries: all column and value loads of a
+// chunk are issued first, then all of its gathers, then the in-order
+// accumulation — so a row costs ~2 memory latencies, not 2 per entry. Loads
+// past the row end / padding slots (ci < 0) are predicated off; padding is
+// never multiplied.
+constexpr int kChunk = 8;
 
 template <class XF>
 __device__ __forceinline__ double row_dot(const RowRef& R, XF xf) {
     double sum = 0.0;
-#pragma unroll 4
-    for (int k = R.b; k < R.e; ++k) sum = ADD(sum, MUL(R.va[k], xf(R.ci[k])));
+    for (int k0 = 0; k0 < R.len; k0 += kChunk) {
+        int c[kChunk];
+        double v[kChunk], xv[kChunk];
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u) {
+            const bool in = k0 + u < R.len;
+            c[u] = in ? R.ci[(k0 + u) * R.stride] : -1;
+            v[u] = in ? R.va[(k0 + u) * R.stride] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u) xv[u] = c[u] >= 0 ? xf(c[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u)
+            if (c[u] >= 0) sum = ADD(sum, MUL(v[u], xv[u]));
+    }
     return sum;
 }
 
 template <class XF1, class XF2>
 __device__ __forceinline__ void row_dot2(const RowRef& R, XF1 xf1, XF2 xf2, double& y1, double& y2) {
     double s1 = 0.0, s2 = 0.0;
-#pragma unroll 4
-    for (int k = R.b; k < R.e; ++k) {
-        const double v = R.va[k];
-        const int c = R.ci[k];
-        s1 = ADD(s1, MUL(v, xf1(c)));
-        s2 = ADD(s2, MUL(v, xf2(c)));
+    for (int k0 = 0; k0 < R.len; k0 += kChunk) {
+        int c[kChunk];
+        double v[kChunk], x1[kChunk], x2[kChunk];
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u) {
+            const bool in = k0 + u < R.len;
+            c[u] = in ? R.ci[(k0 + u) * R.stride] : -1;
+            v[u] = in ? R.va[(k0 + u) * R.stride] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u) {
+            x1[u] = c[u] >= 0 ? xf1(c[u]) : 0.0;
+            x2[u] = c[u] >= 0 ? xf2(c[u]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u)
+            if (c[u] >= 0) {
+                s1 = ADD(s1, MUL(v[u], x1[u]));
+                s2 = ADD(s2, MUL(v[u], x2[u]));
+            }
     }
     y1 = s1;
     y2 = s2;
 }
+
+// Per-row input accessors handed to Op::row: staged (shared memory) or direct.
+struct StagedIn {
+    const double* sv;
+    __device__ __forceinline__ double operator()(int v) const { return sv[v * kBlock]; }
+};
+
+template <int NV>
+struct DirectIn {
+    const double* vp[NV > 0 ? NV : 1];  // by value: stays in registers
+    int i;
+    __device__ __forceinline__ double operator()(int v) const { return __ldg(vp[v] + i); }
+};
 
 // Per-stage shared-memory layout.
 struct StageView {
@@ -282,19 +332,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(Params P, StageCfg S) {
             StageView V = stage_view(stages, S, slot);
             const int i = tile * kBlock + t;
             if (i < P.n) {
-                RowRef R;
+                RowRef R{nullptr, nullptr, 0, 1};
                 if (Op::CSR) {
-                    R.b = V.rp[t];
-                    R.e = V.rp[t + 1];
+                    const int b = V.rp[t];
+                    R.len = V.rp[t + 1] - b;
                     if (H->direct[slot]) {
-                        R.va = P.va;
-                        R.ci = P.ci;
+                        R.va = P.va + b;
+                        R.ci = P.ci + b;
                     } else {
-                        R.va = V.va - H->k0a[slot];
-                        R.ci = V.ci - H->k0c[slot];
+                        R.va = V.va + (b - H->k0a[slot]);
+                        R.ci = V.ci + (b - H->k0c[slot]);
                     }
                 }
-                op.row(P, i, V.vec + t, R, acc);
+                op.row(P, i, StagedIn{V.vec + t}, R, acc);
             }
             __syncwarp();
             if ((t & 31) == 0) mbar_arrive(&H->empty[slot]);
@@ -321,6 +371,77 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(Params P, StageCfg S) {
             for (int d = 0; d < Op::ND; ++d) tot[d] = ADD(tot[d], __ldcg(P.part + d * Gv + q));
         }
         if constexpr (Op::ND > 0) cta_tree_c<Op::ND>(tot, H->red);
+    }
+    if (t == 0) {
+        *counter = 0u;
+        op.finish(P, P.ctrl, tot);
+    }
+}
+
+// ------------------------------------------------------- direct engine
+//
+// The SpMV kernels: 256 threads, one row each, same virtual-CTA loop and
+// canonical reduction as k_stream, no shared-memory staging (all of L1 stays
+// with the x gathers). The matrix is read in SELL-32 layout (a warp's 32 rows
+// are one slice, entry k of the slice's rows contiguous), so every matrix
+// load is a fully coalesced 256 B (values) / 128 B (columns) warp access;
+// per-row vectors are plain coalesced loads.
+template <class Op>
+__global__ void __launch_bounds__(kBlock, 3) k_direct(Params P, StageCfg S) {
+    __shared__ double red[kMaxDots * 32];
+    __shared__ int last_flag;
+    Op op;
+    if (!op.enter(P)) return;
+    const int Gv = S.gvirt, Gp = gridDim.x, ntiles = P.ntiles;
+    const int t = threadIdx.x, lane = t & 31;
+    DirectIn<Op::NV> in;
+#pragma unroll
+    for (int v = 0; v < Op::NV; ++v) in.vp[v] = op.vec(P, v);
+    double acc[Op::ND > 0 ? Op::ND : 1];
+    for (int vb = blockIdx.x; vb < Gv; vb += Gp) {
+#pragma unroll
+        for (int d = 0; d < Op::ND; ++d) acc[d] = 0.0;
+        for (int tile = vb; tile < ntiles; tile += Gv) {
+            const int i = tile * kBlock + t;
+            const int slice = i >> 5;
+            RowRef R;
+            const int b = __ldg(P.sell_ptr + slice);
+            R.len = (__ldg(P.sell_ptr + slice + 1) - b) >> 5;
+            R.va = P.sell_va + b + lane;
+            R.ci = P.sell_ci + b + lane;
+            R.stride = 32;
+            in.i = i;
+            if (i < P.n) op.row(P, i, in, R, acc);
+        }
+        if constexpr (Op::ND > 0) {
+            if (op.sync() != 2) continue;
+            cta_tree<Op::ND>(acc, red);
+            if (t == 0) {
+#pragma unroll
+                for (int d = 0; d < Op::ND; ++d) P.part[d * Gv + vb] = acc[d];
+            }
+        }
+    }
+    const int mode = op.sync();
+    if (mode == 0) return;
+    unsigned int* counter = op.counter(P);
+    __syncthreads();
+    if (t == 0) {
+        __threadfence();
+        last_flag = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last_flag) return;
+    __threadfence();
+    double tot[Op::ND > 0 ? Op::ND : 1];
+#pragma unroll
+    for (int d = 0; d < Op::ND; ++d) tot[d] = 0.0;
+    if (mode == 2) {
+        for (int q = t; q < Gv; q += kBlock) {
+#pragma unroll
+            for (int d = 0; d < Op::ND; ++d) tot[d] = ADD(tot[d], __ldcg(P.part + d * Gv + q));
+        }
+        if constexpr (Op::ND > 0) cta_tree<Op::ND>(tot, red);
     }
     if (t == 0) {
         *counter = 0u;

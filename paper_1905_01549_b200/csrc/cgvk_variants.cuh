@@ -36,7 +36,7 @@ __device__ __forceinline__ bool step_wanted(const Ctrl* c) {
     return c->state == ST_RUNNING && c->k < c->k_limit;
 }
 
-#define SV(v) sv[(v) * kBlock]
+#define SV(v) in(v)
 
 // =====================================================================  HS
 // src/variants.cpp:189-205, paper Alg. 1. V = 3+1 (K1) + 4+3 (K2) vectors.
@@ -55,7 +55,8 @@ struct HsK1 {
     __device__ const double* vec(const Params& P, int v) const { return v == 0 ? P.r : v == 1 ? P.s : P.d; }
     __device__ int sync() const { return 2; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[0]; }
-    __device__ void row(const Params& P, int i, const double* sv, const RowRef&, double* acc) const {
+    template <class In>
+    __device__ void row(const Params& P, int i, const In& in, const RowRef&, double* acc) const {
         const double r = SUB(SV(0), MUL(alpha, SV(1)));
         P.r[i] = r;
         const double rt = PREC ? MUL(SV(2), r) : r;
@@ -105,7 +106,8 @@ struct HsK2 {
     }
     __device__ int sync() const { return mode == MODE_FULL ? 2 : 1; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
-    __device__ void row(const Params& P, int i, const double* sv, const RowRef& R, double* acc) const {
+    template <class In>
+    __device__ void row(const Params& P, int i, const In& in, const RowRef& R, double* acc) const {
         const double po = SV(0);
         P.x[i] = ADD(SV(2), MUL(alpha, po));
         if (mode != MODE_FULL) return;
@@ -163,7 +165,8 @@ struct CgK1 {
     }
     __device__ int sync() const { return (F && !S) ? 1 : 0; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[0]; }
-    __device__ void row(const Params& P, int i, const double* sv, const RowRef&, double*) const {
+    template <class In>
+    __device__ void row(const Params& P, int i, const In& in, const RowRef&, double*) const {
         double p = SV(0), s = SV(1);
         const double r = SV(3);
         if (F) {
@@ -200,7 +203,8 @@ struct CgK2 {
     }
     __device__ int sync() const { return 2; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
-    __device__ void row(const Params& P, int i, const double* sv, const RowRef& R, double* acc) const {
+    template <class In>
+    __device__ void row(const Params& P, int i, const In& in, const RowRef& R, double* acc) const {
         const double* __restrict__ r = P.r;
         const double w = row_dot(R, [&](int j) { return Mg<PREC>(P, j, __ldg(r + j)); });
         P.w[i] = w;
@@ -273,7 +277,8 @@ struct PrK1 {
     }
     __device__ int sync() const { return valid ? 0 : 2; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[0]; }
-    __device__ void row(const Params& P, int i, const double* sv, const RowRef&, double* acc) const {
+    template <class In>
+    __device__ void row(const Params& P, int i, const In& in, const RowRef&, double* acc) const {
         const double s = SV(3), p = SV(1);
         P.x[i] = ADD(SV(0), MUL(alpha, p));
         const double r = SUB(SV(2), MUL(alpha, s));
@@ -316,7 +321,8 @@ struct PrK2 {
     }
     __device__ int sync() const { return 2; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
-    __device__ void row(const Params& P, int i, const double* sv, const RowRef& R, double* acc) const {
+    template <class In>
+    __device__ void row(const Params& P, int i, const In& in, const RowRef& R, double* acc) const {
         const double* __restrict__ p = P.p0;
         const double s = row_dot(R, [&](int j) { return __ldg(p + j); });
         P.s[i] = s;
@@ -396,7 +402,8 @@ struct GvK1 {
     }
     __device__ int sync() const { return S ? 2 : 1; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[0]; }
-    __device__ void row(const Params& P, int i, const double* sv, const RowRef&, double* acc) const {
+    template <class In>
+    __device__ void row(const Params& P, int i, const In& in, const RowRef&, double* acc) const {
         double p = SV(0), s = SV(1), u = SV(2), w = SV(3);
         double st = PREC ? SV(7) : s;
         double rt = PREC ? SV(8) : SV(6);
@@ -473,7 +480,8 @@ struct GvK2 {
     __device__ const double* vec(const Params&, int) const { return nullptr; }
     __device__ int sync() const { return 1; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
-    __device__ void row(const Params& P, int i, const double*, const RowRef& R, double*) const {
+    template <class In>
+    __device__ void row(const Params& P, int i, const In&, const RowRef& R, double*) const {
         const double* __restrict__ w = P.w;
         P.t[i] = row_dot(R, [&](int j) { return Mg<PREC>(P, j, __ldg(w + j)); });
     }
@@ -522,7 +530,8 @@ struct PprK1 {
     }
     __device__ int sync() const { return 2; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[0]; }
-    __device__ void row(const Params& P, int i, const double* sv, const RowRef&, double* acc) const {
+    template <class In>
+    __device__ void row(const Params& P, int i, const In& in, const RowRef&, double* acc) const {
         const double p_old = SV(1), s_old = SV(3), w_old = SV(4), u = SV(5);
         P.x[i] = ADD(SV(0), MUL(alpha, p_old));
         const double r = SUB(SV(2), MUL(alpha, s_old));
@@ -615,7 +624,8 @@ struct PprK2 {
     __device__ const double* vec(const Params&, int) const { return nullptr; }
     __device__ int sync() const { return 1; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
-    __device__ void row(const Params& P, int i, const double*, const RowRef& R, double*) const {
+    template <class In>
+    __device__ void row(const Params& P, int i, const In&, const RowRef& R, double*) const {
         const double* __restrict__ sv_ = PREC ? P.st : P.s;
         const double* __restrict__ rv = PREC ? P.rt : P.r;
         if (P.recompute_w) {
