@@ -594,3 +594,46 @@ double orc_time_steps(orc_solver* s, int iters, int* taken) {
     *taken = k;
     return (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
 }
+
+/* a_norm with the clamp of src/sparse_matrix.cpp:169-178 (sequential dot, as
+ * the reference's diagnostics use) */
+static double a_norm_seq(const orc_solver* s, const double* e, double* tmp) {
+    orc_spmv(s->n, s->rp, s->ci, s->va, e, tmp);
+    double q = dot_seq(s->n, e, tmp);
+    if (q < 0.0) q = 0.0;
+    return sqrt(q);
+}
+
+/* The Table-3 protocol: run() with StopRule::error_reduction(threshold) and
+ * per-iteration probes (src/runner.cpp:32-147, summarize in
+ * src/diagnostics.cpp:111-126): the relative A-norm error after every step;
+ * iters_to_1e5 = first k with ratio < 1e-5 (-1 if none); min_log10_err over
+ * k >= 0. threshold <= 0: fixed budget. Returns the steps taken. */
+int orc_anorm_run(orc_solver* s, const double* x_star, int max_iter, double threshold,
+                  int* iters_to_1e5, double* min_log10_err, int* final_state) {
+    const int64_t n = s->n;
+    double* e = (double*)malloc(sizeof(double) * (size_t)(n ? n : 1));
+    double* tmp = (double*)malloc(sizeof(double) * (size_t)(n ? n : 1));
+    for (int64_t i = 0; i < n; ++i) e[i] = x_star[i] - s->vec[X][i];
+    const double e0 = a_norm_seq(s, e, tmp);
+    double min_ratio = 1.0; /* k = 0 record: ratio 1 */
+    *iters_to_1e5 = -1;
+    int taken = 0, stopped = 0;
+    while (s->state == ST_RUNNING && taken < max_iter) {
+        orc_solver_step(s);
+        ++taken;
+        for (int64_t i = 0; i < n; ++i) e[i] = x_star[i] - s->vec[X][i];
+        const double ratio = a_norm_seq(s, e, tmp) / e0;
+        if (ratio < min_ratio) min_ratio = ratio;
+        if (*iters_to_1e5 < 0 && ratio < 1e-5) *iters_to_1e5 = s->k;
+        if (threshold > 0.0 && ratio < threshold && s->state == ST_RUNNING) {
+            stopped = 1;
+            break;
+        }
+    }
+    *min_log10_err = log10(min_ratio);
+    *final_state = stopped ? ST_CONVERGED : (s->state == ST_RUNNING ? ST_MAXITER : s->state);
+    free(e);
+    free(tmp);
+    return taken;
+}

@@ -67,6 +67,8 @@ int orc_solver_vector(const orc_solver* s, int which, double* out);
 int orc_solve(orc_solver* s, const double* b, int max_iter, double tol, double* upd_hist,
               double* true_hist, int true_cap);
 double orc_time_steps(orc_solver* s, int iters, int* taken);
+int orc_anorm_run(orc_solver* s, const double* x_star, int max_iter, double threshold,
+                  int* iters_to_1e5, double* min_log10_err, int* final_state);
 int orc_config_validate(int variant, int nu_expr, int recompute_nu, int recompute_w,
                         int unsimplified_mu, int track_delta);
 

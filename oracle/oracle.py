@@ -72,6 +72,8 @@ def _load_restatement():
     L.orc_solve.restype = I
     L.orc_time_steps.argtypes = [P, I, C.POINTER(I)]
     L.orc_time_steps.restype = D
+    L.orc_anorm_run.argtypes = [P, P, I, D, C.POINTER(I), C.POINTER(D), C.POINTER(I)]
+    L.orc_anorm_run.restype = I
     L.orc_config_validate.argtypes = [I] * 6
     L.orc_config_validate.restype = I
     return L
@@ -196,6 +198,15 @@ class Restatement(_SolverBase):
 
     def _time(self, *a):
         return _orc.orc_time_steps(self._h, *a)
+
+    def anorm_run(self, x_star, max_iter: int, threshold: float = 1e-5):
+        """Table-3 protocol (run() + error-reduction stop, probes every step)."""
+        xs = _f64(x_star)
+        it, mle, fs = C.c_int(), C.c_double(), C.c_int()
+        taken = _orc.orc_anorm_run(self._h, xs.ctypes.data, max_iter, threshold, C.byref(it),
+                                   C.byref(mle), C.byref(fs))
+        return {"taken": taken, "iters_to_1e5": it.value, "min_log10_err": mle.value,
+                "final_state": fs.value}
 
 
 class Reference(_SolverBase):

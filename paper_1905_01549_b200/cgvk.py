@@ -212,6 +212,14 @@ def device_count() -> int:
     return n.value
 
 
+def device_count_safe() -> int:
+    """0 when no CUDA driver/device is present (used to skip, never to fall back)."""
+    try:
+        return device_count()
+    except CgvkError:
+        return 0
+
+
 @dataclass
 class VariantConfig:
     """POD mirror of VariantConfig (inc/variants.hpp:34-57)."""
