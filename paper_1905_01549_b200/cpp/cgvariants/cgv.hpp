@@ -1,0 +1,428 @@
+// cgv:: — the reference's solver API (proj/include/cgvariants/*.hpp) re-declared
+// over the cgvk C ABI (include/cgvk.h), so reference callers recompile against
+// the B200 path unchanged. Same names, argument meaning and error behaviour:
+// CGVK_EINVAL -> std::invalid_argument, CGVK_ESTATE -> std::logic_error, other
+// failures -> std::runtime_error. Header-only; link with libcgvk.so.
+//
+// Source-compatible additions (the reference's fields are all kept):
+//   * SparseMatrix::device — the matrix resident on the GPU, uploaded on first
+//     use (A is immutable after that, as the reference's sharing contract,
+//     inc/variants.hpp:95-97, already requires);
+//   * SolverState::device / sync_host — the device solver; with sync_host
+//     (default) every step() refreshes the host vectors (parity mode); with it
+//     off, run()/step_n() keep everything on the device.
+#pragma once
+
+#include "cgvk.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <memory>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <tuple>
+#include <vector>
+
+namespace cgv {
+
+using Index = std::int64_t;             // inc/types.hpp:8
+using DenseVector = std::vector<double>;  // inc/types.hpp:9
+
+namespace detail {
+inline void check(int rc) {
+    if (rc == CGVK_OK) return;
+    const std::string msg = cgvk_last_error();
+    if (rc == CGVK_EINVAL) throw std::invalid_argument(msg);
+    if (rc == CGVK_ESTATE) throw std::logic_error(msg);
+    throw std::runtime_error(msg);
+}
+struct MatrixHandle {
+    cgvk_matrix h = nullptr;
+    ~MatrixHandle() { cgvk_matrix_destroy(h); }
+};
+struct SolverHandle {
+    cgvk_solver h = nullptr;
+    ~SolverHandle() { cgvk_solver_destroy(h); }
+};
+}  // namespace detail
+
+// ------------------------------------------------------------ vector ops
+// inc/vector_ops.hpp:15-54 (host reference kernels, sequential order)
+
+inline void require_same_size(std::size_t a, std::size_t b) {
+    if (a != b) throw std::invalid_argument("vector dimension mismatch");
+}
+inline double dot(std::span<const double> x, std::span<const double> y) {
+    require_same_size(x.size(), y.size());
+    double acc = 0.0;
+    for (std::size_t i = 0; i < x.size(); ++i) acc += x[i] * y[i];
+    return acc;
+}
+inline double norm2(std::span<const double> x) { return std::sqrt(dot(x, x)); }
+
+// --------------------------------------------------------- sparse matrix
+// inc/sparse_matrix.hpp:16-57
+
+struct SparseMatrix {
+    Index n = 0;
+    std::vector<Index> row_ptr;
+    std::vector<Index> col_idx;
+    std::vector<double> values;
+    mutable std::shared_ptr<detail::MatrixHandle> device;  // addition
+
+    Index nnz() const { return static_cast<Index>(values.size()); }
+
+    cgvk_matrix on_device(int gpu = 0) const {
+        if (!device) {
+            if (row_ptr.size() != static_cast<std::size_t>(n) + 1)
+                throw std::invalid_argument("row_ptr length must be n+1");
+            auto h = std::make_shared<detail::MatrixHandle>();
+            detail::check(cgvk_matrix_create_csr(n, row_ptr.data(), col_idx.data(), values.data(),
+                                                 gpu, 0, &h->h));
+            device = h;
+        }
+        return device->h;
+    }
+};
+
+using Triplet = std::tuple<Index, Index, double>;
+
+// duplicates summed in input order, exact zeros dropped (sparse_matrix.hpp:25-27)
+inline SparseMatrix csr_from_triplets(Index n, std::vector<Triplet> t) {
+    std::stable_sort(t.begin(), t.end(), [](const Triplet& a, const Triplet& b) {
+        return std::tie(std::get<0>(a), std::get<1>(a)) < std::tie(std::get<0>(b), std::get<1>(b));
+    });
+    SparseMatrix a;
+    a.n = n;
+    a.row_ptr.assign(static_cast<std::size_t>(n) + 1, 0);
+    for (std::size_t i = 0; i < t.size();) {
+        const auto [r, c, v0] = t[i];
+        if (r < 0 || r >= n || c < 0 || c >= n) throw std::invalid_argument("triplet index out of range");
+        double sum = v0;
+        std::size_t j = i + 1;
+        for (; j < t.size() && std::get<0>(t[j]) == r && std::get<1>(t[j]) == c; ++j)
+            sum += std::get<2>(t[j]);
+        if (sum != 0.0) {
+            a.col_idx.push_back(c);
+            a.values.push_back(sum);
+            ++a.row_ptr[static_cast<std::size_t>(r) + 1];
+        }
+        i = j;
+    }
+    for (Index r = 0; r < n; ++r) a.row_ptr[r + 1] += a.row_ptr[r];
+    return a;
+}
+
+// validated on the device (cgvk_matrix_create_csr runs validate_csr there)
+inline void validate_csr(const SparseMatrix& a) {
+    SparseMatrix copy{a.n, a.row_ptr, a.col_idx, a.values, nullptr};
+    copy.on_device();
+}
+
+inline bool is_symmetric(const SparseMatrix& a) {
+    cgvk_matrix h = nullptr;
+    const int rc = cgvk_matrix_create_csr(a.n, a.row_ptr.data(), a.col_idx.data(), a.values.data(), 0,
+                                          CGVK_MATRIX_CHECK_SYMMETRIC, &h);
+    cgvk_matrix_destroy(h);
+    if (rc == CGVK_EINVAL) return false;
+    detail::check(rc);
+    return true;
+}
+
+// y = A x, per-row left-to-right (sparse_matrix.hpp:41-42) — on the GPU
+inline void spmv(const SparseMatrix& a, std::span<const double> x, std::span<double> y) {
+    if (x.size() != static_cast<std::size_t>(a.n) || y.size() != static_cast<std::size_t>(a.n))
+        throw std::invalid_argument("spmv dimension mismatch");
+    detail::check(cgvk_spmv(a.on_device(), x.data(), y.data()));
+}
+inline DenseVector spmv(const SparseMatrix& a, const DenseVector& x) {
+    DenseVector y(static_cast<std::size_t>(a.n));
+    spmv(a, x, y);
+    return y;
+}
+inline void block_spmv(const SparseMatrix& a, std::span<const double> x1, std::span<const double> x2,
+                       std::span<double> y1, std::span<double> y2) {
+    const auto n = static_cast<std::size_t>(a.n);
+    if (x1.size() != n || x2.size() != n || y1.size() != n || y2.size() != n)
+        throw std::invalid_argument("block_spmv dimension mismatch");
+    detail::check(cgvk_block_spmv(a.on_device(), x1.data(), x2.data(), y1.data(), y2.data()));
+}
+
+// ---------------------------------------------------------- preconditioner
+// inc/preconditioner.hpp:13-28
+
+struct Preconditioner {
+    enum class Kind { Identity, Jacobi };
+    Kind kind = Kind::Identity;
+    std::vector<double> inv_diag;
+    const SparseMatrix* source = nullptr;  // addition: the matrix it was built from
+
+    static Preconditioner identity() { return Preconditioner{}; }
+    static Preconditioner jacobi(const SparseMatrix& a) {
+        Preconditioner m;
+        m.kind = Kind::Jacobi;
+        m.source = &a;
+        m.inv_diag.resize(static_cast<std::size_t>(a.n));
+        detail::check(cgvk_jacobi(a.on_device(), m.inv_diag.data()));
+        return m;
+    }
+    void apply(std::span<const double> in, std::span<double> out) const {
+        if (in.size() != out.size()) throw std::invalid_argument("preconditioner dimension mismatch");
+        if (kind == Kind::Identity) {
+            std::copy(in.begin(), in.end(), out.begin());
+            return;
+        }
+        if (in.size() != inv_diag.size()) throw std::invalid_argument("preconditioner dimension mismatch");
+        for (std::size_t i = 0; i < in.size(); ++i) out[i] = inv_diag[i] * in[i];
+    }
+    DenseVector apply(const DenseVector& in) const {
+        DenseVector out(in.size());
+        apply(in, out);
+        return out;
+    }
+    bool is_identity() const { return kind == Kind::Identity; }
+};
+
+inline std::string_view preconditioner_name(Preconditioner::Kind k) {
+    return k == Preconditioner::Kind::Identity ? "none" : "jacobi";
+}
+
+// ---------------------------------------------------------------- variants
+// inc/variants.hpp:17-153
+
+enum class Variant { HS, CG_CG, M, PR, GV, PIPE_PR_M, PIPE_PR };
+enum class NuExpression { Expanded, Simplified, Meurant };
+
+struct VariantConfig {
+    Variant variant = Variant::HS;
+    bool recompute_nu = true;
+    bool recompute_w = true;
+    NuExpression nu_expression = NuExpression::Simplified;
+    bool unsimplified_mu = false;
+    bool track_delta = false;
+
+    static VariantConfig make(Variant v) {
+        const cgvk_variant_config c = cgvk_variant_config_make(static_cast<int>(v));
+        VariantConfig out;
+        out.variant = v;
+        out.nu_expression = static_cast<NuExpression>(c.nu_expression);
+        return out;
+    }
+    cgvk_variant_config to_c() const {
+        return {static_cast<int>(variant), static_cast<int>(nu_expression), recompute_nu, recompute_w,
+                unsimplified_mu, track_delta};
+    }
+    void validate() const {
+        const cgvk_variant_config c = to_c();
+        detail::check(cgvk_variant_config_validate(&c));
+    }
+    bool is_predictor() const {
+        return variant == Variant::M || variant == Variant::PR || variant == Variant::PIPE_PR_M ||
+               variant == Variant::PIPE_PR;
+    }
+    bool is_pipelined() const {
+        return variant == Variant::GV || variant == Variant::PIPE_PR_M || variant == Variant::PIPE_PR;
+    }
+};
+
+inline std::string_view variant_name(Variant v) {
+    constexpr std::string_view names[] = {"hs", "cg", "m", "pr", "gv", "pipe-pr-m", "pipe-pr"};
+    return names[static_cast<int>(v)];
+}
+
+enum class BreakdownReason { None, NuPrimeNonPositive, NuNonPositive, MuNonPositive, NonFinite };
+enum class ConvergedBy { ZeroResidual, ErrorThreshold, Stagnation, Tolerance };
+
+struct SolveStatus {
+    enum class State { Running, Breakdown, MaxIterations, Converged };
+    State state = State::Running;
+    BreakdownReason breakdown = BreakdownReason::None;
+    ConvergedBy criterion = ConvergedBy::ZeroResidual;
+    bool running() const { return state == State::Running; }
+};
+
+struct SolverStats {
+    std::uint64_t spmv_calls = 0, block_spmv_calls = 0, precond_applies = 0, reductions = 0;
+};
+
+struct SolverState {
+    VariantConfig config;
+    const SparseMatrix* a = nullptr;
+    const Preconditioner* m = nullptr;
+    bool preconditioned = false;
+    Index n = 0;
+    int k = 0;
+    SolveStatus status;
+    SolverStats stats;
+    DenseVector x, r, p, s, w, u, t, r_tilde, s_tilde, w_tilde, u_tilde;
+    double alpha = 0.0, beta = 0.0, nu = 0.0, nu_prime = 0.0, mu = 0.0, delta = 0.0,
+           delta_hat = 0.0, gamma = 0.0, eta = 0.0;
+    // additions
+    std::shared_ptr<detail::SolverHandle> device;
+    bool sync_host = true;
+
+    DenseVector& rt() { return preconditioned ? r_tilde : r; }
+    DenseVector& st() { return preconditioned ? s_tilde : s; }
+    DenseVector& wt() { return preconditioned ? w_tilde : w; }
+    DenseVector& ut() { return preconditioned ? u_tilde : u; }
+    int allocated_vectors() const {
+        int c = 0;
+        for (const DenseVector* v : {&x, &r, &p, &s, &w, &u, &t, &r_tilde, &s_tilde, &w_tilde, &u_tilde})
+            c += !v->empty();
+        return c;
+    }
+
+    // Pull status, scalars, counters (and the vectors when sync_host) from the device.
+    void refresh() {
+        cgvk_solve_status st{};
+        cgvk_scalars sc{};
+        cgvk_stats ss{};
+        detail::check(cgvk_solver_status(device->h, &st, &sc, &ss));
+        k = st.k;
+        status.state = static_cast<SolveStatus::State>(st.state);
+        status.breakdown = static_cast<BreakdownReason>(st.breakdown);
+        status.criterion = static_cast<ConvergedBy>(st.criterion);
+        alpha = sc.alpha;
+        beta = sc.beta;
+        nu = sc.nu;
+        nu_prime = sc.nu_prime;
+        mu = sc.mu;
+        delta = sc.delta;
+        delta_hat = sc.delta_hat;
+        gamma = sc.gamma;
+        eta = sc.eta;
+        stats = {ss.spmv_calls, ss.block_spmv_calls, ss.precond_applies, ss.reductions};
+        if (!sync_host) return;
+        DenseVector* vecs[] = {&x, &r, &p, &s, &w, &u, &t, &r_tilde, &s_tilde, &w_tilde, &u_tilde};
+        for (int which = 0; which < 11; ++which) {
+            DenseVector& v = *vecs[which];
+            v.resize(static_cast<std::size_t>(n));
+            if (n == 0 || cgvk_solver_get_vector(device->h, which, v.data()) != CGVK_OK) v.clear();
+        }
+    }
+};
+
+// initialize() (inc/variants.hpp:149-150)
+inline SolverState initialize(const VariantConfig& config, const SparseMatrix& a,
+                              const Preconditioner& m, const DenseVector& b, const DenseVector& x0) {
+    config.validate();
+    if (b.size() != static_cast<std::size_t>(a.n) || x0.size() != static_cast<std::size_t>(a.n))
+        throw std::invalid_argument("right-hand side or initial guess dimension mismatch");
+    if (m.kind == Preconditioner::Kind::Jacobi && m.inv_diag.size() != static_cast<std::size_t>(a.n))
+        throw std::invalid_argument("preconditioner dimension mismatch");
+    SolverState st;
+    st.config = config;
+    st.a = &a;
+    st.m = &m;
+    st.preconditioned = !m.is_identity();
+    st.n = a.n;
+    st.device = std::make_shared<detail::SolverHandle>();
+    const cgvk_variant_config c = config.to_c();
+    detail::check(cgvk_solver_create(a.on_device(), &c, st.preconditioned ? CGVK_PRECOND_JACOBI
+                                                                           : CGVK_PRECOND_IDENTITY,
+                                     b.data(), x0.data(), &st.device->h));
+    st.refresh();
+    return st;
+}
+
+// step() (inc/variants.hpp:153): exactly one iteration
+inline void step(SolverState& st) {
+    if (!st.status.running()) throw std::logic_error("step() on a terminated solver");
+    detail::check(cgvk_solver_step(st.device->h, 1));
+    detail::check(cgvk_solver_sync(st.device->h));
+    st.refresh();
+}
+
+// Performance entry: n iterations as graph replays, one sync at the end.
+inline void step_n(SolverState& st, int n_iters, double rel_tol = 0.0) {
+    if (!st.status.running()) throw std::logic_error("step() on a terminated solver");
+    if (rel_tol > 0.0) detail::check(cgvk_solver_set_tolerance(st.device->h, rel_tol));
+    detail::check(cgvk_solver_step(st.device->h, n_iters));
+    detail::check(cgvk_solver_sync(st.device->h));
+    st.refresh();
+}
+
+// ------------------------------------------------------------------ runner
+// inc/runner.hpp: StopRule, ProbeOptions, run() — the hot-path subset:
+// FixedIterations with probes off runs entirely on the device; probes record
+// the quantities the device path provides (true/updated residual, scalars).
+
+struct StopRule {
+    enum class Kind { FixedIterations, ErrorReduction, ResidualStagnation };
+    Kind kind = Kind::ResidualStagnation;
+    int fixed_count = 0;
+    double error_threshold = 1e-5;
+    int stagnation_window = 50;
+    double stagnation_improvement = 0.01;
+    static StopRule fixed(int count) {
+        StopRule r;
+        r.kind = Kind::FixedIterations;
+        r.fixed_count = count;
+        return r;
+    }
+};
+
+struct ProbeOptions {
+    int cadence = 1;
+    const DenseVector* x_star = nullptr;
+    bool enabled = true;
+};
+
+struct IterationRecord {
+    int k = 0;
+    std::optional<double> true_res_norm, upd_res_norm, alpha, beta, nu, nu_prime;
+};
+
+struct ConvergenceHistory {
+    VariantConfig config;
+    Preconditioner::Kind precond = Preconditioner::Kind::Identity;
+    std::vector<IterationRecord> records;
+    SolveStatus final_status;
+};
+
+inline ConvergenceHistory run(const VariantConfig& config, const SparseMatrix& a,
+                              const Preconditioner& m, const DenseVector& b, const DenseVector& x0,
+                              int max_iter, const StopRule& stop, const ProbeOptions& probe_opts) {
+    if (max_iter < 0) throw std::invalid_argument("max_iter must be >= 0");
+    if (stop.kind != StopRule::Kind::FixedIterations)
+        throw std::invalid_argument("device run(): only StopRule::fixed is on the hot path");
+    ConvergenceHistory h;
+    h.config = config;
+    h.precond = m.kind;
+    SolverState st = initialize(config, a, m, b, x0);
+    st.sync_host = false;
+    auto probe = [&]() {
+        IterationRecord rec;
+        rec.k = st.k;
+        double tr = 0.0;
+        detail::check(cgvk_solver_true_residual(st.device->h, &tr));
+        cgvk_scalars sc{};
+        detail::check(cgvk_solver_status(st.device->h, nullptr, &sc, nullptr));
+        rec.true_res_norm = tr;
+        rec.upd_res_norm = std::sqrt(sc.rr);
+        rec.alpha = st.alpha;
+        if (st.k >= 1) rec.beta = st.beta;
+        rec.nu = st.nu;
+        if (st.config.is_predictor() && st.k >= 1) rec.nu_prime = st.nu_prime;
+        h.records.push_back(rec);
+    };
+    const int budget = std::min(max_iter, stop.fixed_count);
+    const int cadence = probe_opts.cadence >= 1 ? probe_opts.cadence : 1;
+    if (probe_opts.enabled) probe();
+    while (st.status.running() && st.k < budget) {
+        const int chunk = probe_opts.enabled ? std::min(cadence, budget - st.k) : budget - st.k;
+        detail::check(cgvk_solver_step(st.device->h, chunk));
+        detail::check(cgvk_solver_sync(st.device->h));
+        st.refresh();
+        if (probe_opts.enabled) probe();
+    }
+    if (st.status.running()) st.status.state = SolveStatus::State::MaxIterations;
+    h.final_status = st.status;
+    return h;
+}
+
+}  // namespace cgv

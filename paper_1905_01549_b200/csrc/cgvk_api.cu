@@ -617,8 +617,23 @@ int ref_allocated(int v, bool prec) {
     return c;
 }
 
+// Pipeline kernels go out with programmatic stream serialization (PDL): each
+// may start its prologue (barrier init, matrix prefetch) while the previous
+// kernel drains, and synchronises with griddepcontrol.wait before reading its
+// results. CGVK_PDL=0 turns it off (for A/B measurements).
 void launch(cgvk_solver s, const KLaunch& L) {
-    L.fn<<<L.grid, L.threads, L.smem, s->stream>>>(s->P, L.S);
+    static const bool pdl = env_int("CGVK_PDL", 1) != 0;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(L.grid);
+    cfg.blockDim = dim3(L.threads);
+    cfg.dynamicSmemBytes = L.smem;
+    cfg.stream = s->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, L.fn, s->P, L.S);
 }
 
 void launch_iter(cgvk_solver s) {

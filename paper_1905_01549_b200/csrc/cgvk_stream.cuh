@@ -27,6 +27,7 @@ constexpr int kThreads = kBlock + 32;        // + producer warp
 constexpr int kMaxStages = 8;
 constexpr int kRpInts = kBlock + 4;          // row_ptr slice (257 used), padded to 16 B
 constexpr int kMaxVec = 12;
+constexpr bool kInTileGather = false;
 
 struct StageCfg {
     int nstage;     // ring depth
@@ -189,9 +190,24 @@ __device__ __forceinline__ void row_dot2(const RowRef& R, XF1 xf1, XF2 xf2, doub
 }
 
 // Per-row input accessors handed to Op::row: staged (shared memory) or direct.
+// in(v) = vector v at the thread's own row; in.gather(v, j, g) = vector v at
+// column j — from the stage when j lies in the tile (a stencil's +-1 and part
+// of its +-N neighbours), else from global g (L1/L2). Same bits either way.
 struct StagedIn {
-    const double* sv;
+    const double* sv;    // stage vectors + t
+    const double* base;  // stage vectors
+    int r0, rows;
     __device__ __forceinline__ double operator()(int v) const { return sv[v * kBlock]; }
+    // Measured on B200 (profiles/r01): serving in-tile columns from the stage
+    // is slower than L1 (divergent select + bank conflicts), so gathers always
+    // go through L1/L2; the stage path is kept for the in-tile experiment.
+    __device__ __forceinline__ double gather(int v, int j, const double* __restrict__ g) const {
+        if constexpr (kInTileGather) {
+            const unsigned o = static_cast<unsigned>(j - r0);
+            return o < static_cast<unsigned>(rows) ? base[v * kBlock + o] : __ldg(g + j);
+        }
+        return __ldg(g + j);
+    }
 };
 
 template <int NV>
@@ -199,6 +215,9 @@ struct DirectIn {
     const double* vp[NV > 0 ? NV : 1];  // by value: stays in registers
     int i;
     __device__ __forceinline__ double operator()(int v) const { return __ldg(vp[v] + i); }
+    __device__ __forceinline__ double gather(int, int j, const double* __restrict__ g) const {
+        return __ldg(g + j);
+    }
 };
 
 // Per-stage shared-memory layout.
@@ -238,6 +257,42 @@ struct PipeHeader {
     double red[kMaxDots * 32];
 };
 
+// Programmatic dependent launch: wait for the preceding kernel's results /
+// allow the next kernel to start its prologue.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Add expected bytes without arriving (the stage's single arrival comes later).
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+// Issue the CSR part of `tile` into `slot`: row_ptr slice, values, columns
+// (or mark the tile "direct" when it exceeds the stage capacity).
+__device__ __forceinline__ void stage_csr(const Params& P, const StageCfg& S, PipeHeader* H,
+                                          unsigned char* stages, int slot, int tile, uint64_t pol,
+                                          bool) {
+    StageView V = stage_view(stages, S, slot);
+    const int r0 = tile * kBlock;
+    const int rows = min(kBlock, P.n - r0);
+    const uint32_t rp_bytes = ((rows + 1) * 4 + 15) & ~15;
+    const int k0 = __ldg(P.rp + r0), k1 = __ldg(P.rp + r0 + rows);
+    const int k0a = k0 & ~1, k0c = k0 & ~3;
+    const bool direct = k1 - k0c + 4 > S.cap;
+    const uint32_t va_bytes = direct ? 0u : (((k1 - k0a) * 8 + 15) & ~15);
+    const uint32_t ci_bytes = direct ? 0u : (((k1 - k0c) * 4 + 15) & ~15);
+    H->k0a[slot] = k0a;
+    H->k0c[slot] = k0c;
+    H->direct[slot] = direct;
+    mbar_expect_tx_only(&H->full[slot], rp_bytes + va_bytes + ci_bytes);
+    bulk_g2s(V.rp, P.rp + r0, rp_bytes, &H->full[slot], pol);
+    if (!direct) {
+        bulk_g2s(V.va, P.va + k0a, va_bytes, &H->full[slot], pol);
+        bulk_g2s(V.ci, P.ci + k0c, ci_bytes, &H->full[slot], pol);
+    }
+}
+
 // ---------------------------------------------------------------- driver
 //
 // Op contract (all device members):
@@ -253,10 +308,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(Params P, StageCfg S) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PipeHeader* H = reinterpret_cast<PipeHeader*>(smem_raw);
     unsigned char* stages = smem_raw + ((sizeof(PipeHeader) + 127) / 128) * 128;
-    Op op;
-    if (!op.enter(P)) return;  // uniform over the grid
     const int Gv = S.gvirt, Gp = gridDim.x, ntiles = P.ntiles, NS = S.nstage;
     const int warp = threadIdx.x >> 5;
+    const bool producer = threadIdx.x == kConsumers;  // lane 0 of the producer warp
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) {
             mbar_init(&H->full[s], 1);
@@ -266,9 +320,33 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(Params P, StageCfg S) {
     }
     __syncthreads();
 
+    // The matrix does not depend on the previous kernel: under programmatic
+    // dependent launch the producer streams A for its first NS tiles while
+    // that kernel is still finishing, then waits for it.
+    uint64_t pol = 0;
+    int npre = 0;
+    if (Op::CSR && producer) {
+        pol = evict_first_policy();
+        for (int vb = blockIdx.x; vb < Gv && npre < NS; vb += Gp)
+            for (int tile = vb; tile < ntiles && npre < NS; tile += Gv, ++npre)
+                stage_csr(P, S, H, stages, npre, tile, pol, /*arrive=*/false);
+    }
+    pdl_wait();
+    pdl_trigger();
+    Op op;
+    if (!op.enter(P)) {  // uniform over the grid
+        if (producer) {  // drain the prefetch before the CTA exits
+            for (int q = 0; q < npre; ++q) {
+                mbar_arrive(&H->full[q]);
+                mbar_wait(&H->full[q], 0);
+            }
+        }
+        return;
+    }
+
     if (warp == kWarps) {  // ------------------------------ producer warp
-        if ((threadIdx.x & 31) != 0) return;
-        const uint64_t pol = evict_first_policy();
+        if (!producer) return;
+        if (!Op::CSR) pol = evict_first_policy();
         const double* vp[kMaxVec];
 #pragma unroll
         for (int v = 0; v < Op::NV; ++v) vp[v] = op.vec(P, v);
@@ -280,37 +358,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(Params P, StageCfg S) {
                 StageView V = stage_view(stages, S, slot);
                 const int r0 = tile * kBlock;
                 const int rows = min(kBlock, P.n - r0);
-                uint32_t bytes = 0;
-                const uint32_t rp_bytes = ((rows + 1) * 4 + 15) & ~15;
-                int k0a = 0, k0c = 0, direct = 1;
-                uint32_t va_bytes = 0, ci_bytes = 0;
-                if (Op::CSR) {
-                    bytes += rp_bytes;
-                    const int k0 = __ldg(P.rp + r0), k1 = __ldg(P.rp + r0 + rows);
-                    k0a = k0 & ~1;
-                    k0c = k0 & ~3;
-                    if (k1 - k0c + 4 <= S.cap) {
-                        direct = 0;
-                        va_bytes = ((k1 - k0a) * 8 + 15) & ~15;
-                        ci_bytes = ((k1 - k0c) * 4 + 15) & ~15;
-                        bytes += va_bytes + ci_bytes;
-                    }
-                }
+                if (Op::CSR && j >= npre) stage_csr(P, S, H, stages, slot, tile, pol, false);
                 const uint32_t vec_bytes = (rows * 8 + 15) & ~15;
+                uint32_t bytes = 0;
 #pragma unroll
                 for (int v = 0; v < Op::NV; ++v)
                     if (vp[v]) bytes += vec_bytes;
-                H->k0a[slot] = k0a;
-                H->k0c[slot] = k0c;
-                H->direct[slot] = direct;
-                mbar_expect_tx(&H->full[slot], bytes);
-                if (Op::CSR) {
-                    bulk_g2s(V.rp, P.rp + r0, rp_bytes, &H->full[slot], pol);
-                    if (!direct) {
-                        bulk_g2s(V.va, P.va + k0a, va_bytes, &H->full[slot], pol);
-                        bulk_g2s(V.ci, P.ci + k0c, ci_bytes, &H->full[slot], pol);
-                    }
-                }
+                mbar_expect_tx(&H->full[slot], bytes);  // + this thread's arrival
 #pragma unroll
                 for (int v = 0; v < Op::NV; ++v)
                     if (vp[v]) bulk_g2s(V.vec + v * kBlock, vp[v] + r0, vec_bytes, &H->full[slot], pol);
@@ -344,7 +398,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(Params P, StageCfg S) {
                         R.ci = V.ci + (b - H->k0c[slot]);
                     }
                 }
-                op.row(P, i, StagedIn{V.vec + t}, R, acc);
+                const int r0 = tile * kBlock;
+                op.row(P, i, StagedIn{V.vec + t, V.vec, r0, min(kBlock, P.n - r0)}, R, acc);
             }
             __syncwarp();
             if ((t & 31) == 0) mbar_arrive(&H->empty[slot]);
@@ -390,6 +445,8 @@ template <class Op>
 __global__ void __launch_bounds__(kBlock, 3) k_direct(Params P, StageCfg S) {
     __shared__ double red[kMaxDots * 32];
     __shared__ int last_flag;
+    pdl_wait();
+    pdl_trigger();
     Op op;
     if (!op.enter(P)) return;
     const int Gv = S.gvirt, Gp = gridDim.x, ntiles = P.ntiles;

@@ -115,7 +115,10 @@ struct HsK2 {
         const double* __restrict__ pg = pold;
         const double b = beta;
         const double sum =
-            row_dot(R, [&](int j) { return ADD(Mg<PREC>(P, j, __ldg(r + j)), MUL(b, __ldg(pg + j))); });
+            row_dot(R, [&](int j) {
+                const double rj = in.gather(1, j, r);
+                return ADD(PREC ? MUL(in.gather(3, j, P.d), rj) : rj, MUL(b, in.gather(0, j, pg)));
+            });
         const double pi = ADD(PREC ? MUL(SV(3), SV(1)) : SV(1), MUL(b, po));
         pnew[i] = pi;
         P.s[i] = sum;
@@ -206,7 +209,10 @@ struct CgK2 {
     template <class In>
     __device__ void row(const Params& P, int i, const In& in, const RowRef& R, double* acc) const {
         const double* __restrict__ r = P.r;
-        const double w = row_dot(R, [&](int j) { return Mg<PREC>(P, j, __ldg(r + j)); });
+        const double w = row_dot(R, [&](int j) {
+            const double rj = in.gather(0, j, r);
+            return PREC ? MUL(in.gather(1, j, P.d), rj) : rj;
+        });
         P.w[i] = w;
         const double ri = SV(0), rti = PREC ? MUL(SV(1), ri) : ri;
         acc[0] = ADD(acc[0], MUL(rti, ri));
@@ -324,7 +330,7 @@ struct PrK2 {
     template <class In>
     __device__ void row(const Params& P, int i, const In& in, const RowRef& R, double* acc) const {
         const double* __restrict__ p = P.p0;
-        const double s = row_dot(R, [&](int j) { return __ldg(p + j); });
+        const double s = row_dot(R, [&](int j) { return in.gather(0, j, p); });
         P.s[i] = s;
         const double st = PREC ? MUL(SV(3), s) : s;
         const double r = SV(1);
@@ -471,19 +477,22 @@ struct GvK1 {
     }
 };
 
-// t = A M w (streams: A only)
+// t = A M w (streams: A, w [d] — staged for the in-tile gathers)
 template <bool PREC>
 struct GvK2 {
-    static constexpr int NV = 0, ND = 0;
+    static constexpr int NV = kInTileGather ? (PREC ? 2 : 1) : 0, ND = 0;
     static constexpr bool CSR = true;
     __device__ bool enter(const Params& P) { return P.ctrl->mode2 != MODE_SKIP; }
-    __device__ const double* vec(const Params&, int) const { return nullptr; }
+    __device__ const double* vec(const Params& P, int v) const { return v == 0 ? P.w : P.d; }
     __device__ int sync() const { return 1; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
     template <class In>
-    __device__ void row(const Params& P, int i, const In&, const RowRef& R, double*) const {
+    __device__ void row(const Params& P, int i, const In& in, const RowRef& R, double*) const {
         const double* __restrict__ w = P.w;
-        P.t[i] = row_dot(R, [&](int j) { return Mg<PREC>(P, j, __ldg(w + j)); });
+        P.t[i] = row_dot(R, [&](int j) {
+            const double wj = in.gather(0, j, w);
+            return PREC ? MUL(in.gather(1, j, P.d), wj) : wj;
+        });
     }
     __device__ void finish(const Params&, Ctrl* c, const double*) const { c->mode2 = MODE_SKIP; }
 };
@@ -615,26 +624,34 @@ struct PprK1 {
 };
 
 // (u, w) = A (s~, r~) in one traversal, or u = A s~ with recompute_w off
-// (streams: A only)
+// (streams: A, s~ r~ — staged for the in-tile gathers)
 template <bool PREC>
 struct PprK2 {
-    static constexpr int NV = 0, ND = 0;
+    static constexpr int NV = kInTileGather ? 2 : 0, ND = 0;
     static constexpr bool CSR = true;
-    __device__ bool enter(const Params& P) { return P.ctrl->mode2 != MODE_SKIP; }
-    __device__ const double* vec(const Params&, int) const { return nullptr; }
+    bool recw;
+    __device__ bool enter(const Params& P) {
+        recw = P.recompute_w != 0;
+        return P.ctrl->mode2 != MODE_SKIP;
+    }
+    __device__ const double* vec(const Params& P, int v) const {
+        if (v == 0) return PREC ? P.st : P.s;
+        return recw ? (PREC ? P.rt : P.r) : nullptr;
+    }
     __device__ int sync() const { return 1; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
     template <class In>
-    __device__ void row(const Params& P, int i, const In&, const RowRef& R, double*) const {
+    __device__ void row(const Params& P, int i, const In& in, const RowRef& R, double*) const {
         const double* __restrict__ sv_ = PREC ? P.st : P.s;
         const double* __restrict__ rv = PREC ? P.rt : P.r;
-        if (P.recompute_w) {
+        if (recw) {
             double u, w;
-            row_dot2(R, [&](int j) { return __ldg(sv_ + j); }, [&](int j) { return __ldg(rv + j); }, u, w);
+            row_dot2(R, [&](int j) { return in.gather(0, j, sv_); },
+                     [&](int j) { return in.gather(1, j, rv); }, u, w);
             P.u[i] = u;
             P.w[i] = w;
         } else {
-            P.u[i] = row_dot(R, [&](int j) { return __ldg(sv_ + j); });
+            P.u[i] = row_dot(R, [&](int j) { return in.gather(0, j, sv_); });
         }
     }
     __device__ void finish(const Params&, Ctrl* c, const double*) const { c->mode2 = MODE_SKIP; }
