@@ -40,10 +40,14 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 VARIANTS = ["hs", "cg", "m", "pr", "gv", "pipe-pr"]
-# App. A vector traffic per kernel launch (n-length fp64 vectors), Jacobi /
-# none: (update kernel K1, SpMV kernel K2). K2 additionally streams A once.
+# Algorithmic vector traffic per kernel launch (n-length fp64 vectors), Jacobi
+# / none: (update kernel K1, SpMV kernel K2); K2 additionally streams A once.
+# Iteration totals are SURVEY App. A's minimum V (HS 11, CG 13, M/PR 15, GV 21,
+# pipe 19). HS stores r~ in K1 and gathers it in K2 (same total as App. A's
+# split 4+7); CG and GV also store their gathered r~ / w~ (one extra write
+# each) — counted as overhead, not work.
 KERNEL_VECTORS = {
-    "hs": {True: (4, 7), False: (3, 6)},
+    "hs": {True: (5, 6), False: (3, 6)},
     "cg": {True: (10, 3), False: (8, 3)},
     "m": {True: (10, 5), False: (6, 4)},
     "pr": {True: (10, 5), False: (6, 4)},

@@ -153,8 +153,8 @@ int cgvk_precond_apply(cgvk_matrix a, int kind, const double* in, double* out);
  * (reproduced bit-for-bit by oracle/cgv_oracle.c ORC_DOT_TREE). */
 int cgvk_dot(cgvk_matrix a, const double* x, const double* y, double* out);
 /* The reduction-tree parameters the oracle needs: rows per tile (= threads
- * per CTA) and the CTA cap G. */
-int cgvk_reduction_config(cgvk_matrix a, int* block, int* gmax);
+ * per CTA), the CTA cap G and the tile order (0 strided, 1 contiguous). */
+int cgvk_reduction_config(cgvk_matrix a, int* block, int* gmax, int* order);
 
 /* initialize() (inc/variants.hpp:149-150, src/variants.cpp:354-444). The
  * status may already be terminal (zero initial residual, nu0/mu0 <= 0). */

@@ -43,7 +43,8 @@ static double block_tree(double* v, int block) {
     return wsum[0];
 }
 
-static double dot_tree(int64_t n, const double* x, const double* y, int block, int gmax) {
+static double dot_tree(int64_t n, const double* x, const double* y, int block, int gmax,
+                       int order) {
     const int64_t ntiles = (n + block - 1) / block;
     if (ntiles == 0) return 0.0;
     const int64_t G = ntiles < gmax ? ntiles : gmax;
@@ -51,10 +52,14 @@ static double dot_tree(int64_t n, const double* x, const double* y, int block, i
     double* v = (double*)malloc(sizeof(double) * (size_t)block);
     for (int64_t b = 0; b < G; ++b) {
         /* thread t of CTA b: sequential sum over rows tile*block+t of its
-         * tiles b, b+G, b+2G, ... (rows >= n contribute nothing) */
+         * tiles — b, b+G, b+2G, ... (order 0) or the contiguous block
+         * [b*ntiles/G, (b+1)*ntiles/G) (order 1); rows >= n add nothing */
+        const int64_t lo = order ? b * ntiles / G : b;
+        const int64_t hi = order ? (b + 1) * ntiles / G : ntiles;
+        const int64_t step = order ? 1 : G;
         for (int t = 0; t < block; ++t) {
             double acc = 0.0;
-            for (int64_t tile = b; tile < ntiles; tile += G) {
+            for (int64_t tile = lo; tile < hi; tile += step) {
                 const int64_t row = tile * block + t;
                 if (row < n) acc = acc + x[row] * y[row];
             }
@@ -75,11 +80,11 @@ static double dot_tree(int64_t n, const double* x, const double* y, int block, i
 
 double orc_dot(int64_t n, const double* x, const double* y, const orc_dotcfg* cfg) {
     if (!cfg || cfg->mode == ORC_DOT_SEQ) return dot_seq(n, x, y);
-    if (cfg->mode == ORC_DOT_TREE) return dot_tree(n, x, y, cfg->block, cfg->gmax);
+    if (cfg->mode == ORC_DOT_TREE) return dot_tree(n, x, y, cfg->block, cfg->gmax, cfg->order);
     double acc = 0.0; /* rank-ordered sum of per-block trees */
     for (int p = 0; p < cfg->nparts; ++p) {
         const int64_t lo = cfg->part_lo[p], hi = cfg->part_lo[p + 1];
-        acc = acc + dot_tree(hi - lo, x + lo, y + lo, cfg->block, cfg->gmax);
+        acc = acc + dot_tree(hi - lo, x + lo, y + lo, cfg->block, cfg->gmax, cfg->order);
     }
     return acc;
 }

@@ -11,7 +11,8 @@
  *   ORC_DOT_SEQ   left-to-right, exactly inc/vector_ops.hpp:20-25 (the reference)
  *   ORC_DOT_TREE  the GPU's canonical reduction tree: tiles of
  *                 `block` rows, one row per thread; thread t of CTA b sums its
- *                 rows of tiles b, b+G, b+2G, ... sequentially; a warp
+ *                 rows of the contiguous tiles [b*T/G, (b+1)*T/G) (T tiles,
+ *                 G = min(gmax, T)) sequentially; a warp
  *                 shfl_down tree (16,8,4,2,1) and a cross-warp tree give the
  *                 CTA partial; the last CTA sums partials j = t mod block
  *                 sequentially per thread and applies the same block tree.
@@ -36,6 +37,7 @@ typedef struct orc_dotcfg {
     int gmax;              /* CTA count cap; G = min(gmax, ntiles) */
     int nparts;            /* ORC_DOT_PART only */
     const int64_t* part_lo; /* nparts+1 row offsets */
+    int order;             /* tile order: 0 strided (b, b+G, ...), 1 contiguous blocks */
 } orc_dotcfg;
 
 typedef struct orc_solver orc_solver;

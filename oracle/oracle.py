@@ -27,7 +27,7 @@ SCALAR_NAMES = ("alpha", "beta", "nu", "nu_prime", "mu", "delta", "delta_hat", "
 
 class _DotCfg(C.Structure):
     _fields_ = [("mode", C.c_int), ("block", C.c_int), ("gmax", C.c_int), ("nparts", C.c_int),
-                ("part_lo", C.c_void_p)]
+                ("part_lo", C.c_void_p), ("order", C.c_int)]
 
 
 def _f64(a):
@@ -281,13 +281,15 @@ def make_dotcfg(dot):
     parts = None
     if dot == "seq":
         cfg.mode = DOT_SEQ
-    elif dot[0] == "tree":
+    elif dot[0] == "tree":  # ("tree", block, gmax[, order])
         cfg.mode, cfg.block, cfg.gmax = DOT_TREE, dot[1], dot[2]
-    else:
+        cfg.order = dot[3] if len(dot) > 3 else 0
+    else:  # ("part", block, gmax, part_lo[, order])
         parts = _i64(dot[3])
         cfg.mode, cfg.block, cfg.gmax = DOT_PART, dot[1], dot[2]
         cfg.nparts = parts.shape[0] - 1
         cfg.part_lo = parts.ctypes.data
+        cfg.order = dot[4] if len(dot) > 4 else 0
     return cfg, parts
 
 

@@ -146,7 +146,7 @@ def _load() -> C.CDLL:
         "cgvk_jacobi": (I, [P, P]),
         "cgvk_precond_apply": (I, [P, I, P, P]),
         "cgvk_dot": (I, [P, P, P, C.POINTER(D)]),
-        "cgvk_reduction_config": (I, [P, C.POINTER(I), C.POINTER(I)]),
+        "cgvk_reduction_config": (I, [P, C.POINTER(I), C.POINTER(I), C.POINTER(I)]),
         "cgvk_solver_create": (I, [P, C.POINTER(_Config), I, P, P, pp]),
         "cgvk_solver_destroy": (I, [P]),
         "cgvk_solver_set_tolerance": (I, [P, D]),
@@ -326,10 +326,11 @@ class DeviceMatrix:
         _check(_lib.cgvk_dot(self._h, _ptr(x), _ptr(y), C.byref(out)))
         return out.value
 
-    def reduction_config(self) -> tuple[int, int]:
-        b, g = C.c_int(), C.c_int()
-        _check(_lib.cgvk_reduction_config(self._h, C.byref(b), C.byref(g)))
-        return b.value, g.value
+    def reduction_config(self) -> tuple[int, int, int]:
+        """(rows per tile, CTA cap G, tile order) of the canonical dot tree."""
+        b, g, o = C.c_int(), C.c_int(), C.c_int()
+        _check(_lib.cgvk_reduction_config(self._h, C.byref(b), C.byref(g), C.byref(o)))
+        return b.value, g.value, o.value
 
 
 @dataclass

@@ -48,6 +48,12 @@ int set_err(int code, const char* fmt, ...) {
 
 constexpr int kMaxStageCap = 12288;  // CSR entries per stage (tiles above: direct loads)
 
+// Experiment knobs (environment, read at matrix/solver creation).
+int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+
 int grid_elem(int64_t n) {
     int64_t g = (n + 255) / 256;
     if (g > 148 * 16) g = 148 * 16;
@@ -75,6 +81,8 @@ struct cgvk_matrix_s {
     int64_t n = 0, nnz = 0;
     int ntiles = 0, gmax = 0, G = 1, sms = 0;
     int cap = 4;  // CSR entries a pipeline stage holds (max over tiles, capped)
+    int order = 0;  // canonical tile order (fixed per matrix; reported to the oracle)
+    int l2pol = 0;  // TMA L2 policy for the pipeline streams
     int* rp = nullptr;
     int* ci = nullptr;
     double* va = nullptr;
@@ -104,6 +112,8 @@ struct cgvk_matrix_s {
         P.sell_ptr = sell_ptr;
         P.sell_va = sell_va;
         P.sell_ci = sell_ci;
+        P.order = order;
+        P.l2pol = l2pol;
         return P;
     }
 };
@@ -138,6 +148,7 @@ int run_dots(cgvk_matrix a, cudaStream_t stream, double* part, unsigned int* cou
     DotArgs A{};
     A.n = (int)a->n;
     A.ntiles = a->ntiles;
+    A.order = a->order;
     for (int q = 0; q < nd; ++q) {
         A.x[q] = xs[q];
         A.y[q] = ys[q];
@@ -275,6 +286,8 @@ int cgvk_matrix_create_csr(int64_t n, const int64_t* row_ptr, const int64_t* col
     a->n = n;
     a->nnz = nnz;
     a->ntiles = (int)((n + kBlock - 1) / kBlock);
+    a->order = env_int("CGVK_ORDER", 0) ? 1 : 0;
+    a->l2pol = env_int("CGVK_L2POL", 0);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     a->sms = sms;
@@ -378,10 +391,11 @@ int cgvk_matrix_info(cgvk_matrix a, int64_t* n, int64_t* nnz, int* device) {
     return CGVK_OK;
 }
 
-int cgvk_reduction_config(cgvk_matrix a, int* block, int* gmax) {
+int cgvk_reduction_config(cgvk_matrix a, int* block, int* gmax, int* order) {
     if (!a) return set_err(CGVK_EINVAL, "null matrix");
-    *block = kBlock;
-    *gmax = a->gmax;
+    if (block) *block = kBlock;
+    if (gmax) *gmax = a->gmax;
+    if (order) *order = a->order;
     return CGVK_OK;
 }
 
@@ -523,11 +537,6 @@ int balanced_grid(int Gv, int cap) {
 // Tuning knobs (read once per solver; for experiments): CGVK_SPMV_ENGINE =
 // staged (default) | sell, CGVK_NSTAGE = ring depth, CGVK_SMEM_CTAS = CTAs per
 // SM the stage budget targets.
-int env_int(const char* name, int dflt) {
-    const char* v = getenv(name);
-    return v && *v ? atoi(v) : dflt;
-}
-
 bool spmv_sell() {
     const char* v = getenv("CGVK_SPMV_ENGINE");
     return v && strcmp(v, "sell") == 0;
@@ -561,6 +570,7 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
     int ns = (budget - header) / S.stage_bytes;
     if (ns < 2) ns = 2;
     if (ns > 6) ns = 6;
+    if (StagesOf<Op>::value >= 2 && StagesOf<Op>::value < ns) ns = StagesOf<Op>::value;
     const int forced = env_int(Op::CSR ? "CGVK_NSTAGE_SPMV" : "CGVK_NSTAGE", 0);
     if (forced >= 2 && forced <= kMaxStages) ns = forced;
     S.nstage = ns;
@@ -696,8 +706,7 @@ int solver_init(cgvk_solver s, const double* b, const double* x0) {
     const int64_t n = s->n;
     const int v = s->cfg.variant;
     const bool prec = s->prec;
-    const bool stores_rt = prec && (v == CGVK_M || v == CGVK_PR || v == CGVK_GV ||
-                                    v == CGVK_PIPE_PR || v == CGVK_PIPE_PR_M);
+    const bool stores_rt = prec;  // every variant keeps r~ in a buffer when preconditioned
     const bool needs_st = prec && v != CGVK_HS && v != CGVK_CG_CG;
     const bool pipe = v == CGVK_PIPE_PR || v == CGVK_PIPE_PR_M;
     Ctrl c{};
@@ -874,10 +883,9 @@ int cgvk_solver_create(cgvk_matrix a, const cgvk_variant_config* cfg, int precon
     if ((v == CGVK_CG_CG || v == CGVK_GV || pipe) && (rc = dalloc(&s->w, nv))) return bail(rc);
     if ((v == CGVK_GV || pipe) && (rc = dalloc(&s->u, nv))) return bail(rc);
     if (v == CGVK_GV && (rc = dalloc(&s->t, nv))) return bail(rc);
-    if (s->prec && (v == CGVK_M || v == CGVK_PR || v == CGVK_GV || pipe) && (rc = dalloc(&s->rt, nv)))
-        return bail(rc);
+    if (s->prec && (rc = dalloc(&s->rt, nv))) return bail(rc);
     if (s->prec && (v == CGVK_GV || pipe) && (rc = dalloc(&s->st, nv))) return bail(rc);
-    if (s->prec && pipe && (rc = dalloc(&s->wt, nv))) return bail(rc);
+    if (s->prec && (v == CGVK_GV || pipe) && (rc = dalloc(&s->wt, nv))) return bail(rc);
     if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess)
         return bail(set_err(CGVK_ECUDA, "stream create failed"));
     for (double* p : {s->x, s->r, s->p0, s->p1, s->s, s->w, s->u, s->t, s->rt, s->st, s->wt, s->tmp})

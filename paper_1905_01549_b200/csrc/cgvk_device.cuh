@@ -77,7 +77,31 @@ struct Params {
     double* hist;  // rr per iteration
     Ctrl* ctrl;
     int nu_expr, recompute_nu, recompute_w, unsimplified_mu, track_delta;
+    int order;  // canonical tile order (see CGVK_FOR_VB)
+    int l2pol;  // TMA L2 policy: 0 evict_first everything, 1 only the matrix, 2 none
 };
+
+// Balanced contiguous partition: part k of `parts` covers [lo(k), lo(k+1)).
+// Canonical order: virtual CTA vb owns tiles [lo(vb; ntiles, Gv), lo(vb+1));
+// a physical CTA p runs virtual CTAs [lo(p; Gv, Gp), lo(p+1)) — neighbouring
+// rows stay on one SM, so stencil x-gathers hit L1.
+__host__ __device__ __forceinline__ int span_lo(int k, int total, int parts) {
+    return static_cast<int>(static_cast<long long>(k) * total / parts);
+}
+
+// Tile orders (the oracle's orc_dotcfg.order): 0 strided — virtual CTA vb
+// owns tiles vb, vb+Gv, ..., physical CTA p runs vb = p, p+Gp, ...; 1
+// contiguous — the span_lo blocks above.
+#define CGVK_FOR_VB(vb, order, p, Gv, Gp)                                              \
+    for (int vb = (order) ? span_lo((p), (Gv), (Gp)) : (p),                            \
+             vb##_end = (order) ? span_lo((p) + 1, (Gv), (Gp)) : (Gv),                  \
+             vb##_step = (order) ? 1 : (Gp);                                            \
+         vb < vb##_end; vb += vb##_step)
+#define CGVK_FOR_TILE(tile, order, vb, ntiles, Gv)                                     \
+    for (int tile = (order) ? span_lo((vb), (ntiles), (Gv)) : (vb),                    \
+             tile##_end = (order) ? span_lo((vb) + 1, (ntiles), (Gv)) : (ntiles),       \
+             tile##_step = (order) ? 1 : (Gv);                                          \
+         tile < tile##_end; tile += tile##_step)
 
 __device__ __forceinline__ double MUL(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double ADD(double a, double b) { return __dadd_rn(a, b); }

@@ -128,7 +128,7 @@ __global__ void k_scale(int n, const double* __restrict__ d, const double* __res
 }
 
 struct DotArgs {
-    int n, ntiles;
+    int n, ntiles, order;
     const double* x[4];
     const double* y[4];
     int dx[4];  // multiply x by d on the fly
@@ -144,7 +144,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSM) k_dots(DotArgs A) {
     double acc[ND], tot[ND];
 #pragma unroll
     for (int q = 0; q < ND; ++q) acc[q] = 0.0;
-    for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
+    // one CTA per virtual CTA (canonical order)
+    CGVK_FOR_TILE(tile, A.order, static_cast<int>(blockIdx.x), A.ntiles, static_cast<int>(gridDim.x)) {
         const int i = tile * kBlock + threadIdx.x;
         if (i >= A.n) continue;
 #pragma unroll

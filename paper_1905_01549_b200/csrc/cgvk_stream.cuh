@@ -20,6 +20,8 @@
 
 #include "cgvk_device.cuh"
 
+#include <type_traits>
+
 namespace cgvk {
 
 constexpr int kConsumers = kBlock;           // 8 warps, one row each
@@ -27,6 +29,16 @@ constexpr int kThreads = kBlock + 32;        // + producer warp
 constexpr int kMaxStages = 8;
 constexpr int kRpInts = kBlock + 4;          // row_ptr slice (257 used), padded to 16 B
 constexpr int kMaxVec = 12;
+
+// Optional per-Op ring-depth hint: `static constexpr int STAGES`.
+template <class T, class = void>
+struct StagesOf {
+    static constexpr int value = 0;
+};
+template <class T>
+struct StagesOf<T, std::void_t<decltype(T::STAGES)>> {
+    static constexpr int value = T::STAGES;
+};
 constexpr bool kInTileGather = false;
 
 struct StageCfg {
@@ -68,6 +80,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // both addresses 16-byte aligned). Streams are read once: evict-first in L2.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                          uint64_t policy) {
+    if (policy == 0) {  // default L2 policy
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(dst)),
+            "l"(src), "r"(bytes), "r"(smem_u32(bar))
+            : "memory");
+        return;
+    }
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
             smem_u32(dst)),
@@ -257,6 +277,30 @@ struct PipeHeader {
     double red[kMaxDots * 32];
 };
 
+// Last CTA: thread t sums partials q = t, t+256, ... in that order (the
+// canonical fold); all loads are issued before the in-order adds so the fold
+// costs one L2 latency, not Gv/256 of them.
+constexpr int kFoldMax = 8;  // Gv <= 256 * 8
+template <int ND>
+__device__ __noinline__ void fold_partials(const double* part, int Gv, int t, double (&tot)[ND]) {
+    for (int q0 = 0; q0 < Gv; q0 += kConsumers * kFoldMax) {
+        double buf[kFoldMax][ND];
+#pragma unroll
+        for (int u = 0; u < kFoldMax; ++u) {
+            const int q = q0 + t + u * kConsumers;
+#pragma unroll
+            for (int d = 0; d < ND; ++d) buf[u][d] = q < Gv ? __ldcg(part + d * Gv + q) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kFoldMax; ++u) {
+            if (q0 + t + u * kConsumers < Gv) {
+#pragma unroll
+                for (int d = 0; d < ND; ++d) tot[d] = ADD(tot[d], buf[u][d]);
+            }
+        }
+    }
+}
+
 // Programmatic dependent launch: wait for the preceding kernel's results /
 // allow the next kernel to start its prologue.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -326,10 +370,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(Params P, StageCfg S) {
     uint64_t pol = 0;
     int npre = 0;
     if (Op::CSR && producer) {
-        pol = evict_first_policy();
-        for (int vb = blockIdx.x; vb < Gv && npre < NS; vb += Gp)
-            for (int tile = vb; tile < ntiles && npre < NS; tile += Gv, ++npre)
-                stage_csr(P, S, H, stages, npre, tile, pol, /*arrive=*/false);
+        pol = P.l2pol < 2 ? evict_first_policy() : 0;
+        CGVK_FOR_VB(vb, P.order, blockIdx.x, Gv, Gp) {
+            CGVK_FOR_TILE(tile, P.order, vb, ntiles, Gv) {
+                if (npre == NS) break;
+                stage_csr(P, S, H, stages, npre++, tile, pol, /*arrive=*/false);
+            }
+            if (npre == NS) break;
+        }
     }
     pdl_wait();
     pdl_trigger();
@@ -346,13 +394,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(Params P, StageCfg S) {
 
     if (warp == kWarps) {  // ------------------------------ producer warp
         if (!producer) return;
-        if (!Op::CSR) pol = evict_first_policy();
+        if (!Op::CSR) pol = P.l2pol < 2 ? evict_first_policy() : 0;
         const double* vp[kMaxVec];
 #pragma unroll
         for (int v = 0; v < Op::NV; ++v) vp[v] = op.vec(P, v);
         int j = 0;
-        for (int vb = blockIdx.x; vb < Gv; vb += Gp) {
-            for (int tile = vb; tile < ntiles; tile += Gv, ++j) {
+        const uint64_t vpol = P.l2pol == 0 ? pol : 0;
+        CGVK_FOR_VB(vb, P.order, blockIdx.x, Gv, Gp) {
+            CGVK_FOR_TILE(tile, P.order, vb, ntiles, Gv) {
                 const int slot = j % NS;
                 if (j >= NS) mbar_wait(&H->empty[slot], ((j / NS) - 1) & 1);
                 StageView V = stage_view(stages, S, slot);
@@ -367,7 +416,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(Params P, StageCfg S) {
                 mbar_expect_tx(&H->full[slot], bytes);  // + this thread's arrival
 #pragma unroll
                 for (int v = 0; v < Op::NV; ++v)
-                    if (vp[v]) bulk_g2s(V.vec + v * kBlock, vp[v] + r0, vec_bytes, &H->full[slot], pol);
+                    if (vp[v]) bulk_g2s(V.vec + v * kBlock, vp[v] + r0, vec_bytes, &H->full[slot], vpol);
+                ++j;
             }
         }
         return;
@@ -377,12 +427,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(Params P, StageCfg S) {
     const int t = threadIdx.x;
     double acc[Op::ND > 0 ? Op::ND : 1];
     int j = 0;
-    for (int vb = blockIdx.x; vb < Gv; vb += Gp) {
+    CGVK_FOR_VB(vb, P.order, blockIdx.x, Gv, Gp) {
 #pragma unroll
         for (int d = 0; d < Op::ND; ++d) acc[d] = 0.0;
-        for (int tile = vb; tile < ntiles; tile += Gv, ++j) {
-            const int slot = j % NS;
-            mbar_wait(&H->full[slot], (j / NS) & 1);
+        CGVK_FOR_TILE(tile, P.order, vb, ntiles, Gv) {
+            const int jj = j++;
+            const int slot = jj % NS;
+            mbar_wait(&H->full[slot], (jj / NS) & 1);
             StageView V = stage_view(stages, S, slot);
             const int i = tile * kBlock + t;
             if (i < P.n) {
@@ -421,11 +472,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(Params P, StageCfg S) {
 #pragma unroll
     for (int d = 0; d < Op::ND; ++d) tot[d] = 0.0;
     if (mode == 2) {
-        for (int q = t; q < Gv; q += kConsumers) {
-#pragma unroll
-            for (int d = 0; d < Op::ND; ++d) tot[d] = ADD(tot[d], __ldcg(P.part + d * Gv + q));
+        if constexpr (Op::ND > 0) {
+            fold_partials<Op::ND>(P.part, Gv, t, tot);
+            cta_tree_c<Op::ND>(tot, H->red);
         }
-        if constexpr (Op::ND > 0) cta_tree_c<Op::ND>(tot, H->red);
     }
     if (t == 0) {
         *counter = 0u;
@@ -455,10 +505,10 @@ __global__ void __launch_bounds__(kBlock, 3) k_direct(Params P, StageCfg S) {
 #pragma unroll
     for (int v = 0; v < Op::NV; ++v) in.vp[v] = op.vec(P, v);
     double acc[Op::ND > 0 ? Op::ND : 1];
-    for (int vb = blockIdx.x; vb < Gv; vb += Gp) {
+    CGVK_FOR_VB(vb, P.order, blockIdx.x, Gv, Gp) {
 #pragma unroll
         for (int d = 0; d < Op::ND; ++d) acc[d] = 0.0;
-        for (int tile = vb; tile < ntiles; tile += Gv) {
+        CGVK_FOR_TILE(tile, P.order, vb, ntiles, Gv) {
             const int i = tile * kBlock + t;
             const int slice = i >> 5;
             RowRef R;
@@ -494,11 +544,10 @@ __global__ void __launch_bounds__(kBlock, 3) k_direct(Params P, StageCfg S) {
 #pragma unroll
     for (int d = 0; d < Op::ND; ++d) tot[d] = 0.0;
     if (mode == 2) {
-        for (int q = t; q < Gv; q += kBlock) {
-#pragma unroll
-            for (int d = 0; d < Op::ND; ++d) tot[d] = ADD(tot[d], __ldcg(P.part + d * Gv + q));
+        if constexpr (Op::ND > 0) {
+            fold_partials<Op::ND>(P.part, Gv, t, tot);
+            cta_tree<Op::ND>(tot, red);
         }
-        if constexpr (Op::ND > 0) cta_tree<Op::ND>(tot, red);
     }
     if (t == 0) {
         *counter = 0u;

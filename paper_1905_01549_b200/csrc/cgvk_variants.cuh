@@ -59,7 +59,11 @@ struct HsK1 {
     __device__ void row(const Params& P, int i, const In& in, const RowRef&, double* acc) const {
         const double r = SUB(SV(0), MUL(alpha, SV(1)));
         P.r[i] = r;
-        const double rt = PREC ? MUL(SV(2), r) : r;
+        double rt = r;
+        if constexpr (PREC) {  // r~ = M r stored for K2 (its gather and own-row read)
+            rt = MUL(SV(2), r);
+            P.rt[i] = rt;
+        }
         acc[0] = ADD(acc[0], MUL(rt, r));
         acc[1] = ADD(acc[1], MUL(r, r));
     }
@@ -80,11 +84,11 @@ struct HsK1 {
     }
 };
 
-// K2: x += alpha*p_old; p = M r + beta p_old (on the fly for every gathered
-// column); s = A p; mu = <p,s>.   streams: A, p_old r x [d]
+// K2: x += alpha*p_old; p = r~ + beta p_old (on the fly for every gathered
+// column; r~ = M r stored by K1); s = A p; mu = <p,s>.   streams: A, p_old r~ x
 template <bool PREC>
 struct HsK2 {
-    static constexpr int NV = PREC ? 4 : 3, ND = 1;
+    static constexpr int NV = 3, ND = 1;
     static constexpr bool CSR = true;
     int mode;
     const double* pold;
@@ -102,7 +106,7 @@ struct HsK2 {
         return true;
     }
     __device__ const double* vec(const Params& P, int v) const {
-        return v == 0 ? pold : v == 1 ? P.r : v == 2 ? P.x : P.d;
+        return v == 0 ? pold : v == 1 ? (PREC ? P.rt : P.r) : P.x;
     }
     __device__ int sync() const { return mode == MODE_FULL ? 2 : 1; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
@@ -111,15 +115,12 @@ struct HsK2 {
         const double po = SV(0);
         P.x[i] = ADD(SV(2), MUL(alpha, po));
         if (mode != MODE_FULL) return;
-        const double* __restrict__ r = P.r;
+        const double* __restrict__ rtv = PREC ? P.rt : P.r;
         const double* __restrict__ pg = pold;
         const double b = beta;
         const double sum =
-            row_dot(R, [&](int j) {
-                const double rj = in.gather(1, j, r);
-                return ADD(PREC ? MUL(in.gather(3, j, P.d), rj) : rj, MUL(b, in.gather(0, j, pg)));
-            });
-        const double pi = ADD(PREC ? MUL(SV(3), SV(1)) : SV(1), MUL(b, po));
+            row_dot(R, [&](int j) { return ADD(in.gather(1, j, rtv), MUL(b, in.gather(0, j, pg))); });
+        const double pi = ADD(SV(1), MUL(b, po));
         pnew[i] = pi;
         P.s[i] = sum;
         acc[0] = ADD(acc[0], MUL(pi, sum));
@@ -163,7 +164,7 @@ struct CgK1 {
             case 2: return S ? P.x : nullptr;
             case 3: return P.r;
             case 4: return F ? P.w : nullptr;
-            default: return F ? P.d : nullptr;
+            default: return P.d;
         }
     }
     __device__ int sync() const { return (F && !S) ? 1 : 0; }
@@ -180,7 +181,9 @@ struct CgK1 {
         }
         if (S) {
             P.x[i] = ADD(SV(2), MUL(alpha, p));
-            P.r[i] = SUB(r, MUL(alpha, s));
+            const double rn = SUB(r, MUL(alpha, s));
+            P.r[i] = rn;
+            if constexpr (PREC) P.rt[i] = MUL(SV(5), rn);  // r~ = M r for K2's gather
         }
     }
     __device__ void finish(const Params&, Ctrl* c, const double*) const { c->form_pending = 0; }
@@ -191,6 +194,7 @@ template <bool PREC>
 struct CgK2 {
     static constexpr int NV = 4, ND = 5;
     static constexpr bool CSR = true;
+    static constexpr int STAGES = 2;  // measured: a shallower ring leaves L1 to the gathers
     bool unsimp;
     __device__ bool enter(const Params& P) {
         unsimp = P.unsimplified_mu != 0;
@@ -199,7 +203,7 @@ struct CgK2 {
     __device__ const double* vec(const Params& P, int v) const {
         switch (v) {
             case 0: return P.r;
-            case 1: return PREC ? P.d : nullptr;
+            case 1: return PREC ? P.rt : nullptr;
             case 2: return unsimp ? P.s : nullptr;
             default: return unsimp ? P.p0 : nullptr;
         }
@@ -208,13 +212,10 @@ struct CgK2 {
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
     template <class In>
     __device__ void row(const Params& P, int i, const In& in, const RowRef& R, double* acc) const {
-        const double* __restrict__ r = P.r;
-        const double w = row_dot(R, [&](int j) {
-            const double rj = in.gather(0, j, r);
-            return PREC ? MUL(in.gather(1, j, P.d), rj) : rj;
-        });
+        const double* __restrict__ rtv = PREC ? P.rt : P.r;
+        const double w = row_dot(R, [&](int j) { return in.gather(1, j, rtv); });
         P.w[i] = w;
-        const double ri = SV(0), rti = PREC ? MUL(SV(1), ri) : ri;
+        const double ri = SV(0), rti = PREC ? SV(1) : ri;
         acc[0] = ADD(acc[0], MUL(rti, ri));
         acc[1] = ADD(acc[1], MUL(rti, w));
         acc[2] = ADD(acc[2], MUL(ri, ri));
@@ -436,6 +437,7 @@ struct GvK1 {
             }
             w = SUB(w, MUL(alpha, u));
             P.w[i] = w;
+            if constexpr (PREC) P.wt[i] = MUL(SV(9), w);  // w~ = M w for K2's gather
             acc[0] = ADD(acc[0], MUL(rt, r));
             acc[1] = ADD(acc[1], MUL(rt, w));
             acc[2] = ADD(acc[2], MUL(r, r));
@@ -482,17 +484,15 @@ template <bool PREC>
 struct GvK2 {
     static constexpr int NV = kInTileGather ? (PREC ? 2 : 1) : 0, ND = 0;
     static constexpr bool CSR = true;
+    static constexpr int STAGES = 2;  // measured: a shallower ring leaves L1 to the gathers
     __device__ bool enter(const Params& P) { return P.ctrl->mode2 != MODE_SKIP; }
     __device__ const double* vec(const Params& P, int v) const { return v == 0 ? P.w : P.d; }
     __device__ int sync() const { return 1; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
     template <class In>
     __device__ void row(const Params& P, int i, const In& in, const RowRef& R, double*) const {
-        const double* __restrict__ w = P.w;
-        P.t[i] = row_dot(R, [&](int j) {
-            const double wj = in.gather(0, j, w);
-            return PREC ? MUL(in.gather(1, j, P.d), wj) : wj;
-        });
+        const double* __restrict__ wtv = PREC ? P.wt : P.w;  // w~ stored by K1
+        P.t[i] = row_dot(R, [&](int j) { return in.gather(0, j, wtv); });
     }
     __device__ void finish(const Params&, Ctrl* c, const double*) const { c->mode2 = MODE_SKIP; }
 };

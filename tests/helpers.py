@@ -13,8 +13,8 @@ VEC_IDS = list(Vec)
 
 
 def tree_dot(A_dev: cgvk.DeviceMatrix):
-    block, gmax = A_dev.reduction_config()
-    return ("tree", block, gmax)
+    block, gmax, order = A_dev.reduction_config()
+    return ("tree", block, gmax, order)
 
 
 def gpu_state(s: cgvk.Solver) -> dict:

@@ -189,6 +189,7 @@ def test_tree_dot_is_a_sum_of_products():
         x = rng.integers(-1000, 1000, n).astype(np.float64)
         y = rng.integers(-1000, 1000, n).astype(np.float64)
         exact = float(np.dot(x.astype(np.int64), y.astype(np.int64)))
-        assert O.dot(x, y, ("tree", 256, 1776)) == exact
-        assert O.dot(x, y, ("part", 256, 1776, [0, n // 3, n])) == exact
+        for order in (0, 1):
+            assert O.dot(x, y, ("tree", 256, 1776, order)) == exact
+            assert O.dot(x, y, ("part", 256, 1776, [0, n // 3, n], order)) == exact
         assert O.dot(x, y, "seq") == exact
