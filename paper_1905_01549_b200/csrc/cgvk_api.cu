@@ -357,7 +357,9 @@ int cgvk_matrix_create_csr(int64_t n, const int64_t* row_ptr, const int64_t* col
         if (hflags & 4) return bail(set_err(CGVK_EINVAL, "column indices not strictly increasing"));
         if (hflags & 8) return bail(set_err(CGVK_EINVAL, "matrix is not bitwise symmetric"));
     }
-    if ((rc = build_sell(a, row_ptr)) != CGVK_OK) return bail(rc);
+    // the SELL-32 copy only backs the experimental direct SpMV engine
+    const char* eng = getenv("CGVK_SPMV_ENGINE");
+    if (eng && strcmp(eng, "sell") == 0 && (rc = build_sell(a, row_ptr)) != CGVK_OK) return bail(rc);
     *out = a;
     return CGVK_OK;
 }
