@@ -201,6 +201,39 @@ int cgvk_solve(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, const
                const double* x0, int max_iter, double rel_tol, double* x_out,
                cgvk_solve_status* st, cgvk_scalars* sc);
 
+/* ---------------------------------------------------- row-partitioned solve
+ * (SURVEY §8(e)); the reference has no distributed code. Rank r owns rows
+ * [lo[r], lo[r+1]); SpMV rows stay bit-identical to the reference for any P,
+ * dots are rank-local canonical trees summed in rank order. */
+typedef struct cgvk_comm_s* cgvk_comm;
+
+/* Contiguous row blocks cut at multiples of `align` (rows per plane: z-slabs). */
+int cgvk_partition_rows(int64_t n, int nparts, int64_t align, int64_t* lo);
+/* Halo plan of `rank` from its own rows (local row_ptr, global columns):
+ * sizes4 = {lower halo, upper halo, rows sent down, rows sent up}; arrays
+ * (nullable) receive the sorted global halo columns and local send rows. */
+int cgvk_halo_plan(int64_t n, int nranks, const int64_t* lo, int rank, const int64_t* row_ptr,
+                   const int64_t* col_idx, int64_t* sizes4, int64_t* lower, int64_t* upper,
+                   int64_t* send_lo, int64_t* send_hi);
+/* Rank-local matrix: rows [lo[rank], lo[rank+1]) in local numbering
+ * [own | lower halo | upper halo]. */
+int cgvk_matrix_create_rank(int64_t n, int nranks, int rank, const int64_t* lo, const int64_t* row_ptr,
+                            const int64_t* col_idx, const double* values, int device, cgvk_matrix* out);
+/* NCCL transport (one process per GPU; libnccl.so.2 is dlopen'ed). */
+int cgvk_comm_nccl_unique_id(void* id128);
+int cgvk_comm_create_nccl(const void* id128, int nranks, int rank, int device, cgvk_comm* out);
+/* In-process transport: all ranks in this process on one device. */
+int cgvk_comm_create_local(int nranks, int device, cgvk_comm* out);
+int cgvk_comm_destroy(cgvk_comm c);
+/* initialize() across the ranks this process drives (all of them for a local
+ * comm, its own for NCCL); b/x0 are the local rows. */
+int cgvk_group_create(cgvk_comm comm, int nlocal, const cgvk_matrix* As, const cgvk_variant_config* cfg,
+                      int precond, const double* const* b, const double* const* x0, cgvk_solver* out);
+/* n_iters step() calls on every local rank (graph replays incl. exchanges). */
+int cgvk_group_step(const cgvk_solver* solvers, int nlocal, int n_iters);
+/* ||b - A x|| over all ranks. */
+int cgvk_group_true_residual(const cgvk_solver* solvers, int nlocal, double* out);
+
 /* Page-lock / unlock a host buffer (cudaHostRegister) for the e2e path. */
 int cgvk_host_register(void* ptr, uint64_t bytes);
 int cgvk_host_unregister(void* ptr);

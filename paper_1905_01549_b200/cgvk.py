@@ -164,6 +164,16 @@ def _load() -> C.CDLL:
         "cgvk_solve": (I, [P, C.POINTER(_Config), I, P, P, I, D, P, C.POINTER(_Status),
                            C.POINTER(_Scalars)]),
         "cgvk_host_register": (I, [P, C.c_uint64]),
+        "cgvk_partition_rows": (I, [I64, I, I64, P]),
+        "cgvk_halo_plan": (I, [I64, I, P, I, P, P, P, P, P, P, P]),
+        "cgvk_matrix_create_rank": (I, [I64, I, I, P, P, P, P, I, pp]),
+        "cgvk_comm_nccl_unique_id": (I, [P]),
+        "cgvk_comm_create_nccl": (I, [P, I, I, I, pp]),
+        "cgvk_comm_create_local": (I, [I, I, pp]),
+        "cgvk_comm_destroy": (I, [P]),
+        "cgvk_group_create": (I, [P, I, P, C.POINTER(_Config), I, P, P, P]),
+        "cgvk_group_step": (I, [P, I, I]),
+        "cgvk_group_true_residual": (I, [P, I, C.POINTER(D)]),
         "cgvk_host_unregister": (I, [P]),
     }
     for name, (res, args) in sig.items():
@@ -349,10 +359,15 @@ SCALAR_NAMES = ("alpha", "beta", "nu", "nu_prime", "mu", "delta", "delta_hat", "
 class Solver:
     """A device SolverState (inc/variants.hpp:101-143) created by initialize()."""
 
-    def __init__(self, config: VariantConfig, A: DeviceMatrix, precond: Precond, b, x0):
+    def __init__(self, config: VariantConfig, A: DeviceMatrix, precond: Precond, b, x0,
+                 _handle=None):
         self.A = A  # borrowed, kept alive
         self.config = config
         self.precond = Precond(precond)
+        if _handle is not None:  # a rank of a group (created by Group)
+            self._h = _handle
+            self.n = A.n
+            return
         b, x0 = _f64(b), _f64(x0)
         if b.shape != (A.n,) or x0.shape != (A.n,):
             raise InvalidArgument(-1, "right-hand side or initial guess dimension mismatch")
@@ -494,3 +509,121 @@ def host_register(arr: np.ndarray) -> None:
 
 def host_unregister(arr: np.ndarray) -> None:
     _check(_lib.cgvk_host_unregister(_ptr(arr)))
+
+
+# ------------------------------------------------- row-partitioned solves
+
+def partition_rows(n: int, nparts: int, align: int = 1) -> np.ndarray:
+    """Row blocks [lo[r], lo[r+1]) cut at multiples of `align` (z-slabs)."""
+    lo = np.empty(nparts + 1, np.int64)
+    _check(_lib.cgvk_partition_rows(int(n), int(nparts), int(align), _ptr(lo)))
+    return lo
+
+
+def local_rows(csr, lo, rank: int):
+    """Rank `rank`'s rows of a global CSR: local row_ptr, global columns, values."""
+    a, b = int(lo[rank]), int(lo[rank + 1])
+    k0, k1 = int(csr.row_ptr[a]), int(csr.row_ptr[b])
+    return (np.ascontiguousarray(csr.row_ptr[a:b + 1] - k0), np.ascontiguousarray(csr.col_idx[k0:k1]),
+            np.ascontiguousarray(csr.values[k0:k1]))
+
+
+def halo_plan(n: int, lo, rank: int, row_ptr, col_idx) -> dict:
+    lo, rp, ci = _i64(lo), _i64(row_ptr), _i64(col_idx)
+    sizes = np.zeros(4, np.int64)
+    _check(_lib.cgvk_halo_plan(int(n), lo.shape[0] - 1, _ptr(lo), int(rank), _ptr(rp),
+                               _ptr(ci) if ci.size else None, _ptr(sizes), None, None, None, None))
+    arrs = [np.empty(max(int(s), 1), np.int64) for s in sizes]
+    _check(_lib.cgvk_halo_plan(int(n), lo.shape[0] - 1, _ptr(lo), int(rank), _ptr(rp),
+                               _ptr(ci) if ci.size else None, _ptr(sizes), *[_ptr(x) for x in arrs]))
+    names = ("lower", "upper", "send_lo", "send_hi")
+    return {k: a[: int(s)] for k, a, s in zip(names, arrs, sizes)}
+
+
+class RankMatrix(DeviceMatrix):
+    """Rows [lo[rank], lo[rank+1]) of a global n x n matrix, local numbering
+    [own | lower halo | upper halo] (cgvk_matrix_create_rank)."""
+
+    def __init__(self, n: int, lo, rank: int, row_ptr, col_idx, values, device: int = 0):
+        lo, rp, ci, va = _i64(lo), _i64(row_ptr), _i64(col_idx), _f64(values)
+        h = C.c_void_p()
+        _check(_lib.cgvk_matrix_create_rank(int(n), lo.shape[0] - 1, int(rank), _ptr(lo), _ptr(rp),
+                                            _ptr(ci) if ci.size else None,
+                                            _ptr(va) if va.size else None, device, C.byref(h)))
+        self._h = h
+        self.n = int(lo[rank + 1] - lo[rank])
+        self.nnz = int(ci.shape[0])
+        self.device = device
+        self.rank = rank
+        self.lo = lo
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    _check(_lib.cgvk_comm_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class Comm:
+    """Transport of a row-partitioned solve: NCCL (one process per GPU) or
+    'local' (all ranks in this process on one device)."""
+
+    def __init__(self, nranks: int, rank: int = 0, device: int = 0, nccl_id: bytes | None = None):
+        h = C.c_void_p()
+        if nccl_id is None:
+            _check(_lib.cgvk_comm_create_local(int(nranks), device, C.byref(h)))
+            self.kind = "local"
+        else:
+            buf = (C.c_char * 128).from_buffer_copy(nccl_id)
+            _check(_lib.cgvk_comm_create_nccl(buf, int(nranks), int(rank), device, C.byref(h)))
+            self.kind = "nccl"
+        self._h = h
+        self.nranks, self.rank = nranks, rank
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _lib.cgvk_comm_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+
+class Group:
+    """initialize() of one solve over the ranks this process drives."""
+
+    def __init__(self, comm: Comm, mats: list, config: VariantConfig, precond: Precond, bs: list,
+                 x0s: list):
+        self.comm, self.mats = comm, mats
+        bs = [_f64(b) for b in bs]
+        x0s = [_f64(x) for x in x0s]
+        nl = len(mats)
+        hs = (C.c_void_p * nl)(*[m.handle for m in mats])
+        bp = (C.c_void_p * nl)(*[_ptr(b) if b.size else None for b in bs])
+        xp = (C.c_void_p * nl)(*[_ptr(x) if x.size else None for x in x0s])
+        out = (C.c_void_p * nl)()
+        c = config._to_c()
+        _check(_lib.cgvk_group_create(comm._h, nl, hs, C.byref(c), int(precond), bp, xp, out))
+        self._handles = out
+        self.solvers = [Solver(config, m, precond, None, None, _handle=C.c_void_p(out[i]))
+                        for i, m in enumerate(mats)]
+
+    def step(self, n_iters: int = 1) -> None:
+        _check(_lib.cgvk_group_step(self._handles, len(self.mats), int(n_iters)))
+
+    def sync(self) -> None:
+        for s in self.solvers:
+            s.sync()
+
+    def true_residual(self) -> float:
+        out = C.c_double()
+        _check(_lib.cgvk_group_true_residual(self._handles, len(self.mats), C.byref(out)))
+        return out.value
+
+    def vector(self, which: Vec) -> np.ndarray:
+        """The global vector (concatenation of the ranks' own rows; local comm)."""
+        return np.concatenate([s.vector(which) for s in self.solvers])
+
+    def close(self) -> None:
+        for s in self.solvers:
+            s.close()
+        self.solvers = []

@@ -4,14 +4,18 @@
 #include "cgvk.h"
 #include "cgvk_generic.cuh"
 #include "cgvk_variants.cuh"
+#include "cgvk_dist.cuh"
 
 #include <cuda_runtime.h>
 
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -81,6 +85,14 @@ struct cgvk_matrix_s {
     int64_t n = 0, nnz = 0;
     int ntiles = 0, gmax = 0, G = 1, sms = 0;
     int cap = 4;  // CSR entries a pipeline stage holds (max over tiles, capped)
+    int64_t ncols = 0;  // == n, or n + halo for a rank-local matrix
+    // row partition (rank-local matrices; a plain matrix is rank 0 of 1)
+    int nranks = 1, rank = 0;
+    int64_t gn = 0, glo = 0;        // global size, first global row
+    int64_t nlow = 0, nup = 0;      // halo columns: [n, n+nlow) lower, [n+nlow, ncols) upper
+    int64_t nsend_lo = 0, nsend_hi = 0;
+    int* send_lo = nullptr;         // local rows the lower neighbour's halo reads (sorted)
+    int* send_hi = nullptr;         // local rows the upper neighbour's halo reads (sorted)
     int order = 0;  // canonical tile order (fixed per matrix; reported to the oracle)
     int l2pol = 0;  // TMA L2 policy for the pipeline streams
     int* rp = nullptr;
@@ -117,6 +129,9 @@ struct cgvk_matrix_s {
         return P;
     }
 };
+
+int matrix_create(int64_t n, int64_t ncols, const int64_t* row_ptr, const int64_t* col_idx,
+                  const double* values, int device, int flags, bool check_sorted, cgvk_matrix* out);
 
 namespace {
 
@@ -271,6 +286,16 @@ int cgvk_variant_config_validate(const cgvk_variant_config* c) {
 
 int cgvk_matrix_create_csr(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
                            const double* values, int device, int flags, cgvk_matrix* out) {
+    return matrix_create(n, n, row_ptr, col_idx, values, device, flags, true, out);
+}
+
+}  // extern "C"
+
+// n rows; columns in [0, ncols) (ncols > n for a rank's local matrix, whose
+// halo columns are numbered after its own rows and are therefore not sorted
+// within a row — the global CSR order of the entries is what is preserved).
+int matrix_create(int64_t n, int64_t ncols, const int64_t* row_ptr, const int64_t* col_idx,
+                  const double* values, int device, int flags, bool check_sorted, cgvk_matrix* out) {
     if (!out) return set_err(CGVK_EINVAL, "null output handle");
     *out = nullptr;
     if (n < 0) return set_err(CGVK_EINVAL, "negative dimension");
@@ -281,9 +306,12 @@ int cgvk_matrix_create_csr(int64_t n, const int64_t* row_ptr, const int64_t* col
         return set_err(CGVK_EINVAL, "device CSR uses int32 indices: n and nnz must be < 2^31");
     if (nnz > 0 && (!col_idx || !values)) return set_err(CGVK_EINVAL, "null CSR arrays");
     CK(cudaSetDevice(device));
+    if (ncols < n || ncols >= (int64_t(1) << 31) - 256)
+        return set_err(CGVK_EINVAL, "column count out of range");
     auto* a = new cgvk_matrix_s;
     a->device = device;
     a->n = n;
+    a->ncols = ncols;
     a->nnz = nnz;
     a->ntiles = (int)((n + kBlock - 1) / kBlock);
     a->order = env_int("CGVK_ORDER", 0) ? 1 : 0;
@@ -332,8 +360,8 @@ int cgvk_matrix_create_csr(int64_t n, const int64_t* row_ptr, const int64_t* col
     if (e == cudaSuccess && nnz)
         e = cudaMemcpyAsync(a->va, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, a->stream);
     if (e == cudaSuccess) {
-        k_convert_csr<<<grid_elem(nnz > n ? nnz : n + 1), 256, 0, a->stream>>>(n, nnz, rp64, ci64, a->rp,
-                                                                              a->ci, a->flags);
+        k_convert_csr<<<grid_elem(nnz > n ? nnz : n + 1), 256, 0, a->stream>>>(n, ncols, nnz, rp64, ci64,
+                                                                              a->rp, a->ci, a->flags);
         e = cudaGetLastError();
     }
     int hflags = 0;
@@ -346,7 +374,7 @@ int cgvk_matrix_create_csr(int64_t n, const int64_t* row_ptr, const int64_t* col
     if (hflags & 1) return bail(set_err(CGVK_EINVAL, "row_ptr not monotone or wrong end points"));
     if (hflags & 2) return bail(set_err(CGVK_EINVAL, "column index out of range"));
     if (n > 0) {
-        k_check_sorted<<<grid_elem(n), 256, 0, a->stream>>>((int)n, a->rp, a->ci, a->flags);
+        if (check_sorted) k_check_sorted<<<grid_elem(n), 256, 0, a->stream>>>((int)n, a->rp, a->ci, a->flags);
         if (flags & CGVK_MATRIX_CHECK_SYMMETRIC)
             k_check_symmetric<<<grid_elem(n), 256, 0, a->stream>>>((int)n, a->rp, a->ci, a->va,
                                                                    a->flags);
@@ -364,6 +392,8 @@ int cgvk_matrix_create_csr(int64_t n, const int64_t* row_ptr, const int64_t* col
     return CGVK_OK;
 }
 
+extern "C" {
+
 int cgvk_matrix_destroy(cgvk_matrix a) {
     if (!a) return CGVK_OK;
     cudaSetDevice(a->device);
@@ -375,6 +405,8 @@ int cgvk_matrix_destroy(cgvk_matrix a) {
     cudaFree(a->sell_ci);
     cudaFree(a->sell_va);
     cudaFree(a->inv_diag);
+    cudaFree(a->send_lo);
+    cudaFree(a->send_hi);
     cudaFree(a->part);
     cudaFree(a->counter);
     cudaFree(a->out);
@@ -490,6 +522,7 @@ int cgvk_host_unregister(void* ptr) {
 // ===================================================================== solver
 
 using StreamFn = void (*)(Params, StageCfg);
+using FinalizeFn = void (*)(Params, const double*, int);
 
 // One pipelined kernel: function, stage configuration, grid, dynamic smem.
 struct KLaunch {
@@ -520,6 +553,13 @@ struct cgvk_solver_s {
     cudaGraphExec_t g1 = nullptr, g8 = nullptr;
     Params P{};
     int allocated = 0;
+    // row-partitioned solve (cgvk_group_create): this rank's share
+    struct Group* group = nullptr;
+    std::shared_ptr<struct Group> group_ref;  // keeps the group alive while a member lives
+    bool owns_stream = true;
+    double *rank_tot = nullptr, *all_tot = nullptr;
+    double *sbuf_lo = nullptr, *sbuf_hi = nullptr, *rbuf_lo = nullptr, *rbuf_hi = nullptr;
+    FinalizeFn fin1 = nullptr, fin2 = nullptr;
 };
 
 namespace {
@@ -579,7 +619,23 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
     L->smem = (size_t)header + (size_t)ns * S.stage_bytes;
     if (L->smem > (size_t)kSmemPerSM - 1024)
         return set_err(CGVK_EINVAL, "pipeline stage (%d bytes) exceeds shared memory", S.stage_bytes);
-    CK(cudaFuncSetAttribute(L->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L->smem));
+    {   // the attribute is per function: only ever raise it (solvers of other
+        // matrices may already have launches captured with a larger stage)
+        static std::mutex mu;
+        static std::vector<std::pair<const void*, size_t>> set;
+        std::lock_guard<std::mutex> lock(mu);
+        size_t* cur = nullptr;
+        for (auto& e : set)
+            if (e.first == (const void*)L->fn) cur = &e.second;
+        if (!cur) {
+            set.emplace_back((const void*)L->fn, 0);
+            cur = &set.back().second;
+        }
+        if (L->smem > *cur) {
+            CK(cudaFuncSetAttribute(L->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L->smem));
+            *cur = L->smem;
+        }
+    }
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L->fn, kThreads, L->smem));
     if (occ < 1) return set_err(CGVK_ECUDA, "pipeline kernel does not fit on an SM");
@@ -588,25 +644,24 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
     return CGVK_OK;
 }
 
+template <class Op1, class Op2>
+int pick_pair(cgvk_matrix a, KLaunch* k1, KLaunch* k2, FinalizeFn* f1, FinalizeFn* f2) {
+    TRY(make_launch<Op1>(a, k1));
+    TRY(make_launch<Op2>(a, k2));
+    *f1 = k_finalize<Op1>;
+    *f2 = k_finalize<Op2>;
+    return CGVK_OK;
+}
+
 template <bool PREC>
-int pick_kernels(cgvk_matrix a, int v, KLaunch* k1, KLaunch* k2) {
+int pick_kernels(cgvk_matrix a, int v, KLaunch* k1, KLaunch* k2, FinalizeFn* f1, FinalizeFn* f2) {
     switch (v) {
-        case CGVK_HS:
-            TRY(make_launch<HsK1<PREC>>(a, k1));
-            return make_launch<HsK2<PREC>>(a, k2);
-        case CGVK_CG_CG:
-            TRY(make_launch<CgK1<PREC>>(a, k1));
-            return make_launch<CgK2<PREC>>(a, k2);
+        case CGVK_HS: return pick_pair<HsK1<PREC>, HsK2<PREC>>(a, k1, k2, f1, f2);
+        case CGVK_CG_CG: return pick_pair<CgK1<PREC>, CgK2<PREC>>(a, k1, k2, f1, f2);
         case CGVK_M:
-        case CGVK_PR:
-            TRY(make_launch<PrK1<PREC>>(a, k1));
-            return make_launch<PrK2<PREC>>(a, k2);
-        case CGVK_GV:
-            TRY(make_launch<GvK1<PREC>>(a, k1));
-            return make_launch<GvK2<PREC>>(a, k2);
-        default:
-            TRY(make_launch<PprK1<PREC>>(a, k1));
-            return make_launch<PprK2<PREC>>(a, k2);
+        case CGVK_PR: return pick_pair<PrK1<PREC>, PrK2<PREC>>(a, k1, k2, f1, f2);
+        case CGVK_GV: return pick_pair<GvK1<PREC>, GvK2<PREC>>(a, k1, k2, f1, f2);
+        default: return pick_pair<PprK1<PREC>, PprK2<PREC>>(a, k1, k2, f1, f2);
     }
 }
 
@@ -825,11 +880,12 @@ void free_solver(cgvk_solver s) {
     if (s->g1) cudaGraphExecDestroy(s->g1);
     if (s->g8) cudaGraphExecDestroy(s->g8);
     for (double* p : {s->x, s->r, s->p0, s->p1, s->s, s->w, s->u, s->t, s->rt, s->st, s->wt, s->b,
-                      s->tmp, s->part, s->hist, s->dout})
+                      s->tmp, s->part, s->hist, s->dout, s->rank_tot, s->all_tot, s->sbuf_lo, s->sbuf_hi,
+                      s->rbuf_lo, s->rbuf_hi})
         cudaFree(p);
     cudaFree(s->counter);
     cudaFree(s->ctrl);
-    if (s->stream) cudaStreamDestroy(s->stream);
+    if (s->stream && s->owns_stream) cudaStreamDestroy(s->stream);
     delete s;
 }
 
@@ -847,13 +903,15 @@ int materialize(cgvk_solver s) {
 
 extern "C" {
 
-int cgvk_solver_create(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, const double* b,
-                       const double* x0, cgvk_solver* out) {
-    if (!out) return set_err(CGVK_EINVAL, "null output handle");
+}  // extern "C"
+
+// Allocate a solver's device state for matrix `a`, choose its kernels; uses
+// `stream` when given (a local group shares one), else creates its own.
+int solver_alloc(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, cudaStream_t stream,
+                 cgvk_solver* out) {
     *out = nullptr;
     if (!a) return set_err(CGVK_EINVAL, "null matrix");
     TRY(cgvk_variant_config_validate(cfg));
-    if (!b || !x0) return set_err(CGVK_EINVAL, "right-hand side or initial guess dimension mismatch");
     if (precond != CGVK_PRECOND_IDENTITY && precond != CGVK_PRECOND_JACOBI)
         return set_err(CGVK_EINVAL, "unknown preconditioner kind %d", precond);
     CK(cudaSetDevice(a->device));
@@ -875,7 +933,9 @@ int cgvk_solver_create(cgvk_matrix a, const cgvk_variant_config* cfg, int precon
         return code;
     };
     s->hist_cap = 1 << 17;
-    const int64_t nv = n + 32;  // bulk copies of the last tile round up to 16 bytes
+    // + halo columns of a rank-local matrix; + 32: bulk copies of the last
+    // tile round up to 16 bytes
+    const int64_t nv = a->ncols + 32;
     if ((rc = dalloc(&s->x, nv)) || (rc = dalloc(&s->r, nv)) || (rc = dalloc(&s->p0, nv)) ||
         (rc = dalloc(&s->s, nv)) || (rc = dalloc(&s->b, nv)) || (rc = dalloc(&s->tmp, nv)) ||
         (rc = dalloc(&s->part, kMaxDots * (size_t)a->gmax)) || (rc = dalloc(&s->hist, s->hist_cap)) ||
@@ -888,8 +948,12 @@ int cgvk_solver_create(cgvk_matrix a, const cgvk_variant_config* cfg, int precon
     if (s->prec && (rc = dalloc(&s->rt, nv))) return bail(rc);
     if (s->prec && (v == CGVK_GV || pipe) && (rc = dalloc(&s->st, nv))) return bail(rc);
     if (s->prec && (v == CGVK_GV || pipe) && (rc = dalloc(&s->wt, nv))) return bail(rc);
-    if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess)
+    if (stream) {
+        s->stream = stream;
+        s->owns_stream = false;
+    } else if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess) {
         return bail(set_err(CGVK_ECUDA, "stream create failed"));
+    }
     for (double* p : {s->x, s->r, s->p0, s->p1, s->s, s->w, s->u, s->t, s->rt, s->st, s->wt, s->tmp})
         if (p && cudaMemsetAsync(p, 0, 8 * (n ? n : 1), s->stream) != cudaSuccess)
             return bail(set_err(CGVK_ECUDA, "memset failed"));
@@ -919,10 +983,30 @@ int cgvk_solver_create(cgvk_matrix a, const cgvk_variant_config* cfg, int precon
     P.recompute_w = cfg->recompute_w;
     P.unsimplified_mu = cfg->unsimplified_mu;
     P.track_delta = cfg->track_delta;
-    if ((rc = s->prec ? pick_kernels<true>(a, v, &s->k1, &s->k2)
-                      : pick_kernels<false>(a, v, &s->k1, &s->k2)) != CGVK_OK)
+    if ((rc = s->prec ? pick_kernels<true>(a, v, &s->k1, &s->k2, &s->fin1, &s->fin2)
+                      : pick_kernels<false>(a, v, &s->k1, &s->k2, &s->fin1, &s->fin2)) != CGVK_OK)
         return bail(rc);
+    *out = s;
+    return CGVK_OK;
+}
 
+extern "C" {
+
+int cgvk_solver_create(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, const double* b,
+                       const double* x0, cgvk_solver* out) {
+    if (!out) return set_err(CGVK_EINVAL, "null output handle");
+    *out = nullptr;
+    if (!b || !x0) return set_err(CGVK_EINVAL, "right-hand side or initial guess dimension mismatch");
+    if (a && a->nranks > 1)
+        return set_err(CGVK_EINVAL, "a rank-local matrix needs cgvk_group_create");
+    cgvk_solver s = nullptr;
+    TRY(solver_alloc(a, cfg, precond, nullptr, &s));
+    int rc;
+    auto bail = [&](int code) {
+        free_solver(s);
+        return code;
+    };
+    const int64_t n = a->n;
     if (n == 0) {  // r0 is empty: nu0 = 0 = <r,r> -> Converged(ZeroResidual)
         Ctrl c{};
         c.state = ST_CONVERGED;
@@ -961,6 +1045,10 @@ int cgvk_solver_set_tolerance(cgvk_solver s, double rel_tol) {
 int cgvk_solver_step(cgvk_solver s, int n_iters) {
     if (!s) return set_err(CGVK_EINVAL, "null solver");
     if (n_iters < 0) return set_err(CGVK_EINVAL, "n_iters must be >= 0");
+    if (s->group) {  // a rank of a row-partitioned solve: one rank per process steps alone
+        cgvk_solver one[1] = {s};
+        return cgvk_group_step(one, 1, n_iters);
+    }
     if (s->mirror_fresh && s->mirror.state != ST_RUNNING)
         return set_err(CGVK_ESTATE, "step() on a terminated solver");
     if (n_iters == 0 || s->n == 0) return CGVK_OK;
@@ -1195,3 +1283,5 @@ int cgvk_solve(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, const
 }
 
 }  // extern "C"
+
+#include "cgvk_group.inc"

@@ -79,6 +79,8 @@ struct Params {
     int nu_expr, recompute_nu, recompute_w, unsimplified_mu, track_delta;
     int order;  // canonical tile order (see CGVK_FOR_VB)
     int l2pol;  // TMA L2 policy: 0 evict_first everything, 1 only the matrix, 2 none
+    int dist;          // rank of a row-partitioned solve: reducing kernels stop at the
+    double* rank_tot;  // rank-local totals [kMaxDots]; k_finalize folds all ranks
 };
 
 // Balanced contiguous partition: part k of `parts` covers [lo(k), lo(k+1)).

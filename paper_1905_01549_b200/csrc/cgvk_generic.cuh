@@ -12,7 +12,7 @@ namespace cgvk {
 // validate_csr invariants (src/sparse_matrix.cpp:64-82) on the way:
 //   bit 0 row_ptr not monotone / wrong ends, bit 1 column out of range,
 //   bit 2 columns not strictly increasing.
-__global__ void k_convert_csr(int64_t n, int64_t nnz, const int64_t* __restrict__ rp64,
+__global__ void k_convert_csr(int64_t n, int64_t ncols, int64_t nnz, const int64_t* __restrict__ rp64,
                               const int64_t* __restrict__ ci64, int* __restrict__ rp32,
                               int* __restrict__ ci32, int* flags) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -29,7 +29,7 @@ __global__ void k_convert_csr(int64_t n, int64_t nnz, const int64_t* __restrict_
     }
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride) {
         const int64_t c = ci64[k];
-        if (c < 0 || c >= n) f |= 2;
+        if (c < 0 || c >= ncols) f |= 2;
         ci32[k] = (int)c;
     }
     if (f) atomicOr(flags, f);

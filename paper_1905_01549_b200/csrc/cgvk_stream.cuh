@@ -479,6 +479,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(Params P, StageCfg S) {
     }
     if (t == 0) {
         *counter = 0u;
+        if (P.dist && mode == 2) {  // rank total: k_finalize folds all ranks in rank order
+#pragma unroll
+            for (int d = 0; d < Op::ND; ++d) P.rank_tot[d] = tot[d];
+            return;
+        }
         op.finish(P, P.ctrl, tot);
     }
 }
@@ -551,6 +556,11 @@ __global__ void __launch_bounds__(kBlock, 3) k_direct(Params P, StageCfg S) {
     }
     if (t == 0) {
         *counter = 0u;
+        if (P.dist && mode == 2) {  // rank total: k_finalize folds all ranks in rank order
+#pragma unroll
+            for (int d = 0; d < Op::ND; ++d) P.rank_tot[d] = tot[d];
+            return;
+        }
         op.finish(P, P.ctrl, tot);
     }
 }
