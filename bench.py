@@ -19,10 +19,11 @@ cgvk_solve(K iterations) including the b/x0 upload and the x download.
 unchanged reference sources; the C restatement if that library is absent) on
 the host cores: the six variants in six threads, K steps each.
 
-Multi-GPU (torchrun, N>1): row-block (z-slab) strong scaling is not wired
-into this bench yet; each rank runs an independent replica of the workload
-("scaling": "weak", "mode": "replicas") and rank 0 reports the max-over-ranks
-time.
+Multi-GPU (torchrun, N>1): the same global solve row-partitioned into z-slabs
+(one rank per GPU, NCCL halo exchange + rank-ordered reductions; "scaling":
+"strong"); each variant's K iterations are device-timed on every rank and the
+max over ranks is taken. --emulate-ranks P runs the partitioned data path with
+P in-process ranks on one GPU.
 """
 from __future__ import annotations
 
@@ -244,8 +245,7 @@ def workload_config(args, P) -> dict:
     return {"workload": f"{args.config} ({P.A.n} rows, {P.A.nnz} nnz) fp64 CSR, Jacobi, "
                         f"six variants, K fixed iterations each",
             "variants": VARIANTS, "n": P.A.n, "nnz": P.A.nnz, "precond": "jacobi",
-            "l2": "working set > L2 (126 MB); no flush", "parallelism": "replicas" if
-            int(os.environ.get("WORLD_SIZE", "1")) > 1 else "single-gpu"}
+            "l2": "working set > L2 (126 MB); no flush", "parallelism": "single-gpu"}
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -258,6 +258,57 @@ def load_traffic() -> dict:
     return {}
 
 
+ALIGN = {"p2d": 256, "p64": 64 * 64, "p128": 128 * 128, "v256": 256 * 256, "r4m": 1}
+
+
+class SolveSet:
+    """One solver per variant: single-GPU, one NCCL rank of a row-partitioned
+    solve (torchrun, one process per GPU), or P in-process ranks on one GPU
+    (--emulate-ranks, the partitioned data path without NCCL)."""
+
+    def __init__(self, args, P, rank, world, device, dist, pinned=None):
+        from paper_1905_01549_b200 import cgvk
+        from paper_1905_01549_b200.cgvk import Precond, VariantConfig, variant_from_name
+
+        A = P.A
+        rp, ci, va, b, x0 = pinned or (A.row_ptr, A.col_idx, A.values, P.b, P.x0)
+        self.groups, self.solvers, self.comm, self.mats = [], {}, None, []
+        cfgs = {v: VariantConfig.make(variant_from_name(v)) for v in VARIANTS}
+        ranks = world if world > 1 else args.emulate_ranks
+        if ranks <= 1:
+            self.mats = [cgvk.DeviceMatrix(A.n, rp, ci, va, device=device)]
+            for v in VARIANTS:
+                self.solvers[v] = cgvk.initialize(cfgs[v], self.mats[0], Precond.JACOBI, b, x0)
+            return
+        lo = cgvk.partition_rows(A.n, ranks, ALIGN[args.config])
+        Acsr = type(A)(A.n, rp, ci, va)
+        if world > 1:  # NCCL: this process drives rank `rank`
+            nid = cgvk.nccl_unique_id() if rank == 0 else None
+            obj = [nid]
+            dist.broadcast_object_list(obj, src=0)
+            self.comm = cgvk.Comm(world, rank, device, obj[0])
+            mine = [rank]
+        else:
+            self.comm = cgvk.Comm(ranks, 0, device)
+            mine = list(range(ranks))
+        self.mats = [cgvk.RankMatrix(A.n, lo, r, *cgvk.local_rows(Acsr, lo, r), device=device) for r in mine]
+        for v in VARIANTS:
+            g = cgvk.Group(self.comm, self.mats, cfgs[v], Precond.JACOBI,
+                           [b[lo[r]:lo[r + 1]] for r in mine], [x0[lo[r]:lo[r + 1]] for r in mine])
+            self.groups.append(g)
+            self.solvers[v] = g.solvers[0]  # time_steps on member 0 steps the whole local group
+
+    def close(self):
+        for g in self.groups:
+            g.close()
+        for s in self.solvers.values():
+            s.close()
+        for m in self.mats:
+            m.close()
+        if self.comm:
+            self.comm.close()
+
+
 def run_gpu_arm(args, rank, local, world, dist):
     from paper_1905_01549_b200 import cgvk, problems as pb
     from paper_1905_01549_b200.cgvk import Precond, VariantConfig, variant_from_name
@@ -266,13 +317,9 @@ def run_gpu_arm(args, rank, local, world, dist):
     P = pb.config_problem(args.config)
     n, nnz = P.A.n, P.A.nnz
     pk = peaks()
-    A = cgvk.DeviceMatrix.from_csr(P.A, device=device)
-    solvers = {}
-    for v in VARIANTS:
-        s = cgvk.initialize(VariantConfig.make(variant_from_name(v)), A, Precond.JACOBI, P.b, P.x0)
-        solvers[v] = s
-    # warm-up: W iterations per variant (graphs, clocks, caches)
-    for v, s in solvers.items():
+    partitioned = world > 1 or args.emulate_ranks > 1
+    S = SolveSet(args, P, rank, world, device, dist)
+    for v, s in S.solvers.items():  # warm-up: graphs, clocks, caches
         s.time_steps(args.warmup)
 
     clocks = ClockSampler(device) if not args.no_clocks else None
@@ -284,8 +331,10 @@ def run_gpu_arm(args, rank, local, world, dist):
         clocks.mark("t_start")
     per = {}
     total_ms, total_iters = 0.0, 0
-    for v, s in solvers.items():
+    for v, s in S.solvers.items():
+        barrier(dist)
         ms, it = s.time_steps(args.steps)
+        ms = max_over_ranks(dist, ms)
         per[v] = {"ms": ms, "iters": it}
         total_ms += ms
         total_iters += it
@@ -294,26 +343,28 @@ def run_gpu_arm(args, rank, local, world, dist):
         time.sleep(0.05)
     clk = clocks.stop() if clocks else None
     barrier(dist)
-    total_ms = max_over_ranks(dist, total_ms)
+    S.close()
 
-    # per-kernel device times (events around each launch, same stream)
-    prof_iters = min(args.steps, 20)
+    # per-kernel device times (events around each launch, same stream); the
+    # partitioned path interleaves exchanges, so only the single-GPU run has it
     kernels = []
-    for v in VARIANTS:
-        s = cgvk.initialize(VariantConfig.make(variant_from_name(v)), A, Precond.JACOBI, P.b, P.x0)
-        s.time_steps(2)
-        k1, k2, it = s.profile(prof_iters)
-        names = KERNEL_NAMES[v]
-        vec = KERNEL_VECTORS[v][True]
-        b1 = 8 * n * vec[0]
-        b2 = a_bytes(n, nnz) + 8 * n * vec[1]
-        kernels.append({"variant": v, "kernel": names[0], "ms_per_launch": k1 / it,
-                        "bytes_per_launch": b1, "gbs": b1 / (k1 / it * 1e-3) / 1e9})
-        kernels.append({"variant": v, "kernel": names[1], "ms_per_launch": k2 / it,
-                        "bytes_per_launch": b2, "gbs": b2 / (k2 / it * 1e-3) / 1e9})
-        s.close()
-    top = max(kernels, key=lambda k: k["ms_per_launch"])
-    traffic = load_traffic().get(top["kernel"])
+    if not partitioned:
+        A = cgvk.DeviceMatrix.from_csr(P.A, device=device)
+        prof_iters = min(args.steps, 20)
+        for v in VARIANTS:
+            s = cgvk.initialize(VariantConfig.make(variant_from_name(v)), A, Precond.JACOBI, P.b, P.x0)
+            s.time_steps(2)
+            k1, k2, it = s.profile(prof_iters)
+            names = KERNEL_NAMES[v]
+            vec = KERNEL_VECTORS[v][True]
+            b1 = 8 * n * vec[0]
+            b2 = a_bytes(n, nnz) + 8 * n * vec[1]
+            kernels.append({"variant": v, "kernel": names[0], "ms_per_launch": k1 / it,
+                            "bytes_per_launch": b1, "gbs": b1 / (k1 / it * 1e-3) / 1e9})
+            kernels.append({"variant": v, "kernel": names[1], "ms_per_launch": k2 / it,
+                            "bytes_per_launch": b2, "gbs": b2 / (k2 / it * 1e-3) / 1e9})
+            s.close()
+        A.close()
 
     for v in VARIANTS:
         d = per[v]
@@ -321,40 +372,53 @@ def run_gpu_arm(args, rank, local, world, dist):
         bi = iter_bytes(v, n, nnz, True)
         per[v].update({"it_per_s": d["iters"] / (d["ms"] * 1e-3), "us_per_iter": t_iter * 1e6,
                        "bytes_per_iter": bi, "gbs": bi / t_iter / 1e9,
-                       "roofline_frac": bi / t_iter / 1e9 / pk["hbm_gbs"],
-                       "roofline_frac_nominal_8tbs": bi / t_iter / 1e9 / 8000.0})
+                       "roofline_frac": bi / t_iter / 1e9 / (pk["hbm_gbs"] * max(world, 1)),
+                       "roofline_frac_nominal_8tbs": bi / t_iter / 1e9 / (8000.0 * max(world, 1))})
+    if kernels:
+        top = max(kernels, key=lambda k: k["ms_per_launch"])
+        roof = {"bound": "hbm", "kernel": top["kernel"], "variant": top["variant"],
+                "achieved": top["gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": top["gbs"] / pk["hbm_gbs"], "peak_source": pk["source"],
+                "traffic": load_traffic().get(top["kernel"]),
+                "bytes_per_launch": top["bytes_per_launch"], "ms_per_launch": top["ms_per_launch"]}
+    else:  # partitioned: whole-iteration roofline of the slowest variant over all GPUs
+        worst = min(VARIANTS, key=lambda v: per[v]["roofline_frac"])
+        roof = {"bound": "hbm", "kernel": "iteration", "variant": worst,
+                "achieved": per[worst]["gbs"], "peak": pk["hbm_gbs"] * world, "unit": "GB/s",
+                "frac": per[worst]["roofline_frac"], "peak_source": pk["source"], "traffic": None,
+                "bytes_per_launch": per[worst]["bytes_per_iter"],
+                "ms_per_launch": per[worst]["us_per_iter"] * 1e-3}
 
     # e2e through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        rp, ci, va = P.A.row_ptr.copy(), P.A.col_idx.copy(), P.A.values.copy()
-        b, x0 = P.b.copy(), P.x0.copy()
-        xout = np.empty(n)
-        pinned = [rp, ci, va, b, x0, xout]
-        for arr in pinned:
+        arrs = [P.A.row_ptr.copy(), P.A.col_idx.copy(), P.A.values.copy(), P.b.copy(), P.x0.copy()]
+        for arr in arrs:
             cgvk.host_register(arr)
         try:
             barrier(dist)
             t0 = time.perf_counter()
-            A2 = cgvk.DeviceMatrix(n, rp, ci, va, device=device)
+            E = SolveSet(args, P, rank, world, device, dist, pinned=tuple(arrs))
             e2e_iters = 0
-            for v in VARIANTS:
-                x, st, k = cgvk.solve(A2, VariantConfig.make(variant_from_name(v)), Precond.JACOBI,
-                                      b, x0, args.steps)
-                e2e_iters += k
-            A2.close()
+            x = None
+            for v, s in E.solvers.items():
+                s.step(args.steps)
+                s.sync()
+                x = s.x  # result read back each solve
+                e2e_iters += s.k
+            E.close()
             t1 = time.perf_counter()
             barrier(dist)
             wall = max_over_ranks(dist, t1 - t0)
         finally:
-            for arr in pinned:
+            for arr in arrs:
                 cgvk.host_unregister(arr)
-        h2d = rp.nbytes + ci.nbytes + va.nbytes + len(VARIANTS) * (b.nbytes + x0.nbytes)
-        d2h = len(VARIANTS) * xout.nbytes
-        e2e = {"value": world * e2e_iters / wall, "unit": "iterations/s",
+        h2d = sum(a.nbytes for a in arrs[:3]) + len(VARIANTS) * (arrs[3].nbytes + arrs[4].nbytes)
+        d2h = len(VARIANTS) * x.nbytes
+        e2e = {"value": e2e_iters / wall, "unit": "iterations/s",
                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
-               "note": "per solve sweep: int64 CSR + b,x0 per variant up, x per variant down; "
-                       "bytes_per_step = sweep bytes / K"}
+               "note": "per sweep: int64 CSR + b, x0 per variant up (each rank its rows), x per "
+                       "variant down; bytes_per_step = sweep bytes / K (rank 0's share when N > 1)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -368,33 +432,28 @@ def run_gpu_arm(args, rank, local, world, dist):
                          f"(one thread per variant, -O2 -ffp-contract=off build)",
                "per_variant": cper}
 
-    value = world * total_iters / (total_ms * 1e-3)
+    value = total_iters / (total_ms * 1e-3)
     if rank == 0:
         launches = sum(1 + 2 * per[v]["iters"] for v in VARIANTS)
+        cfg = workload_config(args, P)
+        if partitioned:
+            cfg["parallelism"] = (f"row-partitioned z-slabs over {world} GPUs (NCCL)" if world > 1 else
+                                  f"row-partitioned, {args.emulate_ranks} in-process ranks on 1 GPU")
         line = {
             "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (App. B generator: Dirichlet 7-point Laplacian, x* from "
-                    "mt19937_64(1))",
-            "config": workload_config(args, P),
-            "roofline": {"bound": "hbm", "kernel": top["kernel"], "variant": top["variant"],
-                         "achieved": top["gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
-                         "frac": top["gbs"] / pk["hbm_gbs"], "peak_source": pk["source"],
-                         "traffic": traffic,
-                         "bytes_per_launch": top["bytes_per_launch"],
-                         "ms_per_launch": top["ms_per_launch"]},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (App. B generator, x* from mt19937_64(1))",
+            "config": cfg,
+            "roofline": roof,
             "kernels": kernels,
             "per_variant": per,
-            "gpu_launches": launches,
+            "gpu_launches": launches * (1 if world > 1 else max(args.emulate_ranks, 1)),
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
-    for s in solvers.values():
-        s.close()
-    A.close()
     return 0
 
 
@@ -409,6 +468,8 @@ def main():
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--emulate-ranks", type=int, default=1,
+                    help="row-partitioned solve with P in-process ranks on one GPU")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps

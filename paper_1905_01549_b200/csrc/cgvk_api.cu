@@ -889,6 +889,8 @@ void free_solver(cgvk_solver s) {
     delete s;
 }
 
+int group_step_all(cgvk_solver s, int n_iters);  // cgvk_group.inc
+
 int materialize(cgvk_solver s) {
     TRY(refresh_mirror(s));
     if (!s->mirror.form_pending) return CGVK_OK;
@@ -1045,10 +1047,8 @@ int cgvk_solver_set_tolerance(cgvk_solver s, double rel_tol) {
 int cgvk_solver_step(cgvk_solver s, int n_iters) {
     if (!s) return set_err(CGVK_EINVAL, "null solver");
     if (n_iters < 0) return set_err(CGVK_EINVAL, "n_iters must be >= 0");
-    if (s->group) {  // a rank of a row-partitioned solve: one rank per process steps alone
-        cgvk_solver one[1] = {s};
-        return cgvk_group_step(one, 1, n_iters);
-    }
+    // a rank of a row-partitioned solve steps every rank this process drives
+    if (s->group) return group_step_all(s, n_iters);
     if (s->mirror_fresh && s->mirror.state != ST_RUNNING)
         return set_err(CGVK_ESTATE, "step() on a terminated solver");
     if (n_iters == 0 || s->n == 0) return CGVK_OK;
@@ -1212,7 +1212,8 @@ int cgvk_solver_time_steps(cgvk_solver s, int n_iters, double* ms, int* iters) {
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     CK(cudaEventRecord(e0, s->stream));
-    const int rc = cgvk_solver_step(s, n_iters);
+    // a member of an in-process group times the whole group's iterations
+    const int rc = s->group ? group_step_all(s, n_iters) : cgvk_solver_step(s, n_iters);
     CK(cudaEventRecord(e1, s->stream));
     CK(cudaEventSynchronize(e1));
     float f = 0.f;
