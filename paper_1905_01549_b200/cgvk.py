@@ -20,7 +20,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcgvk.so")
+LIB_PATH = os.environ.get("CGVK_LIB") or os.path.join(_HERE, "libcgvk.so")  # CGVK_LIB: A/B builds
 
 
 class CgvkError(RuntimeError):

@@ -607,7 +607,10 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
     S.stage_bytes = (stage_bytes_for(S.cap, S.nvec, Op::CSR) + 127) & ~127;
     S.gvirt = a->G;
     const int header = ((int)sizeof(PipeHeader) + 127) & ~127;
-    const int ctas = env_int("CGVK_SMEM_CTAS", 2);
+    // stage budget: the SpMV kernels target CGVK_SPMV_MIN_CTAS resident CTAs,
+    // the update kernels two
+    const int ctas = env_int(Op::CSR ? "CGVK_SMEM_CTAS_SPMV" : "CGVK_SMEM_CTAS",
+                             Op::CSR ? CGVK_SPMV_MIN_CTAS : 2);
     const int budget = kSmemPerSM / ctas - 2048;
     int ns = (budget - header) / S.stage_bytes;
     if (ns < 2) ns = 2;
@@ -689,7 +692,10 @@ int ref_allocated(int v, bool prec) {
 // kernel drains, and synchronises with griddepcontrol.wait before reading its
 // results. CGVK_PDL=0 turns it off (for A/B measurements).
 void launch(cgvk_solver s, const KLaunch& L) {
-    static const bool pdl = env_int("CGVK_PDL", 1) != 0;
+    // measured (profiles/r01): PDL gains 3-5 % on every variant except HS,
+    // whose short reducing K1 loses ~10 % to it with 3-CTA SpMV kernels
+    static const int pdl_env = env_int("CGVK_PDL", -1);
+    const bool pdl = pdl_env >= 0 ? pdl_env != 0 : s->cfg.variant != CGVK_HS;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(L.grid);
     cfg.blockDim = dim3(L.threads);

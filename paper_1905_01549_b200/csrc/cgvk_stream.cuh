@@ -22,6 +22,13 @@
 
 #include <type_traits>
 
+// Occupancy target of the SpMV kernels (register budget via __launch_bounds__).
+// Measured (profiles/r01): 3 resident CTAs per SM for the SpMV kernels (regs
+// <= 75, two ring stages) beats 2 CTAs with 3 stages by 5-10 % per kernel.
+#ifndef CGVK_SPMV_MIN_CTAS
+#define CGVK_SPMV_MIN_CTAS 3
+#endif
+
 namespace cgvk {
 
 constexpr int kConsumers = kBlock;           // 8 warps, one row each
@@ -158,7 +165,10 @@ struct RowRef {
 // accumulation — so a row costs ~2 memory latencies, not 2 per entry. Loads
 // past the row end / padding slots (ci < 0) are predicated off; padding is
 // never multiplied.
-constexpr int kChunk = 8;
+#ifndef CGVK_CHUNK
+#define CGVK_CHUNK 8
+#endif
+constexpr int kChunk = CGVK_CHUNK;
 
 template <class XF>
 __device__ __forceinline__ double row_dot(const RowRef& R, XF xf) {
@@ -348,7 +358,7 @@ __device__ __forceinline__ void stage_csr(const Params& P, const StageCfg& S, Pi
 //        sv[v * kBlock] = staged value of vector v at row i
 //   void finish(const Params&, Ctrl*, const double* tot)   thread 0, last CTA
 template <class Op>
-__global__ void __launch_bounds__(kThreads, 1) k_stream(Params P, StageCfg S) {
+__global__ void __launch_bounds__(kThreads, Op::CSR ? CGVK_SPMV_MIN_CTAS : 1) k_stream(Params P, StageCfg S) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PipeHeader* H = reinterpret_cast<PipeHeader*>(smem_raw);
     unsigned char* stages = smem_raw + ((sizeof(PipeHeader) + 127) / 128) * 128;
