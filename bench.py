@@ -463,7 +463,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="p128", choices=["p2d", "p64", "p128", "v256", "r4m"])
+    ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "p128"), choices=["p2d", "p64", "p128", "v256", "r4m"])
     ap.add_argument("--cpu-steps", type=int, default=10)
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

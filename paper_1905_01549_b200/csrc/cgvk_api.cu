@@ -5,6 +5,7 @@
 #include "cgvk_generic.cuh"
 #include "cgvk_variants.cuh"
 #include "cgvk_dist.cuh"
+#include "cgvk_persist.cuh"
 
 #include <cuda_runtime.h>
 
@@ -550,6 +551,8 @@ struct cgvk_solver_s {
     bool mirror_fresh = true;
     int k_target = 0;
     KLaunch k1, k2;
+    KLaunch kp;            // persistent cooperative kernel (both phases, all iterations)
+    bool persist = false;  // step() uses kp instead of graph replays
     cudaGraphExec_t g1 = nullptr, g8 = nullptr;
     Params P{};
     int allocated = 0;
@@ -609,8 +612,13 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
     const int header = ((int)sizeof(PipeHeader) + 127) & ~127;
     // stage budget: the SpMV kernels target CGVK_SPMV_MIN_CTAS resident CTAs,
     // the update kernels two
-    const int ctas = env_int(Op::CSR ? "CGVK_SMEM_CTAS_SPMV" : "CGVK_SMEM_CTAS",
-                             Op::CSR ? CGVK_SPMV_MIN_CTAS : 2);
+    int ctas = env_int(Op::CSR ? "CGVK_SMEM_CTAS_SPMV" : "CGVK_SMEM_CTAS", Op::CSR ? CGVK_SPMV_MIN_CTAS : 2);
+    if (Op::CSR && header + 2 * S.stage_bytes > kSmemPerSM / 2 - 2048) {
+        // long rows: a 2-stage ring fills the SM -> one CTA with the full
+        // register file (see k_stream's MINB)
+        L->fn = k_stream<Op, 1>;
+        ctas = 1;
+    }
     const int budget = kSmemPerSM / ctas - 2048;
     int ns = (budget - header) / S.stage_bytes;
     if (ns < 2) ns = 2;
@@ -644,27 +652,61 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
     if (occ < 1) return set_err(CGVK_ECUDA, "pipeline kernel does not fit on an SM");
     L->grid = balanced_grid(a->G, occ * a->sms);
     L->S = S;
+    if (env_int("CGVK_DEBUG", 0))
+        fprintf(stderr, "cgvk launch %s: occ %d/SM grid %d smem %zu nstage %d stage %d B\n", __func__, occ,
+                L->grid, L->smem, S.nstage, S.stage_bytes);
+    return CGVK_OK;
+}
+
+// The persistent kernel of the pair: union stage layout, cooperative launch,
+// grid = co-resident CTAs (balanced over the virtual CTAs).
+template <class Op1, class Op2>
+int make_persist(cgvk_matrix a, KLaunch* L) {
+    L->fn = k_persist<Op1, Op2>;
+    L->threads = kThreads;
+    StageCfg S{};
+    S.nvec = Op1::NV > Op2::NV ? Op1::NV : Op2::NV;
+    S.cap = (Op1::CSR || Op2::CSR) ? a->cap : 0;
+    S.stage_bytes = (stage_bytes_for(S.cap, S.nvec, S.cap > 0) + 127) & ~127;
+    S.gvirt = a->G;
+    const int header = ((int)sizeof(PipeHeader) + 127) & ~127;
+    int ns = (kSmemPerSM / env_int("CGVK_PERSIST_CTAS", 2) - 2048 - header) / S.stage_bytes;
+    if (ns < 2) ns = 2;
+    if (ns > 6) ns = 6;
+    S.nstage = ns;
+    L->smem = (size_t)header + (size_t)ns * S.stage_bytes;
+    if (L->smem > (size_t)kSmemPerSM - 1024) return set_err(CGVK_EINVAL, "persistent stage too large");
+    CK(cudaFuncSetAttribute(L->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L->smem));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L->fn, kThreads, L->smem));
+    if (occ < 1) return set_err(CGVK_ECUDA, "persistent kernel does not fit on an SM");
+    L->grid = balanced_grid(a->G, occ * a->sms);
+    L->S = S;
+    if (env_int("CGVK_DEBUG", 0))
+        fprintf(stderr, "cgvk launch %s: occ %d/SM grid %d smem %zu nstage %d stage %d B\n", __func__, occ,
+                L->grid, L->smem, S.nstage, S.stage_bytes);
     return CGVK_OK;
 }
 
 template <class Op1, class Op2>
-int pick_pair(cgvk_matrix a, KLaunch* k1, KLaunch* k2, FinalizeFn* f1, FinalizeFn* f2) {
-    TRY(make_launch<Op1>(a, k1));
-    TRY(make_launch<Op2>(a, k2));
-    *f1 = k_finalize<Op1>;
-    *f2 = k_finalize<Op2>;
+int pick_pair(cgvk_matrix a, cgvk_solver s) {
+    TRY(make_launch<Op1>(a, &s->k1));
+    TRY(make_launch<Op2>(a, &s->k2));
+    TRY((make_persist<Op1, Op2>(a, &s->kp)));
+    s->fin1 = k_finalize<Op1>;
+    s->fin2 = k_finalize<Op2>;
     return CGVK_OK;
 }
 
 template <bool PREC>
-int pick_kernels(cgvk_matrix a, int v, KLaunch* k1, KLaunch* k2, FinalizeFn* f1, FinalizeFn* f2) {
+int pick_kernels(cgvk_matrix a, int v, cgvk_solver s) {
     switch (v) {
-        case CGVK_HS: return pick_pair<HsK1<PREC>, HsK2<PREC>>(a, k1, k2, f1, f2);
-        case CGVK_CG_CG: return pick_pair<CgK1<PREC>, CgK2<PREC>>(a, k1, k2, f1, f2);
+        case CGVK_HS: return pick_pair<HsK1<PREC>, HsK2<PREC>>(a, s);
+        case CGVK_CG_CG: return pick_pair<CgK1<PREC>, CgK2<PREC>>(a, s);
         case CGVK_M:
-        case CGVK_PR: return pick_pair<PrK1<PREC>, PrK2<PREC>>(a, k1, k2, f1, f2);
-        case CGVK_GV: return pick_pair<GvK1<PREC>, GvK2<PREC>>(a, k1, k2, f1, f2);
-        default: return pick_pair<PprK1<PREC>, PprK2<PREC>>(a, k1, k2, f1, f2);
+        case CGVK_PR: return pick_pair<PrK1<PREC>, PrK2<PREC>>(a, s);
+        case CGVK_GV: return pick_pair<GvK1<PREC>, GvK2<PREC>>(a, s);
+        default: return pick_pair<PprK1<PREC>, PprK2<PREC>>(a, s);
     }
 }
 
@@ -991,8 +1033,7 @@ int solver_alloc(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, cud
     P.recompute_w = cfg->recompute_w;
     P.unsimplified_mu = cfg->unsimplified_mu;
     P.track_delta = cfg->track_delta;
-    if ((rc = s->prec ? pick_kernels<true>(a, v, &s->k1, &s->k2, &s->fin1, &s->fin2)
-                      : pick_kernels<false>(a, v, &s->k1, &s->k2, &s->fin1, &s->fin2)) != CGVK_OK)
+    if ((rc = s->prec ? pick_kernels<true>(a, v, s) : pick_kernels<false>(a, v, s)) != CGVK_OK)
         return bail(rc);
     *out = s;
     return CGVK_OK;
@@ -1032,6 +1073,7 @@ int cgvk_solver_create(cgvk_matrix a, const cgvk_variant_config* cfg, int precon
     if ((rc = solver_init(s, b, x0)) != CGVK_OK) return bail(rc);
     if ((rc = capture(s, 1, &s->g1)) != CGVK_OK || (rc = capture(s, 8, &s->g8)) != CGVK_OK)
         return bail(rc);
+    s->persist = env_int("CGVK_PERSIST", 0) != 0;
     *out = s;
     return CGVK_OK;
 }
@@ -1061,8 +1103,22 @@ int cgvk_solver_step(cgvk_solver s, int n_iters) {
     CK(cudaSetDevice(s->a->device));
     s->k_target += n_iters;
     k_set_limit<<<1, 1, 0, s->stream>>>(s->ctrl, s->k_target);
-    for (int i = 0; i < n_iters / 8; ++i) CK(cudaGraphLaunch(s->g8, s->stream));
-    for (int i = 0; i < n_iters % 8; ++i) CK(cudaGraphLaunch(s->g1, s->stream));
+    if (s->persist) {  // all n iterations in one cooperative launch
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(s->kp.grid);
+        cfg.blockDim = dim3(s->kp.threads);
+        cfg.dynamicSmemBytes = s->kp.smem;
+        cfg.stream = s->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, s->kp.fn, s->P, s->kp.S));
+    } else {
+        for (int i = 0; i < n_iters / 8; ++i) CK(cudaGraphLaunch(s->g8, s->stream));
+        for (int i = 0; i < n_iters % 8; ++i) CK(cudaGraphLaunch(s->g1, s->stream));
+    }
     CK(cudaGetLastError());
     s->mirror_fresh = false;
     return CGVK_OK;

@@ -50,7 +50,8 @@ struct __align__(16) Ctrl {
     int wt_stored;    // pipe-PR: w~ lives in its buffer (nu'-terminal step)
     int hist_cap;
     unsigned int count[2];  // last-CTA arrival counters
-    int pad[2];
+    unsigned int bar_count; // persistent kernel: grid barrier arrivals
+    unsigned int bar_gen;   // persistent kernel: grid barrier generation
 };
 
 struct Params {

@@ -170,9 +170,54 @@ struct RowRef {
 #endif
 constexpr int kChunk = CGVK_CHUNK;
 
+// Software-pipelined form (CGVK_ROW_PIPE=1): the next chunk's loads and
+// gathers are issued before the current chunk is accumulated, so a row of
+// c chunks costs ~1 + c/2 latencies instead of 2c (long rows, e.g. R4M).
+#ifndef CGVK_ROW_PIPE
+#define CGVK_ROW_PIPE 0
+#endif
+
+template <class XF>
+struct ChunkBuf {
+    int c[kChunk];
+    double v[kChunk], x[kChunk];
+    __device__ __forceinline__ void load(const RowRef& R, int k0, XF xf) {
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u) {
+            const bool in = k0 + u < R.len;
+            c[u] = in ? R.ci[(k0 + u) * R.stride] : -1;
+            v[u] = in ? R.va[(k0 + u) * R.stride] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u) x[u] = c[u] >= 0 ? xf(c[u]) : 0.0;
+    }
+    __device__ __forceinline__ void accumulate(double& sum) const {
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u)
+            if (c[u] >= 0) sum = ADD(sum, MUL(v[u], x[u]));
+    }
+};
+
 template <class XF>
 __device__ __forceinline__ double row_dot(const RowRef& R, XF xf) {
     double sum = 0.0;
+    if constexpr (CGVK_ROW_PIPE) {
+        if (R.len <= 0) return sum;
+        ChunkBuf<XF> a, b;
+        a.load(R, 0, xf);
+        int k0 = 0;
+        for (;;) {
+            if (k0 + kChunk >= R.len) { a.accumulate(sum); break; }
+            b.load(R, k0 + kChunk, xf);
+            a.accumulate(sum);
+            k0 += kChunk;
+            if (k0 + kChunk >= R.len) { b.accumulate(sum); break; }
+            a.load(R, k0 + kChunk, xf);
+            b.accumulate(sum);
+            k0 += kChunk;
+        }
+        return sum;
+    }
     for (int k0 = 0; k0 < R.len; k0 += kChunk) {
         int c[kChunk];
         double v[kChunk], xv[kChunk];
@@ -354,11 +399,15 @@ __device__ __forceinline__ void stage_csr(const Params& P, const StageCfg& S, Pi
 //   bool enter(const Params&)            uniform: false -> nothing to do
 //   const double* vec(const Params&, int v)   stream v (nullptr: not staged)
 //   int sync()                           0: none, 1: arrive only, 2: reduce ND dots
-//   void row(const Params&, int i, const double* sv, const RowRef&, double* acc)
-//        sv[v * kBlock] = staged value of vector v at row i
+//   void row(const Params&, int i, const In& in, const RowRef&, double* acc)
+//        in(v) = staged value of vector v at row i, in.gather(v, j, g) = column j
 //   void finish(const Params&, Ctrl*, const double* tot)   thread 0, last CTA
-template <class Op>
-__global__ void __launch_bounds__(kThreads, Op::CSR ? CGVK_SPMV_MIN_CTAS : 1) k_stream(Params P, StageCfg S) {
+// MINB: resident CTAs the register budget is sized for. The SpMV kernels use
+// CGVK_SPMV_MIN_CTAS when their stage lets that many CTAs fit, else 1 — a
+// long-row matrix (R4M, ~27 entries/row) whose 2-stage ring already fills the
+// SM gets the registers to keep a whole chunk of gathers in flight.
+template <class Op, int MINB = (Op::CSR ? CGVK_SPMV_MIN_CTAS : 1)>
+__global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PipeHeader* H = reinterpret_cast<PipeHeader*>(smem_raw);
     unsigned char* stages = smem_raw + ((sizeof(PipeHeader) + 127) / 128) * 128;
