@@ -141,6 +141,7 @@ def _load() -> C.CDLL:
         "cgvk_matrix_create_csr": (I, [I64, P, P, P, I, I, pp]),
         "cgvk_matrix_destroy": (I, [P]),
         "cgvk_matrix_info": (I, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(I)]),
+        "cgvk_matrix_engine": (I, [P, C.POINTER(I), C.POINTER(I)]),
         "cgvk_spmv": (I, [P, P, P]),
         "cgvk_block_spmv": (I, [P, P, P, P, P]),
         "cgvk_jacobi": (I, [P, P]),
@@ -270,8 +271,12 @@ class VariantConfig:
 class DeviceMatrix:
     """SparseMatrix resident on one GPU (int32 CSR + fp64 values)."""
 
+    ENGINES = {None: 0, "csr": 2, "band": 4}
+
     def __init__(self, n: int, row_ptr, col_idx, values, device: int = 0,
-                 check_symmetric: bool = False):
+                 check_symmetric: bool = False, engine: str | None = None):
+        """engine: None = automatic (band for narrow-band long-row matrices),
+        "csr" or "band" (the band engine whenever it applies)."""
         rp, ci, va = _i64(row_ptr), _i64(col_idx), _f64(values)
         if rp.shape[0] != n + 1:
             raise InvalidArgument(-1, "row_ptr length must be n+1")
@@ -280,15 +285,23 @@ class DeviceMatrix:
         h = C.c_void_p()
         _check(_lib.cgvk_matrix_create_csr(n, _ptr(rp), _ptr(ci) if ci.size else None,
                                            _ptr(va) if va.size else None, device,
-                                           1 if check_symmetric else 0, C.byref(h)))
+                                           (1 if check_symmetric else 0) | self.ENGINES[engine],
+                                           C.byref(h)))
         self._h = h
         self.n = int(n)
         self.nnz = int(ci.shape[0])
         self.device = device
 
     @classmethod
-    def from_csr(cls, csr, device: int = 0, check_symmetric: bool = False) -> "DeviceMatrix":
-        return cls(csr.n, csr.row_ptr, csr.col_idx, csr.values, device, check_symmetric)
+    def from_csr(cls, csr, device: int = 0, check_symmetric: bool = False,
+                 engine: str | None = None) -> "DeviceMatrix":
+        return cls(csr.n, csr.row_ptr, csr.col_idx, csr.values, device, check_symmetric, engine)
+
+    def engine(self) -> tuple[str, int]:
+        """("csr" | "band", x-window half-width in 256-row tiles)."""
+        e, h = C.c_int(), C.c_int()
+        _check(_lib.cgvk_matrix_engine(self._h, C.byref(e), C.byref(h)))
+        return ("band" if e.value == 1 else "csr"), h.value
 
     @property
     def handle(self):

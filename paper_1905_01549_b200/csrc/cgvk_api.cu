@@ -6,6 +6,7 @@
 #include "cgvk_variants.cuh"
 #include "cgvk_dist.cuh"
 #include "cgvk_persist.cuh"
+#include "cgvk_band.cuh"
 
 #include <cuda_runtime.h>
 
@@ -99,10 +100,13 @@ struct cgvk_matrix_s {
     int* rp = nullptr;
     int* ci = nullptr;
     double* va = nullptr;
-    int* sell_ptr = nullptr;  // SELL-32 copy of A for the SpMV kernels
-    int* sell_ci = nullptr;
-    double* sell_va = nullptr;
-    int64_t sell_entries = 0;
+    // band engine copy of A (cgvk_band.cuh); band_h < 0: CSR engine
+    int band_h = -1;
+    int* band_off = nullptr;
+    unsigned int* band_meta = nullptr;
+    double* band_va = nullptr;
+    unsigned short* band_ci = nullptr;
+    int64_t band_entries = 0;
     double* inv_diag = nullptr;  // built on first use
     int jacobi_state = 0;        // 0 not built, 1 ok, -1 missing/non-positive diagonal
     cudaStream_t stream = nullptr;
@@ -122,9 +126,11 @@ struct cgvk_matrix_s {
         P.ci = ci;
         P.va = va;
         P.d = inv_diag;
-        P.sell_ptr = sell_ptr;
-        P.sell_va = sell_va;
-        P.sell_ci = sell_ci;
+        P.band_off = band_off;
+        P.band_meta = band_meta;
+        P.band_va = band_va;
+        P.band_ci = band_ci;
+        P.band_h = band_h;
         P.order = order;
         P.l2pol = l2pol;
         return P;
@@ -192,51 +198,91 @@ int ensure_tmp(cgvk_matrix a, int count) {
     return CGVK_OK;
 }
 
-// SELL-32 (sliced ELLPACK, slice = one warp's 32 consecutive rows, sigma = 1:
-// rows keep their order): entry j of row 32s+l at sell_ptr[s] + 32 j + l,
-// slice width = its longest row, padding marked by column -1. Offsets are
-// computed on the host from the reference-layout row_ptr; the fill runs on
-// the device from the validated int32 CSR.
-__global__ void k_fill_sell(int n, const int* __restrict__ rp, const int* __restrict__ ci,
-                            const double* __restrict__ va, const int* __restrict__ sp, int* sci,
-                            double* sva) {
+// Band engine layout (cgvk_band.cuh): SELL-C-sigma, C = 32, sigma = 256.
+// Window half-width H (tiles): every column of tile t lies in tiles
+// [t - H, t + H]. Applicable to a plain (single-rank) matrix whose 16-bit
+// window offsets fit and whose window rings fit in shared memory.
+constexpr int kBandMaxH = 19;  // 2 operands x (2H + 2) x 2 KB <= 160 KB
+
+int band_half_width(int64_t n, const int64_t* row_ptr, const int64_t* col_idx) {
+    int64_t h = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        if (row_ptr[i + 1] == row_ptr[i]) continue;
+        const int64_t t = i / kBlock;
+        const int64_t lo = col_idx[row_ptr[i]] / kBlock, hi = col_idx[row_ptr[i + 1] - 1] / kBlock;
+        if (t - lo > h) h = t - lo;
+        if (hi - t > h) h = hi - t;
+        if (h > kBandMaxH) return -1;
+    }
+    return (int)h;
+}
+
+// entries of row i -> its slot of the SELL-C-sigma layout
+__global__ void k_fill_band(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                            const double* __restrict__ va, const int* __restrict__ slot_of,
+                            const int* __restrict__ off, int H, double* bva, unsigned short* bci) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int base = sp[i >> 5] + (i & 31);
-        for (int k = rp[i], j = 0; k < rp[i + 1]; ++k, ++j) {
-            sci[base + 32 * j] = ci[k];
-            sva[base + 32 * j] = va[k];
+        const int g = slot_of[i];
+        const int t = g >> 8, q = g & 255;
+        const int base = off[t * kWarps + (q >> 5)] + (q & 31);
+        const int wb = (t - H) * kBlock;
+        for (int k = rp[i], e = 0; k < rp[i + 1]; ++k, ++e) {
+            bva[base + 32 * e] = va[k];
+            bci[base + 32 * e] = (unsigned short)(ci[k] - wb);
         }
     }
 }
 
-int build_sell(cgvk_matrix a, const int64_t* row_ptr) {
+int build_band(cgvk_matrix a, const int64_t* row_ptr, int H) {
     const int64_t n = a->n;
-    const int64_t nslots = (int64_t)a->ntiles * kWarps + 1;  // whole tiles, padded
-    std::vector<int> sp(nslots > 0 ? nslots : 1, 0);
-    int64_t off = 0;
-    for (int64_t s = 0; s + 1 < nslots; ++s) {
-        sp[s] = (int)off;
-        int64_t w = 0;
-        for (int64_t i = 32 * s; i < 32 * s + 32 && i < n; ++i) {
-            const int64_t len = row_ptr[i + 1] - row_ptr[i];
-            if (len > w) w = len;
+    const int nt = a->ntiles;
+    std::vector<int> off((size_t)nt * kWarps + 16, 0);
+    std::vector<unsigned int> meta((size_t)nt * kBlock);
+    std::vector<int> slot_of(n > 0 ? n : 1);
+    int64_t cur = 0;
+    int order[kBlock];
+    int64_t len[kBlock];
+    for (int t = 0; t < nt; ++t) {
+        const int64_t r0 = (int64_t)t * kBlock;
+        const int rows = (int)std::min<int64_t>(kBlock, n - r0);
+        for (int q = 0; q < kBlock; ++q) {
+            len[q] = q < rows ? row_ptr[r0 + q + 1] - row_ptr[r0 + q] : 0;
+            order[q] = q;
         }
-        off += 32 * w;
-        if (off >= (int64_t(1) << 31)) return set_err(CGVK_EINVAL, "SELL layout exceeds 2^31 entries");
+        std::stable_sort(order, order + kBlock, [&](int x, int y) { return len[x] > len[y]; });
+        for (int q = 0; q < kBlock; ++q) {
+            if (len[order[q]] >= (1 << 24)) return set_err(CGVK_EINVAL, "row too long for the band engine");
+            meta[(size_t)t * kBlock + q] = (unsigned int)(len[order[q]] << 8) | (unsigned int)order[q];
+            if (order[q] < rows) slot_of[r0 + order[q]] = t * kBlock + q;
+        }
+        for (int s = 0; s < kWarps; ++s) {
+            off[(size_t)t * kWarps + s] = (int)cur;
+            cur += 32 * len[order[32 * s]];  // slices sorted: first row is the longest
+            if (cur >= (int64_t(1) << 31) - 64) return set_err(CGVK_EINVAL, "band layout exceeds 2^31 entries");
+        }
     }
-    sp[nslots - 1] = (int)off;
-    a->sell_entries = off;
-    TRY(dalloc(&a->sell_ptr, nslots));
-    TRY(dalloc(&a->sell_ci, off + 32));
-    TRY(dalloc(&a->sell_va, off + 32));
-    CK(cudaMemcpyAsync(a->sell_ptr, sp.data(), sizeof(int) * nslots, cudaMemcpyHostToDevice, a->stream));
-    CK(cudaMemsetAsync(a->sell_ci, 0xff, sizeof(int) * (off + 32), a->stream));
-    CK(cudaMemsetAsync(a->sell_va, 0, sizeof(double) * (off + 32), a->stream));
+    for (size_t q = (size_t)nt * kWarps; q < off.size(); ++q) off[q] = (int)cur;
+    a->band_entries = cur;
+    int* dslot = nullptr;
+    TRY(dalloc(&a->band_off, off.size()));
+    TRY(dalloc(&a->band_meta, meta.size() + 1));
+    TRY(dalloc(&a->band_va, cur + 32));
+    TRY(dalloc(&a->band_ci, cur + 64));
+    TRY(dalloc(&dslot, slot_of.size()));
+    CK(cudaMemcpyAsync(a->band_off, off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice, a->stream));
+    CK(cudaMemcpyAsync(a->band_meta, meta.data(), sizeof(unsigned int) * meta.size(), cudaMemcpyHostToDevice,
+                       a->stream));
+    CK(cudaMemcpyAsync(dslot, slot_of.data(), sizeof(int) * slot_of.size(), cudaMemcpyHostToDevice, a->stream));
+    CK(cudaMemsetAsync(a->band_va, 0, sizeof(double) * (cur + 32), a->stream));
+    CK(cudaMemsetAsync(a->band_ci, 0, sizeof(unsigned short) * (cur + 64), a->stream));
     if (n > 0)
-        k_fill_sell<<<grid_elem(n), 256, 0, a->stream>>>((int)n, a->rp, a->ci, a->va, a->sell_ptr,
-                                                          a->sell_ci, a->sell_va);
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(a->stream));
+        k_fill_band<<<grid_elem(n), 256, 0, a->stream>>>((int)n, a->rp, a->ci, a->va, dslot, a->band_off, H,
+                                                          a->band_va, a->band_ci);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(a->stream);
+    cudaFree(dslot);
+    if (e != cudaSuccess) return set_err(CGVK_ECUDA, "band layout: %s", cudaGetErrorString(e));
+    a->band_h = H;
     return CGVK_OK;
 }
 
@@ -386,9 +432,23 @@ int matrix_create(int64_t n, int64_t ncols, const int64_t* row_ptr, const int64_
         if (hflags & 4) return bail(set_err(CGVK_EINVAL, "column indices not strictly increasing"));
         if (hflags & 8) return bail(set_err(CGVK_EINVAL, "matrix is not bitwise symmetric"));
     }
-    // the SELL-32 copy only backs the experimental direct SpMV engine
-    const char* eng = getenv("CGVK_SPMV_ENGINE");
-    if (eng && strcmp(eng, "sell") == 0 && (rc = build_sell(a, row_ptr)) != CGVK_OK) return bail(rc);
+    // SpMV engine: band (SELL-C-sigma + shared-memory x window) for a plain
+    // matrix with a narrow band and long rows, else the CSR tile pipeline.
+    // Flags choose explicitly; CGVK_SPMV_ENGINE=csr|band overrides (A/B runs).
+    {
+        int want = (flags & CGVK_MATRIX_ENGINE_CSR) ? 0 : (flags & CGVK_MATRIX_ENGINE_BAND) ? 1 : -1;
+        const char* eng = getenv("CGVK_SPMV_ENGINE");
+        if (eng && strcmp(eng, "csr") == 0) want = 0;
+        if (eng && strcmp(eng, "band") == 0) want = 1;
+        if (want != 0 && ncols == n && n > 0) {
+            const int H = band_half_width(n, row_ptr, col_idx);
+            const bool long_rows = nnz >= (int64_t)env_int("CGVK_BAND_MIN_ROW", 16) * n;
+            if (H >= 0 && (want == 1 || long_rows)) {
+                if ((rc = build_band(a, row_ptr, H)) != CGVK_OK) return bail(rc);
+                a->order = 1;  // the band kernels walk contiguous tile runs
+            }
+        }
+    }
     *out = a;
     return CGVK_OK;
 }
@@ -402,9 +462,10 @@ int cgvk_matrix_destroy(cgvk_matrix a) {
     cudaFree(a->rp);
     cudaFree(a->ci);
     cudaFree(a->va);
-    cudaFree(a->sell_ptr);
-    cudaFree(a->sell_ci);
-    cudaFree(a->sell_va);
+    cudaFree(a->band_off);
+    cudaFree(a->band_meta);
+    cudaFree(a->band_va);
+    cudaFree(a->band_ci);
     cudaFree(a->inv_diag);
     cudaFree(a->send_lo);
     cudaFree(a->send_hi);
@@ -423,6 +484,13 @@ int cgvk_matrix_info(cgvk_matrix a, int64_t* n, int64_t* nnz, int* device) {
     if (n) *n = a->n;
     if (nnz) *nnz = a->nnz;
     if (device) *device = a->device;
+    return CGVK_OK;
+}
+
+int cgvk_matrix_engine(cgvk_matrix a, int* engine, int* band_tiles) {
+    if (!a) return set_err(CGVK_EINVAL, "null matrix");
+    if (engine) *engine = a->band_h >= 0 ? CGVK_ENGINE_BAND : CGVK_ENGINE_CSR;
+    if (band_tiles) *band_tiles = a->band_h >= 0 ? a->band_h : 0;
     return CGVK_OK;
 }
 
@@ -577,30 +645,69 @@ int balanced_grid(int Gv, int cap) {
     return (Gv + per - 1) / per;
 }
 
-// Configure k_stream<Op> for matrix `a`: ring depth chosen so two CTAs fit
-// per SM when the stages allow it, physical grid = resident CTAs (<= Gv).
-// Tuning knobs (read once per solver; for experiments): CGVK_SPMV_ENGINE =
-// staged (default) | sell, CGVK_NSTAGE = ring depth, CGVK_SMEM_CTAS = CTAs per
-// SM the stage budget targets.
-bool spmv_sell() {
-    const char* v = getenv("CGVK_SPMV_ENGINE");
-    return v && strcmp(v, "sell") == 0;
+// The dynamic shared-memory attribute is per function: only ever raise it
+// (solvers of other matrices may already have launches captured with more).
+int raise_smem(const void* fn, size_t bytes) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, size_t>> set;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t* cur = nullptr;
+    for (auto& e : set)
+        if (e.first == fn) cur = &e.second;
+    if (!cur) {
+        set.emplace_back(fn, 0);
+        cur = &set.back().second;
+    }
+    if (bytes > *cur) {
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        *cur = bytes;
+    }
+    return CGVK_OK;
 }
 
+// Band engine launch (cgvk_band.cuh): NS-stage ring for meta + per-row
+// vectors, a window ring of 2H + NS tiles per gathered operand, the per-row
+// contribution buffers; grid = resident CTAs (<= Gv). Knobs (experiments):
+// CGVK_BAND_NSTAGE, CGVK_BAND_PF (L2 prefetch distance in tiles).
+template <class Op>
+int make_band(cgvk_matrix a, KLaunch* L) {
+    L->fn = k_band<Op>;
+    L->threads = kThreads;
+    StageCfg S{};
+    using Shape = BandShape<Op>;
+    S.nvec = Op::NV + Shape::NRAW;
+    S.stage_bytes = band_stage_bytes(S.nvec);
+    S.gvirt = a->G;
+    S.nstage = std::min(std::max(env_int("CGVK_BAND_NSTAGE", 2), 2), kMaxStages);
+    // raw windows are filled NS - 1 tiles ahead by the producer; a combined
+    // window one tile ahead by the consumers
+    S.ring = 2 * a->band_h + (Shape::XF ? 2 : S.nstage);
+    S.pf = std::max(env_int("CGVK_BAND_PF", 0), 0);  // measured: L2 bulk prefetch of the slices slows R4M
+    const int header = ((int)sizeof(PipeHeader) + 127) & ~127;
+    L->smem = (size_t)header + (size_t)S.nstage * S.stage_bytes + (size_t)Shape::NWIN * S.ring * kBlock * 8 +
+              (size_t)2 * Op::ND * kBlock * 8;
+    if (L->smem > (size_t)kSmemPerSM - 1024) return set_err(CGVK_EINVAL, "band window exceeds shared memory");
+    TRY(raise_smem((const void*)L->fn, L->smem));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L->fn, kThreads, L->smem));
+    if (occ < 1) return set_err(CGVK_ECUDA, "band kernel does not fit on an SM");
+    L->grid = balanced_grid(a->G, occ * a->sms);
+    L->S = S;
+    if (env_int("CGVK_DEBUG", 0))
+        fprintf(stderr, "cgvk launch %s: occ %d/SM grid %d smem %zu ring %d tiles\n", __func__, occ, L->grid,
+                L->smem, S.ring);
+    return CGVK_OK;
+}
+
+// Configure k_stream<Op> for matrix `a`: ring depth chosen so two CTAs fit
+// per SM when the stages allow it, physical grid = resident CTAs (<= Gv).
+// The SpMV kernels of a band-engine matrix run k_band instead. Tuning knobs
+// (experiments): CGVK_NSTAGE[_SPMV] = ring depth, CGVK_SMEM_CTAS[_SPMV] = CTAs
+// per SM the stage budget targets.
 template <class Op>
 int make_launch(cgvk_matrix a, KLaunch* L) {
-    if (Op::CSR && spmv_sell()) {  // SpMV kernels: direct engine over SELL-32
-        L->fn = k_direct<Op>;
-        StageCfg S{};
-        S.gvirt = a->G;
-        L->smem = 0;
-        int occ = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L->fn, kBlock, 0));
-        if (occ < 1) return set_err(CGVK_ECUDA, "SpMV kernel does not fit on an SM");
-        L->grid = balanced_grid(a->G, occ * a->sms);
-        L->threads = kBlock;
-        L->S = S;
-        return CGVK_OK;
+    if constexpr (Op::CSR) {
+        if (a->band_h >= 0) return make_band<Op>(a, L);
     }
     L->fn = k_stream<Op>;
     L->threads = kThreads;
@@ -630,23 +737,7 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
     L->smem = (size_t)header + (size_t)ns * S.stage_bytes;
     if (L->smem > (size_t)kSmemPerSM - 1024)
         return set_err(CGVK_EINVAL, "pipeline stage (%d bytes) exceeds shared memory", S.stage_bytes);
-    {   // the attribute is per function: only ever raise it (solvers of other
-        // matrices may already have launches captured with a larger stage)
-        static std::mutex mu;
-        static std::vector<std::pair<const void*, size_t>> set;
-        std::lock_guard<std::mutex> lock(mu);
-        size_t* cur = nullptr;
-        for (auto& e : set)
-            if (e.first == (const void*)L->fn) cur = &e.second;
-        if (!cur) {
-            set.emplace_back((const void*)L->fn, 0);
-            cur = &set.back().second;
-        }
-        if (L->smem > *cur) {
-            CK(cudaFuncSetAttribute(L->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L->smem));
-            *cur = L->smem;
-        }
-    }
+    TRY(raise_smem((const void*)L->fn, L->smem));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L->fn, kThreads, L->smem));
     if (occ < 1) return set_err(CGVK_ECUDA, "pipeline kernel does not fit on an SM");
@@ -1073,7 +1164,7 @@ int cgvk_solver_create(cgvk_matrix a, const cgvk_variant_config* cfg, int precon
     if ((rc = solver_init(s, b, x0)) != CGVK_OK) return bail(rc);
     if ((rc = capture(s, 1, &s->g1)) != CGVK_OK || (rc = capture(s, 8, &s->g8)) != CGVK_OK)
         return bail(rc);
-    s->persist = env_int("CGVK_PERSIST", 0) != 0;
+    s->persist = env_int("CGVK_PERSIST", 0) != 0 && a->band_h < 0;  // (no band persistent kernel)
     *out = s;
     return CGVK_OK;
 }

@@ -71,9 +71,12 @@ struct Params {
     double* rt;
     double* st;
     double* wt;
-    const int* __restrict__ sell_ptr;   // SELL-32: slice offsets (entries), nslices+1
-    const double* __restrict__ sell_va;
-    const int* __restrict__ sell_ci;    // -1 marks padding
+    // band engine (cgvk_band.cuh): SELL-C-sigma copy of A, null when unused
+    const int* __restrict__ band_off;             // slice offsets (entries), ntiles*8+1
+    const unsigned int* __restrict__ band_meta;   // per tile slot: len << 8 | tile-local row
+    const double* __restrict__ band_va;
+    const unsigned short* __restrict__ band_ci;   // column - (tile - band_h) * 256
+    int band_h;                                   // window half-width in tiles
     double* part;  // [kMaxDots][G] CTA partials
     double* hist;  // rr per iteration
     Ctrl* ctrl;

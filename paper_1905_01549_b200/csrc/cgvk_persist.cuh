@@ -70,7 +70,7 @@ __device__ __forceinline__ void persist_consume(const Params& P, const StageCfg&
             StageView V = stage_view(stages, S, slot);
             const int i = tile * kBlock + t;
             if (i < P.n) {
-                RowRef R{nullptr, nullptr, 0, 1};
+                RowRef R{nullptr, nullptr, 0};
                 if (Op::CSR) {
                     const int b = V.rp[t];
                     R.len = V.rp[t + 1] - b;
@@ -82,8 +82,7 @@ __device__ __forceinline__ void persist_consume(const Params& P, const StageCfg&
                         R.ci = V.ci + (b - H->k0c[slot]);
                     }
                 }
-                const int r0 = tile * kBlock;
-                op.row(P, i, StagedIn{V.vec + t, V.vec, r0, min(kBlock, P.n - r0)}, R, acc);
+                op.row(P, i, StagedIn{V.vec + t}, R, acc);
             }
             __syncwarp();
             if ((t & 31) == 0) mbar_arrive(&H->empty[slot]);

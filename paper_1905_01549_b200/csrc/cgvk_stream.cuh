@@ -46,7 +46,6 @@ template <class T>
 struct StagesOf<T, std::void_t<decltype(T::STAGES)>> {
     static constexpr int value = T::STAGES;
 };
-constexpr bool kInTileGather = false;
 
 struct StageCfg {
     int nstage;     // ring depth
@@ -54,6 +53,8 @@ struct StageCfg {
     int nvec;       // staged vectors
     int stage_bytes;
     int gvirt;      // Gv
+    int ring;       // band engine: window ring tiles (2H + nstage)
+    int pf;         // band engine: L2 prefetch distance (tiles)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -149,150 +150,223 @@ __device__ __forceinline__ bool arrive_last_c(unsigned int* counter, int* flag) 
     return last;
 }
 
-// A sparse row as seen by a thread: `len` entries at va[k*stride], ci[k*stride].
-// CSR (staged or global): stride 1, exactly the row's entries. SELL-32: stride
-// 32 (one warp = one slice), len = slice width, padding marked by ci < 0 (a
-// row-length predicate, never a padded multiply). Either way a row is summed
-// left to right in CSR column order (src/sparse_matrix.cpp:112-117).
-struct RowRef {
-    const double* va;
-    const int* ci;
-    int len, stride;
-};
-
 // The row is consumed in chunks of 8 entries: all column and value loads of a
 // chunk are issued first, then all of its gathers, then the in-order
 // accumulation — so a row costs ~2 memory latencies, not 2 per entry. Loads
-// past the row end / padding slots (ci < 0) are predicated off; padding is
-// never multiplied.
+// past the row end are predicated off; nothing past it is ever multiplied.
 #ifndef CGVK_CHUNK
 #define CGVK_CHUNK 8
 #endif
 constexpr int kChunk = CGVK_CHUNK;
 
-// Software-pipelined form (CGVK_ROW_PIPE=1): the next chunk's loads and
-// gathers are issued before the current chunk is accumulated, so a row of
-// c chunks costs ~1 + c/2 latencies instead of 2c (long rows, e.g. R4M).
+// A sparse row as seen by a thread: `len` entries, entry(k) = (column,
+// value) of its k-th entry in CSR column order; a row is always summed left
+// to right in that order (src/sparse_matrix.cpp:112-117).
+// RowRef: CSR (stage or global), the row's entries contiguous.
+struct RowRef {
+    static constexpr int CH = kChunk;  // entries per chunk
+    const double* va;
+    const int* ci;
+    int len;
+    __device__ __forceinline__ void entry(int k, int& c, double& v) const {
+        c = ci[k];
+        v = va[k];
+    }
+};
+
+#ifndef CGVK_BAND_LD
+#define CGVK_BAND_LD 0  // slice loads: 0 ld.global.cs, 1 ld.global.nc, 2 ld.global.cg
+#endif
+
+// BandRow: the band engine's SELL-C-sigma slice (cgvk_band.cuh) — entry k of
+// the thread's row at va[32 k], ci16[32 k] (the warp's 32 rows interleaved, so
+// every load is one coalesced warp access), the column stored as a 16-bit
+// offset from the tile's window base and returned as the index into the
+// shared-memory window ring (tb + offset, wrapped once at RW).
+template <int CHN>
+struct BandRow {
+    static constexpr int CH = CHN;
+    const double* va;
+    const unsigned short* ci;
+    int len, tb, rw;
+    __device__ __forceinline__ void entry(int k, int& c, double& v) const {
+#if CGVK_BAND_LD == 1
+        v = __ldg(va + 32 * k);
+        int q = tb + static_cast<int>(__ldg(ci + 32 * k));
+#elif CGVK_BAND_LD == 2
+        v = __ldcg(va + 32 * k);
+        int q = tb + static_cast<int>(__ldcg(ci + 32 * k));
+#else
+        v = __ldcs(va + 32 * k);
+        int q = tb + static_cast<int>(__ldcs(ci + 32 * k));
+#endif
+        c = q >= rw ? q - rw : q;
+    }
+};
+
+
+// Software-pipelined form (CGVK_ROW_PIPE=1, and always for the band engine,
+// whose matrix loads come from L2): the next chunk's column/value loads are
+// issued before the current chunk is gathered and accumulated.
 #ifndef CGVK_ROW_PIPE
 #define CGVK_ROW_PIPE 0
 #endif
+template <class RR>
+struct RowPipe {
+    static constexpr bool value = CGVK_ROW_PIPE != 0;
+};
+template <int C>
+struct RowPipe<BandRow<C>> {
+    static constexpr bool value = true;
+};
 
-template <class XF>
+template <class RR, class XF>
 struct ChunkBuf {
-    int c[kChunk];
-    double v[kChunk], x[kChunk];
-    __device__ __forceinline__ void load(const RowRef& R, int k0, XF xf) {
+    static constexpr int kC = RR::CH;
+    int c[kC];
+    double v[kC], x[kC];
+    // column/value loads of entries k0 .. k0+7
+    __device__ __forceinline__ void fetch(const RR& R, int k0) {
 #pragma unroll
-        for (int u = 0; u < kChunk; ++u) {
-            const bool in = k0 + u < R.len;
-            c[u] = in ? R.ci[(k0 + u) * R.stride] : -1;
-            v[u] = in ? R.va[(k0 + u) * R.stride] : 0.0;
+        for (int u = 0; u < RR::CH; ++u) {
+            c[u] = -1;
+            v[u] = 0.0;
+            if (k0 + u < R.len) R.entry(k0 + u, c[u], v[u]);
         }
+    }
+    // the gathers (depend on the columns)
+    __device__ __forceinline__ void resolve(XF xf) {
 #pragma unroll
-        for (int u = 0; u < kChunk; ++u) x[u] = c[u] >= 0 ? xf(c[u]) : 0.0;
+        for (int u = 0; u < RR::CH; ++u) x[u] = c[u] >= 0 ? xf(c[u]) : 0.0;
     }
     __device__ __forceinline__ void accumulate(double& sum) const {
 #pragma unroll
-        for (int u = 0; u < kChunk; ++u)
+        for (int u = 0; u < RR::CH; ++u)
             if (c[u] >= 0) sum = ADD(sum, MUL(v[u], x[u]));
     }
 };
 
-template <class XF>
-__device__ __forceinline__ double row_dot(const RowRef& R, XF xf) {
+template <class RR, class XF>
+__device__ __forceinline__ double row_dot(const RR& R, XF xf) {
     double sum = 0.0;
-    if constexpr (CGVK_ROW_PIPE) {
+    if constexpr (RowPipe<RR>::value) {
+        // chunk c+1's loads are in flight while chunk c is gathered and summed
         if (R.len <= 0) return sum;
-        ChunkBuf<XF> a, b;
-        a.load(R, 0, xf);
-        int k0 = 0;
-        for (;;) {
-            if (k0 + kChunk >= R.len) { a.accumulate(sum); break; }
-            b.load(R, k0 + kChunk, xf);
+        ChunkBuf<RR, XF> a, b;
+        a.fetch(R, 0);
+        for (int k0 = 0;; k0 += 2 * RR::CH) {
+            const bool more_b = k0 + RR::CH < R.len;
+            if (more_b) b.fetch(R, k0 + RR::CH);
+            a.resolve(xf);
             a.accumulate(sum);
-            k0 += kChunk;
-            if (k0 + kChunk >= R.len) { b.accumulate(sum); break; }
-            a.load(R, k0 + kChunk, xf);
+            if (!more_b) break;
+            const bool more_a = k0 + 2 * RR::CH < R.len;
+            if (more_a) a.fetch(R, k0 + 2 * RR::CH);
+            b.resolve(xf);
             b.accumulate(sum);
-            k0 += kChunk;
+            if (!more_a) break;
         }
-        return sum;
-    }
-    for (int k0 = 0; k0 < R.len; k0 += kChunk) {
-        int c[kChunk];
-        double v[kChunk], xv[kChunk];
-#pragma unroll
-        for (int u = 0; u < kChunk; ++u) {
-            const bool in = k0 + u < R.len;
-            c[u] = in ? R.ci[(k0 + u) * R.stride] : -1;
-            v[u] = in ? R.va[(k0 + u) * R.stride] : 0.0;
+    } else {
+        for (int k0 = 0; k0 < R.len; k0 += RR::CH) {
+            ChunkBuf<RR, XF> a;
+            a.fetch(R, k0);
+            a.resolve(xf);
+            a.accumulate(sum);
         }
-#pragma unroll
-        for (int u = 0; u < kChunk; ++u) xv[u] = c[u] >= 0 ? xf(c[u]) : 0.0;
-#pragma unroll
-        for (int u = 0; u < kChunk; ++u)
-            if (c[u] >= 0) sum = ADD(sum, MUL(v[u], xv[u]));
     }
     return sum;
 }
 
-template <class XF1, class XF2>
-__device__ __forceinline__ void row_dot2(const RowRef& R, XF1 xf1, XF2 xf2, double& y1, double& y2) {
-    double s1 = 0.0, s2 = 0.0;
-    for (int k0 = 0; k0 < R.len; k0 += kChunk) {
-        int c[kChunk];
-        double v[kChunk], x1[kChunk], x2[kChunk];
+// Two products over one traversal of the row (same per-product order).
+template <class RR, class XF1, class XF2>
+struct ChunkBuf2 {
+    static constexpr int kC = RR::CH;
+    int c[kC];
+    double v[kC], x1[kC], x2[kC];
+    __device__ __forceinline__ void fetch(const RR& R, int k0) {
 #pragma unroll
-        for (int u = 0; u < kChunk; ++u) {
-            const bool in = k0 + u < R.len;
-            c[u] = in ? R.ci[(k0 + u) * R.stride] : -1;
-            v[u] = in ? R.va[(k0 + u) * R.stride] : 0.0;
+        for (int u = 0; u < kC; ++u) {
+            c[u] = -1;
+            v[u] = 0.0;
+            if (k0 + u < R.len) R.entry(k0 + u, c[u], v[u]);
         }
+    }
+    __device__ __forceinline__ void resolve(XF1 f1, XF2 f2) {
 #pragma unroll
-        for (int u = 0; u < kChunk; ++u) {
-            x1[u] = c[u] >= 0 ? xf1(c[u]) : 0.0;
-            x2[u] = c[u] >= 0 ? xf2(c[u]) : 0.0;
+        for (int u = 0; u < kC; ++u) {
+            x1[u] = c[u] >= 0 ? f1(c[u]) : 0.0;
+            x2[u] = c[u] >= 0 ? f2(c[u]) : 0.0;
         }
+    }
+    __device__ __forceinline__ void accumulate(double& s1, double& s2) const {
 #pragma unroll
-        for (int u = 0; u < kChunk; ++u)
+        for (int u = 0; u < kC; ++u)
             if (c[u] >= 0) {
                 s1 = ADD(s1, MUL(v[u], x1[u]));
                 s2 = ADD(s2, MUL(v[u], x2[u]));
             }
     }
+};
+
+template <class RR, class XF1, class XF2>
+__device__ __forceinline__ void row_dot2(const RR& R, XF1 xf1, XF2 xf2, double& y1, double& y2) {
+    double s1 = 0.0, s2 = 0.0;
+    if constexpr (RowPipe<RR>::value) {
+        if (R.len > 0) {
+            ChunkBuf2<RR, XF1, XF2> a, b;
+            a.fetch(R, 0);
+            for (int k0 = 0;; k0 += 2 * RR::CH) {
+                const bool more_b = k0 + RR::CH < R.len;
+                if (more_b) b.fetch(R, k0 + RR::CH);
+                a.resolve(xf1, xf2);
+                a.accumulate(s1, s2);
+                if (!more_b) break;
+                const bool more_a = k0 + 2 * RR::CH < R.len;
+                if (more_a) a.fetch(R, k0 + 2 * RR::CH);
+                b.resolve(xf1, xf2);
+                b.accumulate(s1, s2);
+                if (!more_a) break;
+            }
+        }
+    } else {
+        for (int k0 = 0; k0 < R.len; k0 += RR::CH) {
+            ChunkBuf2<RR, XF1, XF2> a;
+            a.fetch(R, k0);
+            a.resolve(xf1, xf2);
+            a.accumulate(s1, s2);
+        }
+    }
     y1 = s1;
     y2 = s2;
 }
 
-// Per-row input accessors handed to Op::row: staged (shared memory) or direct.
-// in(v) = vector v at the thread's own row; in.gather(v, j, g) = vector v at
-// column j — from the stage when j lies in the tile (a stencil's +-1 and part
-// of its +-N neighbours), else from global g (L1/L2). Same bits either way.
+// Per-row input accessor handed to Op::row by the CSR pipeline: in(v) =
+// staged vector v at the thread's own row; in.gather(k, j, g) = gathered
+// operand k at column j, read from global g through L1/L2 (measured on B200,
+// profiles/r01: for stencils L1 serves the +-1/+-N neighbours better than a
+// shared-memory lookup with its divergent in-tile select).
 struct StagedIn {
-    const double* sv;    // stage vectors + t
-    const double* base;  // stage vectors
-    int r0, rows;
+    const double* sv;  // stage vectors + own row
     __device__ __forceinline__ double operator()(int v) const { return sv[v * kBlock]; }
-    // Measured on B200 (profiles/r01): serving in-tile columns from the stage
-    // is slower than L1 (divergent select + bank conflicts), so gathers always
-    // go through L1/L2; the stage path is kept for the in-tile experiment.
-    __device__ __forceinline__ double gather(int v, int j, const double* __restrict__ g) const {
-        if constexpr (kInTileGather) {
-            const unsigned o = static_cast<unsigned>(j - r0);
-            return o < static_cast<unsigned>(rows) ? base[v * kBlock + o] : __ldg(g + j);
-        }
-        return __ldg(g + j);
-    }
-};
-
-template <int NV>
-struct DirectIn {
-    const double* vp[NV > 0 ? NV : 1];  // by value: stays in registers
-    int i;
-    __device__ __forceinline__ double operator()(int v) const { return __ldg(vp[v] + i); }
     __device__ __forceinline__ double gather(int, int j, const double* __restrict__ g) const {
         return __ldg(g + j);
     }
+    // HS: p_j = r~_j + beta p_old_j formed at the gather
+    __device__ __forceinline__ double gather_p(int j, const double* __restrict__ rt, const double* __restrict__ po,
+                                               double beta) const {
+        return ADD(__ldg(rt + j), MUL(beta, __ldg(po + j)));
+    }
+};
+
+// Optional Op trait for the band engine: `static constexpr bool BAND_XF` — the
+// window holds band_xf(source 0, source 1) instead of the NG raw sources.
+template <class T, class = void>
+struct BandXf {
+    static constexpr bool value = false;
+};
+template <class T>
+struct BandXf<T, std::void_t<decltype(T::BAND_XF)>> {
+    static constexpr bool value = T::BAND_XF;
 };
 
 // Per-stage shared-memory layout.
@@ -496,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
             StageView V = stage_view(stages, S, slot);
             const int i = tile * kBlock + t;
             if (i < P.n) {
-                RowRef R{nullptr, nullptr, 0, 1};
+                RowRef R{nullptr, nullptr, 0};
                 if (Op::CSR) {
                     const int b = V.rp[t];
                     R.len = V.rp[t + 1] - b;
@@ -508,8 +582,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
                         R.ci = V.ci + (b - H->k0c[slot]);
                     }
                 }
-                const int r0 = tile * kBlock;
-                op.row(P, i, StagedIn{V.vec + t, V.vec, r0, min(kBlock, P.n - r0)}, R, acc);
+                op.row(P, i, StagedIn{V.vec + t}, R, acc);
             }
             __syncwarp();
             if ((t & 31) == 0) mbar_arrive(&H->empty[slot]);
@@ -534,83 +607,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
         if constexpr (Op::ND > 0) {
             fold_partials<Op::ND>(P.part, Gv, t, tot);
             cta_tree_c<Op::ND>(tot, H->red);
-        }
-    }
-    if (t == 0) {
-        *counter = 0u;
-        if (P.dist && mode == 2) {  // rank total: k_finalize folds all ranks in rank order
-#pragma unroll
-            for (int d = 0; d < Op::ND; ++d) P.rank_tot[d] = tot[d];
-            return;
-        }
-        op.finish(P, P.ctrl, tot);
-    }
-}
-
-// ------------------------------------------------------- direct engine
-//
-// The SpMV kernels: 256 threads, one row each, same virtual-CTA loop and
-// canonical reduction as k_stream, no shared-memory staging (all of L1 stays
-// with the x gathers). The matrix is read in SELL-32 layout (a warp's 32 rows
-// are one slice, entry k of the slice's rows contiguous), so every matrix
-// load is a fully coalesced 256 B (values) / 128 B (columns) warp access;
-// per-row vectors are plain coalesced loads.
-template <class Op>
-__global__ void __launch_bounds__(kBlock, 3) k_direct(Params P, StageCfg S) {
-    __shared__ double red[kMaxDots * 32];
-    __shared__ int last_flag;
-    pdl_wait();
-    pdl_trigger();
-    Op op;
-    if (!op.enter(P)) return;
-    const int Gv = S.gvirt, Gp = gridDim.x, ntiles = P.ntiles;
-    const int t = threadIdx.x, lane = t & 31;
-    DirectIn<Op::NV> in;
-#pragma unroll
-    for (int v = 0; v < Op::NV; ++v) in.vp[v] = op.vec(P, v);
-    double acc[Op::ND > 0 ? Op::ND : 1];
-    CGVK_FOR_VB(vb, P.order, blockIdx.x, Gv, Gp) {
-#pragma unroll
-        for (int d = 0; d < Op::ND; ++d) acc[d] = 0.0;
-        CGVK_FOR_TILE(tile, P.order, vb, ntiles, Gv) {
-            const int i = tile * kBlock + t;
-            const int slice = i >> 5;
-            RowRef R;
-            const int b = __ldg(P.sell_ptr + slice);
-            R.len = (__ldg(P.sell_ptr + slice + 1) - b) >> 5;
-            R.va = P.sell_va + b + lane;
-            R.ci = P.sell_ci + b + lane;
-            R.stride = 32;
-            in.i = i;
-            if (i < P.n) op.row(P, i, in, R, acc);
-        }
-        if constexpr (Op::ND > 0) {
-            if (op.sync() != 2) continue;
-            cta_tree<Op::ND>(acc, red);
-            if (t == 0) {
-#pragma unroll
-                for (int d = 0; d < Op::ND; ++d) P.part[d * Gv + vb] = acc[d];
-            }
-        }
-    }
-    const int mode = op.sync();
-    if (mode == 0) return;
-    unsigned int* counter = op.counter(P);
-    __syncthreads();
-    if (t == 0) {
-        __threadfence();
-        last_flag = atomicAdd(counter, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!last_flag) return;
-    __threadfence();
-    double tot[Op::ND > 0 ? Op::ND : 1];
-#pragma unroll
-    for (int d = 0; d < Op::ND; ++d) tot[d] = 0.0;
-    if (mode == 2) {
-        if constexpr (Op::ND > 0) {
-            fold_partials<Op::ND>(P.part, Gv, t, tot);
-            cta_tree<Op::ND>(tot, red);
         }
     }
     if (t == 0) {

@@ -18,8 +18,9 @@
 // launch with k_limit = k) before reading vectors. Terminal steps keep the
 // reference's partial-update semantics through `mode2` / `form_pending`.
 //
-// Staged per-row vectors are read as sv[v * kBlock]; SpMV operands are
-// gathered from global memory (L1/L2) by column index.
+// Staged per-row vectors are read as in(v); SpMV operands are gathered by
+// column as in.gather(k, j, g): operand k (0 <= k < NG, source gsrc(P, k)),
+// from global memory g (L1/L2) or from the band engine's shared-memory window.
 #pragma once
 
 #include "cgvk_stream.cuh"
@@ -55,8 +56,8 @@ struct HsK1 {
     __device__ const double* vec(const Params& P, int v) const { return v == 0 ? P.r : v == 1 ? P.s : P.d; }
     __device__ int sync() const { return 2; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[0]; }
-    template <class In>
-    __device__ void row(const Params& P, int i, const In& in, const RowRef&, double* acc) const {
+    template <class In, class RR>
+    __device__ void row(const Params& P, int i, const In& in, const RR&, double* acc) const {
         const double r = SUB(SV(0), MUL(alpha, SV(1)));
         P.r[i] = r;
         double rt = r;
@@ -108,10 +109,16 @@ struct HsK2 {
     __device__ const double* vec(const Params& P, int v) const {
         return v == 0 ? pold : v == 1 ? (PREC ? P.rt : P.r) : P.x;
     }
+    static constexpr int NG = 2;  // gathered: p_old, r~ (combined as p = r~ + beta p_old)
+    __device__ const double* gsrc(const Params& P, int k) const { return k == 0 ? pold : (PREC ? P.rt : P.r); }
+    // band engine: its window holds p itself, formed once per column from the
+    // two sources with the same expression as the on-the-fly gather
+    static constexpr bool BAND_XF = true;
+    __device__ double band_xf(double po, double rt) const { return ADD(rt, MUL(beta, po)); }
     __device__ int sync() const { return mode == MODE_FULL ? 2 : 1; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
-    template <class In>
-    __device__ void row(const Params& P, int i, const In& in, const RowRef& R, double* acc) const {
+    template <class In, class RR>
+    __device__ void row(const Params& P, int i, const In& in, const RR& R, double* acc) const {
         const double po = SV(0);
         P.x[i] = ADD(SV(2), MUL(alpha, po));
         if (mode != MODE_FULL) return;
@@ -119,7 +126,7 @@ struct HsK2 {
         const double* __restrict__ pg = pold;
         const double b = beta;
         const double sum =
-            row_dot(R, [&](int j) { return ADD(in.gather(1, j, rtv), MUL(b, in.gather(0, j, pg))); });
+            row_dot(R, [&](int j) { return in.gather_p(j, rtv, pg, b); });
         const double pi = ADD(SV(1), MUL(b, po));
         pnew[i] = pi;
         P.s[i] = sum;
@@ -169,8 +176,8 @@ struct CgK1 {
     }
     __device__ int sync() const { return (F && !S) ? 1 : 0; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[0]; }
-    template <class In>
-    __device__ void row(const Params& P, int i, const In& in, const RowRef&, double*) const {
+    template <class In, class RR>
+    __device__ void row(const Params& P, int i, const In& in, const RR&, double*) const {
         double p = SV(0), s = SV(1);
         const double r = SV(3);
         if (F) {
@@ -208,12 +215,14 @@ struct CgK2 {
             default: return unsimp ? P.p0 : nullptr;
         }
     }
+    static constexpr int NG = 1;  // gathered: r~
+    __device__ const double* gsrc(const Params& P, int) const { return PREC ? P.rt : P.r; }
     __device__ int sync() const { return 2; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
-    template <class In>
-    __device__ void row(const Params& P, int i, const In& in, const RowRef& R, double* acc) const {
+    template <class In, class RR>
+    __device__ void row(const Params& P, int i, const In& in, const RR& R, double* acc) const {
         const double* __restrict__ rtv = PREC ? P.rt : P.r;
-        const double w = row_dot(R, [&](int j) { return in.gather(1, j, rtv); });
+        const double w = row_dot(R, [&](int j) { return in.gather(0, j, rtv); });
         P.w[i] = w;
         const double ri = SV(0), rti = PREC ? SV(1) : ri;
         acc[0] = ADD(acc[0], MUL(rti, ri));
@@ -284,8 +293,8 @@ struct PrK1 {
     }
     __device__ int sync() const { return valid ? 0 : 2; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[0]; }
-    template <class In>
-    __device__ void row(const Params& P, int i, const In& in, const RowRef&, double* acc) const {
+    template <class In, class RR>
+    __device__ void row(const Params& P, int i, const In& in, const RR&, double* acc) const {
         const double s = SV(3), p = SV(1);
         P.x[i] = ADD(SV(0), MUL(alpha, p));
         const double r = SUB(SV(2), MUL(alpha, s));
@@ -326,10 +335,12 @@ struct PrK2 {
     __device__ const double* vec(const Params& P, int v) const {
         return v == 0 ? P.p0 : v == 1 ? P.r : v == 2 ? P.rt : P.d;
     }
+    static constexpr int NG = 1;  // gathered: p
+    __device__ const double* gsrc(const Params& P, int) const { return P.p0; }
     __device__ int sync() const { return 2; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
-    template <class In>
-    __device__ void row(const Params& P, int i, const In& in, const RowRef& R, double* acc) const {
+    template <class In, class RR>
+    __device__ void row(const Params& P, int i, const In& in, const RR& R, double* acc) const {
         const double* __restrict__ p = P.p0;
         const double s = row_dot(R, [&](int j) { return in.gather(0, j, p); });
         P.s[i] = s;
@@ -409,8 +420,8 @@ struct GvK1 {
     }
     __device__ int sync() const { return S ? 2 : 1; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[0]; }
-    template <class In>
-    __device__ void row(const Params& P, int i, const In& in, const RowRef&, double* acc) const {
+    template <class In, class RR>
+    __device__ void row(const Params& P, int i, const In& in, const RR&, double* acc) const {
         double p = SV(0), s = SV(1), u = SV(2), w = SV(3);
         double st = PREC ? SV(7) : s;
         double rt = PREC ? SV(8) : SV(6);
@@ -479,18 +490,20 @@ struct GvK1 {
     }
 };
 
-// t = A M w (streams: A, w [d] — staged for the in-tile gathers)
+// t = A M w (streams: A; gathers w~ = M w stored by K1)
 template <bool PREC>
 struct GvK2 {
-    static constexpr int NV = kInTileGather ? (PREC ? 2 : 1) : 0, ND = 0;
+    static constexpr int NV = 0, ND = 0;
     static constexpr bool CSR = true;
     static constexpr int STAGES = 2;  // measured: a shallower ring leaves L1 to the gathers
     __device__ bool enter(const Params& P) { return P.ctrl->mode2 != MODE_SKIP; }
-    __device__ const double* vec(const Params& P, int v) const { return v == 0 ? P.w : P.d; }
+    __device__ const double* vec(const Params&, int) const { return nullptr; }
+    static constexpr int NG = 1;  // gathered: w~
+    __device__ const double* gsrc(const Params& P, int) const { return PREC ? P.wt : P.w; }
     __device__ int sync() const { return 1; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
-    template <class In>
-    __device__ void row(const Params& P, int i, const In& in, const RowRef& R, double*) const {
+    template <class In, class RR>
+    __device__ void row(const Params& P, int i, const In& in, const RR& R, double*) const {
         const double* __restrict__ wtv = PREC ? P.wt : P.w;  // w~ stored by K1
         P.t[i] = row_dot(R, [&](int j) { return in.gather(0, j, wtv); });
     }
@@ -539,8 +552,8 @@ struct PprK1 {
     }
     __device__ int sync() const { return 2; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[0]; }
-    template <class In>
-    __device__ void row(const Params& P, int i, const In& in, const RowRef&, double* acc) const {
+    template <class In, class RR>
+    __device__ void row(const Params& P, int i, const In& in, const RR&, double* acc) const {
         const double p_old = SV(1), s_old = SV(3), w_old = SV(4), u = SV(5);
         P.x[i] = ADD(SV(0), MUL(alpha, p_old));
         const double r = SUB(SV(2), MUL(alpha, s_old));
@@ -624,24 +637,26 @@ struct PprK1 {
 };
 
 // (u, w) = A (s~, r~) in one traversal, or u = A s~ with recompute_w off
-// (streams: A, s~ r~ — staged for the in-tile gathers)
+// (streams: A; gathers s~, r~)
 template <bool PREC>
 struct PprK2 {
-    static constexpr int NV = kInTileGather ? 2 : 0, ND = 0;
+    static constexpr int NV = 0, ND = 0;
     static constexpr bool CSR = true;
     bool recw;
     __device__ bool enter(const Params& P) {
         recw = P.recompute_w != 0;
         return P.ctrl->mode2 != MODE_SKIP;
     }
-    __device__ const double* vec(const Params& P, int v) const {
-        if (v == 0) return PREC ? P.st : P.s;
+    __device__ const double* vec(const Params&, int) const { return nullptr; }
+    static constexpr int NG = 2;  // gathered: s~, r~ (the latter only with recompute_w)
+    __device__ const double* gsrc(const Params& P, int k) const {
+        if (k == 0) return PREC ? P.st : P.s;
         return recw ? (PREC ? P.rt : P.r) : nullptr;
     }
     __device__ int sync() const { return 1; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
-    template <class In>
-    __device__ void row(const Params& P, int i, const In& in, const RowRef& R, double*) const {
+    template <class In, class RR>
+    __device__ void row(const Params& P, int i, const In& in, const RR& R, double*) const {
         const double* __restrict__ sv_ = PREC ? P.st : P.s;
         const double* __restrict__ rv = PREC ? P.rt : P.r;
         if (recw) {
