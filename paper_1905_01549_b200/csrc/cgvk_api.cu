@@ -671,14 +671,14 @@ int raise_smem(const void* fn, size_t bytes) {
 // CGVK_BAND_NSTAGE, CGVK_BAND_PF (L2 prefetch distance in tiles).
 template <class Op>
 int make_band(cgvk_matrix a, KLaunch* L) {
-    L->fn = k_band<Op>;
-    L->threads = kThreads;
-    StageCfg S{};
     using Shape = BandShape<Op>;
+    L->fn = k_band<Op>;
+    L->threads = Shape::THREADS;
+    StageCfg S{};
     S.nvec = Op::NV + Shape::NRAW;
     S.stage_bytes = band_stage_bytes(S.nvec);
     S.gvirt = a->G;
-    S.nstage = std::min(std::max(env_int("CGVK_BAND_NSTAGE", 2), 2), kMaxStages);
+    S.nstage = std::min(std::max(env_int("CGVK_BAND_NSTAGE", 2 * Shape::GROUPS), 2), kMaxStages);
     // raw windows are filled NS - 1 tiles ahead by the producer; a combined
     // window one tile ahead by the consumers
     S.ring = 2 * a->band_h + (Shape::XF ? 2 : S.nstage);
@@ -689,7 +689,7 @@ int make_band(cgvk_matrix a, KLaunch* L) {
     if (L->smem > (size_t)kSmemPerSM - 1024) return set_err(CGVK_EINVAL, "band window exceeds shared memory");
     TRY(raise_smem((const void*)L->fn, L->smem));
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L->fn, kThreads, L->smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L->fn, L->threads, L->smem));
     if (occ < 1) return set_err(CGVK_ECUDA, "band kernel does not fit on an SM");
     L->grid = balanced_grid(a->G, occ * a->sms);
     L->S = S;

@@ -51,12 +51,23 @@ struct BandIn {
 
 // Windows a band kernel keeps (one when the Op combines its sources) and the
 // raw source tiles each stage carries for the consumers to combine.
+// Two-window kernels run one CTA per SM; those without dot products (pipe-PR's
+// block SpMV) then use two consumer groups of 8 warps that take alternate
+// tiles, for twice the loads in flight.
 template <class Op>
 struct BandShape {
     static constexpr bool XF = BandXf<Op>::value;
     static constexpr int NWIN = XF ? 1 : Op::NG;
     static constexpr int NRAW = XF ? Op::NG : 0;
+    static constexpr int GROUPS = (NWIN == 2 && Op::ND == 0) ? 2 : 1;
+    static constexpr int THREADS = GROUPS * kBlock + 32;
+    static constexpr int MINB = NWIN == 2 ? 1 : 2;
 };
+
+template <int N>
+__device__ __forceinline__ void named_sync1() {
+    asm volatile("bar.sync 1, %0;" ::"n"(N) : "memory");
+}
 
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
@@ -71,12 +82,14 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes
 #define CGVK_BAND_CHUNK2 8
 #endif
 
-template <class Op, int MINB = (BandShape<Op>::NWIN == 2 ? 1 : 2)>
-__global__ void __launch_bounds__(kThreads, MINB) k_band(Params P, StageCfg S) {
+template <class Op>
+__global__ void __launch_bounds__(BandShape<Op>::THREADS, BandShape<Op>::MINB) k_band(Params P, StageCfg S) {
     static_assert(Op::CSR && Op::NG <= kBandMaxNG, "band engine runs the SpMV kernels");
     using Shape = BandShape<Op>;
     constexpr bool XF = Shape::XF;
     constexpr int NWIN = Shape::NWIN;
+    constexpr int GR = Shape::GROUPS;
+    constexpr int NC = GR * kConsumers;  // consumer threads
     static_assert(!XF || Op::ND > 0, "a combined window relies on the per-tile contribution barrier");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PipeHeader* H = reinterpret_cast<PipeHeader*>(smem_raw);
@@ -103,8 +116,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_band(Params P, StageCfg S) {
     const int vb0 = span_lo(blockIdx.x, Gv, Gp), vb1 = span_lo(blockIdx.x + 1, Gv, Gp);
     const int T0 = span_lo(vb0, ntiles, Gv), T1 = span_lo(vb1, ntiles, Gv);
 
-    if (warp == kWarps) {  // ------------------------------ producer warp
-        if (threadIdx.x != kConsumers) return;
+    if (warp == GR * kWarps) {  // ------------------------- producer warp
+        if (threadIdx.x != NC) return;
         const uint64_t vpol = P.l2pol == 0 ? evict_first_policy() : 0;
         const double* vp[kMaxVec];
 #pragma unroll
@@ -176,7 +189,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_band(Params P, StageCfg S) {
     }
 
     // ------------------------------------------------------ consumer warps
-    const int t = threadIdx.x, lane = t & 31;
+    const int t = threadIdx.x & (kBlock - 1), lane = t & 31, grp = threadIdx.x / kBlock;
+    const int wg = warp & (kWarps - 1);  // warp within its group = slice
     if constexpr (XF) {
         // prologue: the window [T0 - H, T0 + H] of the first tile, combined
         // from global (later tiles get theirs from the stages)
@@ -195,12 +209,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_band(Params P, StageCfg S) {
         const int te = span_lo(vb + 1, ntiles, Gv);
         for (int tile = span_lo(vb, ntiles, Gv); tile < te; ++tile) {
             const int jj = j++;
+            if (GR > 1 && jj % GR != grp) continue;  // the other group's tile
             const int slot = jj % NS;
             mbar_wait(&H->full[slot], (jj / NS) & 1);
             const unsigned char* st = stages + (size_t)slot * S.stage_bytes;
             const unsigned int meta = reinterpret_cast<const unsigned int*>(st)[t];
             const int rl = meta & 255;
-            const int off = reinterpret_cast<const int*>(st + kBandMetaBytes)[warp];
+            const int off = reinterpret_cast<const int*>(st + kBandMetaBytes)[wg];
             const double* sv = reinterpret_cast<const double*>(st + kBandMetaBytes + kBandOffBytes);
             const int r0 = tile * kBlock;
             const int i = r0 + rl;
@@ -245,6 +260,21 @@ __global__ void __launch_bounds__(kThreads, MINB) k_band(Params P, StageCfg S) {
     const int mode = op.sync();
     if (mode == 0) return;
     unsigned int* counter = op.counter(P);
+    if constexpr (GR > 1) {  // no dots: arrive, the last CTA finishes
+        static_assert(GR == 1 || Op::ND == 0, "consumer groups only without dot products");
+        named_sync1<NC>();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            H->last_flag = atomicAdd(counter, 1u) == gridDim.x - 1;
+        }
+        named_sync1<NC>();
+        if (!H->last_flag || threadIdx.x != 0) return;
+        __threadfence();
+        *counter = 0u;
+        const double none[1] = {0.0};
+        op.finish(P, P.ctrl, none);
+        return;
+    }
     if (!arrive_last_c(counter, &H->last_flag)) return;
     double tot[Op::ND > 0 ? Op::ND : 1];
 #pragma unroll

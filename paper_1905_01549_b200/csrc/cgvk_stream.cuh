@@ -278,6 +278,10 @@ __device__ __forceinline__ double row_dot(const RR& R, XF xf) {
 }
 
 // Two products over one traversal of the row (same per-product order).
+// Pipelining it (CGVK_ROW2_PIPE=1) measured slower on R4M (register pressure).
+#ifndef CGVK_ROW2_PIPE
+#define CGVK_ROW2_PIPE 0
+#endif
 template <class RR, class XF1, class XF2>
 struct ChunkBuf2 {
     static constexpr int kC = RR::CH;
@@ -311,7 +315,7 @@ struct ChunkBuf2 {
 template <class RR, class XF1, class XF2>
 __device__ __forceinline__ void row_dot2(const RR& R, XF1 xf1, XF2 xf2, double& y1, double& y2) {
     double s1 = 0.0, s2 = 0.0;
-    if constexpr (RowPipe<RR>::value) {
+    if constexpr (RowPipe<RR>::value && CGVK_ROW2_PIPE) {
         if (R.len > 0) {
             ChunkBuf2<RR, XF1, XF2> a, b;
             a.fetch(R, 0);
