@@ -211,6 +211,49 @@ int cgvk_solve(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, const
                const double* x0, int max_iter, double rel_tol, double* x_out,
                cgvk_solve_status* st, cgvk_scalars* sc);
 
+/* ------------------------------------------------------ run() with probes
+ * run() (inc/runner.hpp:47-49, src/runner.cpp:32-147) with its StopRule
+ * (runner.hpp:9-36) and ProbeOptions (runner.hpp:38-42); every probe
+ * quantity (src/diagnostics.cpp:11-72) and the three-term Lanczos residual
+ * (:74-109) computed on the device from fresh products. */
+enum { CGVK_STOP_FIXED = 0, CGVK_STOP_ERROR_REDUCTION = 1, CGVK_STOP_STAGNATION = 2 };
+typedef struct cgvk_stop_rule {
+    int kind;                      /* CGVK_STOP_* (reference default: stagnation) */
+    int fixed_count;               /* StopRule::fixed */
+    double error_threshold;        /* on ||e_k||_A/||e_0||_A, needs x* (1e-5) */
+    int stagnation_window;         /* 50 */
+    double stagnation_improvement; /* 0.01 */
+} cgvk_stop_rule;
+typedef struct cgvk_probe_options {
+    int enabled;          /* reference default: 1 */
+    int cadence;          /* record every m-th iteration (+ k = 0, terminal, stop) */
+    const double* x_star; /* host, n; NULL disables rel_err_a_norm */
+} cgvk_probe_options;
+/* IterationRecord (inc/diagnostics.hpp:16-29): field f present iff mask bit f. */
+enum {
+    CGVK_REC_REL_ERR_A_NORM = 0, CGVK_REC_TRUE_RES_NORM, CGVK_REC_UPD_RES_NORM,
+    CGVK_REC_RESIDUAL_GAP_NORM, CGVK_REC_NU_GAP, CGVK_REC_W_GAP_NORM, CGVK_REC_S_GAP_NORM,
+    CGVK_REC_LANCZOS_RES_NORM, CGVK_REC_SUCC_ORTH, CGVK_REC_ALPHA, CGVK_REC_BETA, CGVK_REC_NU,
+    CGVK_REC_NU_PRIME, CGVK_REC_FIELDS
+};
+typedef struct cgvk_record {
+    int k;
+    unsigned mask;
+    double v[CGVK_REC_FIELDS];
+} cgvk_record;
+/* Summary (inc/diagnostics.hpp:54-57); has = 0 when absent. */
+typedef struct cgvk_summary {
+    int has;
+    int iters_to_1e5; /* -1 when never reached */
+    double min_log10_err;
+} cgvk_summary;
+/* Records beyond rec_cap are counted in *n_records but not stored. Errors as
+ * the reference: max_iter < 0, error-reduction stop without x*, x0 == x*. */
+int cgvk_run(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, const double* b,
+             const double* x0, int max_iter, const cgvk_stop_rule* stop,
+             const cgvk_probe_options* probe, cgvk_record* records, int rec_cap, int* n_records,
+             cgvk_solve_status* final_status, cgvk_summary* summary, double* x_out);
+
 /* ---------------------------------------------------- row-partitioned solve
  * (SURVEY §8(e)); the reference has no distributed code. Rank r owns rows
  * [lo[r], lo[r+1]); SpMV rows stay bit-identical to the reference for any P,

@@ -118,6 +118,10 @@ def _load_reference():
     L.cgvref_run.argtypes = [P, I, I, P, P, P, I, I, D, I, C.POINTER(I), C.POINTER(D),
                              C.POINTER(I), C.POINTER(I), I, P, P, P, P]
     L.cgvref_mt19937_64.argtypes = [C.c_uint64, I64, P]
+    L.cgvref_run_records.restype = I
+    L.cgvref_run_records.argtypes = [P, I, I, I, I, I, I, I, P, P, P, I, I, I, D, I, D, I, I, P,
+                                     C.POINTER(I), C.POINTER(I), C.POINTER(D), C.POINTER(I), I, P,
+                                     P, P]
     return L
 
 
@@ -340,6 +344,51 @@ def ref_read_mtx(path: str):
     if not h:
         raise ValueError(_ref.cgvref_last_error().decode())
     return RefMatrix(handle=h)
+
+
+RECORD_FIELDS = ("rel_err_a_norm", "true_res_norm", "upd_res_norm", "residual_gap_norm", "nu_gap",
+                 "w_gap_norm", "s_gap_norm", "lanczos_res_norm", "succ_orth", "alpha", "beta", "nu",
+                 "nu_prime")
+
+
+def ref_run_records(A, variant: int, precond: int, b, x0, x_star=None, max_iter: int = 100,
+                    stop=("fixed", 100), probes: bool = True, cadence: int = 1, nu_expr: int = -1,
+                    recompute_nu=True, recompute_w=True, unsimplified_mu=False, track_delta=False,
+                    rec_cap: int = 4096) -> dict:
+    """The reference's run() (proj/src/runner.cpp:32-147) with every probe field.
+    stop: ("fixed", count) | ("error", threshold) | ("stagnation", window, improvement)."""
+    m = RefMatrix(A)
+    b, x0 = _f64(b), _f64(x0)
+    xs = _f64(x_star) if x_star is not None else None
+    kind = {"fixed": 0, "error": 1, "stagnation": 2}[stop[0]]
+    fixed = stop[1] if kind == 0 else 0
+    thr = stop[1] if kind == 1 else 1e-5
+    win = stop[1] if kind == 2 else 50
+    imp = stop[2] if kind == 2 else 0.01
+    fs = (C.c_int * 3)()
+    hs, it, nrec = C.c_int(), C.c_int(), C.c_int()
+    mle = C.c_double()
+    rk = np.zeros(rec_cap, np.int32)
+    rm = np.zeros(rec_cap, np.uint32)
+    rv = np.zeros((rec_cap, 13))
+    rc = _ref.cgvref_run_records(m.h, variant, nu_expr, int(recompute_nu), int(recompute_w),
+                                 int(unsimplified_mu), int(track_delta), precond, _p(b), _p(x0),
+                                 _p(xs) if xs is not None else None, max_iter, kind, fixed, thr, win,
+                                 imp, int(probes), cadence, fs, C.byref(hs), C.byref(it),
+                                 C.byref(mle), C.byref(nrec), rec_cap, rk.ctypes.data,
+                                 rm.ctypes.data, rv.ctypes.data)
+    if rc:
+        raise ValueError(_ref.cgvref_last_error().decode())
+    cnt = min(nrec.value, rec_cap)
+    recs = []
+    for q in range(cnt):
+        r = {"k": int(rk[q])}
+        for f, name in enumerate(RECORD_FIELDS):
+            r[name] = float(rv[q, f]) if rm[q] >> f & 1 else None
+        recs.append(r)
+    return {"state": fs[0], "breakdown": fs[1], "criterion": fs[2], "records": recs,
+            "summary": ({"iters_to_1e5": it.value if it.value >= 0 else None,
+                         "min_log10_err": mle.value} if hs.value else None)}
 
 
 def ref_mt19937_64(seed: int, count: int) -> np.ndarray:

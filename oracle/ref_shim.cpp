@@ -341,6 +341,73 @@ int cgvref_run(void* a, int variant, int precond, const double* b, const double*
     }
 }
 
+// run() with every IterationRecord field (proj/include/cgvariants/diagnostics.hpp:16-29)
+// and the full StopRule / ProbeOptions (runner.hpp:9-45): golden fixtures for
+// the device run(). Per record: k, presence mask (bit f = field f present) and
+// 13 values in field order rel_err_a_norm, true_res_norm, upd_res_norm,
+// residual_gap_norm, nu_gap, w_gap_norm, s_gap_norm, lanczos_res_norm,
+// succ_orth, alpha, beta, nu, nu_prime.
+int cgvref_run_records(void* a, int variant, int nu_expr, int recompute_nu, int recompute_w,
+                       int unsimplified_mu, int track_delta, int precond, const double* b,
+                       const double* x0, const double* x_star, int max_iter, int stop_kind,
+                       int fixed_count, double threshold, int stag_window, double stag_improvement,
+                       int probes, int cadence, int* final_status /* state, breakdown, criterion */,
+                       int* has_summary, int* iters_to_1e5, double* min_log10_err, int* n_records,
+                       int rec_cap, int* rec_k, unsigned* rec_mask, double* rec_vals) {
+    auto* m = static_cast<SparseMatrix*>(a);
+    try {
+        const auto n = static_cast<std::size_t>(m->n);
+        Preconditioner pm = precond ? Preconditioner::jacobi(*m) : Preconditioner::identity();
+        DenseVector bv(b, b + n), xv(x0, x0 + n), xs;
+        if (x_star) xs.assign(x_star, x_star + n);
+        StopRule rule;
+        if (stop_kind == 0) {
+            rule = StopRule::fixed(fixed_count);
+        } else if (stop_kind == 1) {
+            rule = StopRule::error_reduction(threshold);
+        } else {
+            rule = StopRule::stagnation(stag_window, stag_improvement);
+        }
+        ProbeOptions probe;
+        probe.enabled = probes != 0;
+        probe.cadence = cadence;
+        probe.x_star = x_star ? &xs : nullptr;
+        ConvergenceHistory h = run(make_config(variant, nu_expr, recompute_nu, recompute_w,
+                                               unsimplified_mu, track_delta),
+                                   *m, pm, bv, xv, max_iter, rule, probe);
+        final_status[0] = static_cast<int>(h.final_status.state);
+        final_status[1] = static_cast<int>(h.final_status.breakdown);
+        final_status[2] = static_cast<int>(h.final_status.criterion);
+        *has_summary = h.summary.has_value();
+        *iters_to_1e5 = -1;
+        *min_log10_err = 0.0;
+        if (h.summary) {
+            if (h.summary->iters_to_1e5) *iters_to_1e5 = *h.summary->iters_to_1e5;
+            *min_log10_err = h.summary->min_log10_err;
+        }
+        int cnt = 0;
+        for (const auto& rec : h.records) {
+            if (cnt >= rec_cap) break;
+            const std::optional<double>* f[13] = {
+                &rec.rel_err_a_norm, &rec.true_res_norm, &rec.upd_res_norm, &rec.residual_gap_norm,
+                &rec.nu_gap, &rec.w_gap_norm, &rec.s_gap_norm, &rec.lanczos_res_norm, &rec.succ_orth,
+                &rec.alpha, &rec.beta, &rec.nu, &rec.nu_prime};
+            rec_k[cnt] = rec.k;
+            unsigned mask = 0;
+            for (int q = 0; q < 13; ++q) {
+                rec_vals[cnt * 13 + q] = f[q]->value_or(0.0);
+                if (f[q]->has_value()) mask |= 1u << q;
+            }
+            rec_mask[cnt] = mask;
+            ++cnt;
+        }
+        *n_records = static_cast<int>(h.records.size());
+        return 0;
+    } catch (...) {
+        return classify(std::current_exception());
+    }
+}
+
 // std::mt19937_64 stream, used to pin the generators' RNG.
 void cgvref_mt19937_64(uint64_t seed, int64_t count, uint64_t* out) {
     std::mt19937_64 e(seed);

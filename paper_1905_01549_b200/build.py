@@ -25,7 +25,7 @@ NVFLAGS = ["-std=c++17", "-O3", "-lineinfo", "--fmad=false", "-Xcompiler", "-fPI
 
 CUDA_SOURCES = ["cgvk_api.cu"]
 CUDA_DEPS = ["cgvk_api.cu", "cgvk_device.cuh", "cgvk_variants.cuh", "cgvk_generic.cuh",
-             "cgvk_stream.cuh", "cgvk_dist.cuh", "cgvk_group.inc", "cgvk_persist.cuh", "cgvk_band.cuh"]
+             "cgvk_stream.cuh", "cgvk_dist.cuh", "cgvk_group.inc", "cgvk_persist.cuh", "cgvk_band.cuh", "cgvk_run.inc"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:

@@ -127,6 +127,28 @@ class _Stats(C.Structure):
                                           "reductions")]
 
 
+RECORD_FIELDS = ("rel_err_a_norm", "true_res_norm", "upd_res_norm", "residual_gap_norm", "nu_gap",
+                 "w_gap_norm", "s_gap_norm", "lanczos_res_norm", "succ_orth", "alpha", "beta", "nu",
+                 "nu_prime")
+
+
+class _StopRule(C.Structure):
+    _fields_ = [("kind", C.c_int), ("fixed_count", C.c_int), ("error_threshold", C.c_double),
+                ("stagnation_window", C.c_int), ("stagnation_improvement", C.c_double)]
+
+
+class _ProbeOptions(C.Structure):
+    _fields_ = [("enabled", C.c_int), ("cadence", C.c_int), ("x_star", C.c_void_p)]
+
+
+class _Record(C.Structure):
+    _fields_ = [("k", C.c_int), ("mask", C.c_uint), ("v", C.c_double * len(RECORD_FIELDS))]
+
+
+class _Summary(C.Structure):
+    _fields_ = [("has", C.c_int), ("iters_to_1e5", C.c_int), ("min_log10_err", C.c_double)]
+
+
 def _load() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"cgvk CUDA library not built: {LIB_PATH} (run __graft_entry__.build())")
@@ -162,6 +184,9 @@ def _load() -> C.CDLL:
         "cgvk_solver_launches_per_iter": (I, [P]),
         "cgvk_solver_time_steps": (I, [P, I, C.POINTER(D), C.POINTER(I)]),
         "cgvk_solver_profile": (I, [P, I, C.POINTER(D), C.POINTER(D), C.POINTER(I)]),
+        "cgvk_run": (I, [P, C.POINTER(_Config), I, P, P, I, C.POINTER(_StopRule),
+                         C.POINTER(_ProbeOptions), P, I, C.POINTER(I), C.POINTER(_Status),
+                         C.POINTER(_Summary), P]),
         "cgvk_solve": (I, [P, C.POINTER(_Config), I, P, P, I, D, P, C.POINTER(_Status),
                            C.POINTER(_Scalars)]),
         "cgvk_host_register": (I, [P, C.c_uint64]),
@@ -514,6 +539,112 @@ def solve(A: DeviceMatrix, config: VariantConfig, precond: Precond, b, x0, max_i
     _check(_lib.cgvk_solve(A.handle, C.byref(c), int(precond), _ptr(b), _ptr(x0), int(max_iter),
                            float(rel_tol), _ptr(x), C.byref(st), C.byref(sc)))
     return x, SolveStatus(State(st.state), Breakdown(st.breakdown), ConvergedBy(st.criterion)), st.k
+
+
+# ------------------------------------------------------ run() with probes
+
+@dataclass
+class StopRule:
+    """StopRule (inc/runner.hpp:9-36); the default kind is ResidualStagnation."""
+    kind: str = "stagnation"  # "fixed" | "error_reduction" | "stagnation"
+    fixed_count: int = 0
+    error_threshold: float = 1e-5
+    stagnation_window: int = 50
+    stagnation_improvement: float = 0.01
+
+    @classmethod
+    def fixed(cls, count: int) -> "StopRule":
+        return cls("fixed", fixed_count=count)
+
+    @classmethod
+    def error_reduction(cls, threshold: float) -> "StopRule":
+        return cls("error_reduction", error_threshold=threshold)
+
+    @classmethod
+    def stagnation(cls, window: int = 50, improvement: float = 0.01) -> "StopRule":
+        return cls("stagnation", stagnation_window=window, stagnation_improvement=improvement)
+
+    def _to_c(self) -> _StopRule:
+        kind = {"fixed": 0, "error_reduction": 1, "stagnation": 2}[self.kind]
+        return _StopRule(kind, self.fixed_count, self.error_threshold, self.stagnation_window,
+                         self.stagnation_improvement)
+
+
+@dataclass
+class ProbeOptions:
+    """ProbeOptions (inc/runner.hpp:38-42): record every `cadence`-th iteration
+    (plus k = 0 and the last); x_star enables the A-norm error ratios."""
+    cadence: int = 1
+    x_star: np.ndarray | None = None
+    enabled: bool = True
+
+
+@dataclass
+class IterationRecord:
+    """IterationRecord (inc/diagnostics.hpp:16-29); absent fields are None."""
+    k: int = 0
+    rel_err_a_norm: float | None = None
+    true_res_norm: float | None = None
+    upd_res_norm: float | None = None
+    residual_gap_norm: float | None = None
+    nu_gap: float | None = None
+    w_gap_norm: float | None = None
+    s_gap_norm: float | None = None
+    lanczos_res_norm: float | None = None
+    succ_orth: float | None = None
+    alpha: float | None = None
+    beta: float | None = None
+    nu: float | None = None
+    nu_prime: float | None = None
+
+
+@dataclass
+class Summary:
+    iters_to_1e5: int | None
+    min_log10_err: float
+
+
+@dataclass
+class ConvergenceHistory:
+    """ConvergenceHistory (inc/diagnostics.hpp:62-69) plus the final x."""
+    config: VariantConfig
+    precond: Precond
+    records: list
+    final_status: SolveStatus
+    summary: Summary | None
+    x: np.ndarray
+
+
+def run(config: VariantConfig, A: DeviceMatrix, precond: Precond, b, x0, max_iter: int,
+        stop: StopRule | None = None, probe: ProbeOptions | None = None,
+        rec_cap: int | None = None) -> ConvergenceHistory:
+    """run() (inc/runner.hpp:47-49, src/runner.cpp:32-147) on the device:
+    every probe quantity from fresh device products and reductions."""
+    stop = stop if stop is not None else StopRule()
+    probe = probe if probe is not None else ProbeOptions()
+    b, x0 = _f64(b), _f64(x0)
+    xs = _f64(probe.x_star) if probe.x_star is not None else None
+    cap = rec_cap if rec_cap is not None else max_iter + 2
+    recs = (_Record * max(cap, 1))()
+    nrec = C.c_int()
+    st, summ = _Status(), _Summary()
+    x = np.empty(A.n)
+    c = config._to_c()
+    sr = stop._to_c()
+    po = _ProbeOptions(int(probe.enabled), int(probe.cadence), _ptr(xs) if xs is not None else None)
+    _check(_lib.cgvk_run(A.handle, C.byref(c), int(precond), _ptr(b), _ptr(x0), int(max_iter),
+                         C.byref(sr), C.byref(po), C.cast(recs, C.c_void_p), cap, C.byref(nrec),
+                         C.byref(st), C.byref(summ), _ptr(x)))
+    out = []
+    for q in range(min(nrec.value, cap)):
+        r = recs[q]
+        vals = {f: (float(r.v[i]) if r.mask >> i & 1 else None) for i, f in enumerate(RECORD_FIELDS)}
+        out.append(IterationRecord(k=r.k, **vals))
+    summary = (Summary(summ.iters_to_1e5 if summ.iters_to_1e5 >= 0 else None, summ.min_log10_err)
+               if summ.has else None)
+    return ConvergenceHistory(config, Precond(precond), out,
+                              SolveStatus(State(st.state), Breakdown(st.breakdown),
+                                          ConvergedBy(st.criterion)), summary, x)
 
 
 def host_register(arr: np.ndarray) -> None:

@@ -611,6 +611,7 @@ struct cgvk_solver_s {
     double *x = nullptr, *r = nullptr, *p0 = nullptr, *p1 = nullptr, *s = nullptr, *w = nullptr,
            *u = nullptr, *t = nullptr, *rt = nullptr, *st = nullptr, *wt = nullptr, *b = nullptr,
            *tmp = nullptr;
+    double* wpred = nullptr;  // run() with probes on a pipelined PR variant
     double *part = nullptr, *hist = nullptr, *dout = nullptr;
     unsigned int* counter = nullptr;
     int hist_cap = 0;
@@ -1018,7 +1019,7 @@ void free_solver(cgvk_solver s) {
     if (s->stream) cudaStreamSynchronize(s->stream);
     if (s->g1) cudaGraphExecDestroy(s->g1);
     if (s->g8) cudaGraphExecDestroy(s->g8);
-    for (double* p : {s->x, s->r, s->p0, s->p1, s->s, s->w, s->u, s->t, s->rt, s->st, s->wt, s->b,
+    for (double* p : {s->x, s->r, s->p0, s->p1, s->s, s->w, s->u, s->t, s->rt, s->st, s->wt, s->wpred, s->b,
                       s->tmp, s->part, s->hist, s->dout, s->rank_tot, s->all_tot, s->sbuf_lo, s->sbuf_hi,
                       s->rbuf_lo, s->rbuf_hi})
         cudaFree(p);
@@ -1038,6 +1039,67 @@ int materialize(cgvk_solver s) {
     k_set_limit<<<1, 1, 0, s->stream>>>(s->ctrl, s->k_target);
     CK(cudaGetLastError());
     return refresh_mirror(s);
+}
+
+// Device pointer to working vector `which` in the reference's state
+// (SolverState fields, inc/variants.hpp:108-111): deferred beta-recurrences
+// materialised, tilde vectors the fused schedule recomputes on the fly formed
+// into `scratch` (n doubles). CGVK_EINVAL when the variant does not allocate it.
+int vector_device(cgvk_solver s, int which, double* scratch, const double** out) {
+    const int v = s->cfg.variant;
+    const bool pipe = v == CGVK_PIPE_PR || v == CGVK_PIPE_PR_M;
+    const bool prec = s->prec;
+    const double* src = nullptr;
+    const double* scale_src = nullptr;  // out = d∘scale_src
+    bool zeros = false;
+    TRY(materialize(s));
+    const Ctrl& c = s->mirror;
+    switch (which) {
+        case CGVK_VEC_X: src = s->x; break;
+        case CGVK_VEC_R: src = s->r; break;
+        case CGVK_VEC_P: src = (v == CGVK_HS && c.pcur) ? s->p1 : s->p0; break;
+        case CGVK_VEC_S: src = s->s; break;
+        case CGVK_VEC_W: src = s->w; break;
+        case CGVK_VEC_U: src = s->u; break;
+        case CGVK_VEC_T: src = s->t; break;
+        case CGVK_VEC_R_TILDE:
+            if (!prec) break;
+            if (s->rt) src = s->rt;
+            else scale_src = s->r;
+            break;
+        case CGVK_VEC_S_TILDE:
+            if (!prec || v == CGVK_HS || v == CGVK_CG_CG) break;
+            if (s->st) src = s->st;
+            else scale_src = s->s;
+            break;
+        case CGVK_VEC_W_TILDE:
+            if (!prec || !(v == CGVK_GV || pipe)) break;
+            if (v == CGVK_GV) {
+                if (c.k == 0) zeros = true;  // resized, never applied before step 1
+                else scale_src = s->w;
+            } else if (!s->cfg.recompute_w || c.wt_stored) {
+                src = s->wt;
+            } else {
+                scale_src = s->w;
+            }
+            break;
+        case CGVK_VEC_U_TILDE:
+            if (!prec || !pipe) break;
+            scale_src = s->u;
+            break;
+        default: break;
+    }
+    if (!src && !scale_src && !zeros) return set_err(CGVK_EINVAL, "vector %d is not allocated by this variant", which);
+    if (zeros) {
+        CK(cudaMemsetAsync(scratch, 0, 8 * s->n, s->stream));
+        src = scratch;
+    } else if (scale_src) {
+        k_scale<<<grid_elem(s->n), 256, 0, s->stream>>>((int)s->n, s->a->inv_diag, scale_src, scratch);
+        CK(cudaGetLastError());
+        src = scratch;
+    }
+    *out = src;
+    return CGVK_OK;
 }
 
 }  // namespace
@@ -1256,64 +1318,13 @@ int cgvk_solver_status(cgvk_solver s, cgvk_solve_status* st, cgvk_scalars* sc, c
 
 int cgvk_solver_get_vector(cgvk_solver s, int which, double* out) {
     if (!s || !out) return set_err(CGVK_EINVAL, "null argument");
-    const int v = s->cfg.variant;
-    const bool pipe = v == CGVK_PIPE_PR || v == CGVK_PIPE_PR_M;
-    const bool prec = s->prec;
-    const double* src = nullptr;
-    const double* scale_src = nullptr;  // out = d∘scale_src
-    bool zeros = false;
     CK(cudaSetDevice(s->a->device));
     if (s->n == 0) {
         if (which == CGVK_VEC_X || which == CGVK_VEC_R || which == CGVK_VEC_P || which == CGVK_VEC_S)
             return CGVK_OK;
     }
-    TRY(materialize(s));
-    const Ctrl& c = s->mirror;
-    switch (which) {
-        case CGVK_VEC_X: src = s->x; break;
-        case CGVK_VEC_R: src = s->r; break;
-        case CGVK_VEC_P: src = (v == CGVK_HS && c.pcur) ? s->p1 : s->p0; break;
-        case CGVK_VEC_S: src = s->s; break;
-        case CGVK_VEC_W: src = s->w; break;
-        case CGVK_VEC_U: src = s->u; break;
-        case CGVK_VEC_T: src = s->t; break;
-        case CGVK_VEC_R_TILDE:
-            if (!prec) break;
-            if (s->rt) src = s->rt;
-            else scale_src = s->r;
-            break;
-        case CGVK_VEC_S_TILDE:
-            if (!prec || v == CGVK_HS || v == CGVK_CG_CG) break;
-            if (s->st) src = s->st;
-            else scale_src = s->s;
-            break;
-        case CGVK_VEC_W_TILDE:
-            if (!prec || !(v == CGVK_GV || pipe)) break;
-            if (v == CGVK_GV) {
-                if (c.k == 0) zeros = true;  // resized, never applied before step 1
-                else scale_src = s->w;
-            } else if (!s->cfg.recompute_w || c.wt_stored) {
-                src = s->wt;
-            } else {
-                scale_src = s->w;
-            }
-            break;
-        case CGVK_VEC_U_TILDE:
-            if (!prec || !pipe) break;
-            scale_src = s->u;
-            break;
-        default: break;
-    }
-    if (!src && !scale_src && !zeros) return set_err(CGVK_EINVAL, "vector %d is not allocated by this variant", which);
-    if (zeros) {
-        memset(out, 0, 8 * s->n);
-        return CGVK_OK;
-    }
-    if (scale_src) {
-        k_scale<<<grid_elem(s->n), 256, 0, s->stream>>>((int)s->n, s->a->inv_diag, scale_src, s->tmp);
-        CK(cudaGetLastError());
-        src = s->tmp;
-    }
+    const double* src = nullptr;
+    TRY(vector_device(s, which, s->tmp, &src));
     CK(cudaMemcpyAsync(out, src, 8 * s->n, cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
     return CGVK_OK;
@@ -1439,3 +1450,4 @@ int cgvk_solve(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, const
 }  // extern "C"
 
 #include "cgvk_group.inc"
+#include "cgvk_run.inc"

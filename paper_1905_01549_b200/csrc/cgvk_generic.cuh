@@ -127,6 +127,32 @@ __global__ void k_scale(int n, const double* __restrict__ d, const double* __res
         out[i] = d ? MUL(d[i], in[i]) : in[i];
 }
 
+// out = a - b (diagnostics' gap vectors, src/diagnostics.cpp:22-31,52-57)
+__global__ void k_sub(int n, const double* __restrict__ a, const double* __restrict__ b,
+                      double* __restrict__ out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[i] = SUB(a[i], b[i]);
+}
+
+// Three-term Lanczos recurrence residual, src/diagnostics.cpp:74-109:
+// q_k = sign_k r_{k-1} / ||r_{k-1}||, then d_i = (A q_k)_i - (c_{k+1} q_{k+1,i}
+// + c_k q_{k,i} + c_{k-1} q_{k-1,i}) with the same operation order.
+__global__ void k_lanczos_q(int n, double sign, const double* __restrict__ r, double nrm,
+                            double* __restrict__ q) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        q[i] = DIV(MUL(sign, r[i]), nrm);
+}
+__global__ void k_lanczos_d(int n, const double* __restrict__ lhs, const double* __restrict__ qk,
+                            const double* __restrict__ rk, double sign_kp1, double n_k,
+                            const double* __restrict__ rkm2, double sign_km1, double n_km2,
+                            double c_kp1, double c_k, double c_km1, double* __restrict__ d) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double q_kp1 = DIV(MUL(sign_kp1, rk[i]), n_k);
+        const double q_km1 = DIV(MUL(sign_km1, rkm2[i]), n_km2);
+        d[i] = SUB(lhs[i], ADD(ADD(MUL(c_kp1, q_kp1), MUL(c_k, qk[i])), MUL(c_km1, q_km1)));
+    }
+}
+
 struct DotArgs {
     int n, ntiles, order;
     const double* x[4];

@@ -565,6 +565,7 @@ struct PprK1 {
             P.rt[i] = rt;
         }
         const double wn = SUB(w_old, MUL(alpha, u));  // w'_k
+        if (P.wpred) P.wpred[i] = wn;                  // run()'s probes track the prediction
         double wtn = wn;
         if constexpr (PREC) {
             const double d = SV(8);

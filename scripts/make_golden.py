@@ -187,6 +187,44 @@ def cmd_config(name: str, variants: list[str]):
         os.replace(path + ".tmp", path)
 
 
+# run() with probes (proj/src/runner.cpp, proj/src/diagnostics.cpp): the
+# reference's records for a few problems x variants x {none, Jacobi} x stop
+# rules; oracle/run.py (seq order) must reproduce them, the device run() must
+# match oracle/run.py in its own order (tests/test_run*.py).
+RUN_CASES = [
+    # (id, stop, cadence, probes, max_iter)
+    ("fixed25", ("fixed", 25), 1, True, 60),
+    ("error1e-6", ("error", 1e-6), 1, True, 200),
+    ("stag5_c3", ("stagnation", 5, 0.01), 3, True, 80),
+    ("noprobe_stag", ("stagnation", 4, 0.05), 1, False, 60),
+]
+
+
+def run_problems():
+    return {"p2d_24": pb.make_problem("p2d_24", pb.poisson2d(24)),
+            "rs_600": pb.make_problem("rs_600", pb.random_spd(600, 7, 90, 5))}
+
+
+def cmd_run():
+    out = {"fields": list(O.RECORD_FIELDS), "cases": {}}
+    for pname, P in run_problems().items():
+        for v in range(7):
+            for prec in (0, 1):
+                for cid, stop, cad, probes, mx in RUN_CASES:
+                    r = O.ref_run_records(P.A, v, prec, P.b, P.x0, P.x_star, mx, stop, probes, cad)
+                    key = f"{pname}/{v}/{prec}/{cid}"
+                    out["cases"][key] = {
+                        "problem": pname, "variant": v, "precond": prec, "stop": list(stop),
+                        "cadence": cad, "probes": probes, "max_iter": mx,
+                        "state": r["state"], "breakdown": r["breakdown"], "criterion": r["criterion"],
+                        "summary": r["summary"],
+                        "records": [[rec["k"]] + [None if rec[f] is None else float(rec[f]).hex()
+                                                  for f in O.RECORD_FIELDS] for rec in r["records"]]}
+    with open(os.path.join(GOLDEN, "run_records.json"), "w") as f:
+        json.dump(out, f, sort_keys=True)
+    print(len(out["cases"]), "run() cases")
+
+
 if __name__ == "__main__":
     if not O.reference_available():
         sys.exit("oracle/_ref not built (make -C oracle ref)")
@@ -197,6 +235,8 @@ if __name__ == "__main__":
         cmd_table3()
     elif cmd == "small":
         cmd_small()
+    elif cmd == "run":
+        cmd_run()
     elif cmd == "config":
         cmd_config(sys.argv[2], sys.argv[3:] or ["hs", "cg", "m", "pr", "gv", "pipe-pr"])
     else:
