@@ -276,9 +276,12 @@ class SolveSet:
         cfgs = {v: VariantConfig.make(variant_from_name(v)) for v in VARIANTS}
         ranks = world if world > 1 else args.emulate_ranks
         if ranks <= 1:
+            t = time.perf_counter()
             self.mats = [cgvk.DeviceMatrix(A.n, rp, ci, va, device=device)]
+            self.t_matrix = time.perf_counter() - t
             for v in VARIANTS:
                 self.solvers[v] = cgvk.initialize(cfgs[v], self.mats[0], Precond.JACOBI, b, x0)
+            self.t_init = time.perf_counter() - t - self.t_matrix
             return
         lo = cgvk.partition_rows(A.n, ranks, ALIGN[args.config])
         Acsr = type(A)(A.n, rp, ci, va)
@@ -379,7 +382,7 @@ def run_gpu_arm(args, rank, local, world, dist):
         roof = {"bound": "hbm", "kernel": top["kernel"], "variant": top["variant"],
                 "achieved": top["gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": top["gbs"] / pk["hbm_gbs"], "peak_source": pk["source"],
-                "traffic": load_traffic().get(top["kernel"]),
+                "traffic": load_traffic().get(args.config, {}).get(top["kernel"]),
                 "bytes_per_launch": top["bytes_per_launch"], "ms_per_launch": top["ms_per_launch"]}
     else:  # partitioned: whole-iteration roofline of the slowest variant over all GPUs
         worst = min(VARIANTS, key=lambda v: per[v]["roofline_frac"])
@@ -402,6 +405,9 @@ def run_gpu_arm(args, rank, local, world, dist):
             t = time.perf_counter()
             E = SolveSet(args, P, rank, world, device, dist, pinned=tuple(arrs))
             ph["setup_ms"] = 1e3 * (time.perf_counter() - t)
+            if hasattr(E, "t_matrix"):
+                ph["matrix_upload_ms"] = 1e3 * E.t_matrix
+                ph["initialize_ms"] = 1e3 * E.t_init
             its = 0
             xx = None
             t = time.perf_counter()

@@ -179,6 +179,41 @@ static void test_run_fixed() {  // runner.hpp:47-49 with StopRule::fixed
     }
 }
 
+static void test_run_probes() {  // runner.cpp:32-147 + diagnostics.cpp on the device
+    const SparseMatrix a = laplace2d(20);
+    const Preconditioner m = Preconditioner::jacobi(a);
+    const DenseVector xs = random_vector(a.n, 11);
+    const DenseVector b = spmv(a, xs), x0(a.n, 0.0);
+    for (Variant v : kAll) {
+        ProbeOptions probe;
+        probe.x_star = &xs;
+        const ConvergenceHistory h =
+            run(VariantConfig::make(v), a, m, b, x0, 500, StopRule::error_reduction(1e-5), probe);
+        CHECK(h.final_status.state == SolveStatus::State::Converged);
+        CHECK(h.final_status.criterion == ConvergedBy::ErrorThreshold);
+        CHECK(h.summary.has_value() && h.summary->iters_to_1e5.has_value());
+        CHECK(*h.summary->iters_to_1e5 == h.records.back().k);
+        CHECK(*h.records.front().rel_err_a_norm == 1.0);
+        CHECK(*h.records.back().rel_err_a_norm < 1e-5);
+        CHECK(h.records.size() >= 3 && h.records[2].lanczos_res_norm.has_value());
+        CHECK(h.records[1].succ_orth.has_value() && std::abs(*h.records[1].succ_orth) < 1e-8);
+        CHECK(*h.records.back().residual_gap_norm < 1e-8 * *h.records.front().true_res_norm);
+        const bool pipelined = v == Variant::GV || v == Variant::PIPE_PR || v == Variant::PIPE_PR_M;
+        CHECK(h.records.back().s_gap_norm.has_value() == pipelined);
+        CHECK(h.records.back().w_gap_norm.has_value() == pipelined);
+        const bool predictor = v == Variant::M || v == Variant::PR || v == Variant::PIPE_PR ||
+                               v == Variant::PIPE_PR_M;
+        CHECK(h.records.back().nu_gap.has_value() == predictor);
+        // default rule: residual stagnation, probes on
+        const ConvergenceHistory g = run(VariantConfig::make(v), a, m, b, x0, 2000, StopRule{}, ProbeOptions{});
+        CHECK(g.final_status.state == SolveStatus::State::Converged);
+        CHECK(g.final_status.criterion == ConvergedBy::Stagnation);
+    }
+    CHECK_THROWS_AS(run(VariantConfig::make(Variant::HS), a, m, b, x0, 5, StopRule::error_reduction(1e-5),
+                        ProbeOptions{}),
+                    std::invalid_argument);
+}
+
 int main() {
     const std::pair<const char*, std::function<void()>> tests[] = {
         {"initialize_identity", test_initialize_identity},
@@ -188,6 +223,7 @@ int main() {
         {"block_spmv_and_jacobi", test_block_spmv_and_jacobi},
         {"validate", test_validate},
         {"run_fixed", test_run_fixed},
+        {"run_probes", test_run_probes},
     };
     for (const auto& [name, fn] : tests) {
         const int before = g_fail;

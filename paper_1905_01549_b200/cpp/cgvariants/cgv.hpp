@@ -347,9 +347,9 @@ inline void step_n(SolverState& st, int n_iters, double rel_tol = 0.0) {
 }
 
 // ------------------------------------------------------------------ runner
-// inc/runner.hpp: StopRule, ProbeOptions, run() — the hot-path subset:
-// FixedIterations with probes off runs entirely on the device; probes record
-// the quantities the device path provides (true/updated residual, scalars).
+// inc/runner.hpp + inc/diagnostics.hpp: StopRule, ProbeOptions,
+// IterationRecord, Summary, ConvergenceHistory, run() — the whole driver runs
+// on the device (cgvk_run): every probe quantity from fresh device products.
 
 struct StopRule {
     enum class Kind { FixedIterations, ErrorReduction, ResidualStagnation };
@@ -364,6 +364,19 @@ struct StopRule {
         r.fixed_count = count;
         return r;
     }
+    static StopRule error_reduction(double threshold) {
+        StopRule r;
+        r.kind = Kind::ErrorReduction;
+        r.error_threshold = threshold;
+        return r;
+    }
+    static StopRule stagnation(int window = 50, double improvement = 0.01) {
+        StopRule r;
+        r.kind = Kind::ResidualStagnation;
+        r.stagnation_window = window;
+        r.stagnation_improvement = improvement;
+        return r;
+    }
 };
 
 struct ProbeOptions {
@@ -374,54 +387,70 @@ struct ProbeOptions {
 
 struct IterationRecord {
     int k = 0;
-    std::optional<double> true_res_norm, upd_res_norm, alpha, beta, nu, nu_prime;
+    std::optional<double> rel_err_a_norm, true_res_norm, upd_res_norm, residual_gap_norm, nu_gap,
+        w_gap_norm, s_gap_norm, lanczos_res_norm, succ_orth, alpha, beta, nu, nu_prime;
+};
+
+struct Summary {
+    std::optional<int> iters_to_1e5;
+    double min_log10_err = 0.0;
 };
 
 struct ConvergenceHistory {
+    std::string problem_id;
     VariantConfig config;
     Preconditioner::Kind precond = Preconditioner::Kind::Identity;
     std::vector<IterationRecord> records;
     SolveStatus final_status;
+    std::optional<Summary> summary;
 };
 
 inline ConvergenceHistory run(const VariantConfig& config, const SparseMatrix& a,
                               const Preconditioner& m, const DenseVector& b, const DenseVector& x0,
                               int max_iter, const StopRule& stop, const ProbeOptions& probe_opts) {
     if (max_iter < 0) throw std::invalid_argument("max_iter must be >= 0");
-    if (stop.kind != StopRule::Kind::FixedIterations)
-        throw std::invalid_argument("device run(): only StopRule::fixed is on the hot path");
+    config.validate();
+    const auto n = static_cast<std::size_t>(a.n);
+    if (b.size() != n || x0.size() != n)
+        throw std::invalid_argument("right-hand side or initial guess dimension mismatch");
+    if (probe_opts.x_star && probe_opts.x_star->size() != n)
+        throw std::invalid_argument("x* dimension mismatch");
+    const cgvk_variant_config c = config.to_c();
+    const cgvk_stop_rule sr{static_cast<int>(stop.kind), stop.fixed_count, stop.error_threshold,
+                            stop.stagnation_window, stop.stagnation_improvement};
+    const cgvk_probe_options po{probe_opts.enabled ? 1 : 0, probe_opts.cadence,
+                                probe_opts.x_star ? probe_opts.x_star->data() : nullptr};
+    std::vector<cgvk_record> recs(static_cast<std::size_t>(max_iter) + 2);
+    int nrec = 0;
+    cgvk_solve_status fs{};
+    cgvk_summary sm{};
+    detail::check(cgvk_run(a.on_device(), &c, m.is_identity() ? CGVK_PRECOND_IDENTITY : CGVK_PRECOND_JACOBI,
+                           b.data(), x0.data(), max_iter, &sr, &po, recs.data(), static_cast<int>(recs.size()),
+                           &nrec, &fs, &sm, nullptr));
     ConvergenceHistory h;
     h.config = config;
     h.precond = m.kind;
-    SolverState st = initialize(config, a, m, b, x0);
-    st.sync_host = false;
-    auto probe = [&]() {
+    for (int q = 0; q < std::min(nrec, static_cast<int>(recs.size())); ++q) {
+        const cgvk_record& r = recs[q];
         IterationRecord rec;
-        rec.k = st.k;
-        double tr = 0.0;
-        detail::check(cgvk_solver_true_residual(st.device->h, &tr));
-        cgvk_scalars sc{};
-        detail::check(cgvk_solver_status(st.device->h, nullptr, &sc, nullptr));
-        rec.true_res_norm = tr;
-        rec.upd_res_norm = std::sqrt(sc.rr);
-        rec.alpha = st.alpha;
-        if (st.k >= 1) rec.beta = st.beta;
-        rec.nu = st.nu;
-        if (st.config.is_predictor() && st.k >= 1) rec.nu_prime = st.nu_prime;
+        rec.k = r.k;
+        std::optional<double>* f[CGVK_REC_FIELDS] = {
+            &rec.rel_err_a_norm, &rec.true_res_norm, &rec.upd_res_norm, &rec.residual_gap_norm,
+            &rec.nu_gap, &rec.w_gap_norm, &rec.s_gap_norm, &rec.lanczos_res_norm, &rec.succ_orth,
+            &rec.alpha, &rec.beta, &rec.nu, &rec.nu_prime};
+        for (int i = 0; i < CGVK_REC_FIELDS; ++i)
+            if (r.mask >> i & 1u) *f[i] = r.v[i];
         h.records.push_back(rec);
-    };
-    const int budget = std::min(max_iter, stop.fixed_count);
-    const int cadence = probe_opts.cadence >= 1 ? probe_opts.cadence : 1;
-    if (probe_opts.enabled) probe();
-    while (st.status.running() && st.k < budget) {
-        const int chunk = probe_opts.enabled ? std::min(cadence, budget - st.k) : budget - st.k;
-        detail::check(cgvk_solver_step(st.device->h, chunk));
-        detail::check(cgvk_solver_sync(st.device->h));
-        st.refresh();
-        if (probe_opts.enabled) probe();
     }
-    if (st.status.running()) st.status.state = SolveStatus::State::MaxIterations;
-    h.final_status = st.status;
+    h.final_status.state = static_cast<SolveStatus::State>(fs.state);
+    h.final_status.breakdown = static_cast<BreakdownReason>(fs.breakdown);
+    h.final_status.criterion = static_cast<ConvergedBy>(fs.criterion);
+    if (sm.has) {
+        Summary s;
+        if (sm.iters_to_1e5 >= 0) s.iters_to_1e5 = sm.iters_to_1e5;
+        s.min_log10_err = sm.min_log10_err;
+        h.summary = s;
+    }
     return h;
 }
 

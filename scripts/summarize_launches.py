@@ -4,9 +4,10 @@ dram__bytes_write.sum] --csv` launch list: per-kernel launch count, mean and
 total device time, each kernel's share of the solver-loop time (cold-cache,
 serialised: compare SHARES), and the measured DRAM bytes per launch.
 
-usage: summarize_launches.py launches.csv [traffic.json]
-With a second argument, writes {bench kernel name: DRAM bytes per launch}
-(median over launches) for bench.py's roofline.traffic."""
+usage: summarize_launches.py launches.csv [traffic.json config]
+With more arguments, merges {config: {bench kernel name: DRAM bytes per
+launch}} (median over launches) into traffic.json for bench.py's
+roofline.traffic."""
 import collections
 import csv
 import json
@@ -20,7 +21,7 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "
          "msecond": 1e3, "ns": 1e-3, "us": 1, "ms": 1e3}
 
 
-def main(path, traffic_out=None):
+def main(path, traffic_out=None, config=None):
     rows = list(csv.reader(open(path)))
     hdr = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
     h = rows[hdr]
@@ -56,9 +57,15 @@ def main(path, traffic_out=None):
             if op in OPS:
                 traffic[OPS[op]] = statistics.median(dram)
     if traffic_out:
+        try:
+            with open(traffic_out) as f:
+                allcfg = json.load(f)
+        except (OSError, ValueError):
+            allcfg = {}
+        allcfg[config] = traffic
         with open(traffic_out, "w") as f:
-            json.dump(traffic, f, indent=1, sort_keys=True)
+            json.dump(allcfg, f, indent=1, sort_keys=True)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None)
+    main(sys.argv[1], *(sys.argv[2:4] if len(sys.argv) > 3 else ()))
