@@ -275,7 +275,7 @@ class SolveSet:
         self.groups, self.solvers, self.comm, self.mats = [], {}, None, []
         cfgs = {v: VariantConfig.make(variant_from_name(v)) for v in VARIANTS}
         ranks = world if world > 1 else args.emulate_ranks
-        if ranks <= 1:
+        if ranks <= 1 and not args.nccl:
             t = time.perf_counter()
             self.mats = [cgvk.DeviceMatrix(A.n, rp, ci, va, device=device)]
             self.t_matrix = time.perf_counter() - t
@@ -283,12 +283,14 @@ class SolveSet:
                 self.solvers[v] = cgvk.initialize(cfgs[v], self.mats[0], Precond.JACOBI, b, x0)
             self.t_init = time.perf_counter() - t - self.t_matrix
             return
+        ranks = max(ranks, 1)
         lo = cgvk.partition_rows(A.n, ranks, ALIGN[args.config])
         Acsr = type(A)(A.n, rp, ci, va)
-        if world > 1:  # NCCL: this process drives rank `rank`
+        if world > 1 or args.nccl:  # NCCL: this process drives rank `rank`
             nid = cgvk.nccl_unique_id() if rank == 0 else None
             obj = [nid]
-            dist.broadcast_object_list(obj, src=0)
+            if dist is not None:
+                dist.broadcast_object_list(obj, src=0)
             self.comm = cgvk.Comm(world, rank, device, obj[0])
             mine = [rank]
         else:
@@ -320,7 +322,7 @@ def run_gpu_arm(args, rank, local, world, dist):
     P = pb.config_problem(args.config)
     n, nnz = P.A.n, P.A.nnz
     pk = peaks()
-    partitioned = world > 1 or args.emulate_ranks > 1
+    partitioned = world > 1 or args.emulate_ranks > 1 or args.nccl
     S = SolveSet(args, P, rank, world, device, dist)
     for v, s in S.solvers.items():  # warm-up: graphs, clocks, caches
         s.time_steps(args.warmup)
@@ -338,7 +340,7 @@ def run_gpu_arm(args, rank, local, world, dist):
         barrier(dist)
         ms, it = s.time_steps(args.steps)
         ms = max_over_ranks(dist, ms)
-        per[v] = {"ms": ms, "iters": it}
+        per[v] = {"ms": ms, "iters": it, "launches_per_iter": s.launches_per_iter()}
         total_ms += ms
         total_iters += it
     if clocks:
@@ -455,11 +457,14 @@ def run_gpu_arm(args, rank, local, world, dist):
 
     value = total_iters / (total_ms * 1e-3)
     if rank == 0:
-        launches = sum(1 + 2 * per[v]["iters"] for v in VARIANTS)
+        # our kernels in the timed region: one limit-setting launch per step()
+        # call + the captured kernels per iteration (halo pack/unpack and
+        # finalize kernels included when partitioned; NCCL's own not counted)
+        launches = sum(1 + per[v]["launches_per_iter"] * per[v]["iters"] for v in VARIANTS)
         cfg = workload_config(args, P)
         if partitioned:
-            cfg["parallelism"] = (f"row-partitioned z-slabs over {world} GPUs (NCCL)" if world > 1 else
-                                  f"row-partitioned, {args.emulate_ranks} in-process ranks on 1 GPU")
+            cfg["parallelism"] = (f"row-partitioned z-slabs over {world} GPUs (NCCL)" if world > 1 or args.nccl
+                                  else f"row-partitioned, {args.emulate_ranks} in-process ranks on 1 GPU")
         line = {
             "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -469,7 +474,7 @@ def run_gpu_arm(args, rank, local, world, dist):
             "roofline": roof,
             "kernels": kernels,
             "per_variant": per,
-            "gpu_launches": launches * (1 if world > 1 else max(args.emulate_ranks, 1)),
+            "gpu_launches": launches * world,  # every rank launches its own (counted on rank 0)
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clk,
@@ -489,6 +494,8 @@ def main():
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--nccl", action="store_true",
+                    help="row-partitioned path over NCCL even at one rank (transport check)")
     ap.add_argument("--emulate-ranks", type=int, default=1,
                     help="row-partitioned solve with P in-process ranks on one GPU")
     args = ap.parse_args()

@@ -1030,6 +1030,7 @@ void free_solver(cgvk_solver s) {
 }
 
 int group_step_all(cgvk_solver s, int n_iters);  // cgvk_group.inc
+int group_launches_per_iter(cgvk_solver s);      // cgvk_group.inc
 
 int materialize(cgvk_solver s) {
     TRY(refresh_mirror(s));
@@ -1365,7 +1366,10 @@ int cgvk_solver_history(cgvk_solver s, double* out, int cap, int* len) {
 
 void* cgvk_solver_stream(cgvk_solver s) { return s ? (void*)s->stream : nullptr; }
 
-int cgvk_solver_launches_per_iter(cgvk_solver s) { return s ? 2 : 0; }
+int cgvk_solver_launches_per_iter(cgvk_solver s) {
+    if (!s) return 0;
+    return s->group ? group_launches_per_iter(s) : 2;
+}
 
 int cgvk_solver_time_steps(cgvk_solver s, int n_iters, double* ms, int* iters) {
     if (!s || !ms || !iters) return set_err(CGVK_EINVAL, "null argument");

@@ -129,3 +129,30 @@ def test_group_ablations(kw):
         o.step()
     compare(g, o, f"ablation {kw}")
     g.close()
+
+
+@pytest.mark.parametrize("variant", [Variant.HS, Variant.CG_CG, Variant.PR, Variant.GV, Variant.PIPE_PR])
+def test_nccl_transport_single_rank(variant):
+    """The NCCL transport (dlopen'ed libnccl, ncclCommInitRank, the captured
+    AllGather of the rank totals and the grouped halo Send/Recv) on a
+    one-rank communicator — the only NCCL size one GPU admits — bit-exact vs
+    the partitioned oracle, through several graph-replayed batches."""
+    P, align = problem("poisson3d_12_slabs")
+    A = P.A
+    lo = cgvk.partition_rows(A.n, 1, align)
+    mats = [cgvk.RankMatrix(A.n, lo, 0, *cgvk.local_rows(A, lo, 0))]
+    comm = cgvk.Comm(1, 0, 0, cgvk.nccl_unique_id())
+    assert comm.kind == "nccl"
+    g = cgvk.Group(comm, mats, cgvk.VariantConfig.make(variant), Precond.JACOBI, [P.b], [P.x0])
+    block, gmax, order = mats[0].reduction_config()
+    o = O.Restatement(A, int(variant), 1, P.b, P.x0, dot=("part", block, gmax, lo, order))
+    compare(g, o, f"nccl1/{variant.name} init")
+    for k in (1, 8, 3):
+        g.step(k)
+        g.sync()
+        for _ in range(k):
+            if o.state()["state"] == 0:
+                o.step()
+        compare(g, o, f"nccl1/{variant.name} k={o.state()['k']}")
+    g.close()
+    comm.close()
