@@ -826,10 +826,10 @@ int ref_allocated(int v, bool prec) {
 // kernel drains, and synchronises with griddepcontrol.wait before reading its
 // results. CGVK_PDL=0 turns it off (for A/B measurements).
 void launch(cgvk_solver s, const KLaunch& L) {
-    // measured (profiles/r01): PDL gains 3-5 % on every variant except HS,
-    // whose short reducing K1 loses ~10 % to it with 3-CTA SpMV kernels
+    // measured (profiles/r01): PDL gains 3-5 % on every variant; HS's kernels
+    // signal their dependents late (PdlLate), else HS loses ~10 % to it
     static const int pdl_env = env_int("CGVK_PDL", -1);
-    const bool pdl = pdl_env >= 0 ? pdl_env != 0 : s->cfg.variant != CGVK_HS;
+    const bool pdl = pdl_env >= 0 ? pdl_env != 0 : true;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(L.grid);
     cfg.blockDim = dim3(L.threads);

@@ -47,6 +47,7 @@ template <bool PREC>
 struct HsK1 {
     static constexpr int NV = PREC ? 3 : 2, ND = 2;
     static constexpr bool CSR = false;
+    static constexpr bool PDL_LATE = true;  // see cgvk_stream.cuh PdlLate
     double alpha;
     __device__ bool enter(const Params& P) {
         if (!step_wanted(P.ctrl)) return false;
@@ -91,6 +92,7 @@ template <bool PREC>
 struct HsK2 {
     static constexpr int NV = 3, ND = 1;
     static constexpr bool CSR = true;
+    static constexpr bool PDL_LATE = true;
     int mode;
     const double* pold;
     double* pnew;
