@@ -88,12 +88,16 @@ enum {
     CGVK_MATRIX_CHECK_SYMMETRIC = 1, /* is_symmetric (src/sparse_matrix.cpp:84-107) */
     CGVK_MATRIX_ENGINE_CSR = 2,      /* SpMV kernels: TMA-staged CSR tiles only */
     CGVK_MATRIX_ENGINE_BAND = 4,     /* SpMV kernels: band engine whenever it applies */
+    CGVK_MATRIX_ENGINE_SEG = 8,      /* SpMV kernels: segment-window engine whenever it applies */
 };
 
 /* SpMV engine of a matrix (cgvk_matrix_engine). Without an ENGINE flag the
  * band engine (SELL-C-sigma + shared-memory x window) is chosen when every
- * tile's columns lie within a narrow band and rows are long; otherwise CSR. */
-enum { CGVK_ENGINE_CSR = 0, CGVK_ENGINE_BAND = 1 };
+ * tile's columns lie within a narrow band and rows are long; otherwise CSR
+ * with x gathered through L1/L2. The segment-window engine (TMA-staged CSR
+ * with 16-bit columns into the x tiles staged with each tile; needs all
+ * columns within at most 8 tile offsets, e.g. stencils) is opt-in. */
+enum { CGVK_ENGINE_CSR = 0, CGVK_ENGINE_BAND = 1, CGVK_ENGINE_SEG = 2 };
 
 /* POD mirror of VariantConfig (inc/variants.hpp:34-57). */
 typedef struct cgvk_variant_config {
@@ -145,7 +149,8 @@ int cgvk_matrix_create_csr(int64_t n, const int64_t* row_ptr, const int64_t* col
 int cgvk_matrix_destroy(cgvk_matrix a);
 int cgvk_matrix_info(cgvk_matrix a, int64_t* n, int64_t* nnz, int* device);
 /* Engine the variant SpMV kernels use for `a` and, for the band engine, the
- * x-window half-width in 256-row tiles (0 for CSR). */
+ * x-window half-width in 256-row tiles (segment engine: the number of tile
+ * offsets; 0 for CSR). */
 int cgvk_matrix_engine(cgvk_matrix a, int* engine, int* band_tiles);
 
 /* spmv (inc/sparse_matrix.hpp:41-42, src/sparse_matrix.cpp:109-118): y = A*x,

@@ -296,12 +296,13 @@ class VariantConfig:
 class DeviceMatrix:
     """SparseMatrix resident on one GPU (int32 CSR + fp64 values)."""
 
-    ENGINES = {None: 0, "csr": 2, "band": 4}
+    ENGINES = {None: 0, "csr": 2, "band": 4, "seg": 8}
 
     def __init__(self, n: int, row_ptr, col_idx, values, device: int = 0,
                  check_symmetric: bool = False, engine: str | None = None):
-        """engine: None = automatic (band for narrow-band long-row matrices),
-        "csr" or "band" (the band engine whenever it applies)."""
+        """engine: None = automatic (band for narrow-band long-row matrices,
+        seg for stencil-like ones), or "csr" / "band" / "seg" (that engine
+        whenever it applies)."""
         rp, ci, va = _i64(row_ptr), _i64(col_idx), _f64(values)
         if rp.shape[0] != n + 1:
             raise InvalidArgument(-1, "row_ptr length must be n+1")
@@ -323,10 +324,11 @@ class DeviceMatrix:
         return cls(csr.n, csr.row_ptr, csr.col_idx, csr.values, device, check_symmetric, engine)
 
     def engine(self) -> tuple[str, int]:
-        """("csr" | "band", x-window half-width in 256-row tiles)."""
+        """("csr" | "band" | "seg", band: x-window half-width in 256-row
+        tiles; seg: number of staged x-tile offsets; csr: 0)."""
         e, h = C.c_int(), C.c_int()
         _check(_lib.cgvk_matrix_engine(self._h, C.byref(e), C.byref(h)))
-        return ("band" if e.value == 1 else "csr"), h.value
+        return ("csr", "band", "seg")[e.value], h.value
 
     @property
     def handle(self):

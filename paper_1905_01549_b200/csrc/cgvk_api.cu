@@ -107,6 +107,10 @@ struct cgvk_matrix_s {
     double* band_va = nullptr;
     unsigned short* band_ci = nullptr;
     int64_t band_entries = 0;
+    // segment-window engine (cgvk_stream.cuh SEG): tile offsets + 16-bit columns
+    int seg_nd = 0;
+    int seg_d[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned short* ci16 = nullptr;
     double* inv_diag = nullptr;  // built on first use
     int jacobi_state = 0;        // 0 not built, 1 ok, -1 missing/non-positive diagonal
     cudaStream_t stream = nullptr;
@@ -131,6 +135,9 @@ struct cgvk_matrix_s {
         P.band_va = band_va;
         P.band_ci = band_ci;
         P.band_h = band_h;
+        P.ci16 = ci16;
+        P.seg_nd = seg_nd;
+        for (int q = 0; q < 8; ++q) P.seg_d[q] = seg_d[q];
         P.order = order;
         P.l2pol = l2pol;
         return P;
@@ -231,6 +238,54 @@ __global__ void k_fill_band(int n, const int* __restrict__ rp, const int* __rest
             bci[base + 32 * e] = (unsigned short)(ci[k] - wb);
         }
     }
+}
+
+// Segment-window layout: the set D of tile offsets (tile(col) - tile(row))
+// over the whole matrix; applicable when |D| <= 8 (a 7-point stencil has
+// {-N^2/256, -1, 0, 1, N^2/256} for N^2 a multiple of 256).
+constexpr int kSegMax = 8;
+
+int seg_offsets(int64_t n, const int64_t* row_ptr, const int64_t* col_idx, int* d) {
+    int nd = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t t = i / kBlock;
+        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
+            const int64_t off = col_idx[k] / kBlock - t;
+            int q = 0;
+            while (q < nd && d[q] != off) ++q;
+            if (q == nd) {
+                if (nd == kSegMax) return -1;
+                d[nd++] = (int)off;
+            }
+        }
+    }
+    std::sort(d, d + nd);
+    return nd;
+}
+
+__global__ void k_fill_ci16(int n, const int* __restrict__ rp, const int* __restrict__ ci, int nd, Params P,
+                            unsigned short* out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int t = i / kBlock;
+        for (int k = rp[i]; k < rp[i + 1]; ++k) {
+            const int off = ci[k] / kBlock - t;
+            int q = 0;
+            while (q < nd - 1 && P.seg_d[q] != off) ++q;
+            out[k] = (unsigned short)(q * kBlock + (ci[k] & (kBlock - 1)));
+        }
+    }
+}
+
+int build_seg(cgvk_matrix a, const int* d, int nd) {
+    a->seg_nd = nd;
+    for (int q = 0; q < nd; ++q) a->seg_d[q] = d[q];
+    TRY(dalloc(&a->ci16, a->nnz + 32));
+    CK(cudaMemsetAsync(a->ci16, 0, 2 * (a->nnz + 32), a->stream));
+    if (a->n > 0)
+        k_fill_ci16<<<grid_elem(a->n), 256, 0, a->stream>>>((int)a->n, a->rp, a->ci, nd, a->base(), a->ci16);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(a->stream));
+    return CGVK_OK;
 }
 
 int build_band(cgvk_matrix a, const int64_t* row_ptr, int H) {
@@ -367,11 +422,12 @@ int matrix_create(int64_t n, int64_t ncols, const int64_t* row_ptr, const int64_
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     a->sms = sms;
     a->gmax = sms * kVirtualPerSM;
-    {   // stage capacity: the largest tile's CSR span (+ alignment slack)
+    {   // stage capacity: the largest tile's CSR span (+ alignment slack for
+        // the 16-bit columns' 8-entry alignment too)
         int64_t mx = 0;
         for (int64_t r0 = 0; r0 < n; r0 += kBlock) {
             const int64_t r1 = r0 + kBlock < n ? r0 + kBlock : n;
-            const int64_t span = row_ptr[r1] - (row_ptr[r0] & ~int64_t(3)) + 8;
+            const int64_t span = row_ptr[r1] - (row_ptr[r0] & ~int64_t(7)) + 8;
             if (span > mx) mx = span;
         }
         mx = (mx + 3) & ~int64_t(3);
@@ -436,17 +492,27 @@ int matrix_create(int64_t n, int64_t ncols, const int64_t* row_ptr, const int64_
     // matrix with a narrow band and long rows, else the CSR tile pipeline.
     // Flags choose explicitly; CGVK_SPMV_ENGINE=csr|band overrides (A/B runs).
     {
-        int want = (flags & CGVK_MATRIX_ENGINE_CSR) ? 0 : (flags & CGVK_MATRIX_ENGINE_BAND) ? 1 : -1;
+        int want = (flags & CGVK_MATRIX_ENGINE_CSR) ? 0
+                   : (flags & CGVK_MATRIX_ENGINE_BAND) ? 1
+                   : (flags & CGVK_MATRIX_ENGINE_SEG) ? 2 : -1;
         const char* eng = getenv("CGVK_SPMV_ENGINE");
         if (eng && strcmp(eng, "csr") == 0) want = 0;
         if (eng && strcmp(eng, "band") == 0) want = 1;
-        if (want != 0 && ncols == n && n > 0) {
+        if (eng && strcmp(eng, "seg") == 0) want = 2;
+        if ((want == -1 || want == 1) && ncols == n && n > 0) {
             const int H = band_half_width(n, row_ptr, col_idx);
             const bool long_rows = nnz >= (int64_t)env_int("CGVK_BAND_MIN_ROW", 16) * n;
             if (H >= 0 && (want == 1 || long_rows)) {
                 if ((rc = build_band(a, row_ptr, H)) != CGVK_OK) return bail(rc);
                 a->order = 1;  // the band kernels walk contiguous tile runs
             }
+        }
+        // measured: on P128 the segment engine's extra x-tile
+        // copies starve its TMA ring (3.0 vs 4.3 TB/s), so it is opt-in only
+        if (want == 2 && a->band_h < 0 && ncols == n && n > 0) {
+            int d[kSegMax];
+            const int nd = seg_offsets(n, row_ptr, col_idx, d);
+            if (nd > 0 && (rc = build_seg(a, d, nd)) != CGVK_OK) return bail(rc);
         }
     }
     *out = a;
@@ -466,6 +532,7 @@ int cgvk_matrix_destroy(cgvk_matrix a) {
     cudaFree(a->band_meta);
     cudaFree(a->band_va);
     cudaFree(a->band_ci);
+    cudaFree(a->ci16);
     cudaFree(a->inv_diag);
     cudaFree(a->send_lo);
     cudaFree(a->send_hi);
@@ -489,8 +556,8 @@ int cgvk_matrix_info(cgvk_matrix a, int64_t* n, int64_t* nnz, int* device) {
 
 int cgvk_matrix_engine(cgvk_matrix a, int* engine, int* band_tiles) {
     if (!a) return set_err(CGVK_EINVAL, "null matrix");
-    if (engine) *engine = a->band_h >= 0 ? CGVK_ENGINE_BAND : CGVK_ENGINE_CSR;
-    if (band_tiles) *band_tiles = a->band_h >= 0 ? a->band_h : 0;
+    if (engine) *engine = a->band_h >= 0 ? CGVK_ENGINE_BAND : a->seg_nd > 0 ? CGVK_ENGINE_SEG : CGVK_ENGINE_CSR;
+    if (band_tiles) *band_tiles = a->band_h >= 0 ? a->band_h : a->seg_nd;
     return CGVK_OK;
 }
 
@@ -715,7 +782,16 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
     StageCfg S{};
     S.nvec = Op::NV;
     S.cap = Op::CSR ? a->cap : 0;
-    S.stage_bytes = (stage_bytes_for(S.cap, S.nvec, Op::CSR) + 127) & ~127;
+    bool seg = false;
+    if constexpr (Op::CSR) {  // segment engine: x tiles staged with the tile
+        if (a->seg_nd > 0) {
+            seg = true;
+            L->fn = k_stream<Op, CGVK_SPMV_MIN_CTAS, true>;
+            S.nd = a->seg_nd;
+            S.ng = Op::NG;
+        }
+    }
+    S.stage_bytes = (stage_bytes_for(S.cap, S.nvec, Op::CSR, S.nd, S.ng) + 127) & ~127;
     S.gvirt = a->G;
     const int header = ((int)sizeof(PipeHeader) + 127) & ~127;
     // stage budget: the SpMV kernels target CGVK_SPMV_MIN_CTAS resident CTAs,
@@ -725,6 +801,9 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
         // long rows: a 2-stage ring fills the SM -> one CTA with the full
         // register file (see k_stream's MINB)
         L->fn = k_stream<Op, 1>;
+        if constexpr (Op::CSR) {
+            if (seg) L->fn = k_stream<Op, 1, true>;
+        }
         ctas = 1;
     }
     const int budget = kSmemPerSM / ctas - 2048;

@@ -78,6 +78,11 @@ struct Params {
     const double* __restrict__ band_va;
     const unsigned short* __restrict__ band_ci;   // column - (tile - band_h) * 256
     int band_h;                                   // window half-width in tiles
+    // segment-window engine (stencil-like matrices): every column of tile t
+    // lies in one of the tiles t + seg_d[q], q < seg_nd; ci16 = q * 256 + (col & 255)
+    const unsigned short* __restrict__ ci16;
+    int seg_nd;
+    int seg_d[8];
     double* part;  // [kMaxDots][G] CTA partials
     double* hist;  // rr per iteration
     Ctrl* ctrl;

@@ -55,6 +55,8 @@ struct StageCfg {
     int gvirt;      // Gv
     int ring;       // band engine: window ring tiles (2H + nstage)
     int pf;         // band engine: L2 prefetch distance (tiles)
+    int nd;         // segment engine: x tiles staged per gathered operand (0: CSR engine)
+    int ng;         // segment engine: gathered operands staged
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -167,6 +169,19 @@ struct RowRef {
     static constexpr int CH = kChunk;  // entries per chunk
     const double* va;
     const int* ci;
+    int len;
+    __device__ __forceinline__ void entry(int k, int& c, double& v) const {
+        c = ci[k];
+        v = va[k];
+    }
+};
+
+// RowSeg: the segment engine's CSR row — the column stored as the 16-bit
+// index into the stage's staged x tiles (q * 256 + col % 256).
+struct RowSeg {
+    static constexpr int CH = kChunk;
+    const double* va;
+    const unsigned short* ci;
     int len;
     __device__ __forceinline__ void entry(int k, int& c, double& v) const {
         c = ci[k];
@@ -362,6 +377,19 @@ struct StagedIn {
     }
 };
 
+// Segment engine: gathered operand k read from the x tiles staged with the
+// tile (index from RowSeg), no global gather at all.
+struct SegIn {
+    const double* sv;  // stage vectors + own row
+    const double* g0;  // staged x tiles of gathered operand 0 / 1
+    const double* g1;
+    __device__ __forceinline__ double operator()(int v) const { return sv[v * kBlock]; }
+    __device__ __forceinline__ double gather(int k, int q, const double*) const { return (k ? g1 : g0)[q]; }
+    __device__ __forceinline__ double gather_p(int q, const double*, const double*, double beta) const {
+        return ADD(g1[q], MUL(beta, g0[q]));  // HS: operand 0 p_old, operand 1 r~
+    }
+};
+
 // Optional Op trait for the band engine: `static constexpr bool BAND_XF` — the
 // window holds band_xf(source 0, source 1) instead of the NG raw sources.
 template <class T, class = void>
@@ -373,13 +401,19 @@ struct BandXf<T, std::void_t<decltype(T::BAND_XF)>> {
     static constexpr bool value = T::BAND_XF;
 };
 
-// Per-stage shared-memory layout.
+// Per-stage shared-memory layout. CSR engine: row_ptr slice, values, int32
+// columns, vectors. Segment engine (S.nd > 0): 16-bit columns instead, and
+// after the vectors the nd x tiles of each of the ng gathered operands.
 struct StageView {
-    int* rp;      // kRpInts
-    double* va;   // cap
-    int* ci;      // cap
-    double* vec;  // nvec * kBlock
+    int* rp;       // kRpInts
+    double* va;    // cap
+    int* ci;       // cap (CSR engine)
+    unsigned short* ci16;  // cap (segment engine)
+    double* vec;   // nvec * kBlock
+    double* gx;    // ng * nd * kBlock (segment engine)
 };
+
+__host__ __device__ inline int ci_bytes_for(int cap, int nd) { return nd > 0 ? ((cap * 2 + 15) & ~15) : cap * 4; }
 
 __device__ __forceinline__ StageView stage_view(unsigned char* base, const StageCfg& S, int slot) {
     unsigned char* p = base + (size_t)slot * S.stage_bytes;
@@ -389,13 +423,16 @@ __device__ __forceinline__ StageView stage_view(unsigned char* base, const Stage
     v.va = reinterpret_cast<double*>(p);
     p += (size_t)S.cap * 8;
     v.ci = reinterpret_cast<int*>(p);
-    p += (size_t)S.cap * 4;
+    v.ci16 = reinterpret_cast<unsigned short*>(p);
+    p += ci_bytes_for(S.cap, S.nd);
     v.vec = reinterpret_cast<double*>(p);
+    p += (size_t)S.nvec * kBlock * 8;
+    v.gx = reinterpret_cast<double*>(p);
     return v;
 }
 
-__host__ __device__ inline int stage_bytes_for(int cap, int nvec, bool csr) {
-    return kRpInts * 4 + (csr ? cap * 12 : 0) + nvec * kBlock * 8;
+__host__ __device__ inline int stage_bytes_for(int cap, int nvec, bool csr, int nd = 0, int ng = 0) {
+    return kRpInts * 4 + (csr ? cap * 8 + ci_bytes_for(cap, nd) : 0) + nvec * kBlock * 8 + ng * nd * kBlock * 8;
 }
 
 // Header in dynamic shared memory: barriers + per-slot metadata.
@@ -471,10 +508,11 @@ __device__ __forceinline__ void stage_csr(const Params& P, const StageCfg& S, Pi
     const int rows = min(kBlock, P.n - r0);
     const uint32_t rp_bytes = ((rows + 1) * 4 + 15) & ~15;
     const int k0 = __ldg(P.rp + r0), k1 = __ldg(P.rp + r0 + rows);
-    const int k0a = k0 & ~1, k0c = k0 & ~3;
-    const bool direct = k1 - k0c + 4 > S.cap;
+    const bool seg = S.nd > 0;  // 16-bit columns: 16-byte aligned at multiples of 8
+    const int k0a = k0 & ~1, k0c = seg ? k0 & ~7 : k0 & ~3;
+    const bool direct = k1 - k0c + (seg ? 8 : 4) > S.cap;
     const uint32_t va_bytes = direct ? 0u : (((k1 - k0a) * 8 + 15) & ~15);
-    const uint32_t ci_bytes = direct ? 0u : (((k1 - k0c) * 4 + 15) & ~15);
+    const uint32_t ci_bytes = direct ? 0u : (((k1 - k0c) * (seg ? 2 : 4) + 15) & ~15);
     H->k0a[slot] = k0a;
     H->k0c[slot] = k0c;
     H->direct[slot] = direct;
@@ -482,7 +520,8 @@ __device__ __forceinline__ void stage_csr(const Params& P, const StageCfg& S, Pi
     bulk_g2s(V.rp, P.rp + r0, rp_bytes, &H->full[slot], pol);
     if (!direct) {
         bulk_g2s(V.va, P.va + k0a, va_bytes, &H->full[slot], pol);
-        bulk_g2s(V.ci, P.ci + k0c, ci_bytes, &H->full[slot], pol);
+        if (seg) bulk_g2s(V.ci16, P.ci16 + k0c, ci_bytes, &H->full[slot], pol);
+        else bulk_g2s(V.ci, P.ci + k0c, ci_bytes, &H->full[slot], pol);
     }
 }
 
@@ -500,7 +539,9 @@ __device__ __forceinline__ void stage_csr(const Params& P, const StageCfg& S, Pi
 // CGVK_SPMV_MIN_CTAS when their stage lets that many CTAs fit, else 1 — a
 // long-row matrix (R4M, ~27 entries/row) whose 2-stage ring already fills the
 // SM gets the registers to keep a whole chunk of gathers in flight.
-template <class Op, int MINB = (Op::CSR ? CGVK_SPMV_MIN_CTAS : 1)>
+// SEG: the segment engine (S.nd > 0): the stage also carries the x tiles the
+// tile's columns fall in (tile + seg_d[q]); gathers read shared memory.
+template <class Op, int MINB = (Op::CSR ? CGVK_SPMV_MIN_CTAS : 1), bool SEG = false>
 __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PipeHeader* H = reinterpret_cast<PipeHeader*>(smem_raw);
@@ -551,6 +592,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
         const double* vp[kMaxVec];
 #pragma unroll
         for (int v = 0; v < Op::NV; ++v) vp[v] = op.vec(P, v);
+        const double* gp[2] = {nullptr, nullptr};
+        if constexpr (SEG) {
+#pragma unroll
+            for (int k = 0; k < Op::NG; ++k) gp[k] = op.gsrc(P, k);
+        }
         int j = 0;
         const uint64_t vpol = P.l2pol == 0 ? pol : 0;
         CGVK_FOR_VB(vb, P.order, blockIdx.x, Gv, Gp) {
@@ -566,10 +612,32 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
 #pragma unroll
                 for (int v = 0; v < Op::NV; ++v)
                     if (vp[v]) bytes += vec_bytes;
+                if constexpr (SEG) {  // the x tiles this tile's columns fall in
+                    for (int q = 0; q < S.nd; ++q) {
+                        const int u = tile + P.seg_d[q];
+                        if (u < 0 || u >= ntiles) continue;
+                        const uint32_t ub = (min(kBlock, P.n - u * kBlock) * 8 + 15) & ~15;
+#pragma unroll
+                        for (int k = 0; k < Op::NG; ++k)
+                            if (gp[k]) bytes += ub;
+                    }
+                }
                 mbar_expect_tx(&H->full[slot], bytes);  // + this thread's arrival
 #pragma unroll
                 for (int v = 0; v < Op::NV; ++v)
                     if (vp[v]) bulk_g2s(V.vec + v * kBlock, vp[v] + r0, vec_bytes, &H->full[slot], vpol);
+                if constexpr (SEG) {
+                    for (int q = 0; q < S.nd; ++q) {
+                        const int u = tile + P.seg_d[q];
+                        if (u < 0 || u >= ntiles) continue;
+                        const uint32_t ub = (min(kBlock, P.n - u * kBlock) * 8 + 15) & ~15;
+#pragma unroll
+                        for (int k = 0; k < Op::NG; ++k)
+                            if (gp[k])
+                                bulk_g2s(V.gx + (k * S.nd + q) * kBlock, gp[k] + (size_t)u * kBlock, ub,
+                                         &H->full[slot], 0);
+                    }
+                }
                 ++j;
             }
         }
@@ -590,19 +658,32 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
             StageView V = stage_view(stages, S, slot);
             const int i = tile * kBlock + t;
             if (i < P.n) {
-                RowRef R{nullptr, nullptr, 0};
-                if (Op::CSR) {
+                if constexpr (SEG) {
                     const int b = V.rp[t];
-                    R.len = V.rp[t + 1] - b;
+                    RowSeg R{nullptr, nullptr, V.rp[t + 1] - b};
                     if (H->direct[slot]) {
                         R.va = P.va + b;
-                        R.ci = P.ci + b;
+                        R.ci = P.ci16 + b;
                     } else {
                         R.va = V.va + (b - H->k0a[slot]);
-                        R.ci = V.ci + (b - H->k0c[slot]);
+                        R.ci = V.ci16 + (b - H->k0c[slot]);
                     }
+                    op.row(P, i, SegIn{V.vec + t, V.gx, V.gx + S.nd * kBlock}, R, acc);
+                } else {
+                    RowRef R{nullptr, nullptr, 0};
+                    if (Op::CSR) {
+                        const int b = V.rp[t];
+                        R.len = V.rp[t + 1] - b;
+                        if (H->direct[slot]) {
+                            R.va = P.va + b;
+                            R.ci = P.ci + b;
+                        } else {
+                            R.va = V.va + (b - H->k0a[slot]);
+                            R.ci = V.ci + (b - H->k0c[slot]);
+                        }
+                    }
+                    op.row(P, i, StagedIn{V.vec + t}, R, acc);
                 }
-                op.row(P, i, StagedIn{V.vec + t}, R, acc);
             }
             __syncwarp();
             if ((t & 31) == 0) mbar_arrive(&H->empty[slot]);

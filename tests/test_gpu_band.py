@@ -109,3 +109,23 @@ def test_l1_ops_unaffected(bandmats):
     P, A = PROBLEMS["randspd_3000"], bandmats["randspd_3000"]
     x = np.random.default_rng(1).uniform(-1, 1, A.n)
     assert same_bits(A.spmv(x), O.spmv(P.A, x))
+
+
+SEG_PROBLEMS = ["poisson2d_33", "poisson3d_12"]
+
+
+@pytest.mark.parametrize("precond", [Precond.IDENTITY, Precond.JACOBI])
+@pytest.mark.parametrize("variant", ALL_VARIANTS)
+@pytest.mark.parametrize("name", SEG_PROBLEMS)
+def test_segment_engine_bit_exact(name, variant, precond):
+    """Opt-in segment-window engine (16-bit columns into the x tiles staged
+    with each tile): same bits as the CSR engine's order, vs the oracle."""
+    P = PROBLEMS[name]
+    A = cgvk.DeviceMatrix.from_csr(P.A, engine="seg")
+    eng, nd = A.engine()
+    assert eng == "seg" and 1 <= nd <= 8
+    lockstep(P.A, A, variant, precond, P.b, P.x0, steps=15, check_vectors_every=5)
+
+
+def test_segment_engine_not_default():
+    assert cgvk.DeviceMatrix.from_csr(PROBLEMS["poisson3d_12"].A).engine()[0] == "csr"
