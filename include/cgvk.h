@@ -167,6 +167,13 @@ int cgvk_precond_apply(cgvk_matrix a, int kind, const double* in, double* out);
 /* dot (inc/vector_ops.hpp:20-25) in the device's canonical reduction order
  * (reproduced bit-for-bit by oracle/cgv_oracle.c ORC_DOT_TREE). */
 int cgvk_dot(cgvk_matrix a, const double* x, const double* y, double* out);
+/* Device time (ms, mean of `reps` back-to-back launches, CUDA events) of the
+ * L1 operators the reference's cost model abstracts (src/cost_model.cpp:15-30):
+ * ms[CGVK_TIME_SPMV] y = A x, [CGVK_TIME_BLOCK_SPMV] (A x1, A x2) in one pass,
+ * [CGVK_TIME_DOT] one global reduction (dot + last-CTA fold), [CGVK_TIME_COPY]
+ * one n-vector copy. For calibration only (scripts/cost_model.py). */
+enum { CGVK_TIME_SPMV = 0, CGVK_TIME_BLOCK_SPMV, CGVK_TIME_DOT, CGVK_TIME_COPY, CGVK_TIMED_OPS };
+int cgvk_time_ops(cgvk_matrix a, int reps, double* ms);
 /* The reduction-tree parameters the oracle needs: rows per tile (= threads
  * per CTA), the CTA cap G and the tile order (0 strided, 1 contiguous). */
 int cgvk_reduction_config(cgvk_matrix a, int* block, int* gmax, int* order);

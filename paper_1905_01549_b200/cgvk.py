@@ -164,6 +164,7 @@ def _load() -> C.CDLL:
         "cgvk_matrix_destroy": (I, [P]),
         "cgvk_matrix_info": (I, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(I)]),
         "cgvk_matrix_engine": (I, [P, C.POINTER(I), C.POINTER(I)]),
+        "cgvk_time_ops": (I, [P, I, P]),
         "cgvk_spmv": (I, [P, P, P]),
         "cgvk_block_spmv": (I, [P, P, P, P, P]),
         "cgvk_jacobi": (I, [P, P]),
@@ -375,6 +376,12 @@ class DeviceMatrix:
         out = C.c_double()
         _check(_lib.cgvk_dot(self._h, _ptr(x), _ptr(y), C.byref(out)))
         return out.value
+
+    def time_ops(self, reps: int = 50) -> dict:
+        """Device ms per launch of spmv, block_spmv, one dot, one vector copy."""
+        ms = np.zeros(4)
+        _check(_lib.cgvk_time_ops(self._h, int(reps), _ptr(ms)))
+        return dict(zip(("spmv", "block_spmv", "dot", "copy"), ms.tolist()))
 
     def reduction_config(self) -> tuple[int, int, int]:
         """(rows per tile, CTA cap G, tile order) of the canonical dot tree."""

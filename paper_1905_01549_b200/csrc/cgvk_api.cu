@@ -643,6 +643,56 @@ int cgvk_dot(cgvk_matrix a, const double* x, const double* y, double* out) {
     return run_dots(a, a->stream, a->part, a->counter, a->out, 1, xs, ys, nullptr, out);
 }
 
+// Device-timed L1 operators for the cost-model calibration:
+// CUDA events around `reps` back-to-back launches on the matrix's stream.
+int cgvk_time_ops(cgvk_matrix a, int reps, double* ms) {
+    if (!a || !ms || reps < 1) return set_err(CGVK_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lock(a->mu);
+    CK(cudaSetDevice(a->device));
+    for (int q = 0; q < CGVK_TIMED_OPS; ++q) ms[q] = 0.0;
+    if (a->n == 0) return CGVK_OK;
+    TRY(ensure_tmp(a, 4));
+    const int n = (int)a->n;
+    for (int q = 0; q < 4; ++q) CK(cudaMemsetAsync(a->tmp[q], 0, 8 * a->n, a->stream));
+    const Params P = a->base();
+    DotArgs D{};
+    D.n = n;
+    D.ntiles = a->ntiles;
+    D.order = a->order;
+    D.x[0] = a->tmp[0];
+    D.y[0] = a->tmp[1];
+    D.part = a->part;
+    D.counter = a->counter;
+    D.out = a->out;
+    auto op = [&](int which) {
+        switch (which) {
+            case CGVK_TIME_SPMV: k_spmv<<<a->G, kBlock, 0, a->stream>>>(P, a->tmp[0], nullptr, a->tmp[2], 0); break;
+            case CGVK_TIME_BLOCK_SPMV:
+                k_block_spmv<<<a->G, kBlock, 0, a->stream>>>(P, a->tmp[0], a->tmp[1], a->tmp[2], a->tmp[3]);
+                break;
+            case CGVK_TIME_DOT: k_dots<1><<<a->G, kBlock, 0, a->stream>>>(D); break;
+            default: k_scale<<<grid_elem(n), 256, 0, a->stream>>>(n, nullptr, a->tmp[0], a->tmp[2]); break;
+        }
+    };
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    for (int which = 0; which < CGVK_TIMED_OPS; ++which) {
+        op(which);  // warm-up
+        CK(cudaEventRecord(e0, a->stream));
+        for (int r = 0; r < reps; ++r) op(which);
+        CK(cudaEventRecord(e1, a->stream));
+        CK(cudaEventSynchronize(e1));
+        float f = 0.f;
+        CK(cudaEventElapsedTime(&f, e0, e1));
+        ms[which] = f / reps;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    CK(cudaGetLastError());
+    return CGVK_OK;
+}
+
 int cgvk_host_register(void* ptr, uint64_t bytes) {
     CK(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault));
     return CGVK_OK;
