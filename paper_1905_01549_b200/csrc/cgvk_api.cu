@@ -14,6 +14,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -55,10 +56,27 @@ int set_err(int code, const char* fmt, ...) {
 constexpr int kMaxStageCap = 12288;  // CSR entries per stage (tiles above: direct loads)
 
 // Experiment knobs (environment, read at matrix/solver creation).
+// CGVK_DEBUG >= 2: host-side phase timings of matrix / solver creation
+struct PhaseTimer {
+    const char* what;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    bool on;
+    explicit PhaseTimer(const char* w);
+    void mark(const char* phase) {
+        if (!on) return;
+        const auto t = std::chrono::steady_clock::now();
+        fprintf(stderr, "cgvk %s: %s %.2f ms\n", what, phase,
+                std::chrono::duration<double, std::milli>(t - t0).count());
+        t0 = t;
+    }
+};
+
 int env_int(const char* name, int dflt) {
     const char* v = getenv(name);
     return v && *v ? atoi(v) : dflt;
 }
+
+PhaseTimer::PhaseTimer(const char* w) : what(w), on(env_int("CGVK_DEBUG", 0) >= 2) {}
 
 int grid_elem(int64_t n) {
     int64_t g = (n + 255) / 256;
@@ -66,16 +84,47 @@ int grid_elem(int64_t n) {
     return g < 1 ? 1 : (int)g;
 }
 
+// Device memory comes from the device's stream-ordered pool with an
+// unlimited release threshold: after the first solve, matrix and solver
+// setup reuse cached memory instead of mapping fresh pages (measured: plain
+// cudaMalloc/cudaFree made one solver creation take 20-280 ms on the B200
+// boxes, dominating the end-to-end time of a sweep). Allocation and free are
+// ordered on a per-device pool stream; dalloc synchronises it so the memory
+// is usable from any stream, and every owner synchronises its own streams
+// before dfree.
+cudaStream_t pool_stream() {
+    static std::mutex mu;
+    static cudaStream_t streams[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    if (!streams[dev]) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+    }
+    return streams[dev];
+}
+
 template <class T>
 int dalloc(T** p, size_t count) {
     if (count == 0) count = 1;
-    cudaError_t e = cudaMalloc((void**)p, sizeof(T) * count);
+    cudaStream_t st = pool_stream();
+    cudaError_t e = cudaMallocAsync((void**)p, sizeof(T) * count, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
         *p = nullptr;
-        return set_err(CGVK_ENOMEM, "cudaMalloc(%zu bytes): %s", sizeof(T) * count,
+        return set_err(CGVK_ENOMEM, "device allocation (%zu bytes): %s", sizeof(T) * count,
                        cudaGetErrorString(e));
     }
     return CGVK_OK;
+}
+
+void dfree(void* p) {
+    if (p) cudaFreeAsync(p, pool_stream());
 }
 
 }  // namespace
@@ -335,7 +384,7 @@ int build_band(cgvk_matrix a, const int64_t* row_ptr, int H) {
                                                           a->band_va, a->band_ci);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(a->stream);
-    cudaFree(dslot);
+    dfree(dslot);
     if (e != cudaSuccess) return set_err(CGVK_ECUDA, "band layout: %s", cudaGetErrorString(e));
     a->band_h = H;
     return CGVK_OK;
@@ -400,6 +449,7 @@ int matrix_create(int64_t n, int64_t ncols, const int64_t* row_ptr, const int64_
                   const double* values, int device, int flags, bool check_sorted, cgvk_matrix* out) {
     if (!out) return set_err(CGVK_EINVAL, "null output handle");
     *out = nullptr;
+    PhaseTimer pt("matrix_create");
     if (n < 0) return set_err(CGVK_EINVAL, "negative dimension");
     if (!row_ptr) return set_err(CGVK_EINVAL, "row_ptr length must be n+1");
     const int64_t nnz = row_ptr[n];
@@ -453,7 +503,7 @@ int matrix_create(int64_t n, int64_t ncols, const int64_t* row_ptr, const int64_
     // stage the int64 arrays on the device and narrow/validate there
     int64_t *rp64 = nullptr, *ci64 = nullptr;
     if ((rc = dalloc(&rp64, n + 1)) || (rc = dalloc(&ci64, nnz))) {
-        cudaFree(rp64);
+        dfree(rp64);
         return bail(rc);
     }
     cudaError_t e = cudaMemcpyAsync(rp64, row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice,
@@ -471,9 +521,10 @@ int matrix_create(int64_t n, int64_t ncols, const int64_t* row_ptr, const int64_
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(&hflags, a->flags, sizeof(int), cudaMemcpyDeviceToHost, a->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(a->stream);
-    cudaFree(rp64);
-    cudaFree(ci64);
+    dfree(rp64);
+    dfree(ci64);
     if (e != cudaSuccess) return bail(set_err(CGVK_ECUDA, "matrix upload: %s", cudaGetErrorString(e)));
+    pt.mark("host scan + upload + narrow");
     if (hflags & 1) return bail(set_err(CGVK_EINVAL, "row_ptr not monotone or wrong end points"));
     if (hflags & 2) return bail(set_err(CGVK_EINVAL, "column index out of range"));
     if (n > 0) {
@@ -488,6 +539,7 @@ int matrix_create(int64_t n, int64_t ncols, const int64_t* row_ptr, const int64_
         if (hflags & 4) return bail(set_err(CGVK_EINVAL, "column indices not strictly increasing"));
         if (hflags & 8) return bail(set_err(CGVK_EINVAL, "matrix is not bitwise symmetric"));
     }
+    pt.mark("validate");
     // SpMV engine: band (SELL-C-sigma + shared-memory x window) for a plain
     // matrix with a narrow band and long rows, else the CSR tile pipeline.
     // Flags choose explicitly; CGVK_SPMV_ENGINE=csr|band overrides (A/B runs).
@@ -515,6 +567,7 @@ int matrix_create(int64_t n, int64_t ncols, const int64_t* row_ptr, const int64_
             if (nd > 0 && (rc = build_seg(a, d, nd)) != CGVK_OK) return bail(rc);
         }
     }
+    pt.mark("engine layout");
     *out = a;
     return CGVK_OK;
 }
@@ -525,22 +578,22 @@ int cgvk_matrix_destroy(cgvk_matrix a) {
     if (!a) return CGVK_OK;
     cudaSetDevice(a->device);
     if (a->stream) cudaStreamSynchronize(a->stream);
-    cudaFree(a->rp);
-    cudaFree(a->ci);
-    cudaFree(a->va);
-    cudaFree(a->band_off);
-    cudaFree(a->band_meta);
-    cudaFree(a->band_va);
-    cudaFree(a->band_ci);
-    cudaFree(a->ci16);
-    cudaFree(a->inv_diag);
-    cudaFree(a->send_lo);
-    cudaFree(a->send_hi);
-    cudaFree(a->part);
-    cudaFree(a->counter);
-    cudaFree(a->out);
-    cudaFree(a->flags);
-    for (double* t : a->tmp) cudaFree(t);
+    dfree(a->rp);
+    dfree(a->ci);
+    dfree(a->va);
+    dfree(a->band_off);
+    dfree(a->band_meta);
+    dfree(a->band_va);
+    dfree(a->band_ci);
+    dfree(a->ci16);
+    dfree(a->inv_diag);
+    dfree(a->send_lo);
+    dfree(a->send_hi);
+    dfree(a->part);
+    dfree(a->counter);
+    dfree(a->out);
+    dfree(a->flags);
+    for (double* t : a->tmp) dfree(t);
     if (a->stream) cudaStreamDestroy(a->stream);
     delete a;
     return CGVK_OK;
@@ -1151,9 +1204,9 @@ void free_solver(cgvk_solver s) {
     for (double* p : {s->x, s->r, s->p0, s->p1, s->s, s->w, s->u, s->t, s->rt, s->st, s->wt, s->wpred, s->b,
                       s->tmp, s->part, s->hist, s->dout, s->rank_tot, s->all_tot, s->sbuf_lo, s->sbuf_hi,
                       s->rbuf_lo, s->rbuf_hi})
-        cudaFree(p);
-    cudaFree(s->counter);
-    cudaFree(s->ctrl);
+        dfree(p);
+    dfree(s->counter);
+    dfree(s->ctrl);
     if (s->stream && s->owns_stream) cudaStreamDestroy(s->stream);
     delete s;
 }
@@ -1326,6 +1379,7 @@ extern "C" {
 
 int cgvk_solver_create(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, const double* b,
                        const double* x0, cgvk_solver* out) {
+    PhaseTimer pt("solver_create");
     if (!out) return set_err(CGVK_EINVAL, "null output handle");
     *out = nullptr;
     if (!b || !x0) return set_err(CGVK_EINVAL, "right-hand side or initial guess dimension mismatch");
@@ -1353,9 +1407,12 @@ int cgvk_solver_create(cgvk_matrix a, const cgvk_variant_config* cfg, int precon
         *out = s;
         return CGVK_OK;
     }
+    pt.mark("alloc+kernels");
     if ((rc = solver_init(s, b, x0)) != CGVK_OK) return bail(rc);
+    pt.mark("initialize");
     if ((rc = capture(s, 1, &s->g1)) != CGVK_OK || (rc = capture(s, 8, &s->g8)) != CGVK_OK)
         return bail(rc);
+    pt.mark("graphs");
     s->persist = env_int("CGVK_PERSIST", 0) != 0 && a->band_h < 0;  // (no band persistent kernel)
     *out = s;
     return CGVK_OK;
