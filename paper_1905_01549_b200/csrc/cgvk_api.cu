@@ -8,6 +8,8 @@
 #include "cgvk_persist.cuh"
 #include "cgvk_band.cuh"
 
+#include <cub/device/device_scan.cuh>
+
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -260,17 +262,55 @@ int ensure_tmp(cgvk_matrix a, int count) {
 // window offsets fit and whose window rings fit in shared memory.
 constexpr int kBandMaxH = 19;  // 2 operands x (2H + 2) x 2 KB <= 160 KB
 
-int band_half_width(int64_t n, const int64_t* row_ptr, const int64_t* col_idx) {
-    int64_t h = 0;
-    for (int64_t i = 0; i < n; ++i) {
-        if (row_ptr[i + 1] == row_ptr[i]) continue;
-        const int64_t t = i / kBlock;
-        const int64_t lo = col_idx[row_ptr[i]] / kBlock, hi = col_idx[row_ptr[i + 1] - 1] / kBlock;
-        if (t - lo > h) h = t - lo;
-        if (hi - t > h) h = hi - t;
-        if (h > kBandMaxH) return -1;
+// max over rows of the tile distance of the first / last column (columns are
+// sorted, validated on the device before this runs)
+__global__ void k_band_h(int n, const int* __restrict__ rp, const int* __restrict__ ci, int* h) {
+    int m = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        if (rp[i + 1] == rp[i]) continue;
+        const int t = i / kBlock, lo = ci[rp[i]] / kBlock, hi = ci[rp[i + 1] - 1] / kBlock;
+        m = max(m, max(t - lo, hi - t));
     }
-    return (int)h;
+    if (m > 0) atomicMax(h, m);
+}
+
+int band_half_width(cgvk_matrix a) {
+    CK(cudaMemsetAsync(a->flags, 0, sizeof(int), a->stream));
+    k_band_h<<<grid_elem(a->n), 256, 0, a->stream>>>((int)a->n, a->rp, a->ci, a->flags);
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, a->flags, sizeof(int), cudaMemcpyDeviceToHost, a->stream));
+    CK(cudaStreamSynchronize(a->stream));
+    return h > kBandMaxH ? -1 : h;
+}
+
+// One CTA per tile: rows sorted by length, descending and stable (rank =
+// #longer + #equal before), meta word per slot, slot of each row, slice sizes.
+__global__ void __launch_bounds__(kBlock) k_band_tiles(int n, const int* __restrict__ rp, unsigned int* meta,
+                                                       int* slot_of, long long* sizes, int* flags) {
+    __shared__ int len_s[kBlock];
+    __shared__ int sorted_len[kBlock];
+    const int t = blockIdx.x, q = threadIdx.x;
+    const int r0 = t * kBlock, r = r0 + q;
+    const int rows = min(kBlock, n - r0);
+    const int len = q < rows ? rp[r + 1] - rp[r] : 0;
+    len_s[q] = len;
+    __syncthreads();
+    int rank = 0;
+    for (int j = 0; j < kBlock; ++j) {
+        const int lj = len_s[j];
+        rank += (lj > len) || (lj == len && j < q);
+    }
+    if (len >= (1 << 24)) atomicOr(flags, 1);
+    meta[(size_t)t * kBlock + rank] = ((unsigned int)len << 8) | (unsigned int)q;
+    if (q < rows) slot_of[r] = t * kBlock + rank;
+    sorted_len[rank] = len;
+    __syncthreads();
+    if (q < kWarps) sizes[(size_t)t * kWarps + q] = 32ll * sorted_len[32 * q];  // slice 32q+.. : first is longest
+}
+
+__global__ void k_narrow_off(int count, const long long* __restrict__ off64, int* off) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x)
+        off[i] = (int)off64[i];
 }
 
 // entries of row i -> its slot of the SELL-C-sigma layout
@@ -337,54 +377,54 @@ int build_seg(cgvk_matrix a, const int* d, int nd) {
     return CGVK_OK;
 }
 
-int build_band(cgvk_matrix a, const int64_t* row_ptr, int H) {
+// Built on the device (a host sort of every tile cost ~200 ms on R4M).
+int build_band(cgvk_matrix a, int H) {
     const int64_t n = a->n;
     const int nt = a->ntiles;
-    std::vector<int> off((size_t)nt * kWarps + 16, 0);
-    std::vector<unsigned int> meta((size_t)nt * kBlock);
-    std::vector<int> slot_of(n > 0 ? n : 1);
-    int64_t cur = 0;
-    int order[kBlock];
-    int64_t len[kBlock];
-    for (int t = 0; t < nt; ++t) {
-        const int64_t r0 = (int64_t)t * kBlock;
-        const int rows = (int)std::min<int64_t>(kBlock, n - r0);
-        for (int q = 0; q < kBlock; ++q) {
-            len[q] = q < rows ? row_ptr[r0 + q + 1] - row_ptr[r0 + q] : 0;
-            order[q] = q;
-        }
-        std::stable_sort(order, order + kBlock, [&](int x, int y) { return len[x] > len[y]; });
-        for (int q = 0; q < kBlock; ++q) {
-            if (len[order[q]] >= (1 << 24)) return set_err(CGVK_EINVAL, "row too long for the band engine");
-            meta[(size_t)t * kBlock + q] = (unsigned int)(len[order[q]] << 8) | (unsigned int)order[q];
-            if (order[q] < rows) slot_of[r0 + order[q]] = t * kBlock + q;
-        }
-        for (int s = 0; s < kWarps; ++s) {
-            off[(size_t)t * kWarps + s] = (int)cur;
-            cur += 32 * len[order[32 * s]];  // slices sorted: first row is the longest
-            if (cur >= (int64_t(1) << 31) - 64) return set_err(CGVK_EINVAL, "band layout exceeds 2^31 entries");
-        }
-    }
-    for (size_t q = (size_t)nt * kWarps; q < off.size(); ++q) off[q] = (int)cur;
-    a->band_entries = cur;
+    const size_t nslice = (size_t)nt * kWarps;
+    long long* sizes = nullptr;
+    long long* off64 = nullptr;
     int* dslot = nullptr;
-    TRY(dalloc(&a->band_off, off.size()));
-    TRY(dalloc(&a->band_meta, meta.size() + 1));
-    TRY(dalloc(&a->band_va, cur + 32));
-    TRY(dalloc(&a->band_ci, cur + 64));
-    TRY(dalloc(&dslot, slot_of.size()));
-    CK(cudaMemcpyAsync(a->band_off, off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice, a->stream));
-    CK(cudaMemcpyAsync(a->band_meta, meta.data(), sizeof(unsigned int) * meta.size(), cudaMemcpyHostToDevice,
-                       a->stream));
-    CK(cudaMemcpyAsync(dslot, slot_of.data(), sizeof(int) * slot_of.size(), cudaMemcpyHostToDevice, a->stream));
-    CK(cudaMemsetAsync(a->band_va, 0, sizeof(double) * (cur + 32), a->stream));
-    CK(cudaMemsetAsync(a->band_ci, 0, sizeof(unsigned short) * (cur + 64), a->stream));
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    auto cleanup = [&]() {
+        dfree(sizes);
+        dfree(off64);
+        dfree(dslot);
+        dfree(tmp);
+    };
+    int rc;
+    if ((rc = dalloc(&a->band_off, nslice + 16)) || (rc = dalloc(&a->band_meta, (size_t)nt * kBlock + 1)) ||
+        (rc = dalloc(&sizes, nslice + 1)) || (rc = dalloc(&off64, nslice + 1)) || (rc = dalloc(&dslot, n)))
+        return cleanup(), rc;
+    CK(cudaMemsetAsync(a->flags, 0, sizeof(int), a->stream));
+    CK(cudaMemsetAsync(sizes + nslice, 0, sizeof(long long), a->stream));
+    k_band_tiles<<<nt, kBlock, 0, a->stream>>>((int)n, a->rp, a->band_meta, dslot, sizes, a->flags);
+    CK(cudaGetLastError());
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, sizes, off64, (int)nslice + 1, a->stream));
+    if ((rc = dalloc(reinterpret_cast<unsigned char**>(&tmp), tmp_bytes))) return cleanup(), rc;
+    CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, sizes, off64, (int)nslice + 1, a->stream));
+    long long total = 0;
+    int flags = 0;
+    CK(cudaMemcpyAsync(&total, off64 + nslice, sizeof(long long), cudaMemcpyDeviceToHost, a->stream));
+    CK(cudaMemcpyAsync(&flags, a->flags, sizeof(int), cudaMemcpyDeviceToHost, a->stream));
+    CK(cudaStreamSynchronize(a->stream));
+    if (flags & 1) return cleanup(), set_err(CGVK_EINVAL, "row too long for the band engine");
+    if (total >= (1ll << 31) - 64) return cleanup(), set_err(CGVK_EINVAL, "band layout exceeds 2^31 entries");
+    a->band_entries = total;
+    k_narrow_off<<<grid_elem(nslice + 1), 256, 0, a->stream>>>((int)nslice + 1, off64, a->band_off);
+    for (int q = 1; q < 16; ++q)  // padding read by the 48-byte offset copies of the last tile
+        CK(cudaMemcpyAsync(a->band_off + nslice + q, a->band_off + nslice, sizeof(int), cudaMemcpyDeviceToDevice,
+                           a->stream));
+    if ((rc = dalloc(&a->band_va, total + 32)) || (rc = dalloc(&a->band_ci, total + 64))) return cleanup(), rc;
+    CK(cudaMemsetAsync(a->band_va, 0, sizeof(double) * (total + 32), a->stream));
+    CK(cudaMemsetAsync(a->band_ci, 0, sizeof(unsigned short) * (total + 64), a->stream));
     if (n > 0)
         k_fill_band<<<grid_elem(n), 256, 0, a->stream>>>((int)n, a->rp, a->ci, a->va, dslot, a->band_off, H,
                                                           a->band_va, a->band_ci);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(a->stream);
-    dfree(dslot);
+    cleanup();
     if (e != cudaSuccess) return set_err(CGVK_ECUDA, "band layout: %s", cudaGetErrorString(e));
     a->band_h = H;
     return CGVK_OK;
@@ -552,10 +592,10 @@ int matrix_create(int64_t n, int64_t ncols, const int64_t* row_ptr, const int64_
         if (eng && strcmp(eng, "band") == 0) want = 1;
         if (eng && strcmp(eng, "seg") == 0) want = 2;
         if ((want == -1 || want == 1) && ncols == n && n > 0) {
-            const int H = band_half_width(n, row_ptr, col_idx);
             const bool long_rows = nnz >= (int64_t)env_int("CGVK_BAND_MIN_ROW", 16) * n;
-            if (H >= 0 && (want == 1 || long_rows)) {
-                if ((rc = build_band(a, row_ptr, H)) != CGVK_OK) return bail(rc);
+            const int H = (want == 1 || long_rows) ? band_half_width(a) : -1;
+            if (H >= 0) {
+                if ((rc = build_band(a, H)) != CGVK_OK) return bail(rc);
                 a->order = 1;  // the band kernels walk contiguous tile runs
             }
         }
