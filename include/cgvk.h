@@ -89,6 +89,7 @@ enum {
     CGVK_MATRIX_ENGINE_CSR = 2,      /* SpMV kernels: TMA-staged CSR tiles only */
     CGVK_MATRIX_ENGINE_BAND = 4,     /* SpMV kernels: band engine whenever it applies */
     CGVK_MATRIX_ENGINE_SEG = 8,      /* SpMV kernels: segment-window engine whenever it applies */
+    CGVK_MATRIX_ENGINE_CSR16 = 16,   /* SpMV kernels: CSR with 16-bit tile-offset columns */
 };
 
 /* SpMV engine of a matrix (cgvk_matrix_engine). Without an ENGINE flag the
@@ -97,7 +98,7 @@ enum {
  * with x gathered through L1/L2. The segment-window engine (TMA-staged CSR
  * with 16-bit columns into the x tiles staged with each tile; needs all
  * columns within at most 8 tile offsets, e.g. stencils) is opt-in. */
-enum { CGVK_ENGINE_CSR = 0, CGVK_ENGINE_BAND = 1, CGVK_ENGINE_SEG = 2 };
+enum { CGVK_ENGINE_CSR = 0, CGVK_ENGINE_BAND = 1, CGVK_ENGINE_SEG = 2, CGVK_ENGINE_CSR16 = 3 };
 
 /* POD mirror of VariantConfig (inc/variants.hpp:34-57). */
 typedef struct cgvk_variant_config {

@@ -297,7 +297,7 @@ class VariantConfig:
 class DeviceMatrix:
     """SparseMatrix resident on one GPU (int32 CSR + fp64 values)."""
 
-    ENGINES = {None: 0, "csr": 2, "band": 4, "seg": 8}
+    ENGINES = {None: 0, "csr": 2, "band": 4, "seg": 8, "csr16": 16}
 
     def __init__(self, n: int, row_ptr, col_idx, values, device: int = 0,
                  check_symmetric: bool = False, engine: str | None = None):
@@ -329,7 +329,7 @@ class DeviceMatrix:
         tiles; seg: number of staged x-tile offsets; csr: 0)."""
         e, h = C.c_int(), C.c_int()
         _check(_lib.cgvk_matrix_engine(self._h, C.byref(e), C.byref(h)))
-        return ("csr", "band", "seg")[e.value], h.value
+        return ("csr", "band", "seg", "csr16")[e.value], h.value
 
     @property
     def handle(self):

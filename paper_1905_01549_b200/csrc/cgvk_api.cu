@@ -160,6 +160,7 @@ struct cgvk_matrix_s {
     int64_t band_entries = 0;
     // segment-window engine (cgvk_stream.cuh SEG): tile offsets + 16-bit columns
     int seg_nd = 0;
+    int seg_mode = 0;  // 1: x tiles staged (segment engine), 2: 16-bit columns, x via L1 (csr16)
     int seg_d[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     unsigned short* ci16 = nullptr;
     double* inv_diag = nullptr;  // built on first use
@@ -586,11 +587,13 @@ int matrix_create(int64_t n, int64_t ncols, const int64_t* row_ptr, const int64_
     {
         int want = (flags & CGVK_MATRIX_ENGINE_CSR) ? 0
                    : (flags & CGVK_MATRIX_ENGINE_BAND) ? 1
-                   : (flags & CGVK_MATRIX_ENGINE_SEG) ? 2 : -1;
+                   : (flags & CGVK_MATRIX_ENGINE_SEG) ? 2
+                   : (flags & CGVK_MATRIX_ENGINE_CSR16) ? 3 : -1;
         const char* eng = getenv("CGVK_SPMV_ENGINE");
         if (eng && strcmp(eng, "csr") == 0) want = 0;
         if (eng && strcmp(eng, "band") == 0) want = 1;
         if (eng && strcmp(eng, "seg") == 0) want = 2;
+        if (eng && strcmp(eng, "csr16") == 0) want = 3;
         if ((want == -1 || want == 1) && ncols == n && n > 0) {
             const bool long_rows = nnz >= (int64_t)env_int("CGVK_BAND_MIN_ROW", 16) * n;
             const int H = (want == 1 || long_rows) ? band_half_width(a) : -1;
@@ -601,10 +604,11 @@ int matrix_create(int64_t n, int64_t ncols, const int64_t* row_ptr, const int64_
         }
         // measured: on P128 the segment engine's extra x-tile
         // copies starve its TMA ring (3.0 vs 4.3 TB/s), so it is opt-in only
-        if (want == 2 && a->band_h < 0 && ncols == n && n > 0) {
+        if ((want == 2 || want == 3) && a->band_h < 0 && ncols == n && n > 0) {
             int d[kSegMax];
             const int nd = seg_offsets(n, row_ptr, col_idx, d);
             if (nd > 0 && (rc = build_seg(a, d, nd)) != CGVK_OK) return bail(rc);
+            if (nd > 0) a->seg_mode = want == 2 ? 1 : 2;
         }
     }
     pt.mark("engine layout");
@@ -649,7 +653,10 @@ int cgvk_matrix_info(cgvk_matrix a, int64_t* n, int64_t* nnz, int* device) {
 
 int cgvk_matrix_engine(cgvk_matrix a, int* engine, int* band_tiles) {
     if (!a) return set_err(CGVK_EINVAL, "null matrix");
-    if (engine) *engine = a->band_h >= 0 ? CGVK_ENGINE_BAND : a->seg_nd > 0 ? CGVK_ENGINE_SEG : CGVK_ENGINE_CSR;
+    if (engine)
+        *engine = a->band_h >= 0 ? CGVK_ENGINE_BAND
+                  : a->seg_nd > 0 ? (a->seg_mode == 1 ? CGVK_ENGINE_SEG : CGVK_ENGINE_CSR16)
+                                  : CGVK_ENGINE_CSR;
     if (band_tiles) *band_tiles = a->band_h >= 0 ? a->band_h : a->seg_nd;
     return CGVK_OK;
 }
@@ -925,13 +932,17 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
     StageCfg S{};
     S.nvec = Op::NV;
     S.cap = Op::CSR ? a->cap : 0;
-    bool seg = false;
-    if constexpr (Op::CSR) {  // segment engine: x tiles staged with the tile
+    int seg = 0;
+    if constexpr (Op::CSR) {  // 16-bit-column engines
         if (a->seg_nd > 0) {
-            seg = true;
-            L->fn = k_stream<Op, CGVK_SPMV_MIN_CTAS, true>;
+            seg = a->seg_mode;
             S.nd = a->seg_nd;
-            S.ng = Op::NG;
+            if (seg == 1) {  // x tiles staged with the tile
+                L->fn = k_stream<Op, CGVK_SPMV_MIN_CTAS, 1>;
+                S.ng = Op::NG;
+            } else {
+                L->fn = k_stream<Op, CGVK_SPMV_MIN_CTAS, 2>;
+            }
         }
     }
     S.stage_bytes = (stage_bytes_for(S.cap, S.nvec, Op::CSR, S.nd, S.ng) + 127) & ~127;
@@ -945,7 +956,8 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
         // register file (see k_stream's MINB)
         L->fn = k_stream<Op, 1>;
         if constexpr (Op::CSR) {
-            if (seg) L->fn = k_stream<Op, 1, true>;
+            if (seg == 1) L->fn = k_stream<Op, 1, 1>;
+            if (seg == 2) L->fn = k_stream<Op, 1, 2>;
         }
         ctas = 1;
     }

@@ -377,6 +377,21 @@ struct StagedIn {
     }
 };
 
+// RowD: CSR with 16-bit columns (q = offset slot << 8 | col % 256), decoded
+// against the tile's x-tile bases; x still gathered through L1/L2.
+struct RowD {
+    static constexpr int CH = kChunk;
+    const double* va;
+    const unsigned short* ci;
+    const int* base;  // stage header: (tile + seg_d[slot]) * 256
+    int len;
+    __device__ __forceinline__ void entry(int k, int& c, double& v) const {
+        const int q = ci[k];
+        c = base[q >> 8] + (q & (kBlock - 1));
+        v = va[k];
+    }
+};
+
 // Segment engine: gathered operand k read from the x tiles staged with the
 // tile (index from RowSeg), no global gather at all.
 struct SegIn {
@@ -444,6 +459,7 @@ struct PipeHeader {
     int direct[kMaxStages];
     int last_flag;
     int pad[3];
+    int segbase[kMaxStages][8];  // 16-bit-column CSR: first row of each tile offset's x tile
     double red[kMaxDots * 32];
 };
 
@@ -539,9 +555,11 @@ __device__ __forceinline__ void stage_csr(const Params& P, const StageCfg& S, Pi
 // CGVK_SPMV_MIN_CTAS when their stage lets that many CTAs fit, else 1 — a
 // long-row matrix (R4M, ~27 entries/row) whose 2-stage ring already fills the
 // SM gets the registers to keep a whole chunk of gathers in flight.
-// SEG: the segment engine (S.nd > 0): the stage also carries the x tiles the
-// tile's columns fall in (tile + seg_d[q]); gathers read shared memory.
-template <class Op, int MINB = (Op::CSR ? CGVK_SPMV_MIN_CTAS : 1), bool SEG = false>
+// SEG 1: the segment engine (S.nd > 0): the stage also carries the x tiles
+// the tile's columns fall in (tile + seg_d[q]); gathers read shared memory.
+// SEG 2: CSR with 16-bit columns decoded against those tiles' bases, x
+// gathered through L1/L2 (2 B/entry less traffic and stage space).
+template <class Op, int MINB = (Op::CSR ? CGVK_SPMV_MIN_CTAS : 1), int SEG = 0>
 __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PipeHeader* H = reinterpret_cast<PipeHeader*>(smem_raw);
@@ -593,7 +611,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
 #pragma unroll
         for (int v = 0; v < Op::NV; ++v) vp[v] = op.vec(P, v);
         const double* gp[2] = {nullptr, nullptr};
-        if constexpr (SEG) {
+        if constexpr (SEG == 1) {
 #pragma unroll
             for (int k = 0; k < Op::NG; ++k) gp[k] = op.gsrc(P, k);
         }
@@ -612,7 +630,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
 #pragma unroll
                 for (int v = 0; v < Op::NV; ++v)
                     if (vp[v]) bytes += vec_bytes;
-                if constexpr (SEG) {  // the x tiles this tile's columns fall in
+                if constexpr (SEG == 2) {  // x-tile bases for the 16-bit columns
+                    for (int q = 0; q < S.nd; ++q) H->segbase[slot][q] = (tile + P.seg_d[q]) * kBlock;
+                }
+                if constexpr (SEG == 1) {  // the x tiles this tile's columns fall in
                     for (int q = 0; q < S.nd; ++q) {
                         const int u = tile + P.seg_d[q];
                         if (u < 0 || u >= ntiles) continue;
@@ -626,7 +647,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
 #pragma unroll
                 for (int v = 0; v < Op::NV; ++v)
                     if (vp[v]) bulk_g2s(V.vec + v * kBlock, vp[v] + r0, vec_bytes, &H->full[slot], vpol);
-                if constexpr (SEG) {
+                if constexpr (SEG == 1) {
                     for (int q = 0; q < S.nd; ++q) {
                         const int u = tile + P.seg_d[q];
                         if (u < 0 || u >= ntiles) continue;
@@ -658,7 +679,18 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
             StageView V = stage_view(stages, S, slot);
             const int i = tile * kBlock + t;
             if (i < P.n) {
-                if constexpr (SEG) {
+                if constexpr (SEG == 2) {
+                    const int b = V.rp[t];
+                    RowD R{nullptr, nullptr, H->segbase[slot], V.rp[t + 1] - b};
+                    if (H->direct[slot]) {
+                        R.va = P.va + b;
+                        R.ci = P.ci16 + b;
+                    } else {
+                        R.va = V.va + (b - H->k0a[slot]);
+                        R.ci = V.ci16 + (b - H->k0c[slot]);
+                    }
+                    op.row(P, i, StagedIn{V.vec + t}, R, acc);
+                } else if constexpr (SEG == 1) {
                     const int b = V.rp[t];
                     RowSeg R{nullptr, nullptr, V.rp[t + 1] - b};
                     if (H->direct[slot]) {

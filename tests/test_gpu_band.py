@@ -117,13 +117,15 @@ SEG_PROBLEMS = ["poisson2d_33", "poisson3d_12"]
 @pytest.mark.parametrize("precond", [Precond.IDENTITY, Precond.JACOBI])
 @pytest.mark.parametrize("variant", ALL_VARIANTS)
 @pytest.mark.parametrize("name", SEG_PROBLEMS)
-def test_segment_engine_bit_exact(name, variant, precond):
-    """Opt-in segment-window engine (16-bit columns into the x tiles staged
-    with each tile): same bits as the CSR engine's order, vs the oracle."""
+@pytest.mark.parametrize("engine", ["seg", "csr16"])
+def test_segment_engine_bit_exact(name, variant, precond, engine):
+    """Opt-in 16-bit-column engines — seg: columns index the x tiles staged
+    with each tile; csr16: decoded against the tiles' bases, x through L1 —
+    same bits as the CSR engine's order, vs the oracle."""
     P = PROBLEMS[name]
-    A = cgvk.DeviceMatrix.from_csr(P.A, engine="seg")
+    A = cgvk.DeviceMatrix.from_csr(P.A, engine=engine)
     eng, nd = A.engine()
-    assert eng == "seg" and 1 <= nd <= 8
+    assert eng == engine and 1 <= nd <= 8
     lockstep(P.A, A, variant, precond, P.b, P.x0, steps=15, check_vectors_every=5)
 
 
