@@ -945,9 +945,14 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
             }
         }
     }
+    const int header = ((int)sizeof(PipeHeader) + 127) & ~127;
+    if (Op::CSR) {  // two stages must fit one CTA: tiles beyond the capacity go direct
+        while (S.cap > 64 &&
+               header + 2 * ((stage_bytes_for(S.cap, S.nvec, true, S.nd, S.ng) + 127) & ~127) > kSmemPerSM - 1024)
+            S.cap = (S.cap - S.cap / 8) & ~7;
+    }
     S.stage_bytes = (stage_bytes_for(S.cap, S.nvec, Op::CSR, S.nd, S.ng) + 127) & ~127;
     S.gvirt = a->G;
-    const int header = ((int)sizeof(PipeHeader) + 127) & ~127;
     // stage budget: the SpMV kernels target CGVK_SPMV_MIN_CTAS resident CTAs,
     // the update kernels two
     int ctas = env_int(Op::CSR ? "CGVK_SMEM_CTAS_SPMV" : "CGVK_SMEM_CTAS", Op::CSR ? CGVK_SPMV_MIN_CTAS : 2);
@@ -1018,7 +1023,13 @@ template <class Op1, class Op2>
 int pick_pair(cgvk_matrix a, cgvk_solver s) {
     TRY(make_launch<Op1>(a, &s->k1));
     TRY(make_launch<Op2>(a, &s->k2));
-    TRY((make_persist<Op1, Op2>(a, &s->kp)));
+    // the experimental persistent kernel only when asked for (CGVK_PERSIST=1)
+    // and when its union stage fits; otherwise the graph path
+    s->kp = KLaunch{};
+    if (env_int("CGVK_PERSIST", 0) && a->band_h < 0 && make_persist<Op1, Op2>(a, &s->kp) != CGVK_OK) {
+        s->kp = KLaunch{};
+        g_err.clear();
+    }
     s->fin1 = k_finalize<Op1>;
     s->fin2 = k_finalize<Op2>;
     return CGVK_OK;
@@ -1465,7 +1476,7 @@ int cgvk_solver_create(cgvk_matrix a, const cgvk_variant_config* cfg, int precon
     if ((rc = capture(s, 1, &s->g1)) != CGVK_OK || (rc = capture(s, 8, &s->g8)) != CGVK_OK)
         return bail(rc);
     pt.mark("graphs");
-    s->persist = env_int("CGVK_PERSIST", 0) != 0 && a->band_h < 0;  // (no band persistent kernel)
+    s->persist = s->kp.fn != nullptr;  // CGVK_PERSIST=1 and the union stage fit (no band version)
     *out = s;
     return CGVK_OK;
 }
