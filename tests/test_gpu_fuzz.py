@@ -75,3 +75,60 @@ def test_random_structures(seed):
     variant = ALL_VARIANTS[seed % len(ALL_VARIANTS)]
     precond = [Precond.IDENTITY, Precond.JACOBI][seed % 2]
     lockstep(P.A, A, variant, precond, P.b, P.x0, steps=12, check_vectors_every=4)
+
+
+@pytest.mark.parametrize("band,want", [(19 * 256 - 255, "band"), (21 * 256, "csr")])
+def test_band_window_limit(band, want):
+    """Half-width H = 19 tiles is the largest window the band engine keeps;
+    a wider band stays on CSR. Both bit-exact."""
+    P = pb.make_problem("bw", pb.random_spd(40000, 13, band, 17))
+    A = cgvk.DeviceMatrix.from_csr(P.A)
+    assert A.engine()[0] == want
+    for v in (Variant.HS, Variant.PIPE_PR):
+        lockstep(P.A, A, v, Precond.JACOBI, P.b, P.x0, steps=6, check_vectors_every=6)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_l1_operators(seed):
+    from oracle import oracle as O
+    from helpers import same_bits, tree_dot
+    rng = np.random.default_rng(50 + seed)
+    n = int(rng.integers(1, 20000))
+    P = pb.make_problem("l1", pb.random_spd(n, int(rng.integers(0, 16)), int(rng.integers(1, max(2, n))),
+                                            200 + seed))
+    A = cgvk.DeviceMatrix.from_csr(P.A, engine=[None, "band", "csr"][seed % 3])
+    x1, x2 = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    assert same_bits(A.spmv(x1), O.spmv(P.A, x1))
+    y1, y2 = A.block_spmv(x1, x2)
+    assert same_bits(y1, O.spmv(P.A, x1)) and same_bits(y2, O.spmv(P.A, x2))
+    assert same_bits(A.jacobi(), O.jacobi(P.A))
+    assert same_bits(np.float64(A.dot(x1, x2)), np.float64(O.dot(x1, x2, tree_dot(A))))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_partitioned_solves(seed):
+    """Row-partitioned (local transport) solves of random structures, P = 2..5
+    ranks, bit-exact vs the partitioned oracle."""
+    from oracle import oracle as O
+    from test_gpu_group import compare
+    rng = np.random.default_rng(70 + seed)
+    n = int(rng.integers(2000, 40000))
+    nranks = int(rng.integers(2, 6))
+    P = pb.make_problem("pp", pb.random_spd(n, int(rng.integers(2, 14)), int(rng.integers(8, n // (2 * nranks))),
+                                            300 + seed))
+    lo = cgvk.partition_rows(n, nranks, 1)
+    mats = [cgvk.RankMatrix(n, lo, r, *cgvk.local_rows(P.A, lo, r)) for r in range(nranks)]
+    comm = cgvk.Comm(nranks)
+    variant = ALL_VARIANTS[seed % len(ALL_VARIANTS)]
+    g = cgvk.Group(comm, mats, cgvk.VariantConfig.make(variant), Precond.JACOBI,
+                   [P.b[lo[r]:lo[r + 1]] for r in range(nranks)], [P.x0[lo[r]:lo[r + 1]] for r in range(nranks)])
+    block, gmax, order = mats[0].reduction_config()
+    o = O.Restatement(P.A, int(variant), 1, P.b, P.x0, dot=("part", block, gmax, lo, order))
+    for k in range(8):
+        g.step(1)
+        g.sync()
+        if o.state()["state"] == 0:
+            o.step()
+    compare(g, o, f"fuzz-part seed {seed} P{nranks} {variant.name}")
+    g.close()
+    comm.close()
