@@ -955,7 +955,8 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
     S.gvirt = a->G;
     // stage budget: the SpMV kernels target CGVK_SPMV_MIN_CTAS resident CTAs,
     // the update kernels two
-    int ctas = env_int(Op::CSR ? "CGVK_SMEM_CTAS_SPMV" : "CGVK_SMEM_CTAS", Op::CSR ? CGVK_SPMV_MIN_CTAS : 2);
+    int ctas = env_int(Op::CSR ? "CGVK_SMEM_CTAS_SPMV" : "CGVK_SMEM_CTAS",
+                       SmemCtasOf<Op>::value > 0 ? SmemCtasOf<Op>::value : Op::CSR ? CGVK_SPMV_MIN_CTAS : 2);
     if (Op::CSR && header + 2 * S.stage_bytes > kSmemPerSM / 2 - 2048) {
         // long rows: a 2-stage ring fills the SM -> one CTA with the full
         // register file (see k_stream's MINB)

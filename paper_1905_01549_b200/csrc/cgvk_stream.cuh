@@ -37,6 +37,17 @@ constexpr int kMaxStages = 8;
 constexpr int kRpInts = kBlock + 4;          // row_ptr slice (257 used), padded to 16 B
 constexpr int kMaxVec = 12;
 
+// Optional per-Op shared-memory budget hint: `static constexpr int SMEM_CTAS`
+// (resident CTAs per SM the stage ring is sized for).
+template <class T, class = void>
+struct SmemCtasOf {
+    static constexpr int value = 0;
+};
+template <class T>
+struct SmemCtasOf<T, std::void_t<decltype(T::SMEM_CTAS)>> {
+    static constexpr int value = T::SMEM_CTAS;
+};
+
 // Optional per-Op ring-depth hint: `static constexpr int STAGES`.
 template <class T, class = void>
 struct StagesOf {

@@ -269,9 +269,18 @@ struct CgK2 {
 
 // streams: x p r s [r~ d]
 template <bool PREC>
+#ifndef CGVK_PR_K1_CTAS
+#define CGVK_PR_K1_CTAS 3
+#endif
+#ifndef CGVK_PR_LATE
+#define CGVK_PR_LATE 3  // bit 0: K1, bit 1: K2 signal their dependents late
+#endif
 struct PrK1 {
     static constexpr int NV = PREC ? 6 : 4, ND = 1;
     static constexpr bool CSR = false;
+    // measured P128: 3 resident CTAs + late PDL signal, PR 70.5 -> 67.9 us
+    static constexpr int SMEM_CTAS = CGVK_PR_K1_CTAS;
+    static constexpr bool PDL_LATE = (CGVK_PR_LATE & 1) != 0;
     double alpha, beta, nup;
     bool valid;
     __device__ bool enter(const Params& P) {
@@ -324,6 +333,7 @@ template <bool PREC>
 struct PrK2 {
     static constexpr int NV = PREC ? 4 : 2, ND = 6;
     static constexpr bool CSR = true;
+    static constexpr bool PDL_LATE = (CGVK_PR_LATE & 2) != 0;
     double nup;
     bool want_delta, want_dhat;
     __device__ bool enter(const Params& P) {
