@@ -119,20 +119,30 @@ struct HsK2 {
     __device__ double band_xf(double po, double rt) const { return ADD(rt, MUL(beta, po)); }
     __device__ int sync() const { return mode == MODE_FULL ? 2 : 1; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
-    template <class In, class RR>
-    __device__ void row(const Params& P, int i, const In& in, const RR& R, double* acc) const {
-        const double po = SV(0);
-        P.x[i] = ADD(SV(2), MUL(alpha, po));
-        if (mode != MODE_FULL) return;
+    // split form (see cgvk_stream.cuh PairOf): the SpMV product, then the rest
+    static constexpr bool PAIR = true;
+    __device__ bool wants_spmv() const { return mode == MODE_FULL; }
+    template <class In>
+    __device__ auto gfun(const Params& P, const In& in) const {
         const double* __restrict__ rtv = PREC ? P.rt : P.r;
         const double* __restrict__ pg = pold;
         const double b = beta;
-        const double sum =
-            row_dot(R, [&](int j) { return in.gather_p(j, rtv, pg, b); });
-        const double pi = ADD(SV(1), MUL(b, po));
+        return [=](int j) { return in.gather_p(j, rtv, pg, b); };
+    }
+    template <class In>
+    __device__ void apply(const Params& P, int i, const In& in, double sum, double* acc) const {
+        const double po = SV(0);
+        P.x[i] = ADD(SV(2), MUL(alpha, po));
+        if (mode != MODE_FULL) return;
+        const double pi = ADD(SV(1), MUL(beta, po));
         pnew[i] = pi;
         P.s[i] = sum;
         acc[0] = ADD(acc[0], MUL(pi, sum));
+    }
+    template <class In, class RR>
+    __device__ void row(const Params& P, int i, const In& in, const RR& R, double* acc) const {
+        const double sum = wants_spmv() ? row_dot(R, gfun(P, in)) : 0.0;
+        apply(P, i, in, sum, acc);
     }
     __device__ void finish(const Params& P, Ctrl* c, const double* tot) const {
         c->mode2 = MODE_SKIP;
@@ -221,10 +231,19 @@ struct CgK2 {
     __device__ const double* gsrc(const Params& P, int) const { return PREC ? P.rt : P.r; }
     __device__ int sync() const { return 2; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
+    static constexpr bool PAIR = true;
+    __device__ bool wants_spmv() const { return true; }
+    template <class In>
+    __device__ auto gfun(const Params& P, const In& in) const {
+        const double* __restrict__ rtv = PREC ? P.rt : P.r;
+        return [=](int j) { return in.gather(0, j, rtv); };
+    }
     template <class In, class RR>
     __device__ void row(const Params& P, int i, const In& in, const RR& R, double* acc) const {
-        const double* __restrict__ rtv = PREC ? P.rt : P.r;
-        const double w = row_dot(R, [&](int j) { return in.gather(0, j, rtv); });
+        apply(P, i, in, row_dot(R, gfun(P, in)), acc);
+    }
+    template <class In>
+    __device__ void apply(const Params& P, int i, const In& in, double w, double* acc) const {
         P.w[i] = w;
         const double ri = SV(0), rti = PREC ? SV(1) : ri;
         acc[0] = ADD(acc[0], MUL(rti, ri));
@@ -351,10 +370,19 @@ struct PrK2 {
     __device__ const double* gsrc(const Params& P, int) const { return P.p0; }
     __device__ int sync() const { return 2; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
+    static constexpr bool PAIR = true;
+    __device__ bool wants_spmv() const { return true; }
+    template <class In>
+    __device__ auto gfun(const Params& P, const In& in) const {
+        const double* __restrict__ p = P.p0;
+        return [=](int j) { return in.gather(0, j, p); };
+    }
     template <class In, class RR>
     __device__ void row(const Params& P, int i, const In& in, const RR& R, double* acc) const {
-        const double* __restrict__ p = P.p0;
-        const double s = row_dot(R, [&](int j) { return in.gather(0, j, p); });
+        apply(P, i, in, row_dot(R, gfun(P, in)), acc);
+    }
+    template <class In>
+    __device__ void apply(const Params& P, int i, const In& in, double s, double* acc) const {
         P.s[i] = s;
         const double st = PREC ? MUL(SV(3), s) : s;
         const double r = SV(1);
@@ -514,10 +542,18 @@ struct GvK2 {
     __device__ const double* gsrc(const Params& P, int) const { return PREC ? P.wt : P.w; }
     __device__ int sync() const { return 1; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
-    template <class In, class RR>
-    __device__ void row(const Params& P, int i, const In& in, const RR& R, double*) const {
+    static constexpr bool PAIR = true;
+    __device__ bool wants_spmv() const { return true; }
+    template <class In>
+    __device__ auto gfun(const Params& P, const In& in) const {
         const double* __restrict__ wtv = PREC ? P.wt : P.w;  // w~ stored by K1
-        P.t[i] = row_dot(R, [&](int j) { return in.gather(0, j, wtv); });
+        return [=](int j) { return in.gather(0, j, wtv); };
+    }
+    template <class In>
+    __device__ void apply(const Params& P, int i, const In&, double t, double*) const { P.t[i] = t; }
+    template <class In, class RR>
+    __device__ void row(const Params& P, int i, const In& in, const RR& R, double* acc) const {
+        apply(P, i, in, row_dot(R, gfun(P, in)), acc);
     }
     __device__ void finish(const Params&, Ctrl* c, const double*) const { c->mode2 = MODE_SKIP; }
 };
