@@ -290,6 +290,7 @@ __global__ void __launch_bounds__(BandShape<Op>::THREADS, BandShape<Op>::MINB) k
         if (P.dist && mode == 2) {
 #pragma unroll
             for (int d = 0; d < Op::ND; ++d) P.rank_tot[d] = tot[d];
+            if constexpr (HasDistMark<Op>::value) op.dist_mark(P, P.ctrl);
             return;
         }
         op.finish(P, P.ctrl, tot);

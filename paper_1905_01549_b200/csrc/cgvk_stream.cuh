@@ -37,6 +37,21 @@ constexpr int kMaxStages = 8;
 constexpr int kRpInts = kBlock + 4;          // row_ptr slice (257 used), padded to 16 B
 constexpr int kMaxVec = 12;
 
+// Optional Op hook for row-partitioned solves: `void dist_mark(const Params&,
+// Ctrl*) const`, run by the reducing kernel's last CTA when it stops at its
+// rank-local total — the control state the NEXT kernel needs before the
+// exchanged reduction is finalised (GV / pipe-PR overlap that finalisation
+// with their SpMV kernel).
+template <class T, class = void>
+struct HasDistMark {
+    static constexpr bool value = false;
+};
+template <class T>
+struct HasDistMark<T, std::void_t<decltype(std::declval<const T&>().dist_mark(std::declval<const Params&>(),
+                                                                                std::declval<Ctrl*>()))>> {
+    static constexpr bool value = true;
+};
+
 // Optional per-Op shared-memory budget hint: `static constexpr int SMEM_CTAS`
 // (resident CTAs per SM the stage ring is sized for).
 template <class T, class = void>
@@ -759,6 +774,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
         if (P.dist && mode == 2) {  // rank total: k_finalize folds all ranks in rank order
 #pragma unroll
             for (int d = 0; d < Op::ND; ++d) P.rank_tot[d] = tot[d];
+            if constexpr (HasDistMark<Op>::value) op.dist_mark(P, P.ctrl);
             return;
         }
         op.finish(P, P.ctrl, tot);

@@ -498,13 +498,18 @@ struct GvK1 {
             }
         }
     }
+    // row-partitioned: K2 (t = A w~) may start before the exchanged reduction
+    // is finalised, so its go-ahead is set here, by K1 itself
+    __device__ void dist_mark(const Params&, Ctrl* c) const {
+        if (S) c->mode2 = MODE_FULL;
+    }
     __device__ void finish(const Params& P, Ctrl* c, const double* tot) const {
         if (!S) {  // materialisation only
             c->form_pending = 0;
             return;
         }
         c->k += 1;
-        c->mode2 = MODE_FULL;  // t = A w~ precedes the checks in the reference
+        if (!P.dist) c->mode2 = MODE_FULL;  // t = A w~ precedes the checks in the reference
         c->stats[STAT_SPMV] += 1;
         c->stats[STAT_PREC] += PREC;
         c->stats[STAT_RED] += 2;
@@ -600,6 +605,10 @@ struct PprK1 {
     }
     __device__ int sync() const { return 2; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[0]; }
+    // row-partitioned: the block SpMV's go-ahead, set by K1 (see GvK1)
+    __device__ void dist_mark(const Params&, Ctrl* c) const {
+        if (valid) c->mode2 = MODE_FULL;
+    }
     template <class In, class RR>
     __device__ void row(const Params& P, int i, const In& in, const RR&, double* acc) const {
         const double p_old = SV(1), s_old = SV(3), w_old = SV(4), u = SV(5);
@@ -655,7 +664,7 @@ struct PprK1 {
             return;
         }
         c->sc[SB] = beta;
-        c->mode2 = MODE_FULL;  // the block SpMV precedes the checks in the reference
+        if (!P.dist) c->mode2 = MODE_FULL;  // the block SpMV precedes the checks in the reference
         if (recw) {
             c->stats[STAT_BLOCK] += 1;
             c->stats[STAT_PREC] += 2 * PREC;
