@@ -13,9 +13,15 @@
 //
 // Reduction order is the canonical one of cgvk_device.cuh, expressed on
 // "virtual CTAs": virtual CTA vb (0 <= vb < Gv = min(gmax, ntiles)) owns
-// tiles vb, vb+Gv, ...; a physical CTA p runs virtual CTAs p, p+Gp, ... one
-// after the other (Gp = resident CTAs), so the result bits do not depend on
-// how many CTAs fit on the chip.
+// tiles vb, vb+Gv, ... (order 0; order 1: a contiguous run of tiles); a
+// physical CTA p runs virtual CTAs p, p+Gp, ... one after the other (Gp =
+// resident CTAs), so the result bits do not depend on how many CTAs fit on
+// the chip.
+//
+// Opt-in variants of the SpMV kernels (template SEG): 16-bit
+// tile-offset columns with x still through L1 (csr16), or with the x tiles
+// staged by TMA next to the tile (seg). The band engine (cgvk_band.cuh)
+// replaces this kernel for narrow-band long-row matrices.
 #pragma once
 
 #include "cgvk_device.cuh"
