@@ -175,6 +175,9 @@ int cgvk_dot(cgvk_matrix a, const double* x, const double* y, double* out);
  * one n-vector copy. For calibration only (scripts/cost_model.py). */
 enum { CGVK_TIME_SPMV = 0, CGVK_TIME_BLOCK_SPMV, CGVK_TIME_DOT, CGVK_TIME_COPY, CGVK_TIMED_OPS };
 int cgvk_time_ops(cgvk_matrix a, int reps, double* ms);
+/* Experiments only: per-CTA phase timestamps (ns) of the last update / SpMV
+ * kernel launches, [2][1024][8]; CGVK_EINVAL unless built with CGVK_TIMELINE. */
+int cgvk_debug_timeline(unsigned long long* out);
 /* The reduction-tree parameters the oracle needs: rows per tile (= threads
  * per CTA), the CTA cap G and the tile order (0 strided, 1 contiguous). */
 int cgvk_reduction_config(cgvk_matrix a, int* block, int* gmax, int* order);

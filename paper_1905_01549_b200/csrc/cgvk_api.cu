@@ -793,6 +793,19 @@ int cgvk_time_ops(cgvk_matrix a, int reps, double* ms) {
     return CGVK_OK;
 }
 
+// CGVK_TIMELINE builds only (A/B experiments): the per-CTA phase stamps of
+// the last update (0) and SpMV (1) kernel launches, [2][1024][8] ns.
+int cgvk_debug_timeline(unsigned long long* out) {
+#if CGVK_TIMELINE
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpyFromSymbol(out, g_timeline, sizeof(g_timeline)));
+    return CGVK_OK;
+#else
+    (void)out;
+    return set_err(CGVK_EINVAL, "built without CGVK_TIMELINE");
+#endif
+}
+
 int cgvk_host_register(void* ptr, uint64_t bytes) {
     CK(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault));
     return CGVK_OK;
@@ -1388,7 +1401,7 @@ int solver_alloc(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, cud
     const int64_t nv = a->ncols + 32;
     if ((rc = dalloc(&s->x, nv)) || (rc = dalloc(&s->r, nv)) || (rc = dalloc(&s->p0, nv)) ||
         (rc = dalloc(&s->s, nv)) || (rc = dalloc(&s->b, nv)) || (rc = dalloc(&s->tmp, nv)) ||
-        (rc = dalloc(&s->part, kMaxDots * (size_t)a->gmax)) || (rc = dalloc(&s->hist, s->hist_cap)) ||
+        (rc = dalloc(&s->part, kMaxDots * (size_t)a->gmax + 4)) || (rc = dalloc(&s->hist, s->hist_cap)) ||
         (rc = dalloc(&s->dout, 8)) || (rc = dalloc(&s->counter, 4)) || (rc = dalloc(&s->ctrl, 1)))
         return bail(rc);
     if (v == CGVK_HS && (rc = dalloc(&s->p1, nv))) return bail(rc);

@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(BandShape<Op>::THREADS, BandShape<Op>::MINB) k
             mbar_init(&H->full[s], 1);
             mbar_init(&H->empty[s], kWarps);
         }
+        mbar_init(&H->fold_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -281,20 +282,21 @@ __global__ void __launch_bounds__(BandShape<Op>::THREADS, BandShape<Op>::MINB) k
     for (int d = 0; d < Op::ND; ++d) tot[d] = 0.0;
     if (mode == 2) {
         if constexpr (Op::ND > 0) {
-            fold_partials<Op::ND>(P.part, Gv, t, tot);
+            // the idle stage ring and window rings hold the partials
+            fold_last<Op::ND>(P.part, Gv, t, H, stages, (size_t)NS * S.stage_bytes + (size_t)NWIN * RW * 8, tot);
             cta_tree_c<Op::ND>(tot, H->red);
         }
     }
-    if (t == 0) {
-        *counter = 0u;
-        if (P.dist && mode == 2) {
+    if (t == 0) *counter = 0u;
+    if (P.dist && mode == 2) {
+        if (t == 0) {
 #pragma unroll
             for (int d = 0; d < Op::ND; ++d) P.rank_tot[d] = tot[d];
             if constexpr (HasDistMark<Op>::value) op.dist_mark(P, P.ctrl);
-            return;
         }
-        op.finish(P, P.ctrl, tot);
+        return;
     }
+    finish_last(op, P, H, tot, t);
 }
 
 }  // namespace cgvk

@@ -493,7 +493,11 @@ struct PipeHeader {
     int pad[3];
     int segbase[kMaxStages][8];  // 16-bit-column CSR: first row of each tile offset's x tile
     double red[kMaxDots * 32];
+    uint64_t fold_bar;           // last CTA: bulk copy of the partials into the idle ring
+    uint64_t pad2;
+    Ctrl cs;                     // last CTA: the control block finish() works on
 };
+
 
 // Last CTA: thread t sums partials q = t, t+256, ... in that order (the
 // canonical fold); all loads are issued before the in-order adds so the fold
@@ -516,6 +520,63 @@ __device__ __noinline__ void fold_partials(const double* part, int Gv, int t, do
                 for (int d = 0; d < ND; ++d) tot[d] = ADD(tot[d], buf[u][d]);
             }
         }
+    }
+}
+
+// Last CTA, all consumer threads: the partials of every virtual CTA, folded in
+// the canonical order (thread t: q = t, t+256, ...). When they fit the idle
+// stage ring they arrive with ONE bulk copy (one L2 latency, no registers);
+// otherwise fold_partials issues the loads from registers.
+template <int ND>
+__device__ __forceinline__ void fold_last(const double* part, int Gv, int t, PipeHeader* H, unsigned char* ring,
+                                          size_t ring_bytes, double (&tot)[ND]) {
+    const uint32_t bytes = (uint32_t)((ND * Gv * 8 + 15) & ~15);
+    if (bytes > ring_bytes) {
+        fold_partials<ND>(part, Gv, t, tot);
+        return;
+    }
+    if (t == 0) {
+        // the partials were written by other CTAs (generic proxy, released by
+        // their fences + the arrival atomic); order them before the bulk read
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        mbar_expect_tx(&H->fold_bar, bytes);
+        bulk_g2s(ring, part, bytes, &H->fold_bar, 0);
+    }
+    mbar_wait(&H->fold_bar, 0);
+    const double* sp = reinterpret_cast<const double*>(ring);
+    for (int q = t; q < Gv; q += kConsumers) {
+#pragma unroll
+        for (int d = 0; d < ND; ++d) tot[d] = ADD(tot[d], sp[d * Gv + q]);
+    }
+}
+
+// Last CTA, all consumer threads: op.finish on a shared-memory copy of the
+// control block (its read-modify-writes then cost shared-memory latency, not
+// a chain of L2 round trips); only the 4-byte words finish changed are
+// written back, so a concurrent finalize of a row-partitioned solve (GV /
+// pipe-PR: k_finalize on the side stream while K2 ends) never sees its
+// fields overwritten with a stale copy, and the arrival counters stay as the
+// atomics left them.
+constexpr int kCtrlWords = sizeof(Ctrl) / 16;
+template <class Op>
+__device__ __forceinline__ void finish_last(const Op& op, const Params& P, PipeHeader* H, const double* tot, int t) {
+    uint4* cs = reinterpret_cast<uint4*>(&H->cs);
+    uint4* cg = reinterpret_cast<uint4*>(P.ctrl);
+    uint4 orig = make_uint4(0, 0, 0, 0);
+    if (t < kCtrlWords) {
+        orig = __ldcg(cg + t);
+        cs[t] = orig;
+    }
+    consumer_sync();
+    if (t == 0) op.finish(P, &H->cs, tot);
+    consumer_sync();
+    if (t < kCtrlWords) {
+        const uint4 now = cs[t];
+        unsigned int* dst = reinterpret_cast<unsigned int*>(cg + t);
+        if (now.x != orig.x) dst[0] = now.x;
+        if (now.y != orig.y) dst[1] = now.y;
+        if (now.z != orig.z) dst[2] = now.z;
+        if (now.w != orig.w) dst[3] = now.w;
     }
 }
 
@@ -587,6 +648,24 @@ __device__ __forceinline__ void stage_csr(const Params& P, const StageCfg& S, Pi
 // CGVK_SPMV_MIN_CTAS when their stage lets that many CTAs fit, else 1 — a
 // long-row matrix (R4M, ~27 entries/row) whose 2-stage ring already fills the
 // SM gets the registers to keep a whole chunk of gathers in flight.
+// CGVK_TIMELINE=1 (A/B builds only): per-CTA %globaltimer stamps of the
+// kernel's phases, read back with cgvk_debug_timeline.
+#ifndef CGVK_TIMELINE
+#define CGVK_TIMELINE 0
+#endif
+#if CGVK_TIMELINE
+__device__ unsigned long long g_timeline[2][1024][8];
+#endif
+__device__ __forceinline__ void tl_mark(int kernel, int slot) {
+#if CGVK_TIMELINE
+    if (threadIdx.x == 0 && blockIdx.x < 1024) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_timeline[kernel][blockIdx.x][slot] = t;
+    }
+#endif
+}
+
 // SEG 1: the segment engine (S.nd > 0): the stage also carries the x tiles
 // the tile's columns fall in (tile + seg_d[q]); gathers read shared memory.
 // SEG 2: CSR with 16-bit columns decoded against those tiles' bases, x
@@ -604,6 +683,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
             mbar_init(&H->full[s], 1);
             mbar_init(&H->empty[s], kWarps);
         }
+        mbar_init(&H->fold_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -623,7 +703,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
             if (npre == NS) break;
         }
     }
+    tl_mark(Op::CSR, 0);
     pdl_wait();
+    tl_mark(Op::CSR, 1);
     if (!PdlLate<Op>::value) pdl_trigger();
     Op op;
     if (!op.enter(P)) {  // uniform over the grid
@@ -708,6 +790,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
             const int jj = j++;
             const int slot = jj % NS;
             mbar_wait(&H->full[slot], (jj / NS) & 1);
+            if (jj == 0) tl_mark(Op::CSR, 2);
             StageView V = stage_view(stages, S, slot);
             const int i = tile * kBlock + t;
             if (i < P.n) {
@@ -762,29 +845,35 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
         }
     }
     if (PdlLate<Op>::value) pdl_trigger();
+    tl_mark(Op::CSR, 3);
     const int mode = op.sync();
     if (mode == 0) return;
     unsigned int* counter = op.counter(P);
-    if (!arrive_last_c(counter, &H->last_flag)) return;
+    const bool is_last = arrive_last_c(counter, &H->last_flag);
+    tl_mark(Op::CSR, 4);
+    if (!is_last) return;
     double tot[Op::ND > 0 ? Op::ND : 1];
 #pragma unroll
     for (int d = 0; d < Op::ND; ++d) tot[d] = 0.0;
     if (mode == 2) {
         if constexpr (Op::ND > 0) {
-            fold_partials<Op::ND>(P.part, Gv, t, tot);
+            fold_last<Op::ND>(P.part, Gv, t, H, stages, (size_t)NS * S.stage_bytes, tot);
+            tl_mark(Op::CSR, 7);
             cta_tree_c<Op::ND>(tot, H->red);
         }
     }
-    if (t == 0) {
-        *counter = 0u;
-        if (P.dist && mode == 2) {  // rank total: k_finalize folds all ranks in rank order
+    if (t == 0) *counter = 0u;
+    if (P.dist && mode == 2) {  // rank total: k_finalize folds all ranks in rank order
+        if (t == 0) {
 #pragma unroll
             for (int d = 0; d < Op::ND; ++d) P.rank_tot[d] = tot[d];
             if constexpr (HasDistMark<Op>::value) op.dist_mark(P, P.ctrl);
-            return;
         }
-        op.finish(P, P.ctrl, tot);
+        return;
     }
+    tl_mark(Op::CSR, 5);
+    finish_last(op, P, H, tot, t);
+    tl_mark(Op::CSR, 6);
 }
 
 }  // namespace cgvk

@@ -1,0 +1,42 @@
+"""Phase timeline of one iteration's kernels (CGVK_TIMELINE=1 build):
+per-CTA stamps 0 entry, 1 after griddepcontrol.wait, 2 first stage ready,
+3 tiles done, 4 arrival counted, 5 fold done (last CTA), 6 finish done."""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1905_01549_b200 import cgvk, problems as pb  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "p64"
+P = pb.config_problem(cfg)
+A = cgvk.DeviceMatrix.from_csr(P.A)
+lib = cgvk._lib
+lib.cgvk_debug_timeline.argtypes = [C.c_void_p]
+for v in sys.argv[2:] or ["pr", "hs", "gv"]:
+    s = cgvk.initialize(cgvk.VariantConfig.make(cgvk.variant_from_name(v)), A, cgvk.Precond.JACOBI, P.b, P.x0)
+    s.time_steps(20)
+    s.step(1)
+    s.sync()
+    lib.cgvk_debug_timeline_clear() if hasattr(lib, "cgvk_debug_timeline_clear") else None
+    buf = np.zeros((2, 1024, 8), np.uint64)
+    assert lib.cgvk_debug_timeline(buf.ctypes.data) == 0
+    print(f"== {cfg} {v}")
+    t0 = None
+    for k, name in ((0, "K1 update"), (1, "K2 spmv")):
+        b = buf[k].astype(np.int64)
+        live = b[:, 0] > 0
+        b = b[live]
+        if t0 is None:
+            t0 = b[:, 0].min()
+        ent, wt, first, done, arr = (b[:, q] - t0 for q in range(5))
+        fin = b[:, 6][b[:, 6] > 0] - t0 if (b[:, 6] > 0).any() else np.array([0])
+        fold = b[:, 5][b[:, 5] > 0] - t0 if (b[:, 5] > 0).any() else np.array([0])
+        loads = b[:, 7][b[:, 7] > 0] - t0 if (b[:, 7] > 0).any() else np.array([0])
+        print(f"  {name}: CTAs {live.sum():4d} entry {ent.min()/1e3:6.2f}..{ent.max()/1e3:6.2f} us  "
+              f"wait done {wt.min()/1e3:6.2f}..{wt.max()/1e3:6.2f}  first stage {first.min()/1e3:6.2f}..{first.max()/1e3:6.2f}  "
+              f"tiles done {done.min()/1e3:6.2f}..{done.max()/1e3:6.2f}  arrived {arr.max()/1e3:6.2f}  "
+              f"fold loads {loads.max()/1e3:6.2f} fold {fold.max()/1e3:6.2f}  finish {fin.max()/1e3:6.2f}")
+    s.close()
