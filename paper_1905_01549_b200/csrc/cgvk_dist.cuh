@@ -15,19 +15,46 @@ namespace cgvk {
 
 template <class Op>
 __global__ void k_finalize(Params P, const double* __restrict__ all_tot, int nranks) {
-    if (threadIdx.x != 0) return;
+    // one warp: the control block and the rank totals come in with one load
+    // each per lane; enter/finish run on the shared copy; only the words
+    // finish changed are written back (K2 of an overlapped GV / pipe-PR step
+    // may be ending concurrently and writes its own, disjoint field)
+    constexpr int kWords = sizeof(Ctrl) / 4;
+    __shared__ __align__(16) Ctrl cs;
+    __shared__ double at[64 * kMaxDots];
+    const int t = threadIdx.x;
     pdl_wait();
-    Op op;
-    if (!op.enter(P)) return;  // nothing was reduced (or it already finished locally)
-    if (op.sync() != 2) return;
-    double tot[Op::ND > 0 ? Op::ND : 1];
+    unsigned int* cw = reinterpret_cast<unsigned int*>(&cs);
+    unsigned int* gw = reinterpret_cast<unsigned int*>(P.ctrl);
+    unsigned int orig[(kWords + 31) / 32];
 #pragma unroll
-    for (int d = 0; d < Op::ND; ++d) tot[d] = 0.0;
-    for (int r = 0; r < nranks; ++r) {
-#pragma unroll
-        for (int d = 0; d < Op::ND; ++d) tot[d] = ADD(tot[d], all_tot[r * kMaxDots + d]);
+    for (int u = 0; u < (kWords + 31) / 32; ++u) {
+        const int q = t + 32 * u;
+        if (q < kWords) cw[q] = orig[u] = __ldcg(gw + q);
     }
-    op.finish(P, P.ctrl, tot);
+    for (int q = t; q < nranks * kMaxDots; q += 32) at[q] = __ldcg(all_tot + q);
+    __syncwarp();
+    if (t == 0) {
+        Params Q = P;
+        Q.ctrl = &cs;
+        Op op;
+        if (op.enter(Q) && op.sync() == 2) {  // else nothing was reduced (or it finished locally)
+            double tot[Op::ND > 0 ? Op::ND : 1];
+#pragma unroll
+            for (int d = 0; d < Op::ND; ++d) tot[d] = 0.0;
+            for (int r = 0; r < nranks; ++r) {
+#pragma unroll
+                for (int d = 0; d < Op::ND; ++d) tot[d] = ADD(tot[d], at[r * kMaxDots + d]);
+            }
+            op.finish(Q, &cs, tot);
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < (kWords + 31) / 32; ++u) {
+        const int q = t + 32 * u;
+        if (q < kWords && cw[q] != orig[u]) gw[q] = cw[q];
+    }
 }
 
 // The vector a halo exchange moves: `a`, or HS's current p (a/b by ctrl->pcur).
