@@ -146,6 +146,7 @@ struct cgvk_matrix_s {
     int64_t nsend_lo = 0, nsend_hi = 0;
     int* send_lo = nullptr;         // local rows the lower neighbour's halo reads (sorted)
     int* send_hi = nullptr;         // local rows the upper neighbour's halo reads (sorted)
+    int64_t send_lo0 = -1, send_hi0 = -1;  // first row when those rows are contiguous (z-slabs), else -1
     int order = 0;  // canonical tile order (fixed per matrix; reported to the oracle)
     int l2pol = 0;  // TMA L2 policy for the pipeline streams
     int* rp = nullptr;
