@@ -241,11 +241,17 @@ def run_reference_arm(args, rank, world, dist):
 METRIC = "CG iterations/s (six-variant sweep) and effective HBM GB/s per variant"
 
 
-def workload_config(args, P) -> dict:
+def workload_config(args, P, ranks: int = 1) -> dict:
+    per = [iter_bytes(v, P.A.n, P.A.nnz, True) / max(ranks, 1) / 1e6 for v in VARIANTS]
+    lo, hi = min(per), max(per)
+    l2 = (f"per-GPU working set {lo:.0f}-{hi:.0f} MB per iteration > L2 (126 MB); no flush needed"
+          if lo > 126 else
+          f"per-GPU working set {lo:.0f}-{hi:.0f} MB per iteration fits the 126 MB L2: the solve runs "
+          f"L2-resident as it would in use (latency-bound regime, SURVEY 8d); no flush")
     return {"workload": f"{args.config} ({P.A.n} rows, {P.A.nnz} nnz) fp64 CSR, Jacobi, "
                         f"six variants, K fixed iterations each",
             "variants": VARIANTS, "n": P.A.n, "nnz": P.A.nnz, "precond": "jacobi",
-            "l2": "working set > L2 (126 MB); no flush", "parallelism": "single-gpu"}
+            "l2": l2, "parallelism": "single-gpu"}
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -487,7 +493,7 @@ def run_gpu_arm(args, rank, local, world, dist):
         # call + the captured kernels per iteration (halo pack/unpack and
         # finalize kernels included when partitioned; NCCL's own not counted)
         launches = sum(1 + per[v]["launches_per_iter"] * per[v]["iters"] for v in VARIANTS)
-        cfg = workload_config(args, P)
+        cfg = workload_config(args, P, world if partitioned else 1)
         if partitioned:
             cfg["parallelism"] = (f"row-partitioned z-slabs over {world} GPUs (NCCL)" if world > 1 or args.nccl
                                   else f"row-partitioned, {args.emulate_ranks} in-process ranks on 1 GPU")
