@@ -143,6 +143,19 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
     return p;
 }
 
+__device__ __forceinline__ uint64_t evict_last_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+// L2 policy of a pipeline's matrix stream: 0/1 evict-first (streamed once per
+// iteration), 2 none, 3 evict-last (an A that fits L2 with the vectors stays
+// resident across iterations; chosen per matrix by size)
+__device__ __forceinline__ uint64_t matrix_policy(int l2pol) {
+    return l2pol < 2 ? evict_first_policy() : l2pol == 3 ? evict_last_policy() : 0;
+}
+
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
 
 // Canonical CTA tree over the 256 consumer threads (same order as cta_tree).
@@ -694,7 +707,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
     uint64_t pol = 0;
     int npre = 0;
     if (Op::CSR && producer) {
-        pol = P.l2pol < 2 ? evict_first_policy() : 0;
+        pol = matrix_policy(P.l2pol);
         CGVK_FOR_VB(vb, P.order, blockIdx.x, Gv, Gp) {
             CGVK_FOR_TILE(tile, P.order, vb, ntiles, Gv) {
                 if (npre == NS) break;
@@ -720,7 +733,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
 
     if (warp == kWarps) {  // ------------------------------ producer warp
         if (!producer) return;
-        if (!Op::CSR) pol = P.l2pol < 2 ? evict_first_policy() : 0;
+        if (!Op::CSR) pol = P.l2pol < 2 ? evict_first_policy() : 0;  // vectors: never evict-last
         const double* vp[kMaxVec];
 #pragma unroll
         for (int v = 0; v < Op::NV; ++v) vp[v] = op.vec(P, v);
