@@ -806,6 +806,8 @@ int cgvk_debug_timeline(unsigned long long* out) {
 #if CGVK_TIMELINE
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpyFromSymbol(out, g_timeline, sizeof(g_timeline)));
+    static unsigned long long zeros[2 * 1024 * 8] = {};  // read-and-clear
+    CK(cudaMemcpyToSymbol(g_timeline, zeros, sizeof(g_timeline)));
     return CGVK_OK;
 #else
     (void)out;

@@ -18,10 +18,10 @@ lib.cgvk_debug_timeline.argtypes = [C.c_void_p]
 for v in sys.argv[2:] or ["pr", "hs", "gv"]:
     s = cgvk.initialize(cgvk.VariantConfig.make(cgvk.variant_from_name(v)), A, cgvk.Precond.JACOBI, P.b, P.x0)
     s.time_steps(20)
+    buf = np.zeros((2, 1024, 8), np.uint64)
+    lib.cgvk_debug_timeline(buf.ctypes.data)  # read-and-clear
     s.step(1)
     s.sync()
-    lib.cgvk_debug_timeline_clear() if hasattr(lib, "cgvk_debug_timeline_clear") else None
-    buf = np.zeros((2, 1024, 8), np.uint64)
     assert lib.cgvk_debug_timeline(buf.ctypes.data) == 0
     print(f"== {cfg} {v}")
     t0 = None
