@@ -52,6 +52,7 @@ struct __align__(16) Ctrl {
     unsigned int count[2];  // last-CTA arrival counters
     unsigned int bar_count; // persistent kernel: grid barrier arrivals
     unsigned int bar_gen;   // persistent kernel: grid barrier generation
+    unsigned int sched[2];  // dynamic virtual-CTA scheduler of the two kernels (next vb - Gp)
 };
 
 struct Params {

@@ -58,6 +58,25 @@ struct HasDistMark<T, std::void_t<decltype(std::declval<const T&>().dist_mark(st
     static constexpr bool value = true;
 };
 
+// Dynamic virtual-CTA scheduling (CGVK_DYN): a physical CTA runs its first
+// virtual CTA statically (the pre-wait matrix prefetch needs it) and then
+// grabs the next one from a counter, so CTAs that the memory system serves
+// more slowly take fewer virtual CTAs instead of setting the kernel's end.
+// Which physical CTA runs a virtual CTA does not change any bit: partials are
+// indexed by virtual CTA. Only for kernels that always count arrivals (the
+// last CTA resets the counter): an Op opts in with `ALWAYS_ARRIVES = true`.
+#ifndef CGVK_DYN
+#define CGVK_DYN 0
+#endif
+template <class T, class = void>
+struct DynOf {
+    static constexpr bool value = false;
+};
+template <class T>
+struct DynOf<T, std::void_t<decltype(T::ALWAYS_ARRIVES)>> {
+    static constexpr bool value = T::ALWAYS_ARRIVES && CGVK_DYN != 0;
+};
+
 // Optional per-Op shared-memory budget hint: `static constexpr int SMEM_CTAS`
 // (resident CTAs per SM the stage ring is sized for).
 template <class T, class = void>
@@ -506,6 +525,9 @@ struct PipeHeader {
     int pad[3];
     int segbase[kMaxStages][8];  // 16-bit-column CSR: first row of each tile offset's x tile
     double red[kMaxDots * 32];
+    int slot_tile[kMaxStages];   // dynamic scheduling: the stage's tile (-1: no more work),
+    int slot_vb[kMaxStages];     //   its virtual CTA and first / last-tile flags
+    int slot_flags[kMaxStages];
     uint64_t fold_bar;           // last CTA: bulk copy of the partials into the idle ring
     uint64_t pad2;
     Ctrl cs;                     // last CTA: the control block finish() works on
@@ -706,6 +728,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
     // that kernel is still finishing, then waits for it.
     uint64_t pol = 0;
     int npre = 0;
+    const bool dyn = DynOf<Op>::value && P.order == 0;
     if (Op::CSR && producer) {
         pol = matrix_policy(P.l2pol);
         CGVK_FOR_VB(vb, P.order, blockIdx.x, Gv, Gp) {
@@ -713,7 +736,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
                 if (npre == NS) break;
                 stage_csr(P, S, H, stages, npre++, tile, pol, /*arrive=*/false);
             }
-            if (npre == NS) break;
+            if (npre == NS || dyn) break;  // dynamic: only the static first virtual CTA
         }
     }
     tl_mark(Op::CSR, 0);
@@ -744,10 +767,15 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
         }
         int j = 0;
         const uint64_t vpol = P.l2pol == 0 ? pol : 0;
-        CGVK_FOR_VB(vb, P.order, blockIdx.x, Gv, Gp) {
+        auto produce_vb = [&](int vb) {
             CGVK_FOR_TILE(tile, P.order, vb, ntiles, Gv) {
                 const int slot = j % NS;
                 if (j >= NS) mbar_wait(&H->empty[slot], ((j / NS) - 1) & 1);
+                if (dyn) {
+                    H->slot_tile[slot] = tile;
+                    H->slot_vb[slot] = vb;
+                    H->slot_flags[slot] = (tile == vb ? 1 : 0) | (tile + Gv >= ntiles ? 2 : 0);
+                }
                 StageView V = stage_view(stages, S, slot);
                 const int r0 = tile * kBlock;
                 const int rows = min(kBlock, P.n - r0);
@@ -788,6 +816,16 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
                 }
                 ++j;
             }
+        };
+        if (dyn) {
+            unsigned int* sched = P.ctrl->sched + (op.counter(P) - P.ctrl->count);
+            for (int vb = blockIdx.x; vb < Gv; vb = Gp + (int)atomicAdd(sched, 1u)) produce_vb(vb);
+            const int slot = j % NS;  // sentinel stage: no more work
+            if (j >= NS) mbar_wait(&H->empty[slot], ((j / NS) - 1) & 1);
+            H->slot_tile[slot] = -1;
+            mbar_arrive(&H->full[slot]);
+        } else {
+            CGVK_FOR_VB(vb, P.order, blockIdx.x, Gv, Gp) produce_vb(vb);
         }
         return;
     }
@@ -796,65 +834,88 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
     const int t = threadIdx.x;
     double acc[Op::ND > 0 ? Op::ND : 1];
     int j = 0;
-    CGVK_FOR_VB(vb, P.order, blockIdx.x, Gv, Gp) {
-#pragma unroll
-        for (int d = 0; d < Op::ND; ++d) acc[d] = 0.0;
-        CGVK_FOR_TILE(tile, P.order, vb, ntiles, Gv) {
-            const int jj = j++;
-            const int slot = jj % NS;
-            mbar_wait(&H->full[slot], (jj / NS) & 1);
-            if (jj == 0) tl_mark(Op::CSR, 2);
-            StageView V = stage_view(stages, S, slot);
-            const int i = tile * kBlock + t;
-            if (i < P.n) {
-                if constexpr (SEG == 2) {
-                    const int b = V.rp[t];
-                    RowD R{nullptr, nullptr, H->segbase[slot], V.rp[t + 1] - b};
-                    if (H->direct[slot]) {
-                        R.va = P.va + b;
-                        R.ci = P.ci16 + b;
-                    } else {
-                        R.va = V.va + (b - H->k0a[slot]);
-                        R.ci = V.ci16 + (b - H->k0c[slot]);
-                    }
-                    op.row(P, i, StagedIn{V.vec + t}, R, acc);
-                } else if constexpr (SEG == 1) {
-                    const int b = V.rp[t];
-                    RowSeg R{nullptr, nullptr, V.rp[t + 1] - b};
-                    if (H->direct[slot]) {
-                        R.va = P.va + b;
-                        R.ci = P.ci16 + b;
-                    } else {
-                        R.va = V.va + (b - H->k0a[slot]);
-                        R.ci = V.ci16 + (b - H->k0c[slot]);
-                    }
-                    op.row(P, i, SegIn{V.vec + t, V.gx, V.gx + S.nd * kBlock}, R, acc);
+    auto consume_tile = [&](int slot, int tile) {
+        StageView V = stage_view(stages, S, slot);
+        const int i = tile * kBlock + t;
+        if (i < P.n) {
+            if constexpr (SEG == 2) {
+                const int b = V.rp[t];
+                RowD R{nullptr, nullptr, H->segbase[slot], V.rp[t + 1] - b};
+                if (H->direct[slot]) {
+                    R.va = P.va + b;
+                    R.ci = P.ci16 + b;
                 } else {
-                    RowRef R{nullptr, nullptr, 0};
-                    if (Op::CSR) {
-                        const int b = V.rp[t];
-                        R.len = V.rp[t + 1] - b;
-                        if (H->direct[slot]) {
-                            R.va = P.va + b;
-                            R.ci = P.ci + b;
-                        } else {
-                            R.va = V.va + (b - H->k0a[slot]);
-                            R.ci = V.ci + (b - H->k0c[slot]);
-                        }
-                    }
-                    op.row(P, i, StagedIn{V.vec + t}, R, acc);
+                    R.va = V.va + (b - H->k0a[slot]);
+                    R.ci = V.ci16 + (b - H->k0c[slot]);
                 }
+                op.row(P, i, StagedIn{V.vec + t}, R, acc);
+            } else if constexpr (SEG == 1) {
+                const int b = V.rp[t];
+                RowSeg R{nullptr, nullptr, V.rp[t + 1] - b};
+                if (H->direct[slot]) {
+                    R.va = P.va + b;
+                    R.ci = P.ci16 + b;
+                } else {
+                    R.va = V.va + (b - H->k0a[slot]);
+                    R.ci = V.ci16 + (b - H->k0c[slot]);
+                }
+                op.row(P, i, SegIn{V.vec + t, V.gx, V.gx + S.nd * kBlock}, R, acc);
+            } else {
+                RowRef R{nullptr, nullptr, 0};
+                if (Op::CSR) {
+                    const int b = V.rp[t];
+                    R.len = V.rp[t + 1] - b;
+                    if (H->direct[slot]) {
+                        R.va = P.va + b;
+                        R.ci = P.ci + b;
+                    } else {
+                        R.va = V.va + (b - H->k0a[slot]);
+                        R.ci = V.ci + (b - H->k0c[slot]);
+                    }
+                }
+                op.row(P, i, StagedIn{V.vec + t}, R, acc);
             }
-            __syncwarp();
-            if ((t & 31) == 0) mbar_arrive(&H->empty[slot]);
         }
+        __syncwarp();
+        if ((t & 31) == 0) mbar_arrive(&H->empty[slot]);
+    };
+    auto close_vb = [&](int vb) {
         if constexpr (Op::ND > 0) {
-            if (op.sync() != 2) continue;
+            if (op.sync() != 2) return;
             cta_tree_c<Op::ND>(acc, H->red);
             if (t == 0) {
 #pragma unroll
                 for (int d = 0; d < Op::ND; ++d) P.part[d * Gv + vb] = acc[d];
             }
+        }
+    };
+    if (dyn) {
+        for (;;) {
+            const int jj = j++;
+            const int slot = jj % NS;
+            mbar_wait(&H->full[slot], (jj / NS) & 1);
+            const int tile = H->slot_tile[slot];
+            if (tile < 0) break;
+            const int vb = H->slot_vb[slot], fl = H->slot_flags[slot];
+            if (fl & 1) {
+#pragma unroll
+                for (int d = 0; d < Op::ND; ++d) acc[d] = 0.0;
+            }
+            consume_tile(slot, tile);
+            if (fl & 2) close_vb(vb);
+        }
+    } else {
+        CGVK_FOR_VB(vb, P.order, blockIdx.x, Gv, Gp) {
+#pragma unroll
+            for (int d = 0; d < Op::ND; ++d) acc[d] = 0.0;
+            CGVK_FOR_TILE(tile, P.order, vb, ntiles, Gv) {
+                const int jj = j++;
+                const int slot = jj % NS;
+                mbar_wait(&H->full[slot], (jj / NS) & 1);
+                if (jj == 0) tl_mark(Op::CSR, 2);
+                consume_tile(slot, tile);
+            }
+            close_vb(vb);
         }
     }
     if (PdlLate<Op>::value) pdl_trigger();
@@ -875,7 +936,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
             cta_tree_c<Op::ND>(tot, H->red);
         }
     }
-    if (t == 0) *counter = 0u;
+    if (t == 0) {
+        *counter = 0u;
+        if (dyn) P.ctrl->sched[counter - P.ctrl->count] = 0u;
+    }
     if (P.dist && mode == 2) {  // rank total: k_finalize folds all ranks in rank order
         if (t == 0) {
 #pragma unroll

@@ -47,6 +47,7 @@ template <bool PREC>
 struct HsK1 {
     static constexpr int NV = PREC ? 3 : 2, ND = 2;
     static constexpr bool CSR = false;
+    static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     static constexpr bool PDL_LATE = true;  // see cgvk_stream.cuh PdlLate
     double alpha;
     __device__ bool enter(const Params& P) {
@@ -92,6 +93,7 @@ template <bool PREC>
 struct HsK2 {
     static constexpr int NV = 3, ND = 1;
     static constexpr bool CSR = true;
+    static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     static constexpr bool PDL_LATE = true;
     int mode;
     const double* pold;
@@ -213,6 +215,7 @@ template <bool PREC>
 struct CgK2 {
     static constexpr int NV = 4, ND = 5;
     static constexpr bool CSR = true;
+    static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     static constexpr int STAGES = 2;  // measured: a shallower ring leaves L1 to the gathers
     bool unsimp;
     __device__ bool enter(const Params& P) {
@@ -352,6 +355,7 @@ template <bool PREC>
 struct PrK2 {
     static constexpr int NV = PREC ? 4 : 2, ND = 6;
     static constexpr bool CSR = true;
+    static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     static constexpr bool PDL_LATE = (CGVK_PR_LATE & 2) != 0;
     double nup;
     bool want_delta, want_dhat;
@@ -433,6 +437,7 @@ template <bool PREC>
 struct GvK1 {
     static constexpr int NV = PREC ? 10 : 7, ND = 5;
     static constexpr bool CSR = false;
+    static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     bool F, S, unsimp;
     double alpha, beta;
     __device__ bool enter(const Params& P) {
@@ -540,6 +545,7 @@ template <bool PREC>
 struct GvK2 {
     static constexpr int NV = 0, ND = 0;
     static constexpr bool CSR = true;
+    static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     static constexpr int STAGES = 2;  // measured: a shallower ring leaves L1 to the gathers
     __device__ bool enter(const Params& P) { return P.ctrl->mode2 != MODE_SKIP; }
     __device__ const double* vec(const Params&, int) const { return nullptr; }
@@ -575,6 +581,7 @@ template <bool PREC>
 struct PprK1 {
     static constexpr int NV = PREC ? 10 : 6, ND = 6;
     static constexpr bool CSR = false;
+    static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     double alpha, beta, nup;
     bool valid, want_delta, want_dhat, recw;
     __device__ bool enter(const Params& P) {
@@ -700,6 +707,7 @@ template <bool PREC>
 struct PprK2 {
     static constexpr int NV = 0, ND = 0;
     static constexpr bool CSR = true;
+    static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     bool recw;
     __device__ bool enter(const Params& P) {
         recw = P.recompute_w != 0;
