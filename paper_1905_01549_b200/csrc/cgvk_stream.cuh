@@ -565,23 +565,44 @@ __device__ __noinline__ void fold_partials(const double* part, int Gv, int t, do
 template <int ND>
 __device__ __forceinline__ void fold_last(const double* part, int Gv, int t, PipeHeader* H, unsigned char* ring,
                                           size_t ring_bytes, double (&tot)[ND]) {
-    const uint32_t bytes = (uint32_t)((ND * Gv * 8 + 15) & ~15);
-    if (bytes > ring_bytes) {
+    // dots [0, nb) by one bulk copy; up to two more from registers, their loads
+    // issued before the bulk wait so both take one L2 latency together
+    constexpr int kRegDots = 2;
+    const size_t per_dot = (size_t)Gv * 8;
+    const int nb = (int)min((size_t)ND, ring_bytes / per_dot);
+    if (ND - nb > kRegDots || Gv > kConsumers * kFoldMax) {
         fold_partials<ND>(part, Gv, t, tot);
         return;
     }
-    if (t == 0) {
+    if (t == 0 && nb > 0) {
         // the partials were written by other CTAs (generic proxy, released by
         // their fences + the arrival atomic); order them before the bulk read
+        const uint32_t bytes = (uint32_t)((nb * per_dot + 15) & ~(size_t)15);
         asm volatile("fence.proxy.async.global;" ::: "memory");
         mbar_expect_tx(&H->fold_bar, bytes);
         bulk_g2s(ring, part, bytes, &H->fold_bar, 0);
     }
-    mbar_wait(&H->fold_bar, 0);
-    const double* sp = reinterpret_cast<const double*>(ring);
-    for (int q = t; q < Gv; q += kConsumers) {
+    double rv[kRegDots][kFoldMax];
 #pragma unroll
-        for (int d = 0; d < ND; ++d) tot[d] = ADD(tot[d], sp[d * Gv + q]);
+    for (int e = 0; e < kRegDots; ++e) {
+        const int d = nb + e;
+#pragma unroll
+        for (int u = 0; u < kFoldMax; ++u) {
+            const int q = t + u * kConsumers;
+            rv[e][u] = (d < ND && q < Gv) ? __ldcg(part + (size_t)d * Gv + q) : 0.0;
+        }
+    }
+    if (nb > 0) mbar_wait(&H->fold_bar, 0);
+    const double* sp = reinterpret_cast<const double*>(ring);
+#pragma unroll
+    for (int u = 0; u < kFoldMax; ++u) {
+        const int q = t + u * kConsumers;
+        if (q >= Gv) break;
+#pragma unroll
+        for (int d = 0; d < ND; ++d) {
+            const double v = d < nb ? sp[d * Gv + q] : rv[(d - nb) < kRegDots ? d - nb : 0][u];
+            tot[d] = ADD(tot[d], v);
+        }
     }
 }
 
