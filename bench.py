@@ -368,7 +368,8 @@ def run_gpu_arm(args, rank, local, world, dist):
         barrier(dist)
         ms, it = s.time_steps(args.steps)
         ms = max_over_ranks(dist, ms)
-        per[v] = {"ms": ms, "iters": it, "launches_per_iter": s.launches_per_iter()}
+        per[v] = {"ms": ms, "iters": it, "launches_per_iter": s.launches_per_iter(),
+                  "launches": s.launches(args.steps)}
         total_ms += ms
         total_iters += it
     if clocks:
@@ -490,9 +491,10 @@ def run_gpu_arm(args, rank, local, world, dist):
     value = reps * total_iters / (total_ms * 1e-3)
     if rank == 0:
         # our kernels in the timed region: one limit-setting launch per step()
-        # call + the captured kernels per iteration (halo pack/unpack and
-        # finalize kernels included when partitioned; NCCL's own not counted)
-        launches = sum(1 + per[v]["launches_per_iter"] * per[v]["iters"] for v in VARIANTS)
+        # call + the captured kernels of every replayed graph (chained graphs'
+        # tail kernel, halo pack/unpack and finalize kernels included; NCCL's
+        # own not counted)
+        launches = sum(per[v]["launches"] for v in VARIANTS)
         cfg = workload_config(args, P, world if partitioned else 1)
         if partitioned:
             cfg["parallelism"] = (f"row-partitioned z-slabs over {world} GPUs (NCCL)" if world > 1 or args.nccl

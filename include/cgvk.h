@@ -211,6 +211,11 @@ int cgvk_solver_history(cgvk_solver s, double* out, int cap, int* len);
 void* cgvk_solver_stream(cgvk_solver s);
 /* Number of kernel launches one iteration makes (graph nodes / iteration). */
 int cgvk_solver_launches_per_iter(cgvk_solver s);
+/* Kernel launches of one cgvk_solver_step(s, n_iters) call on this rank: the
+ * limit-setting kernel, the captured kernels of every replayed graph
+ * (including the closing tail kernel of each chained graph); NCCL's own
+ * kernels not counted. */
+long long cgvk_solver_launches(cgvk_solver s, int n_iters);
 /* Device-timed step(): CUDA events on the solver's stream around the enqueue
  * of n_iters graph-replayed iterations; synchronises. *iters = iterations
  * actually executed (fewer if the solver terminated). */

@@ -183,6 +183,7 @@ def _load() -> C.CDLL:
         "cgvk_solver_history": (I, [P, P, I, C.POINTER(I)]),
         "cgvk_solver_stream": (P, [P]),
         "cgvk_solver_launches_per_iter": (I, [P]),
+        "cgvk_solver_launches": (C.c_longlong, [P, I]),
         "cgvk_solver_time_steps": (I, [P, I, C.POINTER(D), C.POINTER(I)]),
         "cgvk_solver_profile": (I, [P, I, C.POINTER(D), C.POINTER(D), C.POINTER(I)]),
         "cgvk_run": (I, [P, C.POINTER(_Config), I, P, P, I, C.POINTER(_StopRule),
@@ -503,6 +504,10 @@ class Solver:
 
     def launches_per_iter(self) -> int:
         return _lib.cgvk_solver_launches_per_iter(self._h)
+
+    def launches(self, n_iters: int) -> int:
+        """Kernel launches one step(n_iters) call makes on this rank."""
+        return int(_lib.cgvk_solver_launches(self._h, int(n_iters)))
 
     def time_steps(self, n_iters: int) -> tuple[float, int]:
         """Device time (ms) of n_iters graph-replayed iterations, and how many ran."""

@@ -859,6 +859,7 @@ struct cgvk_solver_s {
     bool mirror_fresh = true;
     int k_target = 0;
     KLaunch k1, k2;
+    KLaunch k1c0, k1c, k2c, kt;  // chained schedule (graphs): see chain_prologue
     KLaunch kp;            // persistent cooperative kernel (both phases, all iterations)
     bool persist = false;  // step() uses kp instead of graph replays
     cudaGraphExec_t g1 = nullptr, g8 = nullptr;
@@ -909,10 +910,10 @@ int raise_smem(const void* fn, size_t bytes) {
 // vectors, a window ring of 2H + NS tiles per gathered operand, the per-row
 // contribution buffers; grid = resident CTAs (<= Gv). Knobs (experiments):
 // CGVK_BAND_NSTAGE, CGVK_BAND_PF (L2 prefetch distance in tiles).
-template <class Op>
+template <class Op, class Prev>
 int make_band(cgvk_matrix a, KLaunch* L) {
     using Shape = BandShape<Op>;
-    L->fn = k_band<Op>;
+    L->fn = k_band<Op, Prev>;
     L->threads = Shape::THREADS;
     StageCfg S{};
     S.nvec = Op::NV + Shape::NRAW;
@@ -944,12 +945,12 @@ int make_band(cgvk_matrix a, KLaunch* L) {
 // The SpMV kernels of a band-engine matrix run k_band instead. Tuning knobs
 // (experiments): CGVK_NSTAGE[_SPMV] = ring depth, CGVK_SMEM_CTAS[_SPMV] = CTAs
 // per SM the stage budget targets.
-template <class Op>
+template <class Op, class Prev>
 int make_launch(cgvk_matrix a, KLaunch* L) {
     if constexpr (Op::CSR) {
-        if (a->band_h >= 0) return make_band<Op>(a, L);
+        if (a->band_h >= 0) return make_band<Op, Prev>(a, L);
     }
-    L->fn = k_stream<Op>;
+    L->fn = k_stream<Op, Prev>;
     L->threads = kThreads;
     StageCfg S{};
     S.nvec = Op::NV;
@@ -960,10 +961,10 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
             seg = a->seg_mode;
             S.nd = a->seg_nd;
             if (seg == 1) {  // x tiles staged with the tile
-                L->fn = k_stream<Op, CGVK_SPMV_MIN_CTAS, 1>;
+                L->fn = k_stream<Op, Prev, CGVK_SPMV_MIN_CTAS, 1>;
                 S.ng = Op::NG;
             } else {
-                L->fn = k_stream<Op, CGVK_SPMV_MIN_CTAS, 2>;
+                L->fn = k_stream<Op, Prev, CGVK_SPMV_MIN_CTAS, 2>;
             }
         }
     }
@@ -982,10 +983,10 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
     if (Op::CSR && header + 2 * S.stage_bytes > kSmemPerSM / 2 - 2048) {
         // long rows: a 2-stage ring fills the SM -> one CTA with the full
         // register file (see k_stream's MINB)
-        L->fn = k_stream<Op, 1>;
+        L->fn = k_stream<Op, Prev, 1>;
         if constexpr (Op::CSR) {
-            if (seg == 1) L->fn = k_stream<Op, 1, 1>;
-            if (seg == 2) L->fn = k_stream<Op, 1, 2>;
+            if (seg == 1) L->fn = k_stream<Op, Prev, 1, 1>;
+            if (seg == 2) L->fn = k_stream<Op, Prev, 1, 2>;
         }
         ctas = 1;
     }
@@ -1044,8 +1045,22 @@ int make_persist(cgvk_matrix a, KLaunch* L) {
 
 template <class Op1, class Op2>
 int pick_pair(cgvk_matrix a, cgvk_solver s) {
-    TRY(make_launch<Op1>(a, &s->k1));
-    TRY(make_launch<Op2>(a, &s->k2));
+    TRY((make_launch<Op1, Op2>(a, &s->k1)));
+    TRY((make_launch<Op2, Op1>(a, &s->k2)));
+    // chained schedule (chain_prologue): K1 first in a graph, K1 folding the
+    // previous K2, K2 folding K1, and the graph's closing tail
+    s->k1c0 = s->k1;
+    s->k1c0.S.chain = CH_ON;
+    s->k1c = s->k1;
+    s->k1c.S.chain = CH_ON | CH_FOLD;
+    s->k2c = s->k2;
+    s->k2c.S.chain = CH_ON | CH_FOLD | CH_ODD;
+    s->kt = KLaunch{};
+    s->kt.fn = k_chain_tail<Op2>;
+    s->kt.grid = 1;
+    s->kt.threads = 32;
+    s->kt.smem = 0;
+    s->kt.S = s->k2.S;
     // the experimental persistent kernel only when asked for (CGVK_PERSIST=1)
     // and when its union stage fits; otherwise the graph path
     s->kp = KLaunch{};
@@ -1116,10 +1131,26 @@ void launch_iter(cgvk_solver s) {
     launch(s, s->k2);
 }
 
+// The chained schedule is the default for graphs; CGVK_CHAIN=0 captures the
+// last-CTA schedule instead (A/B). Row-partitioned ranks never chain (their
+// reductions finish in k_finalize after the exchange).
+bool use_chain() {
+    static const int v = env_int("CGVK_CHAIN", 1);
+    return v != 0;
+}
+
 int capture(cgvk_solver s, int iters, cudaGraphExec_t* exec) {
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
-    for (int i = 0; i < iters; ++i) launch_iter(s);
+    if (use_chain()) {
+        for (int i = 0; i < iters; ++i) {
+            launch(s, i ? s->k1c : s->k1c0);
+            launch(s, s->k2c);
+        }
+        launch(s, s->kt);
+    } else {
+        for (int i = 0; i < iters; ++i) launch_iter(s);
+    }
     CK(cudaStreamEndCapture(s->stream, &g));
     CK(cudaGraphInstantiate(exec, g, 0));
     CK(cudaGraphDestroy(g));
@@ -1410,8 +1441,9 @@ int solver_alloc(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, cud
     const int64_t nv = a->ncols + 32;
     if ((rc = dalloc(&s->x, nv)) || (rc = dalloc(&s->r, nv)) || (rc = dalloc(&s->p0, nv)) ||
         (rc = dalloc(&s->s, nv)) || (rc = dalloc(&s->b, nv)) || (rc = dalloc(&s->tmp, nv)) ||
-        (rc = dalloc(&s->part, kMaxDots * (size_t)a->gmax + 4)) || (rc = dalloc(&s->hist, s->hist_cap)) ||
-        (rc = dalloc(&s->dout, 8)) || (rc = dalloc(&s->counter, 4)) || (rc = dalloc(&s->ctrl, 1)))
+        (rc = dalloc(&s->part, kMaxDots * (size_t)a->gmax + 4)) ||
+        (rc = dalloc(&s->hist, s->hist_cap)) ||
+        (rc = dalloc(&s->dout, 8)) || (rc = dalloc(&s->counter, 4)) || (rc = dalloc(&s->ctrl, 2)))
         return bail(rc);
     if (v == CGVK_HS && (rc = dalloc(&s->p1, nv))) return bail(rc);
     if ((v == CGVK_CG_CG || v == CGVK_GV || pipe) && (rc = dalloc(&s->w, nv))) return bail(rc);
@@ -1450,6 +1482,7 @@ int solver_alloc(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, cud
     P.part = s->part;
     P.hist = s->hist;
     P.ctrl = s->ctrl;
+    P.ctrl_b = s->ctrl + 1;
     P.nu_expr = cfg->nu_expression;
     P.recompute_nu = cfg->recompute_nu;
     P.recompute_w = cfg->recompute_w;
@@ -1641,6 +1674,14 @@ void* cgvk_solver_stream(cgvk_solver s) { return s ? (void*)s->stream : nullptr;
 int cgvk_solver_launches_per_iter(cgvk_solver s) {
     if (!s) return 0;
     return s->group ? group_launches_per_iter(s) : 2;
+}
+
+long long cgvk_solver_launches(cgvk_solver s, int n_iters) {
+    if (!s || n_iters <= 0) return 0;
+    if (s->group) return 1 + (long long)group_launches_per_iter(s) * n_iters;
+    if (s->persist) return 2;
+    const long long graphs = n_iters / 8 + n_iters % 8;
+    return 1 + 2LL * n_iters + (use_chain() ? graphs : 0);
 }
 
 int cgvk_solver_time_steps(cgvk_solver s, int n_iters, double* ms, int* iters) {

@@ -82,7 +82,7 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes
 #define CGVK_BAND_CHUNK2 8
 #endif
 
-template <class Op>
+template <class Op, class Prev>
 __global__ void __launch_bounds__(BandShape<Op>::THREADS, BandShape<Op>::MINB) k_band(Params P, StageCfg S) {
     static_assert(Op::CSR && Op::NG <= kBandMaxNG, "band engine runs the SpMV kernels");
     using Shape = BandShape<Op>;
@@ -110,8 +110,10 @@ __global__ void __launch_bounds__(BandShape<Op>::THREADS, BandShape<Op>::MINB) k
     __syncthreads();
     pdl_wait();
     pdl_trigger();
+    const int chain = S.chain;
+    if (chain) chain_prologue<Prev>(P, chain, H, (chain & CH_ODD) ? P.ctrl : P.ctrl_b);
     Op op;
-    if (!op.enter(P)) return;  // uniform over the grid
+    if (!(chain ? op.enter(with_ctrl(P, &H->cs)) : op.enter(P))) return;  // uniform over the grid
 
     // this CTA's contiguous run of tiles (order 1)
     const int vb0 = span_lo(blockIdx.x, Gv, Gp), vb1 = span_lo(blockIdx.x + 1, Gv, Gp);
@@ -259,7 +261,7 @@ __global__ void __launch_bounds__(BandShape<Op>::THREADS, BandShape<Op>::MINB) k
         }
     }
     const int mode = op.sync();
-    if (mode == 0) return;
+    if (mode == 0 || (chain && mode == 1)) return;  // chained: the next kernel finishes
     unsigned int* counter = op.counter(P);
     if constexpr (GR > 1) {  // no dots: arrive, the last CTA finishes
         static_assert(GR == 1 || Op::ND == 0, "consumer groups only without dot products");
@@ -288,6 +290,13 @@ __global__ void __launch_bounds__(BandShape<Op>::THREADS, BandShape<Op>::MINB) k
         }
     }
     if (t == 0) *counter = 0u;
+    if (chain) {  // the totals; the next kernel runs the scalar tail
+        if (t == 0) {
+#pragma unroll
+            for (int d = 0; d < Op::ND; ++d) ((chain & CH_ODD) ? P.ctrl : P.ctrl_b)->tot[d] = tot[d];
+        }
+        return;
+    }
     if (P.dist && mode == 2) {
         if (t == 0) {
 #pragma unroll

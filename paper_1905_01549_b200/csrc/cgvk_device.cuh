@@ -3,7 +3,8 @@
 //  * Ctrl: the device-resident solver control block — SolverState's scalars
 //    (inc/variants.hpp:122-130), status (:62-86), stats (:88-93) and the
 //    fused-schedule bookkeeping. Written only by the single "last CTA" of a
-//    reducing kernel; read by every CTA at kernel entry.
+//    reducing kernel (or, in the chained schedule, by CTA 0 of the next
+//    kernel into the other of two copies); read by every CTA at kernel entry.
 //  * The canonical reduction tree: one row per thread, per-
 //    thread sequential sums over the tiles b, b+G, ..., a shfl_down warp tree,
 //    a cross-warp tree, and a last-arriving-CTA final pass over the G CTA
@@ -53,7 +54,12 @@ struct __align__(16) Ctrl {
     unsigned int bar_count; // persistent kernel: grid barrier arrivals
     unsigned int bar_gen;   // persistent kernel: grid barrier generation
     unsigned int sched[2];  // dynamic virtual-CTA scheduler of the two kernels (next vb - Gp)
+    // chained schedule (cgvk_stream.cuh chain_prologue): the folded totals of
+    // the kernel that wrote this copy, for its successor's scalar tail
+    double tot[kMaxDots];
+    double pad_[2];
 };
+static_assert(sizeof(Ctrl) == 256, "the control block is two 128-byte lines");
 
 struct Params {
     int n, ntiles;
@@ -85,8 +91,11 @@ struct Params {
     int seg_nd;
     int seg_d[8];
     double* part;  // [kMaxDots][G] CTA partials
-    double* hist;  // rr per iteration
+    double* hist;  // rr per iteration (null: not recorded by this CTA)
     Ctrl* ctrl;
+    // chained schedule (cgvk_stream.cuh chain_prologue): the second control
+    // block (K1 writes ctrl_b, K2 writes ctrl)
+    Ctrl* ctrl_b;
     int nu_expr, recompute_nu, recompute_w, unsimplified_mu, track_delta;
     int order;  // canonical tile order (see CGVK_FOR_VB)
     int l2pol;  // TMA L2 policy: 0 evict_first everything, 1 only the matrix, 2 none
@@ -253,7 +262,7 @@ __device__ __forceinline__ void check_tolerance(Ctrl* c) {
 
 __device__ __forceinline__ void record_rr(const Params& P, Ctrl* c, double rr) {
     c->rr = rr;
-    if (c->k < c->hist_cap) P.hist[c->k] = rr;
+    if (P.hist && c->k < c->hist_cap) P.hist[c->k] = rr;
 }
 
 // CSR row product, left-to-right, each term rounded (sparse_matrix.cpp:112-117).

@@ -108,6 +108,7 @@ struct StageCfg {
     int pf;         // band engine: L2 prefetch distance (tiles)
     int nd;         // segment engine: x tiles staged per gathered operand (0: CSR engine)
     int ng;         // segment engine: gathered operands staged
+    int chain;      // chained schedule: CH_* bits (0: last-CTA finish, in place)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -206,6 +207,7 @@ __device__ __forceinline__ void cta_tree_c(double (&v)[ND], double* sm) {
 __device__ __forceinline__ bool arrive_last_c(unsigned int* counter, int* flag) {
     consumer_sync();
     if (threadIdx.x == 0) {
+        // (measured: a release add instead of fence + add changes nothing)
         __threadfence();
         const unsigned int prev = atomicAdd(counter, 1u);
         *flag = prev == gridDim.x - 1;
@@ -636,6 +638,79 @@ __device__ __forceinline__ void finish_last(const Op& op, const Params& P, PipeH
     }
 }
 
+// ------------------------------------------------------ chained schedule
+//
+// The last-CTA schedule ends every reducing kernel with a chain of round
+// trips on its critical path: the fold, then a load of the control block, the
+// scalar tail, the write-back, the kernel's end — and only then may the next
+// kernel read a scalar. In the chained schedule the last CTA stops at the
+// folded totals (Ctrl::tot of the copy its kernel writes); every CTA of the
+// NEXT kernel brings that copy in with one bulk copy right after
+// griddepcontrol.wait and runs the predecessor's finish on it — the same
+// scalar code on the same bits in every CTA. A kernel whose finish needs no
+// dots (sync() == 1) does not arrive at all. The control block is double-
+// buffered: K1 reads `ctrl` and CTA 0 writes the advanced state to `ctrl_b`;
+// K2 reads `ctrl_b` and writes `ctrl` (no kernel reads the copy it writes).
+// A graph of chained iterations ends with k_chain_tail (one CTA), which
+// finishes the last K2 and leaves `ctrl` complete, as the last-CTA schedule
+// does.
+constexpr int CH_ON = 1;    // chained: totals only, the successor finishes
+constexpr int CH_FOLD = 2;  // run the predecessor's finish first
+constexpr int CH_ODD = 4;   // the iteration's second kernel (K2)
+
+__device__ __forceinline__ Params with_ctrl(const Params& P, Ctrl* c) {
+    Params Q = P;
+    Q.ctrl = c;
+    return Q;
+}
+
+// Words of the control block CTA 0 copies forward (the totals are written by
+// the kernel's last CTA).
+constexpr int kCtrlHead = offsetof(Ctrl, tot) / 16;
+
+// All threads of the CTA. Warp 0 loads the control block (with the
+// predecessor's totals) into H->cs — one coalesced 256-byte load, not a bulk
+// copy, which would queue behind the producer's matrix prefetch in the TMA
+// unit; thread 0 runs the predecessor's finish on it; CTA 0 writes the
+// advanced state to `out`.
+template <class Prev>
+__device__ __forceinline__ void chain_prologue(const Params& P, int chain, PipeHeader* H, Ctrl* out) {
+    const int t = threadIdx.x;
+    if (t < 32) {
+        constexpr int kWords = sizeof(Ctrl) / 16;
+        const uint4* in = reinterpret_cast<const uint4*>((chain & CH_ODD) ? P.ctrl_b : P.ctrl);
+        if (t < kWords) reinterpret_cast<uint4*>(&H->cs)[t] = __ldcg(in + t);
+        __syncwarp();
+    }
+    if (t == 0) {
+        if (chain & CH_FOLD) {
+            Params Q = with_ctrl(P, &H->cs);
+            if (blockIdx.x != 0) Q.hist = nullptr;  // side effects once
+            Prev prev;
+            if (prev.enter(Q)) {
+                const int m = prev.sync();
+                if (m == 2) {
+                    prev.finish(Q, &H->cs, H->cs.tot);
+                } else if (m == 1) {
+                    const double none[kMaxDots] = {};
+                    prev.finish(Q, &H->cs, none);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (blockIdx.x == 0 && t < kCtrlHead)
+        reinterpret_cast<uint4*>(out)[t] = reinterpret_cast<const uint4*>(&H->cs)[t];
+}
+
+// The chained graph's last node: the final K2's scalar tail.
+template <class Prev>
+__global__ void __launch_bounds__(32) k_chain_tail(Params P, StageCfg) {
+    __shared__ __align__(128) PipeHeader H;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    chain_prologue<Prev>(P, CH_ON | CH_FOLD, &H, P.ctrl);
+}
+
 // Programmatic dependent launch: wait for the preceding kernel's results /
 // allow the next kernel to start its prologue. CGVK_PDL_LATE=1 signals the
 // dependents only when a CTA has finished its tiles (before the reduction
@@ -726,7 +801,9 @@ __device__ __forceinline__ void tl_mark(int kernel, int slot) {
 // the tile's columns fall in (tile + seg_d[q]); gathers read shared memory.
 // SEG 2: CSR with 16-bit columns decoded against those tiles' bases, x
 // gathered through L1/L2 (2 B/entry less traffic and stage space).
-template <class Op, int MINB = (Op::CSR ? CGVK_SPMV_MIN_CTAS : 1), int SEG = 0>
+// Prev: the other kernel of the iteration (chained schedule: its partials
+// are folded here, see chain_prologue).
+template <class Op, class Prev, int MINB = (Op::CSR ? CGVK_SPMV_MIN_CTAS : 1), int SEG = 0>
 __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PipeHeader* H = reinterpret_cast<PipeHeader*>(smem_raw);
@@ -749,7 +826,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
     // that kernel is still finishing, then waits for it.
     uint64_t pol = 0;
     int npre = 0;
-    const bool dyn = DynOf<Op>::value && P.order == 0;
+    const bool dyn = DynOf<Op>::value && P.order == 0 && !S.chain;
     if (Op::CSR && producer) {
         pol = matrix_policy(P.l2pol);
         CGVK_FOR_VB(vb, P.order, blockIdx.x, Gv, Gp) {
@@ -764,8 +841,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
     pdl_wait();
     tl_mark(Op::CSR, 1);
     if (!PdlLate<Op>::value) pdl_trigger();
+    const int chain = S.chain;
+    if (chain) {
+        chain_prologue<Prev>(P, chain, H, (chain & CH_ODD) ? P.ctrl : P.ctrl_b);
+        tl_mark(Op::CSR, 5);
+    }
     Op op;
-    if (!op.enter(P)) {  // uniform over the grid
+    if (!(chain ? op.enter(with_ctrl(P, &H->cs)) : op.enter(P))) {  // uniform over the grid
         if (producer) {  // drain the prefetch before the CTA exits
             for (int q = 0; q < npre; ++q) {
                 mbar_arrive(&H->full[q]);
@@ -900,13 +982,14 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
         __syncwarp();
         if ((t & 31) == 0) mbar_arrive(&H->empty[slot]);
     };
+    double* const part = P.part;
     auto close_vb = [&](int vb) {
         if constexpr (Op::ND > 0) {
             if (op.sync() != 2) return;
             cta_tree_c<Op::ND>(acc, H->red);
             if (t == 0) {
 #pragma unroll
-                for (int d = 0; d < Op::ND; ++d) P.part[d * Gv + vb] = acc[d];
+                for (int d = 0; d < Op::ND; ++d) part[d * Gv + vb] = acc[d];
             }
         }
     };
@@ -942,7 +1025,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
     if (PdlLate<Op>::value) pdl_trigger();
     tl_mark(Op::CSR, 3);
     const int mode = op.sync();
-    if (mode == 0) return;
+    if (mode == 0 || (chain && mode == 1)) return;  // chained: the next kernel finishes
     unsigned int* counter = op.counter(P);
     const bool is_last = arrive_last_c(counter, &H->last_flag);
     tl_mark(Op::CSR, 4);
@@ -960,6 +1043,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
     if (t == 0) {
         *counter = 0u;
         if (dyn) P.ctrl->sched[counter - P.ctrl->count] = 0u;
+    }
+    if (chain) {  // the totals; the next kernel runs the scalar tail
+        if (t == 0) {
+#pragma unroll
+            for (int d = 0; d < Op::ND; ++d) ((chain & CH_ODD) ? P.ctrl : P.ctrl_b)->tot[d] = tot[d];
+        }
+        return;
     }
     if (P.dist && mode == 2) {  // rank total: k_finalize folds all ranks in rank order
         if (t == 0) {

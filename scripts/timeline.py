@@ -39,4 +39,7 @@ for v in sys.argv[2:] or ["pr", "hs", "gv"]:
               f"wait done {wt.min()/1e3:6.2f}..{wt.max()/1e3:6.2f}  first stage {first.min()/1e3:6.2f}..{first.max()/1e3:6.2f}  "
               f"tiles done {done.min()/1e3:6.2f}..{done.max()/1e3:6.2f}  arrived {arr.max()/1e3:6.2f}  "
               f"fold loads {loads.max()/1e3:6.2f} fold {fold.max()/1e3:6.2f}  finish {fin.max()/1e3:6.2f}")
+        if os.environ.get("CGVK_CHAIN", "1") != "0" and (b[:, 5] > 0).all():
+            pro = b[:, 5] - t0
+            print(f"      chain prologue done {pro.min()/1e3:6.2f}..{pro.max()/1e3:6.2f}")
     s.close()

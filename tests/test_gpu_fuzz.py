@@ -132,3 +132,44 @@ def test_random_partitioned_solves(seed):
     compare(g, o, f"fuzz-part seed {seed} P{nranks} {variant.name}")
     g.close()
     comm.close()
+
+
+@pytest.mark.parametrize("engine", [None, "band"])
+@pytest.mark.parametrize("variant", ALL_VARIANTS)
+def test_chained_graph_steps_match_the_oracle(variant, engine):
+    """step(n) replays graphs of chained iterations (each K1 after the first
+    runs the previous K2's scalar tail, the graph's tail kernel the last
+    one): 8 + 8 + 3 iterations in one call, then the oracle's 19 steps."""
+    from oracle import oracle as O
+    from helpers import compare_states, compare_vectors, gpu_state, gpu_vectors, oracle_vectors, tree_dot
+    P = pb.make_problem("ch", pb.random_spd(20000, 13, 3000, 21))
+    A = cgvk.DeviceMatrix.from_csr(P.A, engine=engine)
+    for precond in (Precond.IDENTITY, Precond.JACOBI):
+        s = cgvk.initialize(cgvk.VariantConfig.make(variant), A, precond, P.b, P.x0)
+        o = O.Restatement(P.A, int(variant), int(precond), P.b, P.x0, dot=tree_dot(A))
+        s.step(19)
+        s.sync()
+        for _ in range(19):
+            if o.state()["state"] != 0:
+                break
+            o.step()
+        compare_states(gpu_state(s), o.state(), f"{variant.name} chained x19")
+        compare_vectors(gpu_vectors(s), oracle_vectors(o), f"{variant.name} chained x19")
+        s.close()
+
+
+def test_last_cta_schedule_still_bit_exact():
+    """CGVK_CHAIN=0 captures the last-CTA schedule (A/B): same bits."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys; sys.path[:0] = ['tests', '.']\n"
+            "from test_gpu_fuzz import test_chained_graph_steps_match_the_oracle as t\n"
+            "from helpers import ALL_VARIANTS\n"
+            "for v in ALL_VARIANTS:\n"
+            "    t(v, None)\n"
+            "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, CGVK_CHAIN="0"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-2000:]
