@@ -862,7 +862,8 @@ struct cgvk_solver_s {
     KLaunch k1c0, k1c, k2c, kt;  // chained schedule (graphs): see chain_prologue
     KLaunch kp;            // persistent cooperative kernel (both phases, all iterations)
     bool persist = false;  // step() uses kp instead of graph replays
-    cudaGraphExec_t g1 = nullptr, g8 = nullptr;
+    cudaGraphExec_t g1 = nullptr, g8 = nullptr;  // 1- and gn-iteration graphs
+    int gn = 8;
     Params P{};
     int allocated = 0;
     // row-partitioned solve (cgvk_group_create): this rank's share
@@ -1137,6 +1138,13 @@ void launch_iter(cgvk_solver s) {
 bool use_chain() {
     static const int v = env_int("CGVK_CHAIN", 1);
     return v != 0;
+}
+
+// Iterations per long graph (step(n) replays n / gn of them, then 1-iteration
+// graphs); CGVK_GRAPH_ITERS overrides.
+int graph_iters() {
+    static const int v = env_int("CGVK_GRAPH_ITERS", 8);
+    return v < 2 ? 2 : v > 256 ? 256 : v;
 }
 
 int capture(cgvk_solver s, int iters, cudaGraphExec_t* exec) {
@@ -1529,7 +1537,8 @@ int cgvk_solver_create(cgvk_matrix a, const cgvk_variant_config* cfg, int precon
     pt.mark("alloc+kernels");
     if ((rc = solver_init(s, b, x0)) != CGVK_OK) return bail(rc);
     pt.mark("initialize");
-    if ((rc = capture(s, 1, &s->g1)) != CGVK_OK || (rc = capture(s, 8, &s->g8)) != CGVK_OK)
+    s->gn = graph_iters();
+    if ((rc = capture(s, 1, &s->g1)) != CGVK_OK || (rc = capture(s, s->gn, &s->g8)) != CGVK_OK)
         return bail(rc);
     pt.mark("graphs");
     s->persist = s->kp.fn != nullptr;  // CGVK_PERSIST=1 and the union stage fit (no band version)
@@ -1575,8 +1584,8 @@ int cgvk_solver_step(cgvk_solver s, int n_iters) {
         cfg.numAttrs = 1;
         CK(cudaLaunchKernelEx(&cfg, s->kp.fn, s->P, s->kp.S));
     } else {
-        for (int i = 0; i < n_iters / 8; ++i) CK(cudaGraphLaunch(s->g8, s->stream));
-        for (int i = 0; i < n_iters % 8; ++i) CK(cudaGraphLaunch(s->g1, s->stream));
+        for (int i = 0; i < n_iters / s->gn; ++i) CK(cudaGraphLaunch(s->g8, s->stream));
+        for (int i = 0; i < n_iters % s->gn; ++i) CK(cudaGraphLaunch(s->g1, s->stream));
     }
     CK(cudaGetLastError());
     s->mirror_fresh = false;
@@ -1680,7 +1689,7 @@ long long cgvk_solver_launches(cgvk_solver s, int n_iters) {
     if (!s || n_iters <= 0) return 0;
     if (s->group) return 1 + (long long)group_launches_per_iter(s) * n_iters;
     if (s->persist) return 2;
-    const long long graphs = n_iters / 8 + n_iters % 8;
+    const long long graphs = n_iters / s->gn + n_iters % s->gn;
     return 1 + 2LL * n_iters + (use_chain() ? graphs : 0);
 }
 

@@ -1049,6 +1049,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
 #pragma unroll
             for (int d = 0; d < Op::ND; ++d) ((chain & CH_ODD) ? P.ctrl : P.ctrl_b)->tot[d] = tot[d];
         }
+        tl_mark(Op::CSR, 6);
         return;
     }
     if (P.dist && mode == 2) {  // rank total: k_finalize folds all ranks in rank order
