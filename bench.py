@@ -429,7 +429,8 @@ def run_gpu_arm(args, rank, local, world, dist):
     e2e = None
     if not args.no_e2e:
         arrs = [P.A.row_ptr.copy(), P.A.col_idx.copy(), P.A.values.copy(), P.b.copy(), P.x0.copy()]
-        for arr in arrs:
+        xs = {v: np.empty(n) for v in VARIANTS}  # the user's result buffers (registered, like the inputs)
+        for arr in arrs + list(xs.values()):
             cgvk.host_register(arr)
         def sweep():
             # the user's calls: upload A (+ b, x0 per variant), solve K steps,
@@ -447,7 +448,7 @@ def run_gpu_arm(args, rank, local, world, dist):
             for v, s in E.solvers.items():
                 s.step(args.steps)
                 s.sync()
-                xx = s.x  # result read back each solve
+                xx = s.vector(cgvk.Vec.X, out=xs[v]) if hasattr(s, "_h") else s.x  # result read back each solve
                 its += s.k
             ph["solve_ms"] = 1e3 * (time.perf_counter() - t)
             return its, xx, ph, E
@@ -463,7 +464,7 @@ def run_gpu_arm(args, rank, local, world, dist):
             barrier(dist)
             wall = max_over_ranks(dist, t1 - t0)
         finally:
-            for arr in arrs:
+            for arr in arrs + list(xs.values()):
                 cgvk.host_unregister(arr)
         h2d = sum(a.nbytes for a in arrs[:3]) + len(VARIANTS) * (arrs[3].nbytes + arrs[4].nbytes)
         d2h = len(VARIANTS) * x.nbytes

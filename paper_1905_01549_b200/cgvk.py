@@ -475,8 +475,14 @@ class Solver:
         return {f: getattr(s, f) for f in ("spmv_calls", "block_spmv_calls", "precond_applies",
                                            "reductions")}
 
-    def vector(self, which: Vec) -> np.ndarray:
-        out = np.empty(self.n)
+    def vector(self, which: Vec, out: np.ndarray | None = None) -> np.ndarray:
+        """Download a state vector (SolverState field) into `out` (a float64
+        array of n, e.g. one registered with host_register for a direct DMA)
+        or a new array."""
+        if out is None:
+            out = np.empty(self.n)
+        elif out.dtype != np.float64 or out.shape != (self.n,) or not out.flags.c_contiguous:
+            raise InvalidArgument("out must be a contiguous float64 array of n")
         _check(_lib.cgvk_solver_get_vector(self._h, int(which), _ptr(out) if self.n else None))
         return out
 

@@ -88,6 +88,27 @@ struct SmemCtasOf<T, std::void_t<decltype(T::SMEM_CTAS)>> {
     static constexpr int value = T::SMEM_CTAS;
 };
 
+// Optional Op member `static const double* early_vec(const Params&, int v)`:
+// the staged vectors as a function of P alone — the steady-state vec() or a
+// superset of it (extra streams are loaded and ignored). The producer then
+// issues the first NS stages' vectors right after griddepcontrol.wait,
+// overlapping the chained scalar prologue and enter() instead of following
+// them (cgvk_stream.cuh k_stream).
+#ifndef CGVK_EARLY
+#define CGVK_EARLY 2         // stages whose vectors are issued right after the wait
+#endif
+#ifndef CGVK_EARLY_ORDER
+#define CGVK_EARLY_ORDER 0   // 1: only after warp 0's control-block load (chained)
+#endif
+template <class T, class = void>
+struct HasEarlyVec {
+    static constexpr bool value = false;
+};
+template <class T>
+struct HasEarlyVec<T, std::void_t<decltype(T::early_vec(std::declval<const Params&>(), 0))>> {
+    static constexpr bool value = true;
+};
+
 // Optional per-Op ring-depth hint: `static constexpr int STAGES`.
 template <class T, class = void>
 struct StagesOf {
@@ -673,14 +694,19 @@ constexpr int kCtrlHead = offsetof(Ctrl, tot) / 16;
 // copy, which would queue behind the producer's matrix prefetch in the TMA
 // unit; thread 0 runs the predecessor's finish on it; CTA 0 writes the
 // advanced state to `out`.
+// signal: warp 0 releases named barrier 2 (its 32 threads + the producer
+// warp's 32) once the control block has arrived, so a producer that issues
+// stage copies right after the dependency wait queues them behind that load.
 template <class Prev>
-__device__ __forceinline__ void chain_prologue(const Params& P, int chain, PipeHeader* H, Ctrl* out) {
+__device__ __forceinline__ void chain_prologue(const Params& P, int chain, PipeHeader* H, Ctrl* out,
+                                               bool signal = false) {
     const int t = threadIdx.x;
     if (t < 32) {
         constexpr int kWords = sizeof(Ctrl) / 16;
         const uint4* in = reinterpret_cast<const uint4*>((chain & CH_ODD) ? P.ctrl_b : P.ctrl);
         if (t < kWords) reinterpret_cast<uint4*>(&H->cs)[t] = __ldcg(in + t);
         __syncwarp();
+        if (signal) asm volatile("bar.arrive 2, 64;" ::: "memory");
     }
     if (t == 0) {
         if (chain & CH_FOLD) {
@@ -827,30 +853,60 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
     uint64_t pol = 0;
     int npre = 0;
     const bool dyn = DynOf<Op>::value && P.order == 0 && !S.chain;
-    if (Op::CSR && producer) {
-        pol = matrix_policy(P.l2pol);
+    constexpr bool kEarly = HasEarlyVec<Op>::value && SEG == 0 && CGVK_EARLY > 0;
+    int early_tile[kMaxStages];
+    int nearly = 0;  // stages whose vectors are issued right after the wait
+    if (producer && (Op::CSR || (kEarly && !dyn))) {
+        if (Op::CSR) pol = matrix_policy(P.l2pol);
+        int q = 0;
         CGVK_FOR_VB(vb, P.order, blockIdx.x, Gv, Gp) {
             CGVK_FOR_TILE(tile, P.order, vb, ntiles, Gv) {
-                if (npre == NS) break;
-                stage_csr(P, S, H, stages, npre++, tile, pol, /*arrive=*/false);
+                if (q == NS) break;
+                if (Op::CSR) stage_csr(P, S, H, stages, q, tile, pol, /*arrive=*/false);
+                early_tile[q++] = tile;
             }
-            if (npre == NS || dyn) break;  // dynamic: only the static first virtual CTA
+            if (q == NS || dyn) break;  // dynamic: only the static first virtual CTA
         }
+        if (Op::CSR) npre = q;
+        if (kEarly && !dyn) nearly = min(q, CGVK_EARLY);
     }
     tl_mark(Op::CSR, 0);
     pdl_wait();
     tl_mark(Op::CSR, 1);
+    if constexpr (kEarly) {
+        // chained: after warp 0's control-block load (measured: issued
+        // before it, the burst of stage copies delays that load by 1-3 us)
+        if (CGVK_EARLY_ORDER && S.chain && warp == kWarps) asm volatile("bar.sync 2, 64;" ::: "memory");
+        if (producer) {
+            const uint64_t vpol = P.l2pol == 0 ? (Op::CSR ? pol : evict_first_policy()) : 0;
+            for (int q = 0; q < nearly; ++q) {
+                StageView V = stage_view(stages, S, q);
+                const int r0 = early_tile[q] * kBlock;
+                const uint32_t vec_bytes = (min(kBlock, P.n - r0) * 8 + 15) & ~15;
+                uint32_t bytes = 0;
+#pragma unroll
+                for (int v = 0; v < Op::NV; ++v)
+                    if (Op::early_vec(P, v)) bytes += vec_bytes;
+                mbar_expect_tx(&H->full[q], bytes);  // + the stage's arrival
+#pragma unroll
+                for (int v = 0; v < Op::NV; ++v) {
+                    const double* src = Op::early_vec(P, v);
+                    if (src) bulk_g2s(V.vec + v * kBlock, src + r0, vec_bytes, &H->full[q], vpol);
+                }
+            }
+        }
+    }
     if (!PdlLate<Op>::value) pdl_trigger();
     const int chain = S.chain;
     if (chain) {
-        chain_prologue<Prev>(P, chain, H, (chain & CH_ODD) ? P.ctrl : P.ctrl_b);
+        chain_prologue<Prev>(P, chain, H, (chain & CH_ODD) ? P.ctrl : P.ctrl_b, kEarly && CGVK_EARLY_ORDER);
         tl_mark(Op::CSR, 5);
     }
     Op op;
     if (!(chain ? op.enter(with_ctrl(P, &H->cs)) : op.enter(P))) {  // uniform over the grid
         if (producer) {  // drain the prefetch before the CTA exits
-            for (int q = 0; q < npre; ++q) {
-                mbar_arrive(&H->full[q]);
+            for (int q = 0; q < max(npre, nearly); ++q) {
+                if (q >= nearly) mbar_arrive(&H->full[q]);
                 mbar_wait(&H->full[q], 0);
             }
         }
@@ -872,6 +928,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
         const uint64_t vpol = P.l2pol == 0 ? pol : 0;
         auto produce_vb = [&](int vb) {
             CGVK_FOR_TILE(tile, P.order, vb, ntiles, Gv) {
+                if (j < nearly) {  // issued right after the wait
+                    ++j;
+                    continue;
+                }
                 const int slot = j % NS;
                 if (j >= NS) mbar_wait(&H->empty[slot], ((j / NS) - 1) & 1);
                 if (dyn) {
