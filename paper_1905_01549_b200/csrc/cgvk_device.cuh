@@ -23,6 +23,7 @@ constexpr int kBlock = 256;       // rows per tile == threads per CTA
 constexpr int kWarps = kBlock / 32;
 constexpr int kMinBlocksPerSM = 4;  // generic kernels: __launch_bounds__ minimum
 constexpr int kVirtualPerSM = 12;   // canonical G cap = SMs * 12 (divisible by 2, 3, 4, 6 CTAs/SM)
+constexpr int kVirtualPerSMCsr = 3;  // CSR engine: one virtual CTA per physical CTA (3 CTAs/SM)
 constexpr int kMaxDots = 6;
 
 // SolverState scalar slots

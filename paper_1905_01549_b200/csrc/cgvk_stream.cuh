@@ -829,7 +829,10 @@ __device__ __forceinline__ void tl_mark(int kernel, int slot) {
 // gathered through L1/L2 (2 B/entry less traffic and stage space).
 // Prev: the other kernel of the iteration (chained schedule: its partials
 // are folded here, see chain_prologue).
-template <class Op, class Prev, int MINB = (Op::CSR ? CGVK_SPMV_MIN_CTAS : 1), int SEG = 0>
+#ifndef CGVK_K1_MIN_CTAS
+#define CGVK_K1_MIN_CTAS 1  // register budget of the update kernels (resident CTAs)
+#endif
+template <class Op, class Prev, int MINB = (Op::CSR ? CGVK_SPMV_MIN_CTAS : CGVK_K1_MIN_CTAS), int SEG = 0>
 __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PipeHeader* H = reinterpret_cast<PipeHeader*>(smem_raw);
