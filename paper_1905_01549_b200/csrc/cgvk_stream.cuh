@@ -829,6 +829,33 @@ __device__ __forceinline__ void tl_mark(int kernel, int slot) {
 // gathered through L1/L2 (2 B/entry less traffic and stage space).
 // Prev: the other kernel of the iteration (chained schedule: its partials
 // are folded here, see chain_prologue).
+// Two virtual CTAs per physical CTA (order 0; the register-bound update
+// kernels of GV / pipe-PR run 2 CTAs/SM against G = 3 x SMs): their tiles are
+// interleaved — step s takes vCTA s & 1's tile s >> 1 — so the grid still
+// sweeps the tiles in one monotonic pass (tile p + Gp s). Each virtual CTA
+// keeps its own accumulators, so its tiles are still summed in order: the
+// bits are those of the sequential schedule. Returns the tile, -1 (vCTA 1
+// has no tile at this step) or -2 (done).
+// Opt-in per Op (`static constexpr bool RR2 = true`): measured P128 pipe-PR
+// 87.1 -> 84.6 us, V256 657 -> 646 us; GV's K1 loses 1.3 us (off there).
+#ifndef CGVK_RR2
+#define CGVK_RR2 1
+#endif
+template <class T, class = void>
+struct Rr2Of {
+    static constexpr bool value = false;
+};
+template <class T>
+struct Rr2Of<T, std::void_t<decltype(T::RR2)>> {
+    static constexpr bool value = T::RR2 && CGVK_RR2 != 0;
+};
+__device__ __forceinline__ int rr2_tile(int p, int Gp, int Gv, int ntiles, int s) {
+    const int jt = s >> 1;
+    if (p + jt * Gv >= ntiles) return -2;
+    const int tile = p + (s & 1) * Gp + jt * Gv;
+    return tile < ntiles ? tile : -1;
+}
+
 #ifndef CGVK_K1_MIN_CTAS
 #define CGVK_K1_MIN_CTAS 1  // register budget of the update kernels (resident CTAs)
 #endif
@@ -856,19 +883,29 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
     uint64_t pol = 0;
     int npre = 0;
     const bool dyn = DynOf<Op>::value && P.order == 0 && !S.chain;
+    const bool rr2 = Rr2Of<Op>::value && !Op::CSR && !dyn && P.order == 0 && (int)blockIdx.x + Gp < Gv &&
+                     (int)blockIdx.x + 2 * Gp >= Gv;
     constexpr bool kEarly = HasEarlyVec<Op>::value && SEG == 0 && CGVK_EARLY > 0;
     int early_tile[kMaxStages];
     int nearly = 0;  // stages whose vectors are issued right after the wait
     if (producer && (Op::CSR || (kEarly && !dyn))) {
         if (Op::CSR) pol = matrix_policy(P.l2pol);
         int q = 0;
-        CGVK_FOR_VB(vb, P.order, blockIdx.x, Gv, Gp) {
-            CGVK_FOR_TILE(tile, P.order, vb, ntiles, Gv) {
-                if (q == NS) break;
-                if (Op::CSR) stage_csr(P, S, H, stages, q, tile, pol, /*arrive=*/false);
-                early_tile[q++] = tile;
+        if (rr2) {
+            for (int st = 0; q < NS; ++st) {
+                const int tile = rr2_tile(blockIdx.x, Gp, Gv, ntiles, st);
+                if (tile == -2) break;
+                if (tile >= 0) early_tile[q++] = tile;
             }
-            if (q == NS || dyn) break;  // dynamic: only the static first virtual CTA
+        } else {
+            CGVK_FOR_VB(vb, P.order, blockIdx.x, Gv, Gp) {
+                CGVK_FOR_TILE(tile, P.order, vb, ntiles, Gv) {
+                    if (q == NS) break;
+                    if (Op::CSR) stage_csr(P, S, H, stages, q, tile, pol, /*arrive=*/false);
+                    early_tile[q++] = tile;
+                }
+                if (q == NS || dyn) break;  // dynamic: only the static first virtual CTA
+            }
         }
         if (Op::CSR) npre = q;
         if (kEarly && !dyn) nearly = min(q, CGVK_EARLY);
@@ -929,11 +966,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
         }
         int j = 0;
         const uint64_t vpol = P.l2pol == 0 ? pol : 0;
-        auto produce_vb = [&](int vb) {
-            CGVK_FOR_TILE(tile, P.order, vb, ntiles, Gv) {
+        auto produce_tile = [&](int tile, int vb) {
+            {
                 if (j < nearly) {  // issued right after the wait
                     ++j;
-                    continue;
+                    return;
                 }
                 const int slot = j % NS;
                 if (j >= NS) mbar_wait(&H->empty[slot], ((j / NS) - 1) & 1);
@@ -983,7 +1020,16 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
                 ++j;
             }
         };
-        if (dyn) {
+        auto produce_vb = [&](int vb) {
+            CGVK_FOR_TILE(tile, P.order, vb, ntiles, Gv) produce_tile(tile, vb);
+        };
+        if (rr2) {
+            for (int st = 0;; ++st) {
+                const int tile = rr2_tile(blockIdx.x, Gp, Gv, ntiles, st);
+                if (tile == -2) break;
+                if (tile >= 0) produce_tile(tile, blockIdx.x + (st & 1) * Gp);
+            }
+        } else if (dyn) {
             unsigned int* sched = P.ctrl->sched + (op.counter(P) - P.ctrl->count);
             for (int vb = blockIdx.x; vb < Gv; vb = Gp + (int)atomicAdd(sched, 1u)) produce_vb(vb);
             const int slot = j % NS;  // sentinel stage: no more work
@@ -1071,6 +1117,36 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
             consume_tile(slot, tile);
             if (fl & 2) close_vb(vb);
         }
+    } else if (rr2) {
+        // per-tile contributions (one term per dot per row) added into the
+        // owning virtual CTA's accumulators in its tile order
+        double acc0[Op::ND > 0 ? Op::ND : 1], acc1[Op::ND > 0 ? Op::ND : 1];
+#pragma unroll
+        for (int d = 0; d < Op::ND; ++d) acc0[d] = acc1[d] = 0.0;
+        for (int st = 0;; ++st) {
+            const int tile = rr2_tile(blockIdx.x, Gp, Gv, ntiles, st);
+            if (tile == -2) break;
+            if (tile < 0) continue;
+            const int jj = j++;
+            const int slot = jj % NS;
+            mbar_wait(&H->full[slot], (jj / NS) & 1);
+#pragma unroll
+            for (int d = 0; d < Op::ND; ++d) acc[d] = 0.0;
+            consume_tile(slot, tile);
+            if (st & 1) {
+#pragma unroll
+                for (int d = 0; d < Op::ND; ++d) acc1[d] = ADD(acc1[d], acc[d]);
+            } else {
+#pragma unroll
+                for (int d = 0; d < Op::ND; ++d) acc0[d] = ADD(acc0[d], acc[d]);
+            }
+        }
+#pragma unroll
+        for (int d = 0; d < Op::ND; ++d) acc[d] = acc0[d];
+        close_vb(blockIdx.x);
+#pragma unroll
+        for (int d = 0; d < Op::ND; ++d) acc[d] = acc1[d];
+        close_vb(blockIdx.x + Gp);
     } else {
         CGVK_FOR_VB(vb, P.order, blockIdx.x, Gv, Gp) {
 #pragma unroll

@@ -594,6 +594,7 @@ struct GvK2 {
 template <bool PREC>
 struct PprK1 {
     static constexpr int NV = PREC ? 10 : 6, ND = 6;
+    static constexpr bool RR2 = true;  // two virtual CTAs per CTA interleaved (cgvk_stream.cuh rr2_tile)
     static constexpr bool CSR = false;
     static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     double alpha, beta, nup;
