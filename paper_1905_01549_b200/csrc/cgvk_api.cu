@@ -623,9 +623,9 @@ int matrix_create(int64_t n, int64_t ncols, const int64_t* row_ptr, const int64_
     // the grid sweeps the tiles in one monotonic pass (tile p + Gp j) and a
     // stencil's +-N^2 neighbours are still in L2 when gathered; measured
     // against 12 x SMs: V256 +7 %, P64 +14 %, P128 +0.4 %. The
-    // band engine keeps 12 x SMs (its SpMV kernels run 2 CTAs/SM over
-    // contiguous tile runs). CGVK_VPERSM overrides (A/B runs).
-    a->gmax = sms * std::max(1, env_int("CGVK_VPERSM", a->band_h >= 0 ? kVirtualPerSM : kVirtualPerSMCsr));
+    // band engine uses 6 x SMs (its SpMV kernels run 2 CTAs/SM over
+    // contiguous tile runs; R4M +0.8 % vs 12 x SMs). CGVK_VPERSM overrides.
+    a->gmax = sms * std::max(1, env_int("CGVK_VPERSM", a->band_h >= 0 ? kVirtualPerSMBand : kVirtualPerSMCsr));
     if (a->gmax > sms * kVirtualPerSM) return bail(set_err(CGVK_EINVAL, "CGVK_VPERSM above %d", kVirtualPerSM));
     a->G = a->ntiles < a->gmax ? a->ntiles : a->gmax;
     if (a->G < 1) a->G = 1;

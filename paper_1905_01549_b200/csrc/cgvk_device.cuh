@@ -24,6 +24,7 @@ constexpr int kWarps = kBlock / 32;
 constexpr int kMinBlocksPerSM = 4;  // generic kernels: __launch_bounds__ minimum
 constexpr int kVirtualPerSM = 12;   // canonical G cap = SMs * 12 (divisible by 2, 3, 4, 6 CTAs/SM)
 constexpr int kVirtualPerSMCsr = 3;  // CSR engine: one virtual CTA per physical CTA (3 CTAs/SM)
+constexpr int kVirtualPerSMBand = 6; // band engine (SpMV kernels 2 CTAs/SM, update kernels 3)
 constexpr int kMaxDots = 6;
 
 // SolverState scalar slots

@@ -77,7 +77,7 @@ def test_band_ablations_bit_exact(cfg, bandmats):
 
 
 def test_band_many_tiles_per_virtual_cta():
-    """n = 600k: 2344 tiles > the 1776 virtual CTAs, so CTAs walk multi-tile
+    """n = 600k: 2344 tiles > the 888 virtual CTAs (6 x 148), so CTAs walk multi-tile
     runs and the window ring wraps many times."""
     P = pb.make_problem("rs_big", pb.random_spd(600_000, 13, 4096, 11))
     A = cgvk.DeviceMatrix.from_csr(P.A)
