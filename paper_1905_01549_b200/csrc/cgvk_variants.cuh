@@ -27,6 +27,13 @@
 
 namespace cgvk {
 
+#ifndef CGVK_GV_K1_CTAS
+#define CGVK_GV_K1_CTAS 3  // stage ring sized for this many resident CTAs (registers allow 2)
+#endif
+#ifndef CGVK_PPR_K1_CTAS
+#define CGVK_PPR_K1_CTAS 3
+#endif
+
 template <bool PREC>
 __device__ __forceinline__ double Mg(const Params& P, int j, double v) {  // gathered d_j * v
     if constexpr (PREC) return MUL(__ldg(P.d + j), v);
@@ -448,6 +455,7 @@ struct PrK2 {
 template <bool PREC>
 struct GvK1 {
     static constexpr int NV = PREC ? 10 : 7, ND = 5;
+    static constexpr int SMEM_CTAS = CGVK_GV_K1_CTAS;
     static constexpr bool CSR = false;
     static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     bool F, S, unsimp;
@@ -594,6 +602,7 @@ struct GvK2 {
 template <bool PREC>
 struct PprK1 {
     static constexpr int NV = PREC ? 10 : 6, ND = 6;
+    static constexpr int SMEM_CTAS = CGVK_PPR_K1_CTAS;
     static constexpr bool RR2 = true;  // two virtual CTAs per CTA interleaved (cgvk_stream.cuh rr2_tile)
     static constexpr bool CSR = false;
     static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
