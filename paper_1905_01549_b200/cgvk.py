@@ -482,7 +482,7 @@ class Solver:
         if out is None:
             out = np.empty(self.n)
         elif out.dtype != np.float64 or out.shape != (self.n,) or not out.flags.c_contiguous:
-            raise InvalidArgument("out must be a contiguous float64 array of n")
+            raise InvalidArgument(-1, "out must be a contiguous float64 array of n")
         _check(_lib.cgvk_solver_get_vector(self._h, int(which), _ptr(out) if self.n else None))
         return out
 

@@ -121,3 +121,56 @@ def test_residual_history_vs_reference(variant, case, history_mats):
     np.testing.assert_allclose(upd, upd_ref, rtol=rtol, atol=0)
     np.testing.assert_allclose(true, true_ref, rtol=rtol, atol=0)
     np.testing.assert_allclose(s.history(), upd_ref, rtol=rtol, atol=0)
+
+
+# Medium size: 50^3 = 125,000 rows = 489 tiles > the CSR engine's 444 canonical
+# virtual CTAs (3 x 148), so CTAs walk multi-tile virtual CTAs, the
+# register-bound update kernels (GV / pipe-PR K1, 2 CTAs/SM) run two virtual
+# CTAs each, and pipe-PR's K1 interleaves them tile by tile (rr2_tile) with a
+# skipped step where the second virtual CTA has no tile — all bit-exact
+# against the restatement in the device's reduction order, single steps and
+# the 8-iteration graph.
+@pytest.fixture(scope="module")
+def medium():
+    P = pb.make_problem("p50", pb.poisson3d(50))
+    return P, cgvk.DeviceMatrix.from_csr(P.A)
+
+
+@pytest.mark.parametrize("variant", ALL_VARIANTS)
+def test_medium_trajectory_bit_exact(variant, medium):
+    P, A = medium
+    lockstep(P.A, A, variant, Precond.JACOBI, P.b, P.x0, steps=6, check_vectors_every=3)
+
+
+@pytest.mark.parametrize("variant", [Variant.HS, Variant.GV, Variant.PIPE_PR])
+def test_medium_graph_steps_bit_exact(variant, medium):
+    P, A = medium
+    s = cgvk.initialize(cgvk.VariantConfig.make(variant), A, Precond.JACOBI, P.b, P.x0)
+    o = O.Restatement(P.A, int(variant), 1, P.b, P.x0, dot=tree_dot(A))
+    s.step(16)
+    s.sync()
+    for _ in range(16):
+        o.step()
+    assert s.k == o.state()["k"] == 16
+    for w in (cgvk.Vec.X, cgvk.Vec.R, cgvk.Vec.P, cgvk.Vec.S):
+        assert same_bits(s.vector(w), o.vector(int(w))), w.name
+    s.close()
+
+
+def test_vector_into_caller_buffer(medium):
+    """Solver.vector(out=...) downloads into the caller's (registered) array."""
+    P, A = medium
+    s = cgvk.initialize(cgvk.VariantConfig.make(Variant.PR), A, Precond.JACOBI, P.b, P.x0)
+    s.step(3)
+    buf = np.empty(A.n)
+    cgvk.host_register(buf)
+    try:
+        got = s.vector(cgvk.Vec.X, out=buf)
+        assert got is buf and same_bits(buf, s.vector(cgvk.Vec.X))
+    finally:
+        cgvk.host_unregister(buf)
+    with pytest.raises(cgvk.InvalidArgument):
+        s.vector(cgvk.Vec.X, out=np.empty(A.n - 1))
+    with pytest.raises(cgvk.InvalidArgument):
+        s.vector(cgvk.Vec.X, out=np.empty(A.n, dtype=np.float32))
+    s.close()
