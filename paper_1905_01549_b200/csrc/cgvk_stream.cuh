@@ -856,6 +856,23 @@ __device__ __forceinline__ int rr2_tile(int p, int Gp, int Gv, int ntiles, int s
     return tile < ntiles ? tile : -1;
 }
 
+// Reversed sweep (Op trait `REVERSE = true`, kernels without dot products,
+// so the tile order changes no bit): the CTA walks its tiles p + Gp s from
+// the highest s down. The other kernel of the iteration sweeps upwards, so
+// each kernel starts on the tiles its predecessor wrote last — still in L2.
+#ifndef CGVK_REVERSE
+#define CGVK_REVERSE 1
+#endif
+template <class T, class = void>
+struct RevOf {
+    static constexpr bool value = false;
+};
+template <class T>
+struct RevOf<T, std::void_t<decltype(T::REVERSE)>> {
+    static_assert(!T::REVERSE || T::ND == 0, "a reversed sweep would reorder the dot products");
+    static constexpr bool value = T::REVERSE && CGVK_REVERSE != 0;
+};
+
 #ifndef CGVK_K1_MIN_CTAS
 #define CGVK_K1_MIN_CTAS 1  // register budget of the update kernels (resident CTAs)
 #endif
@@ -883,6 +900,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
     uint64_t pol = 0;
     int npre = 0;
     const bool dyn = DynOf<Op>::value && P.order == 0 && !S.chain;
+    // reversed sweep: the CTA's tiles are exactly p + Gp s when Gp divides Gv
+    // (or every virtual CTA is one tile)
+    const bool rev = RevOf<Op>::value && !dyn && P.order == 0 && (Gv % Gp == 0 || Gv == ntiles);
+    const int nrev = rev ? ((int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / Gp + 1 : 0) : 0;
     const bool rr2 = Rr2Of<Op>::value && !Op::CSR && !dyn && P.order == 0 && (int)blockIdx.x + Gp < Gv &&
                      (int)blockIdx.x + 2 * Gp >= Gv;
     constexpr bool kEarly = HasEarlyVec<Op>::value && SEG == 0 && CGVK_EARLY > 0;
@@ -891,7 +912,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
     if (producer && (Op::CSR || (kEarly && !dyn))) {
         if (Op::CSR) pol = matrix_policy(P.l2pol);
         int q = 0;
-        if (rr2) {
+        if (rev) {
+            for (int st = 0; st < nrev && q < NS; ++st) {
+                const int tile = (int)blockIdx.x + Gp * (nrev - 1 - st);
+                if (Op::CSR) stage_csr(P, S, H, stages, q, tile, pol, /*arrive=*/false);
+                early_tile[q++] = tile;
+            }
+        } else if (rr2) {
             for (int st = 0; q < NS; ++st) {
                 const int tile = rr2_tile(blockIdx.x, Gp, Gv, ntiles, st);
                 if (tile == -2) break;
@@ -1023,7 +1050,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
         auto produce_vb = [&](int vb) {
             CGVK_FOR_TILE(tile, P.order, vb, ntiles, Gv) produce_tile(tile, vb);
         };
-        if (rr2) {
+        if (rev) {
+            for (int st = 0; st < nrev; ++st) produce_tile((int)blockIdx.x + Gp * (nrev - 1 - st), -1);
+        } else if (rr2) {
             for (int st = 0;; ++st) {
                 const int tile = rr2_tile(blockIdx.x, Gp, Gv, ntiles, st);
                 if (tile == -2) break;
@@ -1116,6 +1145,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S)
             }
             consume_tile(slot, tile);
             if (fl & 2) close_vb(vb);
+        }
+    } else if (rev) {  // no dot products: nothing to accumulate
+        for (int st = 0; st < nrev; ++st) {
+            const int jj = j++;
+            const int slot = jj % NS;
+            mbar_wait(&H->full[slot], (jj / NS) & 1);
+            consume_tile(slot, (int)blockIdx.x + Gp * (nrev - 1 - st));
         }
     } else if (rr2) {
         // per-tile contributions (one term per dot per row) added into the

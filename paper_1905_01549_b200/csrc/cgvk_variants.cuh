@@ -176,6 +176,9 @@ struct HsK2 {
 template <bool PREC>
 struct CgK1 {
     static constexpr int NV = PREC ? 6 : 5, ND = 0;
+    // no dots: sweeps downwards (cgvk_stream.cuh RevOf); measured CG V256 581 -> 574 us
+    // (GV / pipe-PR's K2 reversed: V256 +6 / +27 us, left forward)
+    static constexpr bool REVERSE = true;
     static constexpr bool CSR = false;
     bool F, S;
     double alpha, beta;
