@@ -18,3 +18,16 @@ print(cfg, mode, " ".join(f"{v}:{x['us_per_iter']:.1f}" for v, x in d["per_varia
 PY
   done
 done
+# the partitioned data path with P in-process ranks on one GPU (halo copies,
+# rank-ordered finalize; no NCCL): per-iteration cost of partitioning
+for cfg in p64 p128; do
+  for P in 2 4 8; do
+    python bench.py --config $cfg --emulate-ranks $P --steps 100 --warmup 5 --no-cpu --no-e2e --no-clocks > gpurun_out/ov_${cfg}_emu$P.json 2>/dev/null
+    python - "$cfg" "$P" <<'PY'
+import json, sys
+cfg, P = sys.argv[1], sys.argv[2]
+d = json.loads(open(f"gpurun_out/ov_{cfg}_emu{P}.json").read().strip().splitlines()[-1])
+print(cfg, f"emulated_{P}_ranks", " ".join(f"{v}:{x['us_per_iter']:.1f}" for v, x in d["per_variant"].items()))
+PY
+  done
+done
