@@ -72,6 +72,18 @@ def build_cpp_shim(force: bool = False) -> str:
     return out
 
 
+def build_mtx_tool(force: bool = False) -> str:
+    """Host-only driver of the shim's Matrix Market reader (tests/test_matrix_market.py)."""
+    cpp = os.path.join(PKG, "cpp")
+    out = os.path.join(cpp, "mtx_tool")
+    src = os.path.join(cpp, "mtx_tool.cpp")
+    deps = [src, os.path.join(cpp, "cgvariants", "matrix_market.hpp"), os.path.join(cpp, "cgvariants", "cgv.hpp")]
+    if force or _stale(out, deps):
+        _run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-I", cpp, "-I", INCLUDE, "-o", out, src,
+              "-L", PKG, "-lcgvk", "-Wl,-rpath,$ORIGIN/.."])
+    return out
+
+
 def build_oracle() -> None:
     oracle = os.path.join(ROOT, "oracle")
     _run(["make", "-s", "-C", oracle, "restatement"])
@@ -83,6 +95,7 @@ def build_all(force: bool = False) -> None:
     build_gen(force)
     build_cuda(force)
     build_cpp_shim(force)
+    build_mtx_tool(force)
     build_oracle()
 
 
