@@ -571,7 +571,9 @@ struct GvK2 {
     static constexpr int NV = 0, ND = 0;
     static constexpr bool CSR = true;
     static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
-    static constexpr int STAGES = 2;  // measured: a shallower ring leaves L1 to the gathers
+    // measured: 2 stages at 4 CTAs/SM (G = 12 x SMs); with G = 3 x SMs the grid
+    // is 3 CTAs/SM and a 3-stage ring is faster (V256 GV 740 -> 697 us)
+    static constexpr int STAGES = 3;
     __device__ bool enter(const Params& P) { return P.ctrl->mode2 != MODE_SKIP; }
     __device__ const double* vec(const Params&, int) const { return nullptr; }
     static constexpr int NG = 1;  // gathered: w~
