@@ -27,6 +27,9 @@
 
 namespace cgvk {
 
+#ifndef CGVK_HS_LATE
+#define CGVK_HS_LATE 3  // HS K1 (1) / K2 (2) signal their dependents after their tiles
+#endif
 #ifndef CGVK_GV_K1_CTAS
 #define CGVK_GV_K1_CTAS 3  // stage ring sized for this many resident CTAs (registers allow 2)
 #endif
@@ -55,7 +58,7 @@ struct HsK1 {
     static constexpr int NV = PREC ? 3 : 2, ND = 2;
     static constexpr bool CSR = false;
     static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
-    static constexpr bool PDL_LATE = true;  // see cgvk_stream.cuh PdlLate
+    static constexpr bool PDL_LATE = (CGVK_HS_LATE & 1) != 0;  // see cgvk_stream.cuh PdlLate
     double alpha;
     __device__ bool enter(const Params& P) {
         if (!step_wanted(P.ctrl)) return false;
@@ -103,7 +106,7 @@ struct HsK2 {
     static constexpr int NV = 3, ND = 1;
     static constexpr bool CSR = true;
     static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
-    static constexpr bool PDL_LATE = true;
+    static constexpr bool PDL_LATE = (CGVK_HS_LATE & 2) != 0;
     int mode;
     const double* pold;
     double* pnew;
