@@ -514,7 +514,12 @@ int matrix_create(int64_t n, int64_t ncols, const int64_t* row_ptr, const int64_
     // (evict-last), a larger one streamed evict-first (measured P64 +3 %)
     {
         const double ws = 12.0 * (double)nnz + 4.0 * (double)n + 8.0 * 12.0 * (double)ncols;
-        a->l2pol = env_int("CGVK_L2POL", ws < 96e6 ? 3 : 0);
+        // one vector larger than half of L2 (V256): streamed vectors keep the
+        // default policy too, only A is evict-first (measured V256 +0.8 %,
+        // P128 -2.3 % — there the evict-first loads leave L2 to the vectors
+        // the next kernel reads)
+        const int dflt = ws < 96e6 ? 3 : 8.0 * (double)ncols > 64e6 ? 1 : 0;
+        a->l2pol = env_int("CGVK_L2POL", dflt);
     }
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
