@@ -931,6 +931,9 @@ template <class Op, class Prev>
 int make_band(cgvk_matrix a, KLaunch* L) {
     using Shape = BandShape<Op>;
     L->fn = k_band<Op, Prev>;
+#if CGVK_BAND_MAXNREG
+    if constexpr (Shape::MINB == 2 && Shape::THREADS == kThreads && Op::ND > 0) L->fn = k_band_nr<Op, Prev>;
+#endif
     L->threads = Shape::THREADS;
     StageCfg S{};
     S.nvec = Op::NV + Shape::NRAW;

@@ -82,8 +82,30 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes
 #define CGVK_BAND_CHUNK2 8
 #endif
 
+// Register cap of the two-CTA band kernels with dot products: __maxnreg__
+// instead of __launch_bounds__(288, 2), under which ptxas settles at 95-96
+// registers. Measured on R4M: 104 registers, still two CTAs per
+// SM, HS 353 -> 342 us, CG 357 -> 353, M/PR 359 -> 352; GV's dot-free K2
+// keeps the launch bounds (395 vs 390 us with the cap). 0 = launch bounds.
+#ifndef CGVK_BAND_MAXNREG
+#define CGVK_BAND_MAXNREG 104
+#endif
+template <class Op, class Prev>
+__device__ __forceinline__ void band_body(const Params& P, const StageCfg& S);
+
 template <class Op, class Prev>
 __global__ void __launch_bounds__(BandShape<Op>::THREADS, BandShape<Op>::MINB) k_band(Params P, StageCfg S) {
+    band_body<Op, Prev>(P, S);
+}
+#if CGVK_BAND_MAXNREG
+template <class Op, class Prev>
+__global__ void __maxnreg__(CGVK_BAND_MAXNREG) k_band_nr(Params P, StageCfg S) {
+    band_body<Op, Prev>(P, S);
+}
+#endif
+
+template <class Op, class Prev>
+__device__ __forceinline__ void band_body(const Params& P, const StageCfg& S) {
     static_assert(Op::CSR && Op::NG <= kBandMaxNG, "band engine runs the SpMV kernels");
     using Shape = BandShape<Op>;
     constexpr bool XF = Shape::XF;
