@@ -971,6 +971,7 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
         if (a->band_h >= 0) return make_band<Op, Prev>(a, L);
     }
     L->fn = k_stream<Op, Prev>;
+    if constexpr (MaxnregOf<Op>::value > 0) L->fn = k_stream_nr<Op, Prev>;
     L->threads = kThreads;
     StageCfg S{};
     S.nvec = Op::NV;

@@ -893,8 +893,32 @@ __device__ __forceinline__ uint64_t staged_policy(const Op& op, const Params& P,
 #ifndef CGVK_K1_MIN_CTAS
 #define CGVK_K1_MIN_CTAS 1  // register budget of the update kernels (resident CTAs)
 #endif
+template <class Op, class Prev, int SEG>
+__device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S);
+
 template <class Op, class Prev, int MINB = (Op::CSR ? CGVK_SPMV_MIN_CTAS : CGVK_K1_MIN_CTAS), int SEG = 0>
 __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S) {
+    stream_body<Op, Prev, SEG>(P, S);
+}
+
+// The same kernel under an explicit register cap (__maxnreg__ cannot be
+// combined with __launch_bounds__): for an Op with `static constexpr int
+// MAXNREG` (cgvk_api.cu make_launch picks it).
+template <class T, class = void>
+struct MaxnregOf {
+    static constexpr int value = 0;
+};
+template <class T>
+struct MaxnregOf<T, std::void_t<decltype(T::MAXNREG)>> {
+    static constexpr int value = T::MAXNREG;
+};
+template <class Op, class Prev>
+__global__ void __maxnreg__(MaxnregOf<Op>::value > 0 ? MaxnregOf<Op>::value : 255) k_stream_nr(Params P, StageCfg S) {
+    stream_body<Op, Prev, 0>(P, S);
+}
+
+template <class Op, class Prev, int SEG>
+__device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PipeHeader* H = reinterpret_cast<PipeHeader*>(smem_raw);
     unsigned char* stages = smem_raw + ((sizeof(PipeHeader) + 127) / 128) * 128;

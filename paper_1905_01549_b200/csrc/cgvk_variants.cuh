@@ -30,6 +30,9 @@ namespace cgvk {
 #ifndef CGVK_HS_LATE
 #define CGVK_HS_LATE 3  // HS K1 (1) / K2 (2) signal their dependents after their tiles
 #endif
+#ifndef CGVK_K1_MAXNREG
+#define CGVK_K1_MAXNREG 0  // > 0: GV / pipe-PR K1 under __maxnreg__ (A/B)
+#endif
 #ifndef CGVK_GV_K1_CTAS
 #define CGVK_GV_K1_CTAS 3  // stage ring sized for this many resident CTAs (registers allow 2)
 #endif
@@ -461,6 +464,7 @@ struct PrK2 {
 template <bool PREC>
 struct GvK1 {
     static constexpr int NV = PREC ? 10 : 7, ND = 5;
+    static constexpr int MAXNREG = CGVK_K1_MAXNREG;
     static constexpr int SMEM_CTAS = CGVK_GV_K1_CTAS;
     static constexpr bool CSR = false;
     static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
@@ -610,6 +614,7 @@ struct GvK2 {
 template <bool PREC>
 struct PprK1 {
     static constexpr int NV = PREC ? 10 : 6, ND = 6;
+    static constexpr int MAXNREG = CGVK_K1_MAXNREG;
     static constexpr int SMEM_CTAS = CGVK_PPR_K1_CTAS;
     static constexpr bool RR2 = true;  // two virtual CTAs per CTA interleaved (cgvk_stream.cuh rr2_tile)
     static constexpr bool CSR = false;
