@@ -33,6 +33,9 @@ namespace cgvk {
 #ifndef CGVK_K1_MAXNREG
 #define CGVK_K1_MAXNREG 0  // > 0: GV / pipe-PR K1 under __maxnreg__ (A/B)
 #endif
+#ifndef CGVK_SPMV_MAXNREG
+#define CGVK_SPMV_MAXNREG 0  // > 0: the CSR SpMV kernels under __maxnreg__ (A/B)
+#endif
 #ifndef CGVK_GV_K1_CTAS
 #define CGVK_GV_K1_CTAS 3  // stage ring sized for this many resident CTAs (registers allow 2)
 #endif
@@ -107,6 +110,7 @@ struct HsK1 {
 template <bool PREC>
 struct HsK2 {
     static constexpr int NV = 3, ND = 1;
+    static constexpr int MAXNREG = CGVK_SPMV_MAXNREG;
     static constexpr bool CSR = true;
     static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     static constexpr bool PDL_LATE = (CGVK_HS_LATE & 2) != 0;
@@ -237,6 +241,7 @@ struct CgK1 {
 template <bool PREC>
 struct CgK2 {
     static constexpr int NV = 4, ND = 5;
+    static constexpr int MAXNREG = CGVK_SPMV_MAXNREG;
     static constexpr bool CSR = true;
     static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     static constexpr int STAGES = 2;  // measured: a shallower ring leaves L1 to the gathers
@@ -381,6 +386,7 @@ struct PrK1 {
 template <bool PREC>
 struct PrK2 {
     static constexpr int NV = PREC ? 4 : 2, ND = 6;
+    static constexpr int MAXNREG = CGVK_SPMV_MAXNREG;
     static constexpr bool CSR = true;
     static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     static constexpr bool PDL_LATE = (CGVK_PR_LATE & 2) != 0;
@@ -576,6 +582,7 @@ struct GvK1 {
 template <bool PREC>
 struct GvK2 {
     static constexpr int NV = 0, ND = 0;
+    static constexpr int MAXNREG = CGVK_SPMV_MAXNREG;
     static constexpr bool CSR = true;
     static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     // measured: 2 stages at 4 CTAs/SM (G = 12 x SMs); with G = 3 x SMs the grid
@@ -744,6 +751,7 @@ struct PprK1 {
 template <bool PREC>
 struct PprK2 {
     static constexpr int NV = 0, ND = 0;
+    static constexpr int MAXNREG = CGVK_SPMV_MAXNREG;
     static constexpr bool CSR = true;
     static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     bool recw;
