@@ -97,9 +97,6 @@ struct SmemCtasOf<T, std::void_t<decltype(T::SMEM_CTAS)>> {
 #ifndef CGVK_EARLY
 #define CGVK_EARLY 2         // stages whose vectors are issued right after the wait
 #endif
-#ifndef CGVK_EARLY_ORDER
-#define CGVK_EARLY_ORDER 0   // 1: only after warp 0's control-block load (chained)
-#endif
 template <class T, class = void>
 struct HasEarlyVec {
     static constexpr bool value = false;
@@ -694,19 +691,14 @@ constexpr int kCtrlHead = offsetof(Ctrl, tot) / 16;
 // copy, which would queue behind the producer's matrix prefetch in the TMA
 // unit; thread 0 runs the predecessor's finish on it; CTA 0 writes the
 // advanced state to `out`.
-// signal: warp 0 releases named barrier 2 (its 32 threads + the producer
-// warp's 32) once the control block has arrived, so a producer that issues
-// stage copies right after the dependency wait queues them behind that load.
 template <class Prev>
-__device__ __forceinline__ void chain_prologue(const Params& P, int chain, PipeHeader* H, Ctrl* out,
-                                               bool signal = false) {
+__device__ __forceinline__ void chain_prologue(const Params& P, int chain, PipeHeader* H, Ctrl* out) {
     const int t = threadIdx.x;
     if (t < 32) {
         constexpr int kWords = sizeof(Ctrl) / 16;
         const uint4* in = reinterpret_cast<const uint4*>((chain & CH_ODD) ? P.ctrl_b : P.ctrl);
         if (t < kWords) reinterpret_cast<uint4*>(&H->cs)[t] = __ldcg(in + t);
         __syncwarp();
-        if (signal) asm volatile("bar.arrive 2, 64;" ::: "memory");
     }
     if (t == 0) {
         if (chain & CH_FOLD) {
@@ -982,9 +974,6 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
     pdl_wait();
     tl_mark(Op::CSR, 1);
     if constexpr (kEarly) {
-        // chained: after warp 0's control-block load (measured: issued
-        // before it, the burst of stage copies delays that load by 1-3 us)
-        if (CGVK_EARLY_ORDER && S.chain && warp == kWarps) asm volatile("bar.sync 2, 64;" ::: "memory");
         if (producer) {
             const uint64_t vpol = P.l2pol == 0 ? (Op::CSR ? pol : evict_first_policy()) : 0;
             for (int q = 0; q < nearly; ++q) {
@@ -1007,7 +996,7 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
     if (!PdlLate<Op>::value) pdl_trigger();
     const int chain = S.chain;
     if (chain) {
-        chain_prologue<Prev>(P, chain, H, (chain & CH_ODD) ? P.ctrl : P.ctrl_b, kEarly && CGVK_EARLY_ORDER);
+        chain_prologue<Prev>(P, chain, H, (chain & CH_ODD) ? P.ctrl : P.ctrl_b);
         tl_mark(Op::CSR, 5);
     }
     Op op;
