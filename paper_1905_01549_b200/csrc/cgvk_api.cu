@@ -971,7 +971,13 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
         if (a->band_h >= 0) return make_band<Op, Prev>(a, L);
     }
     L->fn = k_stream<Op, Prev>;
-    if constexpr (MaxnregOf<Op>::value > 0) L->fn = k_stream_nr<Op, Prev>;
+    // register-capped build of an Op that has one (GV / pipe-PR K1: 72
+    // registers, 3 CTAs/SM): only when the working set fits L2 and the
+    // virtual CTAs outnumber two CTAs per SM (measured P64 GV 18.4 -> 17.5 us,
+    // pipe-PR 19.4 -> 18.8; P2D, whose 256 tiles fit either grid, and P128 /
+    // V256 are slower with it)
+    if constexpr (MaxnregOf<Op>::value > 0)
+        if ((a->l2pol == 3 && a->G > 2 * a->sms) || env_int("CGVK_K1_NR", 0)) L->fn = k_stream_nr<Op, Prev>;
     L->threads = kThreads;
     StageCfg S{};
     S.nvec = Op::NV;

@@ -31,7 +31,7 @@ namespace cgvk {
 #define CGVK_HS_LATE 3  // HS K1 (1) / K2 (2) signal their dependents after their tiles
 #endif
 #ifndef CGVK_K1_MAXNREG
-#define CGVK_K1_MAXNREG 0  // > 0: GV / pipe-PR K1 under __maxnreg__ (A/B)
+#define CGVK_K1_MAXNREG 72  // GV / pipe-PR K1 under __maxnreg__ when the working set fits L2
 #endif
 #ifndef CGVK_SPMV_MAXNREG
 #define CGVK_SPMV_MAXNREG 0  // > 0: the CSR SpMV kernels under __maxnreg__ (A/B)
