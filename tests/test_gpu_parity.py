@@ -174,3 +174,19 @@ def test_vector_into_caller_buffer(medium):
     with pytest.raises(cgvk.InvalidArgument):
         s.vector(cgvk.Vec.X, out=np.empty(A.n, dtype=np.float32))
     s.close()
+
+
+# 278^2 = 77,284 rows = 302 tiles: between the 2-CTA/SM (296) and 3-CTA/SM
+# (444) grids, so G = ntiles, the 2-CTA/SM update kernels run two virtual CTAs
+# in some CTAs and one in others, and CG-CG's reversed sweep walks single
+# tiles — bit-exact against the restatement.
+@pytest.fixture(scope="module")
+def odd302():
+    P = pb.make_problem("p2d278", pb.poisson2d(278))
+    return P, cgvk.DeviceMatrix.from_csr(P.A)
+
+
+@pytest.mark.parametrize("variant", ALL_VARIANTS)
+def test_302_tiles_bit_exact(variant, odd302):
+    P, A = odd302
+    lockstep(P.A, A, variant, Precond.JACOBI, P.b, P.x0, steps=4, check_vectors_every=2)
