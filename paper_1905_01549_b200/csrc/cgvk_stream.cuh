@@ -1023,9 +1023,10 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
         }
         int j = 0;
         const uint64_t vpol = P.l2pol == 0 ? pol : 0;
-        uint64_t vpol_v[kMaxVec];
+        unsigned int normal_mask = 0;  // staged vectors kept at normal L2 priority
 #pragma unroll
-        for (int v = 0; v < Op::NV; ++v) vpol_v[v] = vp[v] ? staged_policy(op, P, vp[v], vpol) : vpol;
+        for (int v = 0; v < Op::NV; ++v)
+            if (vp[v] && staged_policy(op, P, vp[v], vpol) != vpol) normal_mask |= 1u << v;
         auto produce_tile = [&](int tile, int vb) {
             {
                 if (j < nearly) {  // issued right after the wait
@@ -1064,7 +1065,9 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
                 mbar_expect_tx(&H->full[slot], bytes);  // + this thread's arrival
 #pragma unroll
                 for (int v = 0; v < Op::NV; ++v)
-                    if (vp[v]) bulk_g2s(V.vec + v * kBlock, vp[v] + r0, vec_bytes, &H->full[slot], vpol_v[v]);
+                    if (vp[v])
+                        bulk_g2s(V.vec + v * kBlock, vp[v] + r0, vec_bytes, &H->full[slot],
+                                 (normal_mask >> v) & 1u ? 0ull : vpol);
                 if constexpr (SEG == 1) {
                     for (int q = 0; q < S.nd; ++q) {
                         const int u = tile + P.seg_d[q];
