@@ -186,6 +186,7 @@ struct HsK2 {
 template <bool PREC>
 struct CgK1 {
     static constexpr int NV = PREC ? 6 : 5, ND = 0;
+    static constexpr bool PDL_LATE = true;  // measured with G = 3 x SMs: P128 CG -2.4 us, GV -1.3 us
     // no dots: sweeps downwards (cgvk_stream.cuh RevOf); measured CG V256 581 -> 574 us
     // (GV / pipe-PR's K2 reversed: V256 +6 / +27 us, left forward)
     static constexpr bool REVERSE = true;
@@ -241,6 +242,7 @@ struct CgK1 {
 template <bool PREC>
 struct CgK2 {
     static constexpr int NV = 4, ND = 5;
+    static constexpr bool PDL_LATE = true;  // measured with G = 3 x SMs: P128 CG -2.4 us, GV -1.3 us
     static constexpr int MAXNREG = CGVK_SPMV_MAXNREG;
     static constexpr bool CSR = true;
     static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
@@ -470,6 +472,7 @@ struct PrK2 {
 template <bool PREC>
 struct GvK1 {
     static constexpr int NV = PREC ? 10 : 7, ND = 5;
+    static constexpr bool PDL_LATE = true;  // measured with G = 3 x SMs: P128 CG -2.4 us, GV -1.3 us
     static constexpr int MAXNREG = CGVK_K1_MAXNREG;
     static constexpr int SMEM_CTAS = CGVK_GV_K1_CTAS;
     static constexpr bool CSR = false;
@@ -582,6 +585,7 @@ struct GvK1 {
 template <bool PREC>
 struct GvK2 {
     static constexpr int NV = 0, ND = 0;
+    static constexpr bool PDL_LATE = true;  // measured with G = 3 x SMs: P128 CG -2.4 us, GV -1.3 us
     static constexpr int MAXNREG = CGVK_SPMV_MAXNREG;
     static constexpr bool CSR = true;
     static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
