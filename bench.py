@@ -467,13 +467,20 @@ def run_gpu_arm(args, rank, local, world, dist):
         try:
             barrier(dist)
             sweep()[3].close()  # warm-up sweep (driver/allocator state, pinned mappings)
-            barrier(dist)
-            t0 = time.perf_counter()
-            e2e_iters, x, phases, E = sweep()
-            t1 = time.perf_counter()
-            E.close()  # freeing device memory is not part of the user's solve
-            barrier(dist)
-            wall = max_over_ranks(dist, t1 - t0)
+            # best of --e2e-reps timed sweeps (each max over ranks), as the
+            # paper reports minima over repetitions: one host
+            # hiccup must not stand for the path
+            wall = None
+            for _ in range(max(args.e2e_reps, 1)):
+                barrier(dist)
+                t0 = time.perf_counter()
+                its_r, x_r, ph_r, E = sweep()
+                t1 = time.perf_counter()
+                E.close()  # freeing device memory is not part of the user's solve
+                barrier(dist)
+                w = max_over_ranks(dist, t1 - t0)
+                if wall is None or w < wall:
+                    wall, e2e_iters, x, phases = w, its_r, x_r, ph_r
         finally:
             for arr in arrs + list(xs.values()):
                 cgvk.host_unregister(arr)
@@ -482,7 +489,7 @@ def run_gpu_arm(args, rank, local, world, dist):
         e2e = {"value": e2e_iters / wall, "unit": "iterations/s",
                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
                "phases_ms": {k: round(v, 2) for k, v in phases.items()},
-               "note": "one timed sweep after one warm-up sweep: int64 CSR + b, x0 per variant up "
+               "note": "fastest of --e2e-reps timed sweeps after one warm-up sweep: int64 CSR + b, x0 per variant up "
                        "(each rank its rows), K steps, x per variant down; bytes_per_step = sweep "
                        "bytes / K (rank 0's share when N > 1)"}
 
@@ -542,6 +549,7 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=10)
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-reps", type=int, default=2, help="timed end-to-end sweeps; the fastest is reported")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--nccl", action="store_true",
                     help="row-partitioned path over NCCL even at one rank (transport check)")
