@@ -36,6 +36,12 @@ namespace cgvk {
 #ifndef CGVK_SPMV_MAXNREG
 #define CGVK_SPMV_MAXNREG 0  // > 0: the CSR SpMV kernels under __maxnreg__ (A/B)
 #endif
+#ifndef CGVK_CG_LATE
+#define CGVK_CG_LATE 2  // CG-CG K1 (1) / K2 (2) signal their dependents after their tiles
+#endif
+#ifndef CGVK_GV_LATE
+#define CGVK_GV_LATE 3  // GV K1 (1) / K2 (2) signal their dependents after their tiles
+#endif
 #ifndef CGVK_GV_K1_CTAS
 #define CGVK_GV_K1_CTAS 3  // stage ring sized for this many resident CTAs (registers allow 2)
 #endif
@@ -186,7 +192,7 @@ struct HsK2 {
 template <bool PREC>
 struct CgK1 {
     static constexpr int NV = PREC ? 6 : 5, ND = 0;
-    static constexpr bool PDL_LATE = true;  // measured with G = 3 x SMs: P128 CG -2.4 us, GV -1.3 us
+    static constexpr bool PDL_LATE = (CGVK_CG_LATE & 1) != 0;  // measured with G = 3 x SMs
     // no dots: sweeps downwards (cgvk_stream.cuh RevOf); measured CG V256 581 -> 574 us
     // (GV / pipe-PR's K2 reversed: V256 +6 / +27 us, left forward)
     static constexpr bool REVERSE = true;
@@ -242,7 +248,7 @@ struct CgK1 {
 template <bool PREC>
 struct CgK2 {
     static constexpr int NV = 4, ND = 5;
-    static constexpr bool PDL_LATE = true;  // measured with G = 3 x SMs: P128 CG -2.4 us, GV -1.3 us
+    static constexpr bool PDL_LATE = (CGVK_CG_LATE & 2) != 0;
     static constexpr int MAXNREG = CGVK_SPMV_MAXNREG;
     static constexpr bool CSR = true;
     static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
@@ -472,7 +478,7 @@ struct PrK2 {
 template <bool PREC>
 struct GvK1 {
     static constexpr int NV = PREC ? 10 : 7, ND = 5;
-    static constexpr bool PDL_LATE = true;  // measured with G = 3 x SMs: P128 CG -2.4 us, GV -1.3 us
+    static constexpr bool PDL_LATE = (CGVK_GV_LATE & 1) != 0;  // measured with G = 3 x SMs
     static constexpr int MAXNREG = CGVK_K1_MAXNREG;
     static constexpr int SMEM_CTAS = CGVK_GV_K1_CTAS;
     static constexpr bool CSR = false;
@@ -585,7 +591,7 @@ struct GvK1 {
 template <bool PREC>
 struct GvK2 {
     static constexpr int NV = 0, ND = 0;
-    static constexpr bool PDL_LATE = true;  // measured with G = 3 x SMs: P128 CG -2.4 us, GV -1.3 us
+    static constexpr bool PDL_LATE = (CGVK_GV_LATE & 2) != 0;
     static constexpr int MAXNREG = CGVK_SPMV_MAXNREG;
     static constexpr bool CSR = true;
     static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
