@@ -42,6 +42,9 @@ namespace cgvk {
 #ifndef CGVK_GV_LATE
 #define CGVK_GV_LATE 3  // GV K1 (1) / K2 (2) signal their dependents after their tiles
 #endif
+#ifndef CGVK_PPR_LATE
+#define CGVK_PPR_LATE 2  // pipe-PR K1 (1) / K2 (2) signal their dependents after their tiles
+#endif
 #ifndef CGVK_GV_K1_CTAS
 #define CGVK_GV_K1_CTAS 3  // stage ring sized for this many resident CTAs (registers allow 2)
 #endif
@@ -631,6 +634,7 @@ struct GvK2 {
 template <bool PREC>
 struct PprK1 {
     static constexpr int NV = PREC ? 10 : 6, ND = 6;
+    static constexpr bool PDL_LATE = (CGVK_PPR_LATE & 1) != 0;
     static constexpr int MAXNREG = CGVK_K1_MAXNREG;
     static constexpr int SMEM_CTAS = CGVK_PPR_K1_CTAS;
     static constexpr bool RR2 = true;  // two virtual CTAs per CTA interleaved (cgvk_stream.cuh rr2_tile)
@@ -761,6 +765,7 @@ struct PprK1 {
 template <bool PREC>
 struct PprK2 {
     static constexpr int NV = 0, ND = 0;
+    static constexpr bool PDL_LATE = (CGVK_PPR_LATE & 2) != 0;
     static constexpr int MAXNREG = CGVK_SPMV_MAXNREG;
     static constexpr bool CSR = true;
     static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
