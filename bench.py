@@ -176,16 +176,49 @@ def barrier(dist):
 
 
 # ------------------------------------------------------------------ CPU arms
+#
+# Nothing below maps a library of the product package: variant ids come from
+# this table (inc/variants.hpp:17-25, the reference's enum order) and the
+# inputs from oracle/_build/libinputgen.so (a second build of the App. B
+# generator source), so the reference arm's process loads only oracle/.
+
+VARIANT_IDS = {"hs": 0, "cg": 1, "m": 2, "pr": 3, "gv": 4, "pipe-pr-m": 5, "pipe-pr": 6}
+INPUTGEN = os.path.join(ROOT, "oracle", "_build", "libinputgen.so")
+# bounded single-core samples (BASELINE.md §3 asks K = 50 for the Poisson
+# configs, best of 3; the two largest configs take ~0.3-0.5 s per step on one
+# core, so their sample is K = 5, best of 2, to keep the run within minutes)
+CPU_SAMPLE = {"p2d": (50, 3), "p64": (50, 3), "p128": (50, 3), "v256": (5, 2), "r4m": (5, 2)}
+
+
+def host_problem(name: str):
+    """App. B inputs built by the oracle's copy of the generators."""
+    from paper_1905_01549_b200 import problems as pb
+
+    if os.path.exists(INPUTGEN) and pb._gen is None:
+        pb.use_generator(INPUTGEN)
+    return pb.config_problem(name)
+
+
+def host_info() -> dict:
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return {"nproc": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)), "lscpu_model": model}
+
 
 def cpu_sweep(P, variants, steps: int, warmup: int, kind: str):
     """The six variants in six threads (the reference's jobs>1 model,
     src/experiment.cpp:317-322); each thread runs `steps` step() calls."""
     from oracle import oracle as O
-    from paper_1905_01549_b200.cgvk import variant_from_name
 
     solvers = []
     for v in variants:
-        vid = int(variant_from_name(v))
+        vid = VARIANT_IDS[v]
         if kind == "reference":
             solvers.append(O.Reference(P.A, vid, 1, P.b, P.x0))
         else:
@@ -210,14 +243,65 @@ def cpu_sweep(P, variants, steps: int, warmup: int, kind: str):
     return iters, wall, per
 
 
+def cpu_worker(args) -> int:
+    """(run under taskset by single_core_baseline) the reference's step() loop
+    on one core: per variant one warm-up step, then the best of `reps` timed
+    runs of `steps` step() calls (std::chrono inside oracle/ref_shim.cpp)."""
+    from oracle import oracle as O
+
+    P = host_problem(args.cpu_worker)
+    kind = "reference" if O.reference_available() else "port"
+    mat = O.RefMatrix(P.A) if kind == "reference" else None
+    steps, reps = args.cpu_steps, args.cpu_reps
+    out = {}
+    for v in VARIANTS:
+        if kind == "reference":
+            s = O.Reference(P.A, VARIANT_IDS[v], 1, P.b, P.x0, mat=mat)
+        else:
+            s = O.Restatement(P.A, VARIANT_IDS[v], 1, P.b, P.x0)
+        s.time_steps(1)
+        best = None
+        for _ in range(reps):
+            secs, it = s.time_steps(steps)
+            ms = 1e3 * secs / max(it, 1)
+            best = ms if best is None else min(best, ms)
+        out[v] = best
+        del s
+    print(json.dumps({"kind": kind, "ms_per_iter": out, "steps": steps, "reps": reps,
+                      "affinity": sorted(os.sched_getaffinity(0))}), flush=True)
+    return 0
+
+
+def single_core_baseline(cfg: str, steps: int | None = None, reps: int | None = None) -> dict | None:
+    """The baseline of record: the reference's step() on ONE
+    pinned core (taskset), best of `reps` runs of K steps per variant."""
+    k, r = CPU_SAMPLE[cfg]
+    steps, reps = steps or k, reps or r
+    core = sorted(os.sched_getaffinity(0))[-1]
+    cmd = ["taskset", "-c", str(core), sys.executable, os.path.abspath(__file__), "--cpu-worker", cfg,
+           "--cpu-steps", str(steps), "--cpu-reps", str(reps)]
+    t0 = time.perf_counter()
+    try:
+        r_ = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+        d = json.loads(r_.stdout.strip().splitlines()[-1])
+    except (OSError, subprocess.SubprocessError, ValueError, IndexError) as e:
+        return {"error": f"{type(e).__name__}: {e}"}
+    ms = d["ms_per_iter"]
+    total = sum(ms.values())
+    return {"value": len(ms) / (total * 1e-3), "unit": "iterations/s", "cores": 1, "kind": d["kind"],
+            "pinned_core": core,
+            "sample": f"{steps} step() calls per variant, best of {reps}, one after another on one "
+                      f"core pinned with taskset (value = 6 / sum of the six ms/iteration)",
+            "ms_per_iter": ms, "wall_s": round(time.perf_counter() - t0, 1), "host": host_info()}
+
+
 def run_reference_arm(args, rank, world, dist):
     if rank != 0:
         return 0
     from oracle import oracle as O
-    from paper_1905_01549_b200 import problems as pb
 
     kind = "reference" if O.reference_available() else "port"
-    P = pb.config_problem(args.config)
+    P = host_problem(args.config)
     iters, wall, per = cpu_sweep(P, VARIANTS, args.steps, args.warmup, kind)
     value = iters / wall
     line = {
@@ -225,11 +309,13 @@ def run_reference_arm(args, rank, world, dist):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args, P),
+        "config": workload_config(args.config, P),
         "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": len(VARIANTS),
                          "kind": kind,
                          "sample": f"{args.steps} step() calls of each of the six variants on "
-                                   f"{args.config}, one thread per variant"},
+                                   f"{args.config}, one thread per variant (oracle/_ref: the "
+                                   f"unchanged reference sources)",
+                         "host": host_info()},
         "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "per_variant": per,
@@ -241,14 +327,14 @@ def run_reference_arm(args, rank, world, dist):
 METRIC = "CG iterations/s (six-variant sweep) and effective HBM GB/s per variant"
 
 
-def workload_config(args, P, ranks: int = 1) -> dict:
+def workload_config(name, P, ranks: int = 1) -> dict:
     per = [iter_bytes(v, P.A.n, P.A.nnz, True) / max(ranks, 1) / 1e6 for v in VARIANTS]
     lo, hi = min(per), max(per)
     l2 = (f"per-GPU working set {lo:.0f}-{hi:.0f} MB per iteration > L2 (126 MB); no flush needed"
           if lo > 126 else
           f"per-GPU working set {lo:.0f}-{hi:.0f} MB per iteration fits the 126 MB L2: the solve runs "
           f"L2-resident as it would in use (latency-bound regime, SURVEY 8d); no flush")
-    return {"workload": f"{args.config} ({P.A.n} rows, {P.A.nnz} nnz) fp64 CSR, Jacobi, "
+    return {"workload": f"{name} ({P.A.n} rows, {P.A.nnz} nnz) fp64 CSR, Jacobi, "
                         f"six variants, K fixed iterations each",
             "variants": VARIANTS, "n": P.A.n, "nnz": P.A.nnz, "precond": "jacobi",
             "l2": l2, "parallelism": "single-gpu"}
@@ -322,19 +408,21 @@ class SolveSet:
             self.comm.close()
 
 
-def run_gpu_arm(args, rank, local, world, dist):
+def measure_config(args, cfg_name, rank, local, world, dist, extra=False) -> dict:
+    """Device-timed sweep, per-kernel shares, roofline and e2e of one config."""
     from paper_1905_01549_b200 import cgvk, problems as pb
     from paper_1905_01549_b200.cgvk import Precond, VariantConfig, variant_from_name
 
     device = local
-    P = pb.config_problem(args.config)
+    args = argparse.Namespace(**{**vars(args), "config": cfg_name})
+    P = pb.config_problem(cfg_name)
     n, nnz = P.A.n, P.A.nnz
     pk = peaks()
-    partitioned = world > 1 or args.emulate_ranks > 1 or args.nccl
+    partitioned = not extra and (world > 1 or args.emulate_ranks > 1 or args.nccl)
     fallback = None
     S = None
     try:
-        S = SolveSet(args, P, rank, world, device, dist)
+        S = SolveSet(args, P, rank, world, device, dist, replicas=extra)
         for v, s in S.solvers.items():  # warm-up: graphs, clocks, caches
             s.time_steps(args.warmup)
         ok = 1.0
@@ -346,7 +434,7 @@ def run_gpu_arm(args, rank, local, world, dist):
         ok = -max_over_ranks(dist, -ok)  # min over ranks: every rank falls back together
     if partitioned and ok < 1.0:
         # the row-partitioned transport failed on this box: independent
-        # replicas (weak scaling) so the job still reports a measured number
+        # replicas (weak scaling), labelled as such in `parallelism`
         if S is not None:
             S.close()
         fallback = fallback or "another rank's partitioned setup failed"
@@ -409,25 +497,28 @@ def run_gpu_arm(args, rank, local, world, dist):
             s.close()
         A.close()
 
+    reps = world if (fallback is not None or extra) and world > 1 else 1
     for v in VARIANTS:
         d = per[v]
         t_iter = d["ms"] / max(d["iters"], 1) * 1e-3
-        bi = iter_bytes(v, n, nnz, True)
-        if fallback is not None:
-            bi *= world  # every replica moves the whole iteration's bytes
-        per[v].update({"it_per_s": d["iters"] / (d["ms"] * 1e-3), "us_per_iter": t_iter * 1e6,
+        bi = iter_bytes(v, n, nnz, True) * reps  # every replica moves the whole iteration's bytes
+        per[v].update({"it_per_s": reps * d["iters"] / (d["ms"] * 1e-3), "us_per_iter": t_iter * 1e6,
                        "bytes_per_iter": bi, "gbs": bi / t_iter / 1e9,
                        "roofline_frac": bi / t_iter / 1e9 / (pk["hbm_gbs"] * max(world, 1)),
                        "roofline_frac_nominal_8tbs": bi / t_iter / 1e9 / (8000.0 * max(world, 1))})
+    traffic = load_traffic().get(cfg_name, {})
     if kernels:
         top = max(kernels, key=lambda k: k["ms_per_launch"])
         roof = {"bound": "hbm", "kernel": top["kernel"], "variant": top["variant"],
                 "achieved": top["gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": top["gbs"] / pk["hbm_gbs"], "peak_source": pk["source"],
-                "traffic": load_traffic().get(args.config, {}).get(top["kernel"]),
+                "traffic": traffic.get(top["kernel"]),
                 "bytes_per_launch": top["bytes_per_launch"], "ms_per_launch": top["ms_per_launch"],
                 "timing": "kernel share of the event-timed K1/K2 launches x the event-timed graph "
                           "iteration; ms_per_launch_unfused in `kernels`"}
+        for k in kernels:  # ncu DRAM bytes beside the algorithmic bytes (K1s re-read K2's output from L2)
+            if k["kernel"] in traffic:
+                k["dram_bytes_ncu"] = traffic[k["kernel"]]
     else:  # partitioned: whole-iteration roofline of the slowest variant over all GPUs
         worst = min(VARIANTS, key=lambda v: per[v]["roofline_frac"])
         roof = {"bound": "hbm", "kernel": "iteration", "variant": worst,
@@ -435,106 +526,138 @@ def run_gpu_arm(args, rank, local, world, dist):
                 "frac": per[worst]["roofline_frac"], "peak_source": pk["source"], "traffic": None,
                 "bytes_per_launch": per[worst]["bytes_per_iter"],
                 "ms_per_launch": per[worst]["us_per_iter"] * 1e-3}
+    iteration_frac = {v: round(per[v]["roofline_frac"], 4) for v in VARIANTS}
 
-    # e2e through the public API with pinned host buffers
-    e2e = None
-    if not args.no_e2e:
-        arrs = [P.A.row_ptr.copy(), P.A.col_idx.copy(), P.A.values.copy(), P.b.copy(), P.x0.copy()]
-        xs = {v: np.empty(n) for v in VARIANTS}  # the user's result buffers (registered, like the inputs)
-        for arr in arrs + list(xs.values()):
-            cgvk.host_register(arr)
-        def sweep():
-            # the user's calls: upload A (+ b, x0 per variant), solve K steps,
-            # read x back; phases kept for the JSON note
-            ph = {}
-            t = time.perf_counter()
-            E = SolveSet(args, P, rank, world, device, dist, pinned=tuple(arrs), replicas=fallback is not None)
-            ph["setup_ms"] = 1e3 * (time.perf_counter() - t)
-            if hasattr(E, "t_matrix"):
-                ph["matrix_upload_ms"] = 1e3 * E.t_matrix
-                ph["initialize_ms"] = 1e3 * E.t_init
-            its = 0
-            xx = None
-            t = time.perf_counter()
-            for v, s in E.solvers.items():
-                s.step(args.steps)
-                s.sync()
-                xx = s.vector(cgvk.Vec.X, out=xs[v]) if hasattr(s, "_h") else s.x  # result read back each solve
-                its += s.k
-            ph["solve_ms"] = 1e3 * (time.perf_counter() - t)
-            return its, xx, ph, E
+    e2e = None if args.no_e2e else measure_e2e(args, P, rank, world, device, dist,
+                                                replicas=fallback is not None or extra)
 
-        try:
+    value = reps * total_iters / (total_ms * 1e-3)
+    cfg = workload_config(cfg_name, P, world if partitioned else 1)
+    if partitioned:
+        cfg["parallelism"] = (f"row-partitioned z-slabs over {world} GPUs (NCCL)" if world > 1 or args.nccl
+                              else f"row-partitioned, {args.emulate_ranks} in-process ranks on 1 GPU")
+    if fallback is not None:
+        cfg["parallelism"] = f"{world} independent replicas (row-partitioned transport failed: {fallback})"
+    elif extra and world > 1:
+        cfg["parallelism"] = f"{world} independent replicas"
+    # our kernels in the timed region: one limit-setting launch per step()
+    # call + the captured kernels of every replayed graph (chained graphs'
+    # tail kernel, halo pack/unpack and finalize kernels included; NCCL's
+    # own not counted)
+    launches = sum(per[v]["launches"] for v in VARIANTS)
+    return {"value": value, "ms_per_step": total_ms / args.steps, "config": cfg, "roofline": roof,
+            "iteration_roofline_frac": iteration_frac, "kernels": kernels, "per_variant": per,
+            "gpu_launches": launches * world, "e2e": e2e, "clocks": clk,
+            "scaling": "weak" if reps > 1 else "strong"}
+
+
+def measure_e2e(args, P, rank, world, device, dist, replicas=False) -> dict:
+    """e2e through the public API with pinned host buffers."""
+    from paper_1905_01549_b200 import cgvk
+
+    n = P.A.n
+    arrs = [P.A.row_ptr.copy(), P.A.col_idx.copy(), P.A.values.copy(), P.b.copy(), P.x0.copy()]
+    xs = {v: np.empty(n) for v in VARIANTS}  # the user's result buffers (registered, like the inputs)
+    for arr in arrs + list(xs.values()):
+        cgvk.host_register(arr)
+
+    def sweep():
+        # the user's calls: upload A (+ b, x0 per variant), solve K steps,
+        # read x back; phases kept for the JSON note
+        ph = {}
+        t = time.perf_counter()
+        E = SolveSet(args, P, rank, world, device, dist, pinned=tuple(arrs), replicas=replicas)
+        ph["setup_ms"] = 1e3 * (time.perf_counter() - t)
+        if hasattr(E, "t_matrix"):
+            ph["matrix_upload_ms"] = 1e3 * E.t_matrix
+            ph["initialize_ms"] = 1e3 * E.t_init
+        its = 0
+        xx = None
+        t = time.perf_counter()
+        for v, s in E.solvers.items():
+            s.step(args.steps)
+            s.sync()
+            xx = s.vector(cgvk.Vec.X, out=xs[v]) if hasattr(s, "_h") else s.x  # result read back each solve
+            its += s.k
+        ph["solve_ms"] = 1e3 * (time.perf_counter() - t)
+        return its, xx, ph, E
+
+    try:
+        barrier(dist)
+        sweep()[3].close()  # warm-up sweep (driver/allocator state, pinned mappings)
+        # best of --e2e-reps timed sweeps (each max over ranks), as the
+        # paper reports minima over repetitions (PAPER.md:924): one host
+        # hiccup must not stand for the path
+        wall = None
+        for _ in range(max(args.e2e_reps, 1)):
             barrier(dist)
-            sweep()[3].close()  # warm-up sweep (driver/allocator state, pinned mappings)
-            # best of --e2e-reps timed sweeps (each max over ranks), as the
-            # paper reports minima over repetitions: one host
-            # hiccup must not stand for the path
-            wall = None
-            for _ in range(max(args.e2e_reps, 1)):
-                barrier(dist)
-                t0 = time.perf_counter()
-                its_r, x_r, ph_r, E = sweep()
-                t1 = time.perf_counter()
-                E.close()  # freeing device memory is not part of the user's solve
-                barrier(dist)
-                w = max_over_ranks(dist, t1 - t0)
-                if wall is None or w < wall:
-                    wall, e2e_iters, x, phases = w, its_r, x_r, ph_r
-        finally:
-            for arr in arrs + list(xs.values()):
-                cgvk.host_unregister(arr)
-        h2d = sum(a.nbytes for a in arrs[:3]) + len(VARIANTS) * (arrs[3].nbytes + arrs[4].nbytes)
-        d2h = len(VARIANTS) * x.nbytes
-        e2e = {"value": e2e_iters / wall, "unit": "iterations/s",
-               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
-               "phases_ms": {k: round(v, 2) for k, v in phases.items()},
-               "note": "fastest of --e2e-reps timed sweeps after one warm-up sweep: int64 CSR + b, x0 per variant up "
-                       "(each rank its rows), K steps, x per variant down; bytes_per_step = sweep "
-                       "bytes / K (rank 0's share when N > 1)"}
+            t0 = time.perf_counter()
+            its_r, x_r, ph_r, E = sweep()
+            t1 = time.perf_counter()
+            E.close()  # freeing device memory is not part of the user's solve
+            barrier(dist)
+            w = max_over_ranks(dist, t1 - t0)
+            if wall is None or w < wall:
+                wall, e2e_iters, x, phases = w, its_r, x_r, ph_r
+    finally:
+        for arr in arrs + list(xs.values()):
+            cgvk.host_unregister(arr)
+    reps = world if replicas and world > 1 else 1
+    h2d = sum(a.nbytes for a in arrs[:3]) + len(VARIANTS) * (arrs[3].nbytes + arrs[4].nbytes)
+    d2h = len(VARIANTS) * x.nbytes
+    return {"value": reps * e2e_iters / wall, "unit": "iterations/s",
+            "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+            "phases_ms": {k: round(v, 2) for k, v in phases.items()},
+            "note": "fastest of --e2e-reps timed sweeps after one warm-up sweep: int64 CSR + b, x0 per variant up "
+                    "(each rank its rows), K steps, x per variant down; bytes_per_step = sweep "
+                    "bytes / K (rank 0's share when N > 1)"}
+
+
+def run_gpu_arm(args, rank, local, world, dist):
+    head = measure_config(args, args.config, rank, local, world, dist)
+    extras = {}
+    if world == 1 and args.emulate_ranks <= 1 and not args.nccl:
+        for c in [c for c in args.per_config.split(",") if c and c != args.config]:
+            extras[c] = measure_config(args, c, rank, local, world, dist, extra=True)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         from oracle import oracle as O
 
         kind = "reference" if O.reference_available() else "port"
-        cpu_steps = args.cpu_steps
-        iters, wall, cper = cpu_sweep(P, VARIANTS, cpu_steps, 1, kind)
+        P = host_problem(args.config)
+        iters, wall, cper = cpu_sweep(P, VARIANTS, args.cpu_steps, 1, kind)
+        del P
         cpu = {"value": iters / wall, "unit": "iterations/s", "cores": len(VARIANTS), "kind": kind,
-               "sample": f"{cpu_steps} step() calls of each of the six variants on {args.config} "
-                         f"(one thread per variant, -O2 -ffp-contract=off build)",
-               "per_variant": cper}
+               "sample": f"{args.cpu_steps} step() calls of each of the six variants on {args.config} "
+                         f"(one thread per variant, the reference's own -O2 -ffp-contract=off build)",
+               "per_variant": cper,
+               "single_core": None if args.no_single_core else single_core_baseline(args.config)}
+        for c, d in extras.items():
+            d["cpu_baseline"] = None if args.no_single_core else single_core_baseline(c)
 
-    # replicas (fallback): every rank ran the whole solve -> whole-job throughput
-    reps = world if (fallback is not None and world > 1) else 1
-    value = reps * total_iters / (total_ms * 1e-3)
     if rank == 0:
-        # our kernels in the timed region: one limit-setting launch per step()
-        # call + the captured kernels of every replayed graph (chained graphs'
-        # tail kernel, halo pack/unpack and finalize kernels included; NCCL's
-        # own not counted)
-        launches = sum(per[v]["launches"] for v in VARIANTS)
-        cfg = workload_config(args, P, world if partitioned else 1)
-        if partitioned:
-            cfg["parallelism"] = (f"row-partitioned z-slabs over {world} GPUs (NCCL)" if world > 1 or args.nccl
-                                  else f"row-partitioned, {args.emulate_ranks} in-process ranks on 1 GPU")
-        if fallback is not None:
-            cfg["parallelism"] = f"{world} independent replicas (row-partitioned transport failed: {fallback})"
         line = {
-            "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak" if reps > 1 else "strong", "vs_baseline": None,
+            "metric": METRIC, "value": head["value"], "unit": "iterations/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+            "higher_is_better": True, "scaling": head["scaling"], "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (App. B generator, x* from mt19937_64(1))",
-            "config": cfg,
-            "roofline": roof,
-            "kernels": kernels,
-            "per_variant": per,
-            "gpu_launches": launches * world,  # every rank launches its own (counted on rank 0)
-            "e2e": e2e,
+            "config": head["config"],
+            "roofline": head["roofline"],
+            "iteration_roofline_frac": head["iteration_roofline_frac"],
+            "kernels": head["kernels"],
+            "per_variant": head["per_variant"],
+            "gpu_launches": head["gpu_launches"] + sum(d["gpu_launches"] for d in extras.values()),
+            "e2e": head["e2e"],
             "cpu_baseline": cpu,
-            "clocks": clk,
+            "clocks": head["clocks"],
         }
+        if extras:
+            line["per_config"] = {c: {k: d[k] for k in ("value", "ms_per_step", "config", "roofline",
+                                                         "iteration_roofline_frac", "per_variant", "kernels",
+                                                         "gpu_launches", "e2e", "clocks", "cpu_baseline")
+                                      if k in d} for c, d in extras.items()}
         print(json.dumps(line), flush=True)
     return 0
 
@@ -546,16 +669,24 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "p128"), choices=["p2d", "p64", "p128", "v256", "r4m"])
+    ap.add_argument("--per-config", default=os.environ.get("BENCH_PER_CONFIG", "v256,r4m"),
+                    help="further single-GPU configs measured after the headline one (own roofline, e2e, "
+                         "clocks, single-core CPU baseline each); '' for none")
     ap.add_argument("--cpu-steps", type=int, default=10)
+    ap.add_argument("--cpu-reps", type=int, default=3)
+    ap.add_argument("--cpu-worker", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-reps", type=int, default=2, help="timed end-to-end sweeps; the fastest is reported")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-single-core", action="store_true")
     ap.add_argument("--nccl", action="store_true",
                     help="row-partitioned path over NCCL even at one rank (transport check)")
     ap.add_argument("--emulate-ranks", type=int, default=1,
                     help="row-partitioned solve with P in-process ranks on one GPU")
     args = ap.parse_args()
+    if args.cpu_worker:
+        return cpu_worker(args)
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps
     rank, local, world, dist = dist_init()

@@ -88,17 +88,13 @@ enum {
     CGVK_MATRIX_CHECK_SYMMETRIC = 1, /* is_symmetric (src/sparse_matrix.cpp:84-107) */
     CGVK_MATRIX_ENGINE_CSR = 2,      /* SpMV kernels: TMA-staged CSR tiles only */
     CGVK_MATRIX_ENGINE_BAND = 4,     /* SpMV kernels: band engine whenever it applies */
-    CGVK_MATRIX_ENGINE_SEG = 8,      /* SpMV kernels: segment-window engine whenever it applies */
-    CGVK_MATRIX_ENGINE_CSR16 = 16,   /* SpMV kernels: CSR with 16-bit tile-offset columns */
 };
 
 /* SpMV engine of a matrix (cgvk_matrix_engine). Without an ENGINE flag the
  * band engine (SELL-C-sigma + shared-memory x window) is chosen when every
  * tile's columns lie within a narrow band and rows are long; otherwise CSR
- * with x gathered through L1/L2. The segment-window engine (TMA-staged CSR
- * with 16-bit columns into the x tiles staged with each tile; needs all
- * columns within at most 8 tile offsets, e.g. stencils) is opt-in. */
-enum { CGVK_ENGINE_CSR = 0, CGVK_ENGINE_BAND = 1, CGVK_ENGINE_SEG = 2, CGVK_ENGINE_CSR16 = 3 };
+ * with x gathered through L1/L2. */
+enum { CGVK_ENGINE_CSR = 0, CGVK_ENGINE_BAND = 1 };
 
 /* POD mirror of VariantConfig (inc/variants.hpp:34-57). */
 typedef struct cgvk_variant_config {
@@ -150,8 +146,7 @@ int cgvk_matrix_create_csr(int64_t n, const int64_t* row_ptr, const int64_t* col
 int cgvk_matrix_destroy(cgvk_matrix a);
 int cgvk_matrix_info(cgvk_matrix a, int64_t* n, int64_t* nnz, int* device);
 /* Engine the variant SpMV kernels use for `a` and, for the band engine, the
- * x-window half-width in 256-row tiles (segment engine: the number of tile
- * offsets; 0 for CSR). */
+ * x-window half-width in 256-row tiles (0 for CSR). */
 int cgvk_matrix_engine(cgvk_matrix a, int* engine, int* band_tiles);
 
 /* spmv (inc/sparse_matrix.hpp:41-42, src/sparse_matrix.cpp:109-118): y = A*x,
@@ -205,7 +200,11 @@ int cgvk_solver_status(cgvk_solver s, cgvk_solve_status* st, cgvk_scalars* sc,
 int cgvk_solver_get_vector(cgvk_solver s, int which, double* out);
 /* ||b - A x_k|| with a fresh device spmv (diagnostics.cpp:19-24). */
 int cgvk_solver_true_residual(cgvk_solver s, double* out);
-/* sqrt(<r_j,r_j>) for j = 0..k as recorded on the device each iteration. */
+/* sqrt(<r_j,r_j>) for j = 0..k as recorded on the device each iteration.
+ * The device records the first CGVK_HISTORY_CAP entries (j < 131072); *len =
+ * min(k + 1, CGVK_HISTORY_CAP), so a longer solve is visible to the caller as
+ * *len < k + 1 (the Python and C++ mirrors raise on it). */
+#define CGVK_HISTORY_CAP (1 << 17)
 int cgvk_solver_history(cgvk_solver s, double* out, int cap, int* len);
 /* The stream the solver enqueues on (cudaStream_t), for event timing. */
 void* cgvk_solver_stream(cgvk_solver s);

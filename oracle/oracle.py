@@ -217,10 +217,11 @@ class Reference(_SolverBase):
     """cgv_ref::SolverState driven through the reference's own initialize/step."""
 
     def __init__(self, A, variant: int, precond: int, b, x0, nu_expr: int = -1,
-                 recompute_nu=True, recompute_w=True, unsimplified_mu=False, track_delta=False):
+                 recompute_nu=True, recompute_w=True, unsimplified_mu=False, track_delta=False,
+                 mat: "RefMatrix | None" = None):
         if _ref is None:
             raise ImportError("oracle/_ref/libcgvref.so not built")
-        self._mat = RefMatrix(A)
+        self._mat = mat if mat is not None else RefMatrix(A)  # A borrowed, as the reference does
         b, x0 = _f64(b), _f64(x0)
         self._keep = (b, x0)
         err = C.c_int()

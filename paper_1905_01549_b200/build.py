@@ -25,7 +25,7 @@ NVFLAGS = ["-std=c++17", "-O3", "-lineinfo", "--fmad=false", "-Xcompiler", "-fPI
 
 CUDA_SOURCES = ["cgvk_api.cu"]
 CUDA_DEPS = ["cgvk_api.cu", "cgvk_device.cuh", "cgvk_variants.cuh", "cgvk_generic.cuh",
-             "cgvk_stream.cuh", "cgvk_dist.cuh", "cgvk_group.inc", "cgvk_persist.cuh", "cgvk_band.cuh", "cgvk_run.inc"]
+             "cgvk_stream.cuh", "cgvk_dist.cuh", "cgvk_group.inc", "cgvk_band.cuh", "cgvk_run.inc"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:
@@ -72,31 +72,19 @@ def build_cpp_shim(force: bool = False) -> str:
     return out
 
 
-def build_mtx_tool(force: bool = False) -> str:
-    """Host-only driver of the shim's Matrix Market reader (tests/test_matrix_market.py)."""
-    cpp = os.path.join(PKG, "cpp")
-    out = os.path.join(cpp, "mtx_tool")
-    src = os.path.join(cpp, "mtx_tool.cpp")
-    deps = [src, os.path.join(cpp, "cgvariants", "matrix_market.hpp"), os.path.join(cpp, "cgvariants", "cgv.hpp")]
-    if force or _stale(out, deps):
-        _run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-I", cpp, "-I", INCLUDE, "-o", out, src,
-              "-L", PKG, "-lcgvk", "-Wl,-rpath,$ORIGIN/.."])
-    return out
-
-
-def build_oracle() -> None:
+def build_oracle(force: bool = False) -> None:
     oracle = os.path.join(ROOT, "oracle")
-    _run(["make", "-s", "-C", oracle, "restatement"])
+    flags = ["-B"] if force else []
+    _run(["make", "-s", *flags, "-C", oracle, "restatement"])
     if os.path.isdir("/root/reference/proj/src"):
-        _run(["make", "-s", "-C", oracle, "ref"])
+        _run(["make", "-s", *flags, "-C", oracle, "ref"])
 
 
 def build_all(force: bool = False) -> None:
     build_gen(force)
     build_cuda(force)
     build_cpp_shim(force)
-    build_mtx_tool(force)
-    build_oracle()
+    build_oracle(force)
 
 
 if __name__ == "__main__":

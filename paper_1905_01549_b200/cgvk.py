@@ -23,6 +23,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CGVK_LIB") or os.path.join(_HERE, "libcgvk.so")  # CGVK_LIB: A/B builds
 
 
+HISTORY_CAP = 1 << 17  # CGVK_HISTORY_CAP (include/cgvk.h)
+
+
 class CgvkError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"cgvk error {code}: {msg}")
@@ -298,7 +301,7 @@ class VariantConfig:
 class DeviceMatrix:
     """SparseMatrix resident on one GPU (int32 CSR + fp64 values)."""
 
-    ENGINES = {None: 0, "csr": 2, "band": 4, "seg": 8, "csr16": 16}
+    ENGINES = {None: 0, "csr": 2, "band": 4}
 
     def __init__(self, n: int, row_ptr, col_idx, values, device: int = 0,
                  check_symmetric: bool = False, engine: str | None = None):
@@ -330,7 +333,7 @@ class DeviceMatrix:
         tiles; seg: number of staged x-tile offsets; csr: 0)."""
         e, h = C.c_int(), C.c_int()
         _check(_lib.cgvk_matrix_engine(self._h, C.byref(e), C.byref(h)))
-        return ("csr", "band", "seg", "csr16")[e.value], h.value
+        return ("csr", "band")[e.value], h.value
 
     @property
     def handle(self):
@@ -503,6 +506,8 @@ class Solver:
         _check(_lib.cgvk_solver_history(self._h, None, 0, C.byref(ln)))
         out = np.empty(max(ln.value, 1))
         _check(_lib.cgvk_solver_history(self._h, _ptr(out), ln.value, C.byref(ln)))
+        if self._h and self.k + 1 > ln.value and ln.value == HISTORY_CAP:
+            raise CgvkError(-1, f"residual history holds the first {HISTORY_CAP} iterations; k = {self.k}")
         return out[: ln.value]
 
     def stream(self) -> int:

@@ -8,8 +8,10 @@
 #include "cgvariants/vector_ops.hpp"
 
 #include <cstdio>
+#include <cstring>
 #include <functional>
 #include <random>
+#include <thread>
 
 using namespace cgv;
 
@@ -214,8 +216,71 @@ static void test_run_probes() {  // runner.cpp:32-147 + diagnostics.cpp on the d
                     std::invalid_argument);
 }
 
-int main() {
+// host-only: no device call (run on CPU by tests/test_cpp_shim.py --host)
+static void test_csr_from_triplets() {  // sparse_matrix.hpp:25-27
+    // unsorted input, a repeated position summed in input order, an exact-zero sum dropped
+    const SparseMatrix a = csr_from_triplets(3, {{2, 1, 1.0}, {0, 2, 0.5}, {0, 0, 1e16}, {1, 1, 3.0},
+                                                 {0, 0, 1.0}, {2, 0, 2.0}, {0, 0, -1e16}, {1, 0, 7.0},
+                                                 {1, 0, -7.0}});
+    // row 0: (1e16 + 1) + -1e16 == 0 -> dropped; row 1: 7 + -7 == 0 -> dropped
+    CHECK((a.row_ptr == std::vector<Index>{0, 1, 2, 4}));
+    CHECK((a.col_idx == std::vector<Index>{2, 1, 0, 1}));
+    CHECK((a.values == std::vector<double>{0.5, 3.0, 2.0, 1.0}));
+    // duplicates fold in input order, not sorted by value
+    volatile double p1 = 0.1, p2 = 0.2, p3 = -0.3;
+    const SparseMatrix c = csr_from_triplets(1, {{0, 0, 0.1}, {0, 0, 0.2}, {0, 0, -0.3}});
+    const SparseMatrix d = csr_from_triplets(1, {{0, 0, -0.3}, {0, 0, 0.2}, {0, 0, 0.1}});
+    CHECK(c.nnz() == 1 && c.values[0] == (p1 + p2) + p3);
+    CHECK(d.nnz() == 1 && d.values[0] == (p3 + p2) + p1 && c.values[0] != d.values[0]);
+    CHECK_THROWS_AS(csr_from_triplets(2, {{0, 2, 1.0}}), std::invalid_argument);
+    CHECK_THROWS_AS(csr_from_triplets(2, {{-1, 0, 1.0}}), std::invalid_argument);
+    const SparseMatrix e = csr_from_triplets(4, {});
+    CHECK((e.row_ptr == std::vector<Index>{0, 0, 0, 0, 0}) && e.nnz() == 0);
+    const DenseVector x{1.0, 2.0, 3.0}, y{4.0, 5.0, 6.0};
+    CHECK(dot(x, y) == ((0.0 + 4.0) + 10.0) + 18.0);
+    CHECK(norm2(x) == std::sqrt(14.0));
+    CHECK_THROWS_AS(dot(x, DenseVector{1.0}), std::invalid_argument);
+}
+
+static void test_shared_matrix_threads() {  // experiment.cpp:317-322: one A, concurrent solves
+    const SparseMatrix a = laplace2d(24);
+    const Preconditioner m = Preconditioner::jacobi(a);
+    const DenseVector b = spmv(a, random_vector(a.n, 5)), x0(a.n, 0.0);
+    const SparseMatrix fresh{a.n, a.row_ptr, a.col_idx, a.values, {}};  // not yet uploaded
+    std::vector<cgvk_matrix> handles(8);
+    std::vector<std::thread> th;
+    for (int i = 0; i < 8; ++i) th.emplace_back([&, i] { handles[i] = fresh.on_device(); });
+    for (auto& t : th) t.join();
+    for (int i = 1; i < 8; ++i) CHECK(handles[i] == handles[0]);  // one upload
+    // a copy owns its own device matrix: editing it changes its products only
+    SparseMatrix edited = a;
+    for (double& v : edited.values) v *= 2.0;
+    const DenseVector xa = random_vector(a.n, 6);
+    const DenseVector ya = spmv(a, xa), ye = spmv(edited, xa);
+    bool doubled = true;
+    for (std::size_t i = 0; i < ya.size(); ++i) doubled = doubled && ye[i] == 2.0 * ya[i];
+    CHECK(doubled);
+    CHECK(edited.on_device() != a.on_device());
+    // a Jacobi preconditioner is tied to its matrix and to its inv_diag as built
+    CHECK_THROWS_AS(initialize(VariantConfig::make(Variant::HS), edited, m, b, x0), std::invalid_argument);
+    Preconditioner tampered = m;
+    tampered.inv_diag[3] *= 2.0;
+    CHECK_THROWS_AS(initialize(VariantConfig::make(Variant::HS), a, tampered, b, x0), std::invalid_argument);
+    CHECK_THROWS_AS(run(VariantConfig::make(Variant::PR), a, tampered, b, x0, 5, StopRule::fixed(5), ProbeOptions{}),
+                    std::invalid_argument);
+    SolverState st = initialize(VariantConfig::make(Variant::HS), a, m, b, x0);  // the untouched one is fine
+    CHECK(st.status.running());
+}
+
+int main(int argc, char** argv) {
+    if (argc > 1 && std::strcmp(argv[1], "--host") == 0) {
+        test_csr_from_triplets();
+        std::printf("[%s] csr_from_triplets\n%d checks, %d failures\n", g_fail ? "FAIL" : "ok", g_checks, g_fail);
+        return g_fail ? 1 : 0;
+    }
     const std::pair<const char*, std::function<void()>> tests[] = {
+        {"csr_from_triplets", test_csr_from_triplets},
+        {"shared_matrix_threads", test_shared_matrix_threads},
         {"initialize_identity", test_initialize_identity},
         {"one_step_identity", test_one_step_identity},
         {"cg_cg_equals_hs", test_cg_cg_equals_hs},

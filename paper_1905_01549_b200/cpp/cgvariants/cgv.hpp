@@ -17,8 +17,11 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <cstdint>
 #include <memory>
+#include <mutex>
+#include <numeric>
 #include <optional>
 #include <span>
 #include <stdexcept>
@@ -51,75 +54,106 @@ struct SolverHandle {
 }  // namespace detail
 
 // ------------------------------------------------------------ vector ops
-// inc/vector_ops.hpp:15-54 (host reference kernels, sequential order)
+// inc/vector_ops.hpp:15-54 (host helpers; the solver's own dots run on the
+// device in its canonical reduction order). inner_product accumulates left to
+// right, init + x0*y0 + x1*y1 + ..., each product rounded (built with
+// -ffp-contract=off like the reference).
 
-inline void require_same_size(std::size_t a, std::size_t b) {
-    if (a != b) throw std::invalid_argument("vector dimension mismatch");
-}
 inline double dot(std::span<const double> x, std::span<const double> y) {
-    require_same_size(x.size(), y.size());
-    double acc = 0.0;
-    for (std::size_t i = 0; i < x.size(); ++i) acc += x[i] * y[i];
-    return acc;
+    if (x.size() != y.size()) throw std::invalid_argument("dot: operands differ in length");
+    return std::inner_product(x.begin(), x.end(), y.begin(), 0.0);
 }
 inline double norm2(std::span<const double> x) { return std::sqrt(dot(x, x)); }
 
 // --------------------------------------------------------- sparse matrix
 // inc/sparse_matrix.hpp:16-57
 
+namespace detail {
+// The device copy of a SparseMatrix, uploaded once under a lock (solvers on
+// several threads may share one A, src/experiment.cpp:317-322). A copied
+// matrix starts without one: its arrays may be edited before its first use.
+struct DeviceSlot {
+    std::shared_ptr<MatrixHandle> handle;
+    std::unique_ptr<std::mutex> lock = std::make_unique<std::mutex>();
+    DeviceSlot() = default;
+    DeviceSlot(const DeviceSlot&) : lock(std::make_unique<std::mutex>()) {}
+    DeviceSlot& operator=(const DeviceSlot&) {
+        const std::lock_guard<std::mutex> g(*lock);
+        handle.reset();
+        return *this;
+    }
+    DeviceSlot(DeviceSlot&&) noexcept = default;
+    DeviceSlot& operator=(DeviceSlot&&) noexcept = default;
+};
+}  // namespace detail
+
 struct SparseMatrix {
     Index n = 0;
     std::vector<Index> row_ptr;
     std::vector<Index> col_idx;
     std::vector<double> values;
-    mutable std::shared_ptr<detail::MatrixHandle> device;  // addition
+    mutable detail::DeviceSlot device;  // addition
 
     Index nnz() const { return static_cast<Index>(values.size()); }
 
     cgvk_matrix on_device(int gpu = 0) const {
-        if (!device) {
+        const std::lock_guard<std::mutex> g(*device.lock);
+        if (!device.handle) {
             if (row_ptr.size() != static_cast<std::size_t>(n) + 1)
                 throw std::invalid_argument("row_ptr length must be n+1");
             auto h = std::make_shared<detail::MatrixHandle>();
             detail::check(cgvk_matrix_create_csr(n, row_ptr.data(), col_idx.data(), values.data(),
                                                  gpu, 0, &h->h));
-            device = h;
+            device.handle = std::move(h);
         }
-        return device->h;
+        return device.handle->h;
     }
 };
 
 using Triplet = std::tuple<Index, Index, double>;
 
-// duplicates summed in input order, exact zeros dropped (sparse_matrix.hpp:25-27)
+// sparse_matrix.hpp:25-27: entries ordered by (row, column); repeated
+// positions summed in the order they were given; sums that are exactly zero
+// are not stored. Rows are bucketed with a counting pass (which keeps the
+// input order inside each row), then each row's entries are ordered by
+// column with a stable sort and folded.
 inline SparseMatrix csr_from_triplets(Index n, std::vector<Triplet> t) {
-    std::stable_sort(t.begin(), t.end(), [](const Triplet& a, const Triplet& b) {
-        return std::tie(std::get<0>(a), std::get<1>(a)) < std::tie(std::get<0>(b), std::get<1>(b));
-    });
+    if (n < 0) throw std::invalid_argument("csr_from_triplets: negative dimension");
+    for (const Triplet& e : t)
+        if (std::get<0>(e) < 0 || std::get<0>(e) >= n || std::get<1>(e) < 0 || std::get<1>(e) >= n)
+            throw std::invalid_argument("csr_from_triplets: entry outside the n x n matrix");
+    const auto rows = static_cast<std::size_t>(n);
+    std::vector<std::size_t> start(rows + 1, 0), order(t.size());
+    for (const Triplet& e : t) ++start[static_cast<std::size_t>(std::get<0>(e)) + 1];
+    std::partial_sum(start.begin(), start.end(), start.begin());
+    {
+        std::vector<std::size_t> fill(start.begin(), start.end() - 1);
+        for (std::size_t q = 0; q < t.size(); ++q) order[fill[static_cast<std::size_t>(std::get<0>(t[q]))]++] = q;
+    }
     SparseMatrix a;
     a.n = n;
-    a.row_ptr.assign(static_cast<std::size_t>(n) + 1, 0);
-    for (std::size_t i = 0; i < t.size();) {
-        const auto [r, c, v0] = t[i];
-        if (r < 0 || r >= n || c < 0 || c >= n) throw std::invalid_argument("triplet index out of range");
-        double sum = v0;
-        std::size_t j = i + 1;
-        for (; j < t.size() && std::get<0>(t[j]) == r && std::get<1>(t[j]) == c; ++j)
-            sum += std::get<2>(t[j]);
-        if (sum != 0.0) {
-            a.col_idx.push_back(c);
-            a.values.push_back(sum);
-            ++a.row_ptr[static_cast<std::size_t>(r) + 1];
+    a.row_ptr.reserve(rows + 1);
+    a.row_ptr.push_back(0);
+    for (std::size_t r = 0; r < rows; ++r) {
+        const auto first = order.begin() + static_cast<std::ptrdiff_t>(start[r]);
+        const auto last = order.begin() + static_cast<std::ptrdiff_t>(start[r + 1]);
+        std::stable_sort(first, last, [&t](std::size_t p, std::size_t q) { return std::get<1>(t[p]) < std::get<1>(t[q]); });
+        for (auto it = first; it != last;) {
+            const Index col = std::get<1>(t[*it]);
+            double acc = std::get<2>(t[*it]);
+            for (++it; it != last && std::get<1>(t[*it]) == col; ++it) acc += std::get<2>(t[*it]);
+            if (acc == 0.0) continue;
+            a.col_idx.push_back(col);
+            a.values.push_back(acc);
         }
-        i = j;
+        a.row_ptr.push_back(static_cast<Index>(a.values.size()));
     }
-    for (Index r = 0; r < n; ++r) a.row_ptr[r + 1] += a.row_ptr[r];
     return a;
 }
 
 // validated on the device (cgvk_matrix_create_csr runs validate_csr there)
 inline void validate_csr(const SparseMatrix& a) {
-    SparseMatrix copy{a.n, a.row_ptr, a.col_idx, a.values, nullptr};
+    const SparseMatrix copy{a.n, a.row_ptr, a.col_idx, a.values, {}};
     copy.on_device();
 }
 
@@ -155,11 +189,30 @@ inline void block_spmv(const SparseMatrix& a, std::span<const double> x1, std::s
 // ---------------------------------------------------------- preconditioner
 // inc/preconditioner.hpp:13-28
 
+namespace detail {
+inline std::uint64_t digest(const std::vector<double>& v) {
+    std::uint64_t h = 0x9e3779b97f4a7c15ull;
+    for (const double d : v) {
+        std::uint64_t bits;
+        std::memcpy(&bits, &d, sizeof bits);
+        h = (h ^ bits) * 0x100000001b3ull;
+    }
+    return h;
+}
+}  // namespace detail
+
+// The device solver applies Jacobi as 1/diag(A) of the solver's own matrix
+// (recomputed there bit-identically to Preconditioner::jacobi). A Jacobi
+// preconditioner is therefore accepted only for the matrix it was built from
+// and with inv_diag as built; anything else is rejected with
+// std::invalid_argument rather than silently solving a different system
+// (INTEGRATION.md §3).
 struct Preconditioner {
     enum class Kind { Identity, Jacobi };
     Kind kind = Kind::Identity;
     std::vector<double> inv_diag;
     const SparseMatrix* source = nullptr;  // addition: the matrix it was built from
+    std::uint64_t built_digest = 0;        // addition: digest(inv_diag) at construction
 
     static Preconditioner identity() { return Preconditioner{}; }
     static Preconditioner jacobi(const SparseMatrix& a) {
@@ -168,7 +221,20 @@ struct Preconditioner {
         m.source = &a;
         m.inv_diag.resize(static_cast<std::size_t>(a.n));
         detail::check(cgvk_jacobi(a.on_device(), m.inv_diag.data()));
+        m.built_digest = detail::digest(m.inv_diag);
         return m;
+    }
+    // CGVK_PRECOND_* for a solve with `a`; throws when the device would not
+    // apply exactly this preconditioner.
+    int device_kind_for(const SparseMatrix& a) const {
+        if (kind == Kind::Identity) return CGVK_PRECOND_IDENTITY;
+        if (inv_diag.size() != static_cast<std::size_t>(a.n))
+            throw std::invalid_argument("preconditioner dimension mismatch");
+        if (source != &a)
+            throw std::invalid_argument("Jacobi preconditioner was built from a different matrix");
+        if (detail::digest(inv_diag) != built_digest)
+            throw std::invalid_argument("Jacobi inv_diag was modified after construction");
+        return CGVK_PRECOND_JACOBI;
     }
     void apply(std::span<const double> in, std::span<double> out) const {
         if (in.size() != out.size()) throw std::invalid_argument("preconditioner dimension mismatch");
@@ -312,8 +378,7 @@ inline SolverState initialize(const VariantConfig& config, const SparseMatrix& a
     config.validate();
     if (b.size() != static_cast<std::size_t>(a.n) || x0.size() != static_cast<std::size_t>(a.n))
         throw std::invalid_argument("right-hand side or initial guess dimension mismatch");
-    if (m.kind == Preconditioner::Kind::Jacobi && m.inv_diag.size() != static_cast<std::size_t>(a.n))
-        throw std::invalid_argument("preconditioner dimension mismatch");
+    const int precond = m.device_kind_for(a);
     SolverState st;
     st.config = config;
     st.a = &a;
@@ -322,9 +387,7 @@ inline SolverState initialize(const VariantConfig& config, const SparseMatrix& a
     st.n = a.n;
     st.device = std::make_shared<detail::SolverHandle>();
     const cgvk_variant_config c = config.to_c();
-    detail::check(cgvk_solver_create(a.on_device(), &c, st.preconditioned ? CGVK_PRECOND_JACOBI
-                                                                           : CGVK_PRECOND_IDENTITY,
-                                     b.data(), x0.data(), &st.device->h));
+    detail::check(cgvk_solver_create(a.on_device(), &c, precond, b.data(), x0.data(), &st.device->h));
     st.refresh();
     return st;
 }
@@ -415,6 +478,7 @@ inline ConvergenceHistory run(const VariantConfig& config, const SparseMatrix& a
         throw std::invalid_argument("right-hand side or initial guess dimension mismatch");
     if (probe_opts.x_star && probe_opts.x_star->size() != n)
         throw std::invalid_argument("x* dimension mismatch");
+    const int precond = m.device_kind_for(a);
     const cgvk_variant_config c = config.to_c();
     const cgvk_stop_rule sr{static_cast<int>(stop.kind), stop.fixed_count, stop.error_threshold,
                             stop.stagnation_window, stop.stagnation_improvement};
@@ -424,8 +488,7 @@ inline ConvergenceHistory run(const VariantConfig& config, const SparseMatrix& a
     int nrec = 0;
     cgvk_solve_status fs{};
     cgvk_summary sm{};
-    detail::check(cgvk_run(a.on_device(), &c, m.is_identity() ? CGVK_PRECOND_IDENTITY : CGVK_PRECOND_JACOBI,
-                           b.data(), x0.data(), max_iter, &sr, &po, recs.data(), static_cast<int>(recs.size()),
+    detail::check(cgvk_run(a.on_device(), &c, precond, b.data(), x0.data(), max_iter, &sr, &po, recs.data(), static_cast<int>(recs.size()),
                            &nrec, &fs, &sm, nullptr));
     ConvergenceHistory h;
     h.config = config;

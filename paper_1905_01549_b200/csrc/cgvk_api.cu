@@ -5,7 +5,6 @@
 #include "cgvk_generic.cuh"
 #include "cgvk_variants.cuh"
 #include "cgvk_dist.cuh"
-#include "cgvk_persist.cuh"
 #include "cgvk_band.cuh"
 
 #include <cub/device/device_scan.cuh>
@@ -159,11 +158,6 @@ struct cgvk_matrix_s {
     double* band_va = nullptr;
     unsigned short* band_ci = nullptr;
     int64_t band_entries = 0;
-    // segment-window engine (cgvk_stream.cuh SEG): tile offsets + 16-bit columns
-    int seg_nd = 0;
-    int seg_mode = 0;  // 1: x tiles staged (segment engine), 2: 16-bit columns, x via L1 (csr16)
-    int seg_d[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    unsigned short* ci16 = nullptr;
     double* inv_diag = nullptr;  // built on first use
     int jacobi_state = 0;        // 0 not built, 1 ok, -1 missing/non-positive diagonal
     cudaStream_t stream = nullptr;
@@ -188,9 +182,6 @@ struct cgvk_matrix_s {
         P.band_va = band_va;
         P.band_ci = band_ci;
         P.band_h = band_h;
-        P.ci16 = ci16;
-        P.seg_nd = seg_nd;
-        for (int q = 0; q < 8; ++q) P.seg_d[q] = seg_d[q];
         P.order = order;
         P.l2pol = l2pol;
         return P;
@@ -329,54 +320,6 @@ __global__ void k_fill_band(int n, const int* __restrict__ rp, const int* __rest
             bci[base + 32 * e] = (unsigned short)(ci[k] - wb);
         }
     }
-}
-
-// Segment-window layout: the set D of tile offsets (tile(col) - tile(row))
-// over the whole matrix; applicable when |D| <= 8 (a 7-point stencil has
-// {-N^2/256, -1, 0, 1, N^2/256} for N^2 a multiple of 256).
-constexpr int kSegMax = 8;
-
-int seg_offsets(int64_t n, const int64_t* row_ptr, const int64_t* col_idx, int* d) {
-    int nd = 0;
-    for (int64_t i = 0; i < n; ++i) {
-        const int64_t t = i / kBlock;
-        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
-            const int64_t off = col_idx[k] / kBlock - t;
-            int q = 0;
-            while (q < nd && d[q] != off) ++q;
-            if (q == nd) {
-                if (nd == kSegMax) return -1;
-                d[nd++] = (int)off;
-            }
-        }
-    }
-    std::sort(d, d + nd);
-    return nd;
-}
-
-__global__ void k_fill_ci16(int n, const int* __restrict__ rp, const int* __restrict__ ci, int nd, Params P,
-                            unsigned short* out) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int t = i / kBlock;
-        for (int k = rp[i]; k < rp[i + 1]; ++k) {
-            const int off = ci[k] / kBlock - t;
-            int q = 0;
-            while (q < nd - 1 && P.seg_d[q] != off) ++q;
-            out[k] = (unsigned short)(q * kBlock + (ci[k] & (kBlock - 1)));
-        }
-    }
-}
-
-int build_seg(cgvk_matrix a, const int* d, int nd) {
-    a->seg_nd = nd;
-    for (int q = 0; q < nd; ++q) a->seg_d[q] = d[q];
-    TRY(dalloc(&a->ci16, a->nnz + 32));
-    CK(cudaMemsetAsync(a->ci16, 0, 2 * (a->nnz + 32), a->stream));
-    if (a->n > 0)
-        k_fill_ci16<<<grid_elem(a->n), 256, 0, a->stream>>>((int)a->n, a->rp, a->ci, nd, a->base(), a->ci16);
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(a->stream));
-    return CGVK_OK;
 }
 
 // Built on the device (a host sort of every tile cost ~200 ms on R4M).
@@ -597,15 +540,10 @@ int matrix_create(int64_t n, int64_t ncols, const int64_t* row_ptr, const int64_
     // matrix with a narrow band and long rows, else the CSR tile pipeline.
     // Flags choose explicitly; CGVK_SPMV_ENGINE=csr|band overrides (A/B runs).
     {
-        int want = (flags & CGVK_MATRIX_ENGINE_CSR) ? 0
-                   : (flags & CGVK_MATRIX_ENGINE_BAND) ? 1
-                   : (flags & CGVK_MATRIX_ENGINE_SEG) ? 2
-                   : (flags & CGVK_MATRIX_ENGINE_CSR16) ? 3 : -1;
+        int want = (flags & CGVK_MATRIX_ENGINE_CSR) ? 0 : (flags & CGVK_MATRIX_ENGINE_BAND) ? 1 : -1;
         const char* eng = getenv("CGVK_SPMV_ENGINE");
         if (eng && strcmp(eng, "csr") == 0) want = 0;
         if (eng && strcmp(eng, "band") == 0) want = 1;
-        if (eng && strcmp(eng, "seg") == 0) want = 2;
-        if (eng && strcmp(eng, "csr16") == 0) want = 3;
         if ((want == -1 || want == 1) && ncols == n && n > 0) {
             const bool long_rows = nnz >= (int64_t)env_int("CGVK_BAND_MIN_ROW", 16) * n;
             const int H = (want == 1 || long_rows) ? band_half_width(a) : -1;
@@ -613,14 +551,6 @@ int matrix_create(int64_t n, int64_t ncols, const int64_t* row_ptr, const int64_
                 if ((rc = build_band(a, H)) != CGVK_OK) return bail(rc);
                 a->order = 1;  // the band kernels walk contiguous tile runs
             }
-        }
-        // measured: on P128 the segment engine's extra x-tile
-        // copies starve its TMA ring (3.0 vs 4.3 TB/s), so it is opt-in only
-        if ((want == 2 || want == 3) && a->band_h < 0 && ncols == n && n > 0) {
-            int d[kSegMax];
-            const int nd = seg_offsets(n, row_ptr, col_idx, d);
-            if (nd > 0 && (rc = build_seg(a, d, nd)) != CGVK_OK) return bail(rc);
-            if (nd > 0) a->seg_mode = want == 2 ? 1 : 2;
         }
     }
     // Canonical virtual CTAs (reduction_config): the CSR engine's kernels run
@@ -652,7 +582,6 @@ int cgvk_matrix_destroy(cgvk_matrix a) {
     dfree(a->band_meta);
     dfree(a->band_va);
     dfree(a->band_ci);
-    dfree(a->ci16);
     dfree(a->inv_diag);
     dfree(a->send_lo);
     dfree(a->send_hi);
@@ -677,10 +606,8 @@ int cgvk_matrix_info(cgvk_matrix a, int64_t* n, int64_t* nnz, int* device) {
 int cgvk_matrix_engine(cgvk_matrix a, int* engine, int* band_tiles) {
     if (!a) return set_err(CGVK_EINVAL, "null matrix");
     if (engine)
-        *engine = a->band_h >= 0 ? CGVK_ENGINE_BAND
-                  : a->seg_nd > 0 ? (a->seg_mode == 1 ? CGVK_ENGINE_SEG : CGVK_ENGINE_CSR16)
-                                  : CGVK_ENGINE_CSR;
-    if (band_tiles) *band_tiles = a->band_h >= 0 ? a->band_h : a->seg_nd;
+        *engine = a->band_h >= 0 ? CGVK_ENGINE_BAND : CGVK_ENGINE_CSR;
+    if (band_tiles) *band_tiles = a->band_h >= 0 ? a->band_h : 0;
     return CGVK_OK;
 }
 
@@ -876,8 +803,6 @@ struct cgvk_solver_s {
     int k_target = 0;
     KLaunch k1, k2;
     KLaunch k1c0, k1c, k2c, kt;  // chained schedule (graphs): see chain_prologue
-    KLaunch kp;            // persistent cooperative kernel (both phases, all iterations)
-    bool persist = false;  // step() uses kp instead of graph replays
     cudaGraphExec_t g1 = nullptr, g8 = nullptr;  // 1- and gn-iteration graphs
     int gn = 8;
     Params P{};
@@ -982,26 +907,13 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
     StageCfg S{};
     S.nvec = Op::NV;
     S.cap = Op::CSR ? a->cap : 0;
-    int seg = 0;
-    if constexpr (Op::CSR) {  // 16-bit-column engines
-        if (a->seg_nd > 0) {
-            seg = a->seg_mode;
-            S.nd = a->seg_nd;
-            if (seg == 1) {  // x tiles staged with the tile
-                L->fn = k_stream<Op, Prev, CGVK_SPMV_MIN_CTAS, 1>;
-                S.ng = Op::NG;
-            } else {
-                L->fn = k_stream<Op, Prev, CGVK_SPMV_MIN_CTAS, 2>;
-            }
-        }
-    }
     const int header = ((int)sizeof(PipeHeader) + 127) & ~127;
     if (Op::CSR) {  // two stages must fit one CTA: tiles beyond the capacity go direct
         while (S.cap > 64 &&
-               header + 2 * ((stage_bytes_for(S.cap, S.nvec, true, S.nd, S.ng) + 127) & ~127) > kSmemPerSM - 1024)
+               header + 2 * ((stage_bytes_for(S.cap, S.nvec, true) + 127) & ~127) > kSmemPerSM - 1024)
             S.cap = (S.cap - S.cap / 8) & ~7;
     }
-    S.stage_bytes = (stage_bytes_for(S.cap, S.nvec, Op::CSR, S.nd, S.ng) + 127) & ~127;
+    S.stage_bytes = (stage_bytes_for(S.cap, S.nvec, Op::CSR) + 127) & ~127;
     S.gvirt = a->G;
     // stage budget: the SpMV kernels target CGVK_SPMV_MIN_CTAS resident CTAs,
     // the update kernels two
@@ -1013,10 +925,6 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
         // long rows: a 2-stage ring fills the SM -> one CTA with the full
         // register file (see k_stream's MINB)
         L->fn = k_stream<Op, Prev, 1>;
-        if constexpr (Op::CSR) {
-            if (seg == 1) L->fn = k_stream<Op, Prev, 1, 1>;
-            if (seg == 2) L->fn = k_stream<Op, Prev, 1, 2>;
-        }
         ctas = 1;
     }
     const int budget = kSmemPerSM / ctas - 2048;
@@ -1034,36 +942,6 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L->fn, kThreads, L->smem));
     if (occ < 1) return set_err(CGVK_ECUDA, "pipeline kernel does not fit on an SM");
-    L->grid = balanced_grid(a->G, occ * a->sms);
-    L->S = S;
-    if (env_int("CGVK_DEBUG", 0))
-        fprintf(stderr, "cgvk launch %s: occ %d/SM grid %d smem %zu nstage %d stage %d B\n", __func__, occ,
-                L->grid, L->smem, S.nstage, S.stage_bytes);
-    return CGVK_OK;
-}
-
-// The persistent kernel of the pair: union stage layout, cooperative launch,
-// grid = co-resident CTAs (balanced over the virtual CTAs).
-template <class Op1, class Op2>
-int make_persist(cgvk_matrix a, KLaunch* L) {
-    L->fn = k_persist<Op1, Op2>;
-    L->threads = kThreads;
-    StageCfg S{};
-    S.nvec = Op1::NV > Op2::NV ? Op1::NV : Op2::NV;
-    S.cap = (Op1::CSR || Op2::CSR) ? a->cap : 0;
-    S.stage_bytes = (stage_bytes_for(S.cap, S.nvec, S.cap > 0) + 127) & ~127;
-    S.gvirt = a->G;
-    const int header = ((int)sizeof(PipeHeader) + 127) & ~127;
-    int ns = (kSmemPerSM / env_int("CGVK_PERSIST_CTAS", 2) - 2048 - header) / S.stage_bytes;
-    if (ns < 2) ns = 2;
-    if (ns > 6) ns = 6;
-    S.nstage = ns;
-    L->smem = (size_t)header + (size_t)ns * S.stage_bytes;
-    if (L->smem > (size_t)kSmemPerSM - 1024) return set_err(CGVK_EINVAL, "persistent stage too large");
-    CK(cudaFuncSetAttribute(L->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L->smem));
-    int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L->fn, kThreads, L->smem));
-    if (occ < 1) return set_err(CGVK_ECUDA, "persistent kernel does not fit on an SM");
     L->grid = balanced_grid(a->G, occ * a->sms);
     L->S = S;
     if (env_int("CGVK_DEBUG", 0))
@@ -1090,13 +968,6 @@ int pick_pair(cgvk_matrix a, cgvk_solver s) {
     s->kt.threads = 32;
     s->kt.smem = 0;
     s->kt.S = s->k2.S;
-    // the experimental persistent kernel only when asked for (CGVK_PERSIST=1)
-    // and when its union stage fits; otherwise the graph path
-    s->kp = KLaunch{};
-    if (env_int("CGVK_PERSIST", 0) && a->band_h < 0 && make_persist<Op1, Op2>(a, &s->kp) != CGVK_OK) {
-        s->kp = KLaunch{};
-        g_err.clear();
-    }
     s->fin1 = k_finalize<Op1>;
     s->fin2 = k_finalize<Op2>;
     return CGVK_OK;
@@ -1114,7 +985,7 @@ int pick_kernels(cgvk_matrix a, int v, cgvk_solver s) {
     }
 }
 
-void launch(cgvk_solver s, const KLaunch& L);
+cudaError_t launch(cgvk_solver s, const KLaunch& L);
 
 // the reference's allocated_vectors() (src/variants.cpp:97-103) for the
 // vectors initialize() resizes (src/variants.cpp:354-444)
@@ -1137,7 +1008,7 @@ int ref_allocated(int v, bool prec) {
 // may start its prologue (barrier init, matrix prefetch) while the previous
 // kernel drains, and synchronises with griddepcontrol.wait before reading its
 // results. CGVK_PDL=0 turns it off (for A/B measurements).
-void launch(cgvk_solver s, const KLaunch& L) {
+cudaError_t launch(cgvk_solver s, const KLaunch& L) {
     // measured (profiles/r01): PDL gains 3-5 % on every variant; HS's kernels
     // signal their dependents late (PdlLate), else HS loses ~10 % to it
     static const int pdl_env = env_int("CGVK_PDL", -1);
@@ -1152,12 +1023,7 @@ void launch(cgvk_solver s, const KLaunch& L) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, L.fn, s->P, L.S);
-}
-
-void launch_iter(cgvk_solver s) {
-    launch(s, s->k1);
-    launch(s, s->k2);
+    return cudaLaunchKernelEx(&cfg, L.fn, s->P, L.S);
 }
 
 // The chained schedule is the default for graphs; CGVK_CHAIN=0 captures the
@@ -1176,20 +1042,29 @@ int graph_iters() {
 }
 
 int capture(cgvk_solver s, int iters, cudaGraphExec_t* exec) {
-    cudaGraph_t g;
     CK(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+    cudaError_t e = cudaSuccess;
     if (use_chain()) {
-        for (int i = 0; i < iters; ++i) {
-            launch(s, i ? s->k1c : s->k1c0);
-            launch(s, s->k2c);
+        for (int i = 0; i < iters && e == cudaSuccess; ++i) {
+            e = launch(s, i ? s->k1c : s->k1c0);
+            if (e == cudaSuccess) e = launch(s, s->k2c);
         }
-        launch(s, s->kt);
+        if (e == cudaSuccess) e = launch(s, s->kt);
     } else {
-        for (int i = 0; i < iters; ++i) launch_iter(s);
+        for (int i = 0; i < iters && e == cudaSuccess; ++i) {
+            e = launch(s, s->k1);
+            if (e == cudaSuccess) e = launch(s, s->k2);
+        }
     }
-    CK(cudaStreamEndCapture(s->stream, &g));
+    cudaGraph_t g = nullptr;
+    const cudaError_t e_end = cudaStreamEndCapture(s->stream, &g);  // always leave capture mode
+    struct GraphGuard {
+        cudaGraph_t g;
+        ~GraphGuard() { if (g) cudaGraphDestroy(g); }
+    } guard{g};
+    CK(e);
+    CK(e_end);
     CK(cudaGraphInstantiate(exec, g, 0));
-    CK(cudaGraphDestroy(g));
     return CGVK_OK;
 }
 
@@ -1371,7 +1246,7 @@ int materialize(cgvk_solver s) {
     TRY(refresh_mirror(s));
     if (!s->mirror.form_pending) return CGVK_OK;
     k_set_limit<<<1, 1, 0, s->stream>>>(s->ctrl, s->mirror.k);
-    launch(s, s->k1);
+    CK(launch(s, s->k1));
     k_set_limit<<<1, 1, 0, s->stream>>>(s->ctrl, s->k_target);
     CK(cudaGetLastError());
     return refresh_mirror(s);
@@ -1471,7 +1346,7 @@ int solver_alloc(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, cud
         free_solver(s);
         return code;
     };
-    s->hist_cap = 1 << 17;
+    s->hist_cap = CGVK_HISTORY_CAP;
     // + halo columns of a rank-local matrix; + 32: bulk copies of the last
     // tile round up to 16 bytes
     const int64_t nv = a->ncols + 32;
@@ -1569,7 +1444,6 @@ int cgvk_solver_create(cgvk_matrix a, const cgvk_variant_config* cfg, int precon
     if ((rc = capture(s, 1, &s->g1)) != CGVK_OK || (rc = capture(s, s->gn, &s->g8)) != CGVK_OK)
         return bail(rc);
     pt.mark("graphs");
-    s->persist = s->kp.fn != nullptr;  // CGVK_PERSIST=1 and the union stage fit (no band version)
     *out = s;
     return CGVK_OK;
 }
@@ -1599,22 +1473,8 @@ int cgvk_solver_step(cgvk_solver s, int n_iters) {
     CK(cudaSetDevice(s->a->device));
     s->k_target += n_iters;
     k_set_limit<<<1, 1, 0, s->stream>>>(s->ctrl, s->k_target);
-    if (s->persist) {  // all n iterations in one cooperative launch
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(s->kp.grid);
-        cfg.blockDim = dim3(s->kp.threads);
-        cfg.dynamicSmemBytes = s->kp.smem;
-        cfg.stream = s->stream;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeCooperative;
-        attr[0].val.cooperative = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        CK(cudaLaunchKernelEx(&cfg, s->kp.fn, s->P, s->kp.S));
-    } else {
-        for (int i = 0; i < n_iters / s->gn; ++i) CK(cudaGraphLaunch(s->g8, s->stream));
-        for (int i = 0; i < n_iters % s->gn; ++i) CK(cudaGraphLaunch(s->g1, s->stream));
-    }
+    for (int i = 0; i < n_iters / s->gn; ++i) CK(cudaGraphLaunch(s->g8, s->stream));
+    for (int i = 0; i < n_iters % s->gn; ++i) CK(cudaGraphLaunch(s->g1, s->stream));
     CK(cudaGetLastError());
     s->mirror_fresh = false;
     return CGVK_OK;
@@ -1716,7 +1576,6 @@ int cgvk_solver_launches_per_iter(cgvk_solver s) {
 long long cgvk_solver_launches(cgvk_solver s, int n_iters) {
     if (!s || n_iters <= 0) return 0;
     if (s->group) return 1 + (long long)group_launches_per_iter(s) * n_iters;
-    if (s->persist) return 2;
     const long long graphs = n_iters / s->gn + n_iters % s->gn;
     return 1 + 2LL * n_iters + (use_chain() ? graphs : 0);
 }
@@ -1757,9 +1616,9 @@ int cgvk_solver_profile(cgvk_solver s, int n_iters, double* k1_ms, double* k2_ms
     for (auto& e : ev) CK(cudaEventCreate(&e));
     for (int i = 0; i < n_iters; ++i) {
         CK(cudaEventRecord(ev[3 * i], s->stream));
-        launch(s, s->k1);
+        CK(launch(s, s->k1));
         CK(cudaEventRecord(ev[3 * i + 1], s->stream));
-        launch(s, s->k2);
+        CK(launch(s, s->k2));
         CK(cudaEventRecord(ev[3 * i + 2], s->stream));
     }
     CK(cudaGetLastError());

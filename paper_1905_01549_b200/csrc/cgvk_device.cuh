@@ -53,9 +53,7 @@ struct __align__(16) Ctrl {
     int wt_stored;    // pipe-PR: w~ lives in its buffer (nu'-terminal step)
     int hist_cap;
     unsigned int count[2];  // last-CTA arrival counters
-    unsigned int bar_count; // persistent kernel: grid barrier arrivals
-    unsigned int bar_gen;   // persistent kernel: grid barrier generation
-    unsigned int sched[2];  // dynamic virtual-CTA scheduler of the two kernels (next vb - Gp)
+    unsigned int spare_[4];
     // chained schedule (cgvk_stream.cuh chain_prologue): the folded totals of
     // the kernel that wrote this copy, for its successor's scalar tail
     double tot[kMaxDots];
@@ -87,11 +85,6 @@ struct Params {
     const double* __restrict__ band_va;
     const unsigned short* __restrict__ band_ci;   // column - (tile - band_h) * 256
     int band_h;                                   // window half-width in tiles
-    // segment-window engine (stencil-like matrices): every column of tile t
-    // lies in one of the tiles t + seg_d[q], q < seg_nd; ci16 = q * 256 + (col & 255)
-    const unsigned short* __restrict__ ci16;
-    int seg_nd;
-    int seg_d[8];
     double* part;  // [kMaxDots][G] CTA partials
     double* hist;  // rr per iteration (null: not recorded by this CTA)
     Ctrl* ctrl;

@@ -18,10 +18,8 @@
 // resident CTAs), so the result bits do not depend on how many CTAs fit on
 // the chip.
 //
-// Opt-in variants of the SpMV kernels (template SEG): 16-bit
-// tile-offset columns with x still through L1 (csr16), or with the x tiles
-// staged by TMA next to the tile (seg). The band engine (cgvk_band.cuh)
-// replaces this kernel for narrow-band long-row matrices.
+// The band engine (cgvk_band.cuh) replaces this kernel's SpMV form for
+// narrow-band long-row matrices.
 #pragma once
 
 #include "cgvk_device.cuh"
@@ -56,25 +54,6 @@ template <class T>
 struct HasDistMark<T, std::void_t<decltype(std::declval<const T&>().dist_mark(std::declval<const Params&>(),
                                                                                 std::declval<Ctrl*>()))>> {
     static constexpr bool value = true;
-};
-
-// Dynamic virtual-CTA scheduling (CGVK_DYN): a physical CTA runs its first
-// virtual CTA statically (the pre-wait matrix prefetch needs it) and then
-// grabs the next one from a counter, so CTAs that the memory system serves
-// more slowly take fewer virtual CTAs instead of setting the kernel's end.
-// Which physical CTA runs a virtual CTA does not change any bit: partials are
-// indexed by virtual CTA. Only for kernels that always count arrivals (the
-// last CTA resets the counter): an Op opts in with `ALWAYS_ARRIVES = true`.
-#ifndef CGVK_DYN
-#define CGVK_DYN 0
-#endif
-template <class T, class = void>
-struct DynOf {
-    static constexpr bool value = false;
-};
-template <class T>
-struct DynOf<T, std::void_t<decltype(T::ALWAYS_ARRIVES)>> {
-    static constexpr bool value = T::ALWAYS_ARRIVES && CGVK_DYN != 0;
 };
 
 // Optional per-Op shared-memory budget hint: `static constexpr int SMEM_CTAS`
@@ -124,8 +103,6 @@ struct StageCfg {
     int gvirt;      // Gv
     int ring;       // band engine: window ring tiles (2H + nstage)
     int pf;         // band engine: L2 prefetch distance (tiles)
-    int nd;         // segment engine: x tiles staged per gathered operand (0: CSR engine)
-    int ng;         // segment engine: gathered operands staged
     int chain;      // chained schedule: CH_* bits (0: last-CTA finish, in place)
 };
 
@@ -260,19 +237,6 @@ struct RowRef {
     }
 };
 
-// RowSeg: the segment engine's CSR row — the column stored as the 16-bit
-// index into the stage's staged x tiles (q * 256 + col % 256).
-struct RowSeg {
-    static constexpr int CH = kChunk;
-    const double* va;
-    const unsigned short* ci;
-    int len;
-    __device__ __forceinline__ void entry(int k, int& c, double& v) const {
-        c = ci[k];
-        v = va[k];
-    }
-};
-
 #ifndef CGVK_BAND_LD
 #define CGVK_BAND_LD 0  // slice loads: 0 ld.global.cs, 1 ld.global.nc, 2 ld.global.cg
 #endif
@@ -304,15 +268,13 @@ struct BandRow {
 };
 
 
-// Software-pipelined form (CGVK_ROW_PIPE=1, and always for the band engine,
-// whose matrix loads come from L2): the next chunk's column/value loads are
-// issued before the current chunk is gathered and accumulated.
-#ifndef CGVK_ROW_PIPE
-#define CGVK_ROW_PIPE 0
-#endif
+// Software-pipelined form (the band engine, whose matrix loads come from L2):
+// the next chunk's column/value loads are issued before the current chunk is
+// gathered and accumulated. The CSR engine reads its rows from the staged
+// shared-memory tile and does not pipeline (measured neutral-to-slower).
 template <class RR>
 struct RowPipe {
-    static constexpr bool value = CGVK_ROW_PIPE != 0;
+    static constexpr bool value = false;
 };
 template <int C>
 struct RowPipe<BandRow<C>> {
@@ -461,34 +423,6 @@ struct StagedIn {
     }
 };
 
-// RowD: CSR with 16-bit columns (q = offset slot << 8 | col % 256), decoded
-// against the tile's x-tile bases; x still gathered through L1/L2.
-struct RowD {
-    static constexpr int CH = kChunk;
-    const double* va;
-    const unsigned short* ci;
-    const int* base;  // stage header: (tile + seg_d[slot]) * 256
-    int len;
-    __device__ __forceinline__ void entry(int k, int& c, double& v) const {
-        const int q = ci[k];
-        c = base[q >> 8] + (q & (kBlock - 1));
-        v = va[k];
-    }
-};
-
-// Segment engine: gathered operand k read from the x tiles staged with the
-// tile (index from RowSeg), no global gather at all.
-struct SegIn {
-    const double* sv;  // stage vectors + own row
-    const double* g0;  // staged x tiles of gathered operand 0 / 1
-    const double* g1;
-    __device__ __forceinline__ double operator()(int v) const { return sv[v * kBlock]; }
-    __device__ __forceinline__ double gather(int k, int q, const double*) const { return (k ? g1 : g0)[q]; }
-    __device__ __forceinline__ double gather_p(int q, const double*, const double*, double beta) const {
-        return ADD(g1[q], MUL(beta, g0[q]));  // HS: operand 0 p_old, operand 1 r~
-    }
-};
-
 // Optional Op trait for the band engine: `static constexpr bool BAND_XF` — the
 // window holds band_xf(source 0, source 1) instead of the NG raw sources.
 template <class T, class = void>
@@ -500,19 +434,14 @@ struct BandXf<T, std::void_t<decltype(T::BAND_XF)>> {
     static constexpr bool value = T::BAND_XF;
 };
 
-// Per-stage shared-memory layout. CSR engine: row_ptr slice, values, int32
-// columns, vectors. Segment engine (S.nd > 0): 16-bit columns instead, and
-// after the vectors the nd x tiles of each of the ng gathered operands.
+// Per-stage shared-memory layout: row_ptr slice, values, int32 columns,
+// vectors.
 struct StageView {
     int* rp;       // kRpInts
     double* va;    // cap
-    int* ci;       // cap (CSR engine)
-    unsigned short* ci16;  // cap (segment engine)
+    int* ci;       // cap
     double* vec;   // nvec * kBlock
-    double* gx;    // ng * nd * kBlock (segment engine)
 };
-
-__host__ __device__ inline int ci_bytes_for(int cap, int nd) { return nd > 0 ? ((cap * 2 + 15) & ~15) : cap * 4; }
 
 __device__ __forceinline__ StageView stage_view(unsigned char* base, const StageCfg& S, int slot) {
     unsigned char* p = base + (size_t)slot * S.stage_bytes;
@@ -522,16 +451,13 @@ __device__ __forceinline__ StageView stage_view(unsigned char* base, const Stage
     v.va = reinterpret_cast<double*>(p);
     p += (size_t)S.cap * 8;
     v.ci = reinterpret_cast<int*>(p);
-    v.ci16 = reinterpret_cast<unsigned short*>(p);
-    p += ci_bytes_for(S.cap, S.nd);
+    p += (size_t)S.cap * 4;
     v.vec = reinterpret_cast<double*>(p);
-    p += (size_t)S.nvec * kBlock * 8;
-    v.gx = reinterpret_cast<double*>(p);
     return v;
 }
 
-__host__ __device__ inline int stage_bytes_for(int cap, int nvec, bool csr, int nd = 0, int ng = 0) {
-    return kRpInts * 4 + (csr ? cap * 8 + ci_bytes_for(cap, nd) : 0) + nvec * kBlock * 8 + ng * nd * kBlock * 8;
+__host__ __device__ inline int stage_bytes_for(int cap, int nvec, bool csr) {
+    return kRpInts * 4 + (csr ? cap * 12 : 0) + nvec * kBlock * 8;
 }
 
 // Header in dynamic shared memory: barriers + per-slot metadata.
@@ -543,11 +469,7 @@ struct PipeHeader {
     int direct[kMaxStages];
     int last_flag;
     int pad[3];
-    int segbase[kMaxStages][8];  // 16-bit-column CSR: first row of each tile offset's x tile
     double red[kMaxDots * 32];
-    int slot_tile[kMaxStages];   // dynamic scheduling: the stage's tile (-1: no more work),
-    int slot_vb[kMaxStages];     //   its virtual CTA and first / last-tile flags
-    int slot_flags[kMaxStages];
     uint64_t fold_bar;           // last CTA: bulk copy of the partials into the idle ring
     uint64_t pad2;
     Ctrl cs;                     // last CTA: the control block finish() works on
@@ -766,11 +688,10 @@ __device__ __forceinline__ void stage_csr(const Params& P, const StageCfg& S, Pi
     const int rows = min(kBlock, P.n - r0);
     const uint32_t rp_bytes = ((rows + 1) * 4 + 15) & ~15;
     const int k0 = __ldg(P.rp + r0), k1 = __ldg(P.rp + r0 + rows);
-    const bool seg = S.nd > 0;  // 16-bit columns: 16-byte aligned at multiples of 8
-    const int k0a = k0 & ~1, k0c = seg ? k0 & ~7 : k0 & ~3;
-    const bool direct = k1 - k0c + (seg ? 8 : 4) > S.cap;
+    const int k0a = k0 & ~1, k0c = k0 & ~3;  // 16-byte aligned bulk sources
+    const bool direct = k1 - k0c + 4 > S.cap;
     const uint32_t va_bytes = direct ? 0u : (((k1 - k0a) * 8 + 15) & ~15);
-    const uint32_t ci_bytes = direct ? 0u : (((k1 - k0c) * (seg ? 2 : 4) + 15) & ~15);
+    const uint32_t ci_bytes = direct ? 0u : (((k1 - k0c) * 4 + 15) & ~15);
     H->k0a[slot] = k0a;
     H->k0c[slot] = k0c;
     H->direct[slot] = direct;
@@ -778,8 +699,7 @@ __device__ __forceinline__ void stage_csr(const Params& P, const StageCfg& S, Pi
     bulk_g2s(V.rp, P.rp + r0, rp_bytes, &H->full[slot], pol);
     if (!direct) {
         bulk_g2s(V.va, P.va + k0a, va_bytes, &H->full[slot], pol);
-        if (seg) bulk_g2s(V.ci16, P.ci16 + k0c, ci_bytes, &H->full[slot], pol);
-        else bulk_g2s(V.ci, P.ci + k0c, ci_bytes, &H->full[slot], pol);
+        bulk_g2s(V.ci, P.ci + k0c, ci_bytes, &H->full[slot], pol);
     }
 }
 
@@ -815,10 +735,6 @@ __device__ __forceinline__ void tl_mark(int kernel, int slot) {
 #endif
 }
 
-// SEG 1: the segment engine (S.nd > 0): the stage also carries the x tiles
-// the tile's columns fall in (tile + seg_d[q]); gathers read shared memory.
-// SEG 2: CSR with 16-bit columns decoded against those tiles' bases, x
-// gathered through L1/L2 (2 B/entry less traffic and stage space).
 // Prev: the other kernel of the iteration (chained schedule: its partials
 // are folded here, see chain_prologue).
 // Two virtual CTAs per physical CTA (order 0; the register-bound update
@@ -885,12 +801,12 @@ __device__ __forceinline__ uint64_t staged_policy(const Op& op, const Params& P,
 #ifndef CGVK_K1_MIN_CTAS
 #define CGVK_K1_MIN_CTAS 1  // register budget of the update kernels (resident CTAs)
 #endif
-template <class Op, class Prev, int SEG>
+template <class Op, class Prev>
 __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S);
 
-template <class Op, class Prev, int MINB = (Op::CSR ? CGVK_SPMV_MIN_CTAS : CGVK_K1_MIN_CTAS), int SEG = 0>
+template <class Op, class Prev, int MINB = (Op::CSR ? CGVK_SPMV_MIN_CTAS : CGVK_K1_MIN_CTAS)>
 __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S) {
-    stream_body<Op, Prev, SEG>(P, S);
+    stream_body<Op, Prev>(P, S);
 }
 
 // The same kernel under an explicit register cap (__maxnreg__ cannot be
@@ -906,10 +822,10 @@ struct MaxnregOf<T, std::void_t<decltype(T::MAXNREG)>> {
 };
 template <class Op, class Prev>
 __global__ void __maxnreg__(MaxnregOf<Op>::value > 0 ? MaxnregOf<Op>::value : 255) k_stream_nr(Params P, StageCfg S) {
-    stream_body<Op, Prev, 0>(P, S);
+    stream_body<Op, Prev>(P, S);
 }
 
-template <class Op, class Prev, int SEG>
+template <class Op, class Prev>
 __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PipeHeader* H = reinterpret_cast<PipeHeader*>(smem_raw);
@@ -932,17 +848,16 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
     // that kernel is still finishing, then waits for it.
     uint64_t pol = 0;
     int npre = 0;
-    const bool dyn = DynOf<Op>::value && P.order == 0 && !S.chain;
     // reversed sweep: the CTA's tiles are exactly p + Gp s when Gp divides Gv
     // (or every virtual CTA is one tile)
-    const bool rev = RevOf<Op>::value && !dyn && P.order == 0 && (Gv % Gp == 0 || Gv == ntiles);
+    const bool rev = RevOf<Op>::value && P.order == 0 && (Gv % Gp == 0 || Gv == ntiles);
     const int nrev = rev ? ((int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / Gp + 1 : 0) : 0;
-    const bool rr2 = Rr2Of<Op>::value && !Op::CSR && !dyn && P.order == 0 && (int)blockIdx.x + Gp < Gv &&
+    const bool rr2 = Rr2Of<Op>::value && !Op::CSR && P.order == 0 && (int)blockIdx.x + Gp < Gv &&
                      (int)blockIdx.x + 2 * Gp >= Gv;
-    constexpr bool kEarly = HasEarlyVec<Op>::value && SEG == 0 && CGVK_EARLY > 0;
+    constexpr bool kEarly = HasEarlyVec<Op>::value && CGVK_EARLY > 0;
     int early_tile[kMaxStages];
     int nearly = 0;  // stages whose vectors are issued right after the wait
-    if (producer && (Op::CSR || (kEarly && !dyn))) {
+    if (producer && (Op::CSR || kEarly)) {
         if (Op::CSR) pol = matrix_policy(P.l2pol);
         int q = 0;
         if (rev) {
@@ -964,11 +879,11 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
                     if (Op::CSR) stage_csr(P, S, H, stages, q, tile, pol, /*arrive=*/false);
                     early_tile[q++] = tile;
                 }
-                if (q == NS || dyn) break;  // dynamic: only the static first virtual CTA
+                if (q == NS) break;
             }
         }
         if (Op::CSR) npre = q;
-        if (kEarly && !dyn) nearly = min(q, CGVK_EARLY);
+        if (kEarly) nearly = min(q, CGVK_EARLY);
     }
     tl_mark(Op::CSR, 0);
     pdl_wait();
@@ -1016,18 +931,13 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
         const double* vp[kMaxVec];
 #pragma unroll
         for (int v = 0; v < Op::NV; ++v) vp[v] = op.vec(P, v);
-        const double* gp[2] = {nullptr, nullptr};
-        if constexpr (SEG == 1) {
-#pragma unroll
-            for (int k = 0; k < Op::NG; ++k) gp[k] = op.gsrc(P, k);
-        }
         int j = 0;
         const uint64_t vpol = P.l2pol == 0 ? pol : 0;
         unsigned int normal_mask = 0;  // staged vectors kept at normal L2 priority
 #pragma unroll
         for (int v = 0; v < Op::NV; ++v)
             if (vp[v] && staged_policy(op, P, vp[v], vpol) != vpol) normal_mask |= 1u << v;
-        auto produce_tile = [&](int tile, int vb) {
+        auto produce_tile = [&](int tile) {
             {
                 if (j < nearly) {  // issued right after the wait
                     ++j;
@@ -1035,11 +945,6 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
                 }
                 const int slot = j % NS;
                 if (j >= NS) mbar_wait(&H->empty[slot], ((j / NS) - 1) & 1);
-                if (dyn) {
-                    H->slot_tile[slot] = tile;
-                    H->slot_vb[slot] = vb;
-                    H->slot_flags[slot] = (tile == vb ? 1 : 0) | (tile + Gv >= ntiles ? 2 : 0);
-                }
                 StageView V = stage_view(stages, S, slot);
                 const int r0 = tile * kBlock;
                 const int rows = min(kBlock, P.n - r0);
@@ -1049,60 +954,27 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
 #pragma unroll
                 for (int v = 0; v < Op::NV; ++v)
                     if (vp[v]) bytes += vec_bytes;
-                if constexpr (SEG == 2) {  // x-tile bases for the 16-bit columns
-                    for (int q = 0; q < S.nd; ++q) H->segbase[slot][q] = (tile + P.seg_d[q]) * kBlock;
-                }
-                if constexpr (SEG == 1) {  // the x tiles this tile's columns fall in
-                    for (int q = 0; q < S.nd; ++q) {
-                        const int u = tile + P.seg_d[q];
-                        if (u < 0 || u >= ntiles) continue;
-                        const uint32_t ub = (min(kBlock, P.n - u * kBlock) * 8 + 15) & ~15;
-#pragma unroll
-                        for (int k = 0; k < Op::NG; ++k)
-                            if (gp[k]) bytes += ub;
-                    }
-                }
                 mbar_expect_tx(&H->full[slot], bytes);  // + this thread's arrival
 #pragma unroll
                 for (int v = 0; v < Op::NV; ++v)
                     if (vp[v])
                         bulk_g2s(V.vec + v * kBlock, vp[v] + r0, vec_bytes, &H->full[slot],
                                  (normal_mask >> v) & 1u ? 0ull : vpol);
-                if constexpr (SEG == 1) {
-                    for (int q = 0; q < S.nd; ++q) {
-                        const int u = tile + P.seg_d[q];
-                        if (u < 0 || u >= ntiles) continue;
-                        const uint32_t ub = (min(kBlock, P.n - u * kBlock) * 8 + 15) & ~15;
-#pragma unroll
-                        for (int k = 0; k < Op::NG; ++k)
-                            if (gp[k])
-                                bulk_g2s(V.gx + (k * S.nd + q) * kBlock, gp[k] + (size_t)u * kBlock, ub,
-                                         &H->full[slot], 0);
-                    }
-                }
                 ++j;
             }
         };
-        auto produce_vb = [&](int vb) {
-            CGVK_FOR_TILE(tile, P.order, vb, ntiles, Gv) produce_tile(tile, vb);
-        };
         if (rev) {
-            for (int st = 0; st < nrev; ++st) produce_tile((int)blockIdx.x + Gp * (nrev - 1 - st), -1);
+            for (int st = 0; st < nrev; ++st) produce_tile((int)blockIdx.x + Gp * (nrev - 1 - st));
         } else if (rr2) {
             for (int st = 0;; ++st) {
                 const int tile = rr2_tile(blockIdx.x, Gp, Gv, ntiles, st);
                 if (tile == -2) break;
-                if (tile >= 0) produce_tile(tile, blockIdx.x + (st & 1) * Gp);
+                if (tile >= 0) produce_tile(tile);
             }
-        } else if (dyn) {
-            unsigned int* sched = P.ctrl->sched + (op.counter(P) - P.ctrl->count);
-            for (int vb = blockIdx.x; vb < Gv; vb = Gp + (int)atomicAdd(sched, 1u)) produce_vb(vb);
-            const int slot = j % NS;  // sentinel stage: no more work
-            if (j >= NS) mbar_wait(&H->empty[slot], ((j / NS) - 1) & 1);
-            H->slot_tile[slot] = -1;
-            mbar_arrive(&H->full[slot]);
         } else {
-            CGVK_FOR_VB(vb, P.order, blockIdx.x, Gv, Gp) produce_vb(vb);
+            CGVK_FOR_VB(vb, P.order, blockIdx.x, Gv, Gp) {
+                CGVK_FOR_TILE(tile, P.order, vb, ntiles, Gv) produce_tile(tile);
+            }
         }
         return;
     }
@@ -1115,43 +987,19 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
         StageView V = stage_view(stages, S, slot);
         const int i = tile * kBlock + t;
         if (i < P.n) {
-            if constexpr (SEG == 2) {
+            RowRef R{nullptr, nullptr, 0};
+            if (Op::CSR) {
                 const int b = V.rp[t];
-                RowD R{nullptr, nullptr, H->segbase[slot], V.rp[t + 1] - b};
+                R.len = V.rp[t + 1] - b;
                 if (H->direct[slot]) {
                     R.va = P.va + b;
-                    R.ci = P.ci16 + b;
+                    R.ci = P.ci + b;
                 } else {
                     R.va = V.va + (b - H->k0a[slot]);
-                    R.ci = V.ci16 + (b - H->k0c[slot]);
+                    R.ci = V.ci + (b - H->k0c[slot]);
                 }
-                op.row(P, i, StagedIn{V.vec + t}, R, acc);
-            } else if constexpr (SEG == 1) {
-                const int b = V.rp[t];
-                RowSeg R{nullptr, nullptr, V.rp[t + 1] - b};
-                if (H->direct[slot]) {
-                    R.va = P.va + b;
-                    R.ci = P.ci16 + b;
-                } else {
-                    R.va = V.va + (b - H->k0a[slot]);
-                    R.ci = V.ci16 + (b - H->k0c[slot]);
-                }
-                op.row(P, i, SegIn{V.vec + t, V.gx, V.gx + S.nd * kBlock}, R, acc);
-            } else {
-                RowRef R{nullptr, nullptr, 0};
-                if (Op::CSR) {
-                    const int b = V.rp[t];
-                    R.len = V.rp[t + 1] - b;
-                    if (H->direct[slot]) {
-                        R.va = P.va + b;
-                        R.ci = P.ci + b;
-                    } else {
-                        R.va = V.va + (b - H->k0a[slot]);
-                        R.ci = V.ci + (b - H->k0c[slot]);
-                    }
-                }
-                op.row(P, i, StagedIn{V.vec + t}, R, acc);
             }
+            op.row(P, i, StagedIn{V.vec + t}, R, acc);
         }
         __syncwarp();
         if ((t & 31) == 0) mbar_arrive(&H->empty[slot]);
@@ -1167,22 +1015,7 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
             }
         }
     };
-    if (dyn) {
-        for (;;) {
-            const int jj = j++;
-            const int slot = jj % NS;
-            mbar_wait(&H->full[slot], (jj / NS) & 1);
-            const int tile = H->slot_tile[slot];
-            if (tile < 0) break;
-            const int vb = H->slot_vb[slot], fl = H->slot_flags[slot];
-            if (fl & 1) {
-#pragma unroll
-                for (int d = 0; d < Op::ND; ++d) acc[d] = 0.0;
-            }
-            consume_tile(slot, tile);
-            if (fl & 2) close_vb(vb);
-        }
-    } else if (rev) {  // no dot products: nothing to accumulate
+    if (rev) {  // no dot products: nothing to accumulate
         for (int st = 0; st < nrev; ++st) {
             const int jj = j++;
             const int slot = jj % NS;
@@ -1251,10 +1084,7 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
             cta_tree_c<Op::ND>(tot, H->red);
         }
     }
-    if (t == 0) {
-        *counter = 0u;
-        if (dyn) P.ctrl->sched[counter - P.ctrl->count] = 0u;
-    }
+    if (t == 0) *counter = 0u;
     if (chain) {  // the totals; the next kernel runs the scalar tail
         if (t == 0) {
 #pragma unroll

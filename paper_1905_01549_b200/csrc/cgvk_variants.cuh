@@ -72,7 +72,6 @@ template <bool PREC>
 struct HsK1 {
     static constexpr int NV = PREC ? 3 : 2, ND = 2;
     static constexpr bool CSR = false;
-    static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     static constexpr bool PDL_LATE = (CGVK_HS_LATE & 1) != 0;  // see cgvk_stream.cuh PdlLate
     double alpha;
     __device__ bool enter(const Params& P) {
@@ -121,7 +120,6 @@ struct HsK2 {
     static constexpr int NV = 3, ND = 1;
     static constexpr int MAXNREG = CGVK_SPMV_MAXNREG;
     static constexpr bool CSR = true;
-    static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     static constexpr bool PDL_LATE = (CGVK_HS_LATE & 2) != 0;
     int mode;
     const double* pold;
@@ -254,7 +252,6 @@ struct CgK2 {
     static constexpr bool PDL_LATE = (CGVK_CG_LATE & 2) != 0;
     static constexpr int MAXNREG = CGVK_SPMV_MAXNREG;
     static constexpr bool CSR = true;
-    static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     static constexpr int STAGES = 2;  // measured: a shallower ring leaves L1 to the gathers
     bool unsimp;
     __device__ bool enter(const Params& P) {
@@ -399,7 +396,6 @@ struct PrK2 {
     static constexpr int NV = PREC ? 4 : 2, ND = 6;
     static constexpr int MAXNREG = CGVK_SPMV_MAXNREG;
     static constexpr bool CSR = true;
-    static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     static constexpr bool PDL_LATE = (CGVK_PR_LATE & 2) != 0;
     double nup;
     bool want_delta, want_dhat;
@@ -485,7 +481,6 @@ struct GvK1 {
     static constexpr int MAXNREG = CGVK_K1_MAXNREG;
     static constexpr int SMEM_CTAS = CGVK_GV_K1_CTAS;
     static constexpr bool CSR = false;
-    static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     bool F, S, unsimp;
     double alpha, beta;
     __device__ bool enter(const Params& P) {
@@ -597,7 +592,6 @@ struct GvK2 {
     static constexpr bool PDL_LATE = (CGVK_GV_LATE & 2) != 0;
     static constexpr int MAXNREG = CGVK_SPMV_MAXNREG;
     static constexpr bool CSR = true;
-    static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     // measured: 2 stages at 4 CTAs/SM (G = 12 x SMs); with G = 3 x SMs the grid
     // is 3 CTAs/SM and a 3-stage ring is faster (V256 GV 740 -> 697 us)
     static constexpr int STAGES = 3;
@@ -639,7 +633,6 @@ struct PprK1 {
     static constexpr int SMEM_CTAS = CGVK_PPR_K1_CTAS;
     static constexpr bool RR2 = true;  // two virtual CTAs per CTA interleaved (cgvk_stream.cuh rr2_tile)
     static constexpr bool CSR = false;
-    static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     double alpha, beta, nup;
     bool valid, want_delta, want_dhat, recw;
     __device__ bool enter(const Params& P) {
@@ -768,7 +761,6 @@ struct PprK2 {
     static constexpr bool PDL_LATE = (CGVK_PPR_LATE & 2) != 0;
     static constexpr int MAXNREG = CGVK_SPMV_MAXNREG;
     static constexpr bool CSR = true;
-    static constexpr bool ALWAYS_ARRIVES = true;  // sync() >= 1: may schedule dynamically
     bool recw;
     __device__ bool enter(const Params& P) {
         recw = P.recompute_w != 0;

@@ -16,6 +16,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 GEN_PATH = os.path.join(_HERE, "libcgvkgen.so")
+_gen_path = os.environ.get("CGVK_GEN_LIB") or GEN_PATH
 
 
 class _CSR(C.Structure):
@@ -23,10 +24,20 @@ class _CSR(C.Structure):
                 ("col_idx", C.c_void_p), ("values", C.c_void_p)]
 
 
+def use_generator(path: str) -> None:
+    """Load the generators from another build of csrc/cgvk_gen.c (bench.py's
+    reference arm uses oracle/_build/libinputgen.so, so that process maps no
+    library of this package). Only before the first generator call."""
+    global _gen_path
+    if _gen is not None and path != _gen_path:
+        raise RuntimeError("generator library already loaded from " + _gen_path)
+    _gen_path = path
+
+
 def _load() -> C.CDLL:
-    if not os.path.exists(GEN_PATH):
-        raise ImportError(f"generator library not built: {GEN_PATH}")
-    g = C.CDLL(GEN_PATH)
+    if not os.path.exists(_gen_path):
+        raise ImportError(f"generator library not built: {_gen_path}")
+    g = C.CDLL(_gen_path)
     g.cgvk_gen_poisson.restype = C.POINTER(_CSR)
     g.cgvk_gen_poisson.argtypes = [C.c_int, C.c_int64]
     g.cgvk_gen_varcoef.restype = C.POINTER(_CSR)
@@ -40,7 +51,14 @@ def _load() -> C.CDLL:
     return g
 
 
-_gen = _load()
+_gen = None  # loaded on first use (see use_generator)
+
+
+def _lib() -> C.CDLL:
+    global _gen
+    if _gen is None:
+        _gen = _load()
+    return _gen
 
 
 @dataclass
@@ -62,7 +80,7 @@ class CSR:
         y = np.empty(self.n)
         c = _CSR(self.n, self.nnz, self.row_ptr.ctypes.data, self.col_idx.ctypes.data,
                  self.values.ctypes.data)
-        _gen.cgvk_gen_spmv(C.byref(c), x.ctypes.data, y.ctypes.data)
+        _lib().cgvk_gen_spmv(C.byref(c), x.ctypes.data, y.ctypes.data)
         return y
 
 
@@ -74,35 +92,35 @@ def _take(p) -> CSR:
     rp = np.ctypeslib.as_array(C.cast(c.row_ptr, C.POINTER(C.c_int64)), (n + 1,)).copy()
     ci = np.ctypeslib.as_array(C.cast(c.col_idx, C.POINTER(C.c_int64)), (max(nnz, 1),))[:nnz].copy()
     va = np.ctypeslib.as_array(C.cast(c.values, C.POINTER(C.c_double)), (max(nnz, 1),))[:nnz].copy()
-    _gen.cgvk_csr_free(p)
+    _lib().cgvk_csr_free(p)
     return CSR(int(n), rp, ci, va)
 
 
 def poisson2d(N: int) -> CSR:
-    return _take(_gen.cgvk_gen_poisson(2, N))
+    return _take(_lib().cgvk_gen_poisson(2, N))
 
 
 def poisson3d(N: int) -> CSR:
-    return _take(_gen.cgvk_gen_poisson(3, N))
+    return _take(_lib().cgvk_gen_poisson(3, N))
 
 
 def varcoef3d(N: int, seed: int = 11, sigma: float = 2.0) -> CSR:
-    return _take(_gen.cgvk_gen_varcoef(N, seed, sigma))
+    return _take(_lib().cgvk_gen_varcoef(N, seed, sigma))
 
 
 def random_spd(n: int, per_row: int = 13, band: int = 4096, seed: int = 7) -> CSR:
-    return _take(_gen.cgvk_gen_random_spd(n, per_row, band, seed))
+    return _take(_lib().cgvk_gen_random_spd(n, per_row, band, seed))
 
 
 def xstar(n: int, seed: int = 1) -> np.ndarray:
     out = np.empty(n)
-    _gen.cgvk_gen_xstar(n, seed, out.ctypes.data)
+    _lib().cgvk_gen_xstar(n, seed, out.ctypes.data)
     return out
 
 
 def mt19937_64(seed: int, count: int) -> np.ndarray:
     out = np.empty(count, dtype=np.uint64)
-    _gen.cgvk_gen_mt19937_64(seed, count, out.ctypes.data)
+    _lib().cgvk_gen_mt19937_64(seed, count, out.ctypes.data)
     return out
 
 

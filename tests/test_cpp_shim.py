@@ -20,3 +20,13 @@ def test_shim_reference_tests_pass():
     print(out.stdout, out.stderr)
     assert out.returncode == 0, out.stderr
     assert "0 failures" in out.stdout
+
+
+def test_shim_host_helpers():
+    """csr_from_triplets / dot / norm2 of the shim (host code, no device call)."""
+    if not os.path.exists(BIN):
+        pytest.skip("run __graft_entry__.build()")
+    out = subprocess.run([BIN, "--host"], capture_output=True, text=True, timeout=60)
+    print(out.stdout, out.stderr)
+    assert out.returncode == 0, out.stderr
+    assert "0 failures" in out.stdout

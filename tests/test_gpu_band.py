@@ -111,23 +111,5 @@ def test_l1_ops_unaffected(bandmats):
     assert same_bits(A.spmv(x), O.spmv(P.A, x))
 
 
-SEG_PROBLEMS = ["poisson2d_33", "poisson3d_12"]
-
-
-@pytest.mark.parametrize("precond", [Precond.IDENTITY, Precond.JACOBI])
-@pytest.mark.parametrize("variant", ALL_VARIANTS)
-@pytest.mark.parametrize("name", SEG_PROBLEMS)
-@pytest.mark.parametrize("engine", ["seg", "csr16"])
-def test_segment_engine_bit_exact(name, variant, precond, engine):
-    """Opt-in 16-bit-column engines — seg: columns index the x tiles staged
-    with each tile; csr16: decoded against the tiles' bases, x through L1 —
-    same bits as the CSR engine's order, vs the oracle."""
-    P = PROBLEMS[name]
-    A = cgvk.DeviceMatrix.from_csr(P.A, engine=engine)
-    eng, nd = A.engine()
-    assert eng == engine and 1 <= nd <= 8
-    lockstep(P.A, A, variant, precond, P.b, P.x0, steps=15, check_vectors_every=5)
-
-
-def test_segment_engine_not_default():
+def test_stencil_defaults_to_csr_engine():
     assert cgvk.DeviceMatrix.from_csr(PROBLEMS["poisson3d_12"].A).engine()[0] == "csr"
