@@ -18,7 +18,15 @@ exists; the GPU box only reads the outputs.
              the first 50 updated and true residual norms, iterations to
              ||r||/||b|| <= 1e-8, the final true residual.
 
-Usage: make_golden.py mtx | table3 | small | config <name> [variant ...]
+  tree       tests/golden/tree_<name>.json — the same BASELINE configs through
+             the C restatement in the B200's reduction order (ORC_DOT_TREE
+             with the (block, gmax, order) cgvk_reduction_config reports on a
+             148-SM B200): per variant the first 50 iterations' updated and
+             true residual norms, alpha and beta as hex floats, and the
+             measured distance of those norms from the reference's sequential
+             ones (config_<name>.json) — the reorder floor.
+
+Usage: make_golden.py mtx | table3 | small | config <name> [variant ...] | tree <name> [variant ...]
 """
 from __future__ import annotations
 
@@ -187,6 +195,70 @@ def cmd_config(name: str, variants: list[str]):
         os.replace(path + ".tmp", path)
 
 
+# reduction tree of a 148-SM B200 per config (cgvk_reduction_config): the CSR
+# engine G = 3 x SMs in strided tile order, the band engine (R4M) 6 x SMs in
+# contiguous order
+B200_TREE = {"p2d": (256, 444, 0), "p64": (256, 444, 0), "p128": (256, 444, 0), "v256": (256, 444, 0),
+             "r4m": (256, 888, 1)}
+
+
+def rel_dist(a, b) -> float:
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.max(np.abs(a - b) / np.abs(b)))
+
+
+def cmd_tree(name: str, variants: list[str]):
+    path = os.path.join(GOLDEN, f"tree_{name}.json")
+    seq = json.load(open(os.path.join(GOLDEN, f"config_{name}.json")))
+    P = pb.config_problem(name)
+    block, gmax, order = B200_TREE[name]
+    dot = ("tree", block, gmax, order)
+    for v in variants:
+        t0 = time.time()
+        s = O.Restatement(P.A, VARIANT_IDS[v], 1, P.b, P.x0, dot=dot)
+
+        def norms():
+            r = s.vector(1)
+            x = s.vector(0)
+            e = P.b - O.spmv(P.A, x)
+            return np.sqrt(O.dot(r, r, dot)), np.sqrt(O.dot(e, e, dot))
+
+        upd, tru, alpha, beta = [], [], [], []
+        u, t = norms()
+        upd.append(u)
+        tru.append(t)
+        for _ in range(50):
+            s.step()
+            sc = s.state()["scalars"]
+            alpha.append(sc["alpha"])
+            beta.append(sc["beta"])
+            u, t = norms()
+            upd.append(u)
+            tru.append(t)
+        ref = seq["variants"][v]
+        ref_upd = [float.fromhex(x) for x in ref["upd_res_first51"]]
+        ref_tru = [float.fromhex(x) for x in ref["true_res_first51"]]
+        rec = {"reduction": [block, gmax, order],
+               "upd_res_first51": [float(x).hex() for x in upd],
+               "true_res_first51": [float(x).hex() for x in tru],
+               "alpha_1_50": [float(x).hex() for x in alpha],
+               "beta_1_50": [float(x).hex() for x in beta],
+               "floor_upd_vs_reference": rel_dist(upd, ref_upd),
+               "floor_true_vs_reference": rel_dist(tru, ref_tru),
+               "cpu_seconds": time.time() - t0}
+        print(name, v, rec["floor_upd_vs_reference"], rec["floor_true_vs_reference"],
+              f"{time.time() - t0:.1f}s", flush=True)
+        cur = json.load(open(path)) if os.path.exists(path) else {"config": name, "variants": {}}
+        cur["variants"][v] = rec
+        cur.update({"n": P.A.n, "nnz": P.A.nnz, "precond": "jacobi",
+                    "protocol": "C restatement (oracle/cgv_oracle.c) with ORC_DOT_TREE in the B200's "
+                                "reduction order; norms of r_k and b - A x_k in that order; floor = max "
+                                "relative distance of those norms from config_<name>.json (the reference)"})
+        with open(path + ".tmp", "w") as f:
+            json.dump(cur, f, indent=1, sort_keys=True)
+        os.replace(path + ".tmp", path)
+
+
 # run() with probes (proj/src/runner.cpp, proj/src/diagnostics.cpp): the
 # reference's records for a few problems x variants x {none, Jacobi} x stop
 # rules; oracle/run.py (seq order) must reproduce them, the device run() must
@@ -239,5 +311,7 @@ if __name__ == "__main__":
         cmd_run()
     elif cmd == "config":
         cmd_config(sys.argv[2], sys.argv[3:] or ["hs", "cg", "m", "pr", "gv", "pipe-pr"])
+    elif cmd == "tree":
+        cmd_tree(sys.argv[2], sys.argv[3:] or ["hs", "cg", "m", "pr", "gv", "pipe-pr"])
     else:
         sys.exit(__doc__)

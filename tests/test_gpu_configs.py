@@ -3,10 +3,15 @@ reference's own CPU solves recorded in tests/golden/config_<name>.json
 (scripts/make_golden.py config ...). North-star bars, with the tolerances
 written here:
 
-* per-iteration updated and true residual norms within 1e-10 relative of the
-  reference for the first 50 iterations (RTOL_HISTORY; GV: RTOL_HISTORY_GV,
-  its measured reorder floor — the GPU is bit-identical to the GPU-order
-  oracle, so its distance from the sequential-order reference IS that floor);
+* the first 50 iterations' updated and true residual norms, alpha and beta
+  BIT-IDENTICAL to the C restatement run in the B200's reduction order at
+  full size (tests/golden/tree_<name>.json, scripts/make_golden.py tree);
+* those norms within 1e-10 relative of the reference's sequential-order ones
+  (RTOL_HISTORY) — except where the committed reorder floor of the
+  restatement itself (tree vs sequential order, measured on the CPU and
+  stored in tree_<name>.json; test_oracle.py recomputes it from the two
+  golden files) is larger: then within that floor x FLOOR_MARGIN (GV, whose
+  true residual carries the reorder difference forward, SURVEY E7);
 * iterations to ||r||/||b|| <= 1e-8 within +-2 % (ITER_TOL);
 * final true residual within a factor of 2 (TRUE_RES_FACTOR).
 
@@ -29,7 +34,7 @@ from helpers import same_bits
 pytestmark = pytest.mark.gpu
 
 RTOL_HISTORY = 1e-10
-RTOL_HISTORY_GV = 1e-9
+FLOOR_MARGIN = 1.0 + 1e-6  # the GPU equals the tree oracle bit for bit: its distance IS the floor
 ITER_TOL = 0.02
 TRUE_RES_FACTOR = 2.0
 VARIANTS = {"hs": Variant.HS, "cg": Variant.CG_CG, "m": Variant.M, "pr": Variant.PR,
@@ -37,6 +42,14 @@ VARIANTS = {"hs": Variant.HS, "cg": Variant.CG_CG, "m": Variant.M, "pr": Variant
 CONFIGS = ["p2d", "p64", "p128", "v256", "r4m"]
 
 _cache = {}
+
+
+def tree_golden(cfg):
+    path = os.path.join(GOLDEN, f"tree_{cfg}.json")
+    if not os.path.exists(path):
+        pytest.skip(f"no tree-order golden file for {cfg}")
+    with open(path) as f:
+        return json.load(f)
 
 
 def golden(cfg):
@@ -66,17 +79,29 @@ def test_history_and_solve_vs_reference(cfg, v):
     if v not in g["variants"]:
         pytest.skip("variant missing from golden file")
     gv = g["variants"][v]
+    tg = tree_golden(cfg)["variants"][v]
     P, A = problem(cfg)
-    assert A.n == g["n"] and A.nnz == g["nnz"]
+    assert int(A.n) == int(g["n"]) and int(A.nnz) == int(g["nnz"])
+    assert list(A.reduction_config()) == tg["reduction"], "golden made for another reduction tree"
     s = cgvk.initialize(cgvk.VariantConfig.make(VARIANTS[v]), A, Precond.JACOBI, P.b, P.x0)
-    true = [s.true_residual()]
+    true, alpha, beta = [s.true_residual()], [], []
     for _ in range(50):
         cgvk.step(s)
+        sc = s.scalars()
+        alpha.append(sc["alpha"])
+        beta.append(sc["beta"])
         true.append(s.true_residual())
     upd = s.history()[:51]
-    rtol = RTOL_HISTORY_GV if v == "gv" else RTOL_HISTORY
-    np.testing.assert_allclose(upd, hexlist(gv["upd_res_first51"]), rtol=rtol, atol=0)
-    np.testing.assert_allclose(true, hexlist(gv["true_res_first51"]), rtol=rtol, atol=0)
+    # bit-identical to the restatement in the device's reduction order
+    assert same_bits(upd, hexlist(tg["upd_res_first51"]))
+    assert same_bits(np.array(true), hexlist(tg["true_res_first51"]))
+    assert same_bits(np.array(alpha), hexlist(tg["alpha_1_50"]))
+    assert same_bits(np.array(beta), hexlist(tg["beta_1_50"]))
+    # and within the north star's 1e-10 of the reference, or its reorder floor
+    rtol_u = max(RTOL_HISTORY, tg["floor_upd_vs_reference"] * FLOOR_MARGIN)
+    rtol_t = max(RTOL_HISTORY, tg["floor_true_vs_reference"] * FLOOR_MARGIN)
+    np.testing.assert_allclose(upd, hexlist(gv["upd_res_first51"]), rtol=rtol_u, atol=0)
+    np.testing.assert_allclose(true, hexlist(gv["true_res_first51"]), rtol=rtol_t, atol=0)
     # continue to ||r|| <= 1e-8 ||b|| on the graph path
     s.set_tolerance(1e-8)
     s.step(4 * gv["iters_to_1e-8"])

@@ -193,3 +193,27 @@ def test_tree_dot_is_a_sum_of_products():
             assert O.dot(x, y, ("tree", 256, 1776, order)) == exact
             assert O.dot(x, y, ("part", 256, 1776, [0, n // 3, n], order)) == exact
         assert O.dot(x, y, "seq") == exact
+
+
+@pytest.mark.parametrize("cfg", ["p2d", "p64", "p128", "v256", "r4m"])
+def test_tree_golden_floor_consistent(cfg):
+    """tests/golden/tree_<cfg>.json (the restatement in the B200's reduction
+    order, scripts/make_golden.py tree) against config_<cfg>.json (the
+    reference itself): the committed reorder floor is exactly the distance of
+    the two committed histories, the first entries (before any iteration's
+    dot order matters beyond the norm itself) agree to a few ulps, and every
+    floor is reported against the north star's 1e-10."""
+    tp = os.path.join(GOLDEN, f"tree_{cfg}.json")
+    if not os.path.exists(tp):
+        pytest.skip("no tree golden")
+    tree = json.load(open(tp))
+    ref = json.load(open(os.path.join(GOLDEN, f"config_{cfg}.json")))
+    for v, tg in tree["variants"].items():
+        rv = ref["variants"][v]
+        for key, fk in (("upd_res_first51", "floor_upd_vs_reference"), ("true_res_first51", "floor_true_vs_reference")):
+            a = np.array([float.fromhex(x) for x in tg[key]])
+            b = np.array([float.fromhex(x) for x in rv[key]])
+            assert len(a) == len(b) == 51
+            assert float(np.max(np.abs(a - b) / np.abs(b))) == tg[fk], (v, key)
+            assert abs(a[0] - b[0]) <= 8 * np.spacing(b[0]), (v, key)  # ||r0||: one reordered dot
+        assert len(tg["alpha_1_50"]) == len(tg["beta_1_50"]) == 50
