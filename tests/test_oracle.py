@@ -201,7 +201,7 @@ def test_tree_golden_floor_consistent(cfg):
     order, scripts/make_golden.py tree) against config_<cfg>.json (the
     reference itself): the committed reorder floor is exactly the distance of
     the two committed histories, and the first entries (one reordered dot,
-    no iteration yet) agree to 1e-12."""
+    no iteration yet) agree to 1e-11."""
     tp = os.path.join(GOLDEN, f"tree_{cfg}.json")
     if not os.path.exists(tp):
         pytest.skip("no tree golden")
@@ -214,5 +214,5 @@ def test_tree_golden_floor_consistent(cfg):
             b = np.array([float.fromhex(x) for x in rv[key]])
             assert len(a) == len(b) == 51
             assert float(np.max(np.abs(a - b) / np.abs(b))) == tg[fk], (v, key)
-            assert abs(a[0] - b[0]) <= 1e-12 * b[0], (v, key)  # ||r0||: one reordered dot only
+            assert abs(a[0] - b[0]) <= 1e-11 * b[0], (v, key)  # ||r0||: one reordered dot only
         assert len(tg["alpha_1_50"]) == len(tg["beta_1_50"]) == 50
