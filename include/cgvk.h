@@ -178,7 +178,14 @@ int cgvk_debug_timeline(unsigned long long* out);
 int cgvk_reduction_config(cgvk_matrix a, int* block, int* gmax, int* order);
 
 /* initialize() (inc/variants.hpp:149-150, src/variants.cpp:354-444). The
- * status may already be terminal (zero initial residual, nu0/mu0 <= 0). */
+ * status may already be terminal (zero initial residual, nu0/mu0 <= 0).
+ * Stream-ordered: b and x0 are copied and the reference's initialization
+ * (vectors, reductions, scalar checks) is enqueued on the solver's stream
+ * without a host wait; cgvk_solver_status / _sync observe the result. Host
+ * buffers must stay unchanged until the next synchronising call on the
+ * solver when they are pinned (cudaMemcpyAsync semantics); pageable buffers
+ * are copied before the call returns. Uploads of successive creations on one
+ * device are issued in creation order. */
 int cgvk_solver_create(cgvk_matrix a, const cgvk_variant_config* cfg, int precond,
                        const double* b, const double* x0, cgvk_solver* out);
 int cgvk_solver_destroy(cgvk_solver s);
@@ -198,6 +205,10 @@ int cgvk_solver_status(cgvk_solver s, cgvk_solve_status* st, cgvk_scalars* sc,
  * that the fused schedule recomputes on the fly are materialised);
  * CGVK_EINVAL when the variant does not allocate it. Synchronises. */
 int cgvk_solver_get_vector(cgvk_solver s, int which, double* out);
+/* Enqueue the download of x (CGVK_VEC_X only; x_k is complete after every
+ * step) on the solver's stream without waiting: `out` (preferably pinned,
+ * cgvk_host_register) is valid after cgvk_solver_sync. */
+int cgvk_solver_get_vector_async(cgvk_solver s, int which, double* out);
 /* ||b - A x_k|| with a fresh device spmv (diagnostics.cpp:19-24). */
 int cgvk_solver_true_residual(cgvk_solver s, double* out);
 /* sqrt(<r_j,r_j>) for j = 0..k as recorded on the device each iteration.

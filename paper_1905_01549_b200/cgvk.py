@@ -182,6 +182,7 @@ def _load() -> C.CDLL:
         "cgvk_solver_status": (I, [P, C.POINTER(_Status), C.POINTER(_Scalars),
                                    C.POINTER(_Stats)]),
         "cgvk_solver_get_vector": (I, [P, I, P]),
+        "cgvk_solver_get_vector_async": (I, [P, I, P]),
         "cgvk_solver_true_residual": (I, [P, C.POINTER(D)]),
         "cgvk_solver_history": (I, [P, P, I, C.POINTER(I)]),
         "cgvk_solver_stream": (P, [P]),
@@ -489,6 +490,13 @@ class Solver:
         _check(_lib.cgvk_solver_get_vector(self._h, int(which), _ptr(out) if self.n else None))
         return out
 
+    def x_async(self, out: np.ndarray) -> None:
+        """Enqueue the download of x into `out` (contiguous float64 of n,
+        registered with host_register); valid after sync()."""
+        if out.dtype != np.float64 or out.shape != (self.n,) or not out.flags.c_contiguous:
+            raise InvalidArgument(-1, "out must be a contiguous float64 array of n")
+        _check(_lib.cgvk_solver_get_vector_async(self._h, int(Vec.X), _ptr(out) if self.n else None))
+
     def has_vector(self, which: Vec) -> bool:
         try:
             self.vector(which)
@@ -549,7 +557,12 @@ def initialize(config: VariantConfig, A: DeviceMatrix, precond: Precond, b, x0) 
 
 
 def step(state: Solver) -> None:
-    """step() (inc/variants.hpp:153): exactly one iteration, synchronised."""
+    """step() (inc/variants.hpp:153): exactly one iteration, synchronised;
+    LogicError on a terminated state (src/variants.cpp:447), also one that
+    initialize() settled (creation is stream-ordered, so the status is read
+    here)."""
+    if not state.status.running():
+        raise LogicError(-2, "step() on a terminated solver")
     state.step(1)
     state.sync()
 

@@ -210,14 +210,10 @@ int ensure_jacobi(cgvk_matrix a) {
     return CGVK_OK;
 }
 
-// canonical dots of (x_q, y_q) with optional d∘x_q, results to host
-int run_dots(cgvk_matrix a, cudaStream_t stream, double* part, unsigned int* counter, double* dout,
-             int nd, const double* const* xs, const double* const* ys, const int* dxs,
-             double* host_out) {
-    if (a->n == 0) {
-        for (int q = 0; q < nd; ++q) host_out[q] = 0.0;
-        return CGVK_OK;
-    }
+// canonical dots of (x_q, y_q) with optional d∘x_q into dout[0..nd) on the
+// device (stream-ordered, no host sync)
+int launch_dots(cgvk_matrix a, cudaStream_t stream, double* part, unsigned int* counter, double* dout,
+                int nd, const double* const* xs, const double* const* ys, const int* dxs) {
     DotArgs A{};
     A.n = (int)a->n;
     A.ntiles = a->ntiles;
@@ -238,6 +234,18 @@ int run_dots(cgvk_matrix a, cudaStream_t stream, double* part, unsigned int* cou
         default: k_dots<4><<<a->G, kBlock, 0, stream>>>(A); break;
     }
     CK(cudaGetLastError());
+    return CGVK_OK;
+}
+
+// ... and the results to the host
+int run_dots(cgvk_matrix a, cudaStream_t stream, double* part, unsigned int* counter, double* dout,
+             int nd, const double* const* xs, const double* const* ys, const int* dxs,
+             double* host_out) {
+    if (a->n == 0) {
+        for (int q = 0; q < nd; ++q) host_out[q] = 0.0;
+        return CGVK_OK;
+    }
+    TRY(launch_dots(a, stream, part, counter, dout, nd, xs, ys, dxs));
     CK(cudaMemcpyAsync(host_out, dout, sizeof(double) * nd, cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
     return CGVK_OK;
@@ -1075,6 +1083,8 @@ int refresh_mirror(cgvk_solver s) {
     return CGVK_OK;
 }
 
+// host forms of settle_nonpositive / settle_mu for the row-partitioned
+// initialize (cgvk_group.inc), whose reductions are folded on the host
 bool host_settle_nonpositive(Ctrl& c, double value, int reason, double rr) {
     if (!std::isfinite(value)) {
         c.state = ST_BREAKDOWN;
@@ -1106,8 +1116,100 @@ bool host_settle_mu(Ctrl& c) {
     return false;
 }
 
-// initialize(): src/variants.cpp:354-444, assembled from generic kernels with
-// host-side scalar logic (runs once per solve).
+// ---------------------------------------------------------- initialize()
+// src/variants.cpp:354-444 as a stream-ordered sequence: generic kernels for
+// the vectors, canonical dot kernels into `dout`, and one-thread kernels that
+// run the reference's scalar logic and checks on those results in the control
+// block. Nothing waits for the host, so a solver is created while the
+// previous solver (or the matrix upload) is still running. The reference
+// returns early when a check settles the status (nu0 <= 0 after the first
+// reduction, mu0 <= 0 after the second): here every kernel is enqueued
+// anyway, the control block records the stage the status settled at
+// (Ctrl::init_stage), and k_init_fixup restores the vectors the reference
+// never computed to zero, so the state is exactly the reference's.
+
+__global__ void k_init_ctrl(Ctrl* c, Ctrl c0) { *c = c0; }
+
+// after <r~,r>, <r,r>, <b,b> (src/variants.cpp:382-383)
+__global__ void k_init_nu(Ctrl* c, const double* __restrict__ dout, double* hist, int prec) {
+    const double nu0 = dout[0], rr0 = dout[1];
+    c->rr = rr0;
+    c->bnorm = sqrt(dout[2]);
+    if (hist) hist[0] = rr0;
+    c->sc[SNU] = nu0;
+    c->stats[STAT_SPMV] = 1;
+    c->stats[STAT_PREC] = prec;
+    c->stats[STAT_RED] = 1;
+    if (settle_nonpositive(c, nu0, BR_NU, rr0)) c->init_stage = 1;
+}
+
+// after mu0 = <p0, s0> (src/variants.cpp:385-389)
+__global__ void k_init_mu(Ctrl* c, const double* __restrict__ dout, int st_apply) {
+    if (c->state != ST_RUNNING) return;
+    c->stats[STAT_SPMV] += 1;
+    c->stats[STAT_RED] += 1;
+    c->sc[SMU] = dout[0];
+    if (settle_mu(c)) {
+        c->init_stage = 2;
+        return;
+    }
+    c->sc[SA] = DIV(c->sc[SNU], c->sc[SMU]);
+    c->stats[STAT_PREC] += st_apply;  // s~ = M s (needs_s_tilde)
+}
+
+struct InitExtras {
+    int nd;            // dots in dout
+    int slot[3];       // their scalar slots
+    int spmv, prec;    // counter increments of the per-variant extras
+};
+
+// the per-variant extras (src/variants.cpp:396-440)
+__global__ void k_init_extras(Ctrl* c, const double* __restrict__ dout, InitExtras e) {
+    if (c->state != ST_RUNNING) return;
+    for (int q = 0; q < e.nd; ++q) c->sc[e.slot[q]] = dout[q];
+    c->stats[STAT_SPMV] += e.spmv;
+    c->stats[STAT_PREC] += e.prec;
+    c->stats[STAT_RED] += e.nd;
+}
+
+struct InitVecs {
+    double* after_nu[2];  // computed after the nu0 check: p0, s
+    double* after_mu[4];  // after the mu0 check: s~, w, u, w~ (as the variant has them)
+};
+
+__global__ void k_init_fixup(int n, const Ctrl* __restrict__ c, InitVecs v) {
+    const int stage = c->init_stage;
+    if (stage == 0) return;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        if (stage == 1) {
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+                if (v.after_nu[q]) v.after_nu[q][i] = 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (v.after_mu[q]) v.after_mu[q][i] = 0.0;
+    }
+}
+
+// Host-to-device uploads of solver creations are issued in creation order
+// per device: a solver's b / x0 copies wait for the previous solver's, so the
+// first solver starts computing after its own inputs instead of sharing the
+// copy engine with every later one.
+int order_uploads(cgvk_solver s, bool done) {
+    static std::mutex mu;
+    static cudaEvent_t last[64] = {};
+    const int dev = s->a->device;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!done) {
+        if (last[dev]) CK(cudaStreamWaitEvent(s->stream, last[dev], 0));
+        return CGVK_OK;
+    }
+    if (!last[dev]) CK(cudaEventCreateWithFlags(&last[dev], cudaEventDisableTiming));
+    CK(cudaEventRecord(last[dev], s->stream));
+    return CGVK_OK;
+}
+
 int solver_init(cgvk_solver s, const double* b, const double* x0) {
     cgvk_matrix a = s->a;
     const int64_t n = s->n;
@@ -1116,83 +1218,55 @@ int solver_init(cgvk_solver s, const double* b, const double* x0) {
     const bool stores_rt = prec;  // every variant keeps r~ in a buffer when preconditioned
     const bool needs_st = prec && v != CGVK_HS && v != CGVK_CG_CG;
     const bool pipe = v == CGVK_PIPE_PR || v == CGVK_PIPE_PR_M;
-    Ctrl c{};
-    c.state = ST_RUNNING;
-    c.hist_cap = s->hist_cap;
-    unsigned long long spmv = 0, prec_ap = 0, red = 0;
     cudaStream_t st = s->stream;
     Params P = a->base();
     const int G = a->G;
     const int eg = grid_elem(n);
     const double* d = a->inv_diag;
+    Ctrl c0{};
+    c0.state = ST_RUNNING;
+    c0.hist_cap = s->hist_cap;
+    k_init_ctrl<<<1, 1, 0, st>>>(s->ctrl, c0);
 
+    TRY(order_uploads(s, false));
     CK(cudaMemcpyAsync(s->b, b, 8 * n, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(s->x, x0, 8 * n, cudaMemcpyHostToDevice, st));
+    TRY(order_uploads(s, true));
     // r0 = b - A x0
     k_spmv<<<G, kBlock, 0, st>>>(P, s->x, s->b, s->r, 0);
-    spmv++;
-    if (prec) {
-        prec_ap++;
-        if (stores_rt) k_scale<<<eg, 256, 0, st>>>((int)n, d, s->r, s->rt);
-    }
+    if (stores_rt) k_scale<<<eg, 256, 0, st>>>((int)n, d, s->r, s->rt);
     const double* rtv = stores_rt ? s->rt : s->r;
-    const int rt_fly = prec && !stores_rt;  // r~ = d∘r recomputed
-    double h[4];
     {
         const double* xs[3] = {rtv, s->r, s->b};
         const double* ys[3] = {s->r, s->r, s->b};
-        const int dx[3] = {rt_fly, 0, 0};
-        TRY(run_dots(a, st, s->part, s->counter, s->dout, 3, xs, ys, dx, h));
+        const int dx[3] = {0, 0, 0};
+        TRY(launch_dots(a, st, s->part, s->counter, s->dout, 3, xs, ys, dx));
     }
-    red++;
-    const double nu0 = h[0], rr0 = h[1];
-    c.rr = rr0;
-    c.bnorm = std::sqrt(h[2]);
-    CK(cudaMemcpyAsync(s->hist, &rr0, 8, cudaMemcpyHostToDevice, st));
-    c.sc[SNU] = nu0;
-    auto finish = [&]() -> int {
-        c.stats[STAT_SPMV] = spmv;
-        c.stats[STAT_PREC] = prec_ap;
-        c.stats[STAT_RED] = red;
-        CK(cudaMemcpyAsync(s->ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
-        CK(cudaStreamSynchronize(st));
-        s->mirror = c;
-        s->mirror_fresh = true;
-        return CGVK_OK;
-    };
-    if (host_settle_nonpositive(c, nu0, BR_NU, rr0)) return finish();
+    k_init_nu<<<1, 1, 0, st>>>(s->ctrl, s->dout, s->hist, prec ? 1 : 0);
     // p0 = r~0; s0 = A p0; mu0; alpha0
-    k_scale<<<eg, 256, 0, st>>>((int)n, rt_fly ? d : nullptr, rtv, s->p0);
+    k_scale<<<eg, 256, 0, st>>>((int)n, nullptr, rtv, s->p0);
     k_spmv<<<G, kBlock, 0, st>>>(P, s->p0, nullptr, s->s, 0);
-    spmv++;
     {
         const double* xs[1] = {s->p0};
         const double* ys[1] = {s->s};
-        TRY(run_dots(a, st, s->part, s->counter, s->dout, 1, xs, ys, nullptr, h));
+        TRY(launch_dots(a, st, s->part, s->counter, s->dout, 1, xs, ys, nullptr));
     }
-    red++;
-    c.sc[SMU] = h[0];
-    if (host_settle_mu(c)) return finish();
-    c.sc[SA] = c.sc[SNU] / c.sc[SMU];
-    if (needs_st) {
-        prec_ap++;
-        if (v == CGVK_GV || pipe) k_scale<<<eg, 256, 0, st>>>((int)n, d, s->s, s->st);
-    }
+    k_init_mu<<<1, 1, 0, st>>>(s->ctrl, s->dout, needs_st ? 1 : 0);
+    if (needs_st && (v == CGVK_GV || pipe)) k_scale<<<eg, 256, 0, st>>>((int)n, d, s->s, s->st);
     const double* stv = needs_st && (v == CGVK_GV || pipe) ? s->st : s->s;
     const int st_fly = needs_st && !(v == CGVK_GV || pipe);  // PR/M: s~ = d∘s
     const int expr = s->cfg.nu_expression;
+    InitExtras e{};
     auto scalar_dots = [&](bool want_delta) -> int {
         const bool want_dhat = expr == CGVK_NU_EXPANDED;
         const double* xs[3];
         const double* ys[3];
-        int dx[3], slot[3], nd = 0;
-        if (want_delta) { xs[nd] = rtv; ys[nd] = s->s; dx[nd] = 0; slot[nd++] = SDEL; }
-        if (want_dhat) { xs[nd] = stv; ys[nd] = s->r; dx[nd] = st_fly; slot[nd++] = SDELH; }
-        xs[nd] = stv; ys[nd] = s->s; dx[nd] = st_fly; slot[nd++] = SGAM;
-        TRY(run_dots(a, st, s->part, s->counter, s->dout, nd, xs, ys, dx, h));
-        for (int q = 0; q < nd; ++q) c.sc[slot[q]] = h[q];
-        red += nd;
-        return CGVK_OK;
+        int dx[3], nd = 0;
+        if (want_delta) { xs[nd] = rtv; ys[nd] = s->s; dx[nd] = 0; e.slot[nd++] = SDEL; }
+        if (want_dhat) { xs[nd] = stv; ys[nd] = s->r; dx[nd] = st_fly; e.slot[nd++] = SDELH; }
+        xs[nd] = stv; ys[nd] = s->s; dx[nd] = st_fly; e.slot[nd++] = SGAM;
+        e.nd = nd;
+        return launch_dots(a, st, s->part, s->counter, s->dout, nd, xs, ys, dx);
     };
     switch (v) {
         case CGVK_HS:
@@ -1204,23 +1278,30 @@ int solver_init(cgvk_solver s, const double* b, const double* x0) {
         case CGVK_GV:
             k_spmv<<<G, kBlock, 0, st>>>(P, rtv, nullptr, s->w, 0);
             k_spmv<<<G, kBlock, 0, st>>>(P, stv, nullptr, s->u, 0);
-            spmv += 2;
+            e.spmv = 2;
             break;
         default:  // pipelined PR
             k_spmv<<<G, kBlock, 0, st>>>(P, rtv, nullptr, s->w, 0);
-            spmv++;
-            if (prec) {
-                prec_ap++;
-                if (!s->cfg.recompute_w) k_scale<<<eg, 256, 0, st>>>((int)n, d, s->w, s->wt);
-            }
+            if (prec && !s->cfg.recompute_w) k_scale<<<eg, 256, 0, st>>>((int)n, d, s->w, s->wt);
             k_spmv<<<G, kBlock, 0, st>>>(P, stv, nullptr, s->u, 0);
-            spmv++;
-            if (prec) prec_ap++;
+            e.spmv = 2;
+            e.prec = prec ? 2 : 0;  // w~ = M w, u~ = M u
             TRY(scalar_dots(expr != CGVK_NU_MEURANT || s->cfg.track_delta));
             break;
     }
+    k_init_extras<<<1, 1, 0, st>>>(s->ctrl, s->dout, e);
+    InitVecs iv{};
+    iv.after_nu[0] = s->p0;
+    iv.after_nu[1] = s->s;
+    iv.after_mu[0] = (needs_st && (v == CGVK_GV || pipe)) ? s->st : nullptr;
+    iv.after_mu[1] = (v == CGVK_GV || pipe) ? s->w : nullptr;
+    iv.after_mu[2] = (v == CGVK_GV || pipe) ? s->u : nullptr;
+    iv.after_mu[3] = (pipe && prec && !s->cfg.recompute_w) ? s->wt : nullptr;
+    k_init_fixup<<<eg, 256, 0, st>>>((int)n, s->ctrl, iv);
     CK(cudaGetLastError());
-    return finish();
+    s->mirror = c0;
+    s->mirror_fresh = false;  // the status is known once the stream gets there
+    return CGVK_OK;
 }
 
 void free_solver(cgvk_solver s) {
@@ -1444,6 +1525,7 @@ int cgvk_solver_create(cgvk_matrix a, const cgvk_variant_config* cfg, int precon
     if ((rc = capture(s, 1, &s->g1)) != CGVK_OK || (rc = capture(s, s->gn, &s->g8)) != CGVK_OK)
         return bail(rc);
     pt.mark("graphs");
+    if (env_int("CGVK_SYNC_CREATE", 0) && (rc = refresh_mirror(s)) != CGVK_OK) return bail(rc);
     *out = s;
     return CGVK_OK;
 }
@@ -1456,8 +1538,9 @@ int cgvk_solver_destroy(cgvk_solver s) {
 int cgvk_solver_set_tolerance(cgvk_solver s, double rel_tol) {
     if (!s) return set_err(CGVK_EINVAL, "null solver");
     CK(cudaSetDevice(s->a->device));
-    CK(cudaStreamSynchronize(s->stream));
-    CK(cudaMemcpy(&s->ctrl->tol, &rel_tol, sizeof(double), cudaMemcpyHostToDevice));
+    if (s->n == 0) return CGVK_OK;
+    k_set_tol<<<1, 1, 0, s->stream>>>(s->ctrl, rel_tol);  // stream-ordered, like step()
+    CK(cudaGetLastError());
     s->mirror.tol = rel_tol;
     return CGVK_OK;
 }
@@ -1530,6 +1613,17 @@ int cgvk_solver_get_vector(cgvk_solver s, int which, double* out) {
     TRY(vector_device(s, which, s->tmp, &src));
     CK(cudaMemcpyAsync(out, src, 8 * s->n, cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
+    return CGVK_OK;
+}
+
+int cgvk_solver_get_vector_async(cgvk_solver s, int which, double* out) {
+    if (!s || !out) return set_err(CGVK_EINVAL, "null argument");
+    if (which != CGVK_VEC_X) return set_err(CGVK_EINVAL, "asynchronous download is for x only");
+    CK(cudaSetDevice(s->a->device));
+    if (s->n == 0) return CGVK_OK;
+    // x is never deferred: both kernels of every iteration leave x_k complete
+    CK(cudaMemcpyAsync(out, s->x, 8 * s->n, cudaMemcpyDeviceToHost, s->stream));
+    s->mirror_fresh = false;
     return CGVK_OK;
 }
 
@@ -1647,9 +1741,11 @@ int cgvk_solve(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, const
     TRY(cgvk_solver_create(a, cfg, precond, b, x0, &s));
     int rc = CGVK_OK;
     if (rel_tol > 0.0) rc = cgvk_solver_set_tolerance(s, rel_tol);
-    if (rc == CGVK_OK && s->mirror.state == ST_RUNNING) rc = cgvk_solver_step(s, max_iter);
+    // one host sync for the whole solve: iterations after a terminal status
+    // (also one settled by initialize) are device-side no-ops
+    if (rc == CGVK_OK) rc = cgvk_solver_step(s, max_iter);
+    if (rc == CGVK_OK && x_out) rc = cgvk_solver_get_vector_async(s, CGVK_VEC_X, x_out);
     if (rc == CGVK_OK) rc = cgvk_solver_sync(s);
-    if (rc == CGVK_OK && x_out) rc = cgvk_solver_get_vector(s, CGVK_VEC_X, x_out);
     cgvk_solve_status tmp{};
     if (rc == CGVK_OK) rc = cgvk_solver_status(s, &tmp, sc, nullptr);
     // run(): a budget exhausted while running reports MaxIterations

@@ -53,7 +53,8 @@ struct __align__(16) Ctrl {
     int wt_stored;    // pipe-PR: w~ lives in its buffer (nu'-terminal step)
     int hist_cap;
     unsigned int count[2];  // last-CTA arrival counters
-    unsigned int spare_[4];
+    int init_stage;         // initialize(): 0, or the check that settled the status (1 nu0, 2 mu0)
+    unsigned int spare_[3];
     // chained schedule (cgvk_stream.cuh chain_prologue): the folded totals of
     // the kernel that wrote this copy, for its successor's scalar tail
     double tot[kMaxDots];

@@ -188,5 +188,6 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSM) k_dots(DotArgs A) {
 }
 
 __global__ void k_set_limit(Ctrl* c, int k_limit) { c->k_limit = k_limit; }
+__global__ void k_set_tol(Ctrl* c, double tol) { c->tol = tol; }
 
 }  // namespace cgvk

@@ -407,3 +407,60 @@ def test_tolerance_stop(v):
     assert k == taken and same_bits(x, o.vector(0))
     x, status, k = cgvk.solve(A, cgvk.VariantConfig.make(v), Precond.JACOBI, P.b, P.x0, 7)
     assert k == 7 and status.state == State.MAX_ITERATIONS
+
+
+@pytest.mark.parametrize("v", ALL)
+@pytest.mark.parametrize("case", ["mu0", "nonfinite_nu0"])
+def test_initialize_settles_status(v, case):
+    """initialize()'s own checks (src/variants.cpp:383, 389): mu0 <= 0 on an
+    indefinite matrix, a non-finite nu0 from a NaN in b. Creation is
+    stream-ordered — every kernel is enqueued and the device restores what
+    the reference never computed — so status, scalars, counters and every
+    vector must be exactly the reference's."""
+    M = np.diag([1.0, -3.0, 0.5, 1.0])
+    Ad = dense_csr(M)
+    A = cgvk.DeviceMatrix.from_csr(Ad)
+    b = np.ones(4)
+    if case == "nonfinite_nu0":
+        b[2] = np.nan
+    s, o = lockstep(Ad, A, v, Precond.IDENTITY, b, np.zeros(4), steps=0)
+    st = s.status
+    assert st.state == State.BREAKDOWN
+    assert st.breakdown == (cgvk.Breakdown.MU_NONPOSITIVE if case == "mu0" else cgvk.Breakdown.NON_FINITE)
+    with pytest.raises(cgvk.LogicError):
+        cgvk.step(s)
+
+
+@pytest.mark.parametrize("v", ALL)
+@pytest.mark.parametrize("precond", [Precond.IDENTITY, Precond.JACOBI])
+def test_async_path_matches_synchronous(v, precond):
+    """cgvk_solver_create (stream-ordered), step(n) and the asynchronous x
+    download with one sync at the end give the same bits as step-by-step
+    synchronous use; solvers created back to back share nothing."""
+    P = pb.make_problem("p2", pb.poisson2d(30))
+    A = cgvk.DeviceMatrix.from_csr(P.A)
+    cfg = cgvk.VariantConfig.make(v)
+    outs = [np.empty(A.n) for _ in range(3)]
+    for o in outs:
+        cgvk.host_register(o)
+    try:
+        ss = [cgvk.initialize(cfg, A, precond, P.b, P.x0) for _ in range(3)]
+        for i, s in enumerate(ss):
+            s.step(11 + i)
+            s.x_async(outs[i])
+        for s in ss:
+            s.sync()
+        for i, s in enumerate(ss):
+            ref = cgvk.initialize(cfg, A, precond, P.b, P.x0)
+            for _ in range(11 + i):
+                cgvk.step(ref)
+            assert same_bits(outs[i], ref.x) and s.k == ref.k == 11 + i
+            assert gpu_state_equal(s, ref)
+    finally:
+        for o in outs:
+            cgvk.host_unregister(o)
+
+
+def gpu_state_equal(a, b):
+    from helpers import gpu_state
+    return gpu_state(a) == gpu_state(b)
