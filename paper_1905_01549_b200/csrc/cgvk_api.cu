@@ -1346,6 +1346,13 @@ int vector_device(cgvk_solver s, int which, double* scratch, const double** out)
     bool zeros = false;
     TRY(materialize(s));
     const Ctrl& c = s->mirror;
+    // initialize() settled the status before resizing the later vectors
+    // (src/variants.cpp:383, 389)
+    if (c.init_stage == 1 && which != CGVK_VEC_X && which != CGVK_VEC_R && which != CGVK_VEC_R_TILDE)
+        return set_err(CGVK_EINVAL, "vector %d was not allocated: initialize() stopped at nu0", which);
+    if (c.init_stage == 2 && which != CGVK_VEC_X && which != CGVK_VEC_R && which != CGVK_VEC_R_TILDE &&
+        which != CGVK_VEC_P && which != CGVK_VEC_S)
+        return set_err(CGVK_EINVAL, "vector %d was not allocated: initialize() stopped at mu0", which);
     switch (which) {
         case CGVK_VEC_X: src = s->x; break;
         case CGVK_VEC_R: src = s->r; break;
@@ -1579,7 +1586,12 @@ int cgvk_solver_status(cgvk_solver s, cgvk_solve_status* st, cgvk_scalars* sc, c
         st->breakdown = c.reason;
         st->criterion = c.criterion;
         st->k = c.k;
-        st->allocated_vectors = s->allocated;
+        // initialize() returns before resizing the later vectors when a check
+        // settles the status (src/variants.cpp:383, 389): x r (r~) after the
+        // nu0 check, + p s after the mu0 check
+        st->allocated_vectors = c.init_stage == 1   ? 2 + s->prec
+                                : c.init_stage == 2 ? 4 + s->prec
+                                                    : s->allocated;
     }
     if (sc) {
         sc->alpha = c.sc[SA];
