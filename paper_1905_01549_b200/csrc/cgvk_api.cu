@@ -872,7 +872,8 @@ int make_band(cgvk_matrix a, KLaunch* L) {
     S.nvec = Op::NV + Shape::NRAW;
     S.stage_bytes = band_stage_bytes(S.nvec);
     S.gvirt = a->G;
-    S.nstage = std::min(std::max(env_int("CGVK_BAND_NSTAGE", 2 * Shape::GROUPS), 2), kMaxStages);
+    const int ns_default = 2 * Shape::GROUPS;  // measured R4M: GV K2 350 us at 2 vs 375 at 4; pipe-PR 344 at 4 vs 372 at 8
+    S.nstage = std::min(std::max(env_int("CGVK_BAND_NSTAGE", ns_default), 2), kMaxStages);
     // raw windows are filled NS - 1 tiles ahead by the producer; a combined
     // window one tile ahead by the consumers
     S.ring = 2 * a->band_h + (Shape::XF ? 2 : S.nstage);

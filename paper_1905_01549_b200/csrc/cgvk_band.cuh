@@ -214,8 +214,20 @@ __device__ __forceinline__ void band_body(const Params& P, const StageCfg& S) {
     }
 
     // ------------------------------------------------------ consumer warps
+    //
+    // Slices of a tile are sorted by row length, so slice 0 is the longest
+    // (R4M: its longest row averages 38 entries against a 28-entry mean over
+    // the slices). Kernels without dot products have no per-tile barrier:
+    // their warps rotate over the slices (warp w takes slice (w + tile) % 8),
+    // so every warp does the same work over any 8 tiles and the stage ring
+    // absorbs the drift (measured R4M: GV K2 283 -> 265 us, pipe-PR K2 313 ->
+    // 284 us). Kernels with dot products exchange the per-row contributions
+    // through shared memory after every tile (one CTA barrier), so there the
+    // longest slice sets each tile's time whatever the map; taking tiles in
+    // pairs with balanced slices measured 1.6-2.2x slower (register spills and
+    // a second copy of the row loop), see DESIGN.md §9.
     const int t = threadIdx.x & (kBlock - 1), lane = t & 31, grp = threadIdx.x / kBlock;
-    const int wg = warp & (kWarps - 1);  // warp within its group = slice
+    const int wg = warp & (kWarps - 1);  // warp within its group
     if constexpr (XF) {
         // prologue: the window [T0 - H, T0 + H] of the first tile, combined
         // from global (later tiles get theirs from the stages)
@@ -238,25 +250,26 @@ __device__ __forceinline__ void band_body(const Params& P, const StageCfg& S) {
             const int slot = jj % NS;
             mbar_wait(&H->full[slot], (jj / NS) & 1);
             const unsigned char* st = stages + (size_t)slot * S.stage_bytes;
-            const unsigned int meta = reinterpret_cast<const unsigned int*>(st)[t];
-            const int rl = meta & 255;
-            const int off = reinterpret_cast<const int*>(st + kBandMetaBytes)[wg];
             const double* sv = reinterpret_cast<const double*>(st + kBandMetaBytes + kBandOffBytes);
-            const int r0 = tile * kBlock;
-            const int i = r0 + rl;
             if constexpr (XF) {  // combine window tile tile + H + 1 (used from the next tile on)
                 const int u = tile + HB + 1;
                 if (u < ntiles && u * kBlock + t < P.n)
                     win[(u % RT) * kBlock + t] = op.band_xf(sv[Op::NV * kBlock + t], sv[(Op::NV + 1) * kBlock + t]);
             }
+            const int slice = Op::ND > 0 ? wg : (wg + jj / GR) & (kWarps - 1);
+            const unsigned int meta = reinterpret_cast<const unsigned int*>(st)[slice * 32 + lane];
+            const int rl = meta & 255;
+            const int off = reinterpret_cast<const int*>(st + kBandMetaBytes)[slice];
+            const int r0 = tile * kBlock;
+            const int i = r0 + rl;
             double tmp[Op::ND > 0 ? Op::ND : 1];
 #pragma unroll
             for (int d = 0; d < Op::ND; ++d) tmp[d] = 0.0;
             if (i < P.n) {
                 int tb = (tile - HB) % RT;
                 if (tb < 0) tb += RT;
-                const BandRow<NWIN == 2 ? CGVK_BAND_CHUNK2 : CGVK_BAND_CHUNK> R{P.band_va + off + lane, P.band_ci + off + lane, static_cast<int>(meta >> 8),
-                                tb * kBlock, RW};
+                const BandRow<NWIN == 2 ? CGVK_BAND_CHUNK2 : CGVK_BAND_CHUNK> R{
+                    P.band_va + off + lane, P.band_ci + off + lane, static_cast<int>(meta >> 8), tb * kBlock, RW};
                 op.row(P, i, BandIn{sv + rl, win, win + RW}, R, tmp);
             }
             __syncwarp();
