@@ -395,7 +395,8 @@ class SolveSet:
         self.mats = [cgvk.RankMatrix(A.n, lo, r, *cgvk.local_rows(Acsr, lo, r), device=device) for r in mine]
         for v in VARIANTS:
             g = cgvk.Group(self.comm, self.mats, cfgs[v], Precond.JACOBI,
-                           [b[lo[r]:lo[r + 1]] for r in mine], [x0[lo[r]:lo[r + 1]] for r in mine])
+                           [b[lo[r]:lo[r + 1]] for r in mine], [x0[lo[r]:lo[r + 1]] for r in mine],
+                           p2p=args.p2p)
             self.groups.append(g)
             self.solvers[v] = g.solvers[0]  # time_steps on member 0 steps the whole local group
 
@@ -536,8 +537,10 @@ def measure_config(args, cfg_name, rank, local, world, dist, extra=False) -> dic
     value = reps * total_iters / (total_ms * 1e-3)
     cfg = workload_config(cfg_name, P, world if partitioned else 1)
     if partitioned:
-        cfg["parallelism"] = (f"row-partitioned z-slabs over {world} GPUs (NCCL)" if world > 1 or args.nccl
-                              else f"row-partitioned, {args.emulate_ranks} in-process ranks on 1 GPU")
+        via = "peer memory (in-kernel stores + stamps)" if args.p2p else "NCCL"
+        cfg["parallelism"] = (f"row-partitioned z-slabs over {world} GPUs ({via})" if world > 1 or args.nccl
+                              else f"row-partitioned, {args.emulate_ranks} in-process ranks on 1 GPU"
+                                   + (" (peer-memory exchange)" if args.p2p else " (copy exchange)"))
     if fallback is not None:
         cfg["parallelism"] = f"{world} independent replicas (row-partitioned transport failed: {fallback})"
     elif extra and world > 1:
@@ -688,6 +691,8 @@ def main():
     ap.add_argument("--no-single-core", action="store_true")
     ap.add_argument("--nccl", action="store_true",
                     help="row-partitioned path over NCCL even at one rank (transport check)")
+    ap.add_argument("--p2p", action="store_true",
+                    help="row-partitioned solves exchange through peer memory inside the kernels (CGVK_GROUP_P2P)")
     ap.add_argument("--emulate-ranks", type=int, default=1,
                     help="row-partitioned solve with P in-process ranks on one GPU")
     args = ap.parse_args()

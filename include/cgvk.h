@@ -299,8 +299,14 @@ int cgvk_partition_rows(int64_t n, int nparts, int64_t align, int64_t* lo);
 int cgvk_halo_plan(int64_t n, int nranks, const int64_t* lo, int rank, const int64_t* row_ptr,
                    const int64_t* col_idx, int64_t* sizes4, int64_t* lower, int64_t* upper,
                    int64_t* send_lo, int64_t* send_hi);
+/* Rank-local column numbering of `rank`'s rows (global columns in col_idx,
+ * local row_ptr from 0): own columns first, then the lower and upper halo
+ * from *hbase = own rows rounded up to 32 (0 halo: *hbase = own rows).
+ * Host only; cgvk_matrix_create_rank uses exactly this numbering. */
+int cgvk_rank_local_columns(int64_t n, int nranks, const int64_t* lo, int rank, const int64_t* row_ptr,
+                            const int64_t* col_idx, int64_t* local_col_idx, int64_t* hbase);
 /* Rank-local matrix: rows [lo[rank], lo[rank+1]) in local numbering
- * [own | lower halo | upper halo]. */
+ * [own | pad | lower halo | upper halo] (cgvk_rank_local_columns). */
 int cgvk_matrix_create_rank(int64_t n, int nranks, int rank, const int64_t* lo, const int64_t* row_ptr,
                             const int64_t* col_idx, const double* values, int device, cgvk_matrix* out);
 /* NCCL transport (one process per GPU; libnccl.so.2 is dlopen'ed). */
@@ -313,6 +319,19 @@ int cgvk_comm_destroy(cgvk_comm c);
  * comm, its own for NCCL); b/x0 are the local rows. */
 int cgvk_group_create(cgvk_comm comm, int nlocal, const cgvk_matrix* As, const cgvk_variant_config* cfg,
                       int precond, const double* const* b, const double* const* x0, cgvk_solver* out);
+/* Group flags. CGVK_GROUP_P2P: the iteration exchanges halos and rank totals
+ * through peer memory inside the kernels (stores + stamps over NVLink, no
+ * NCCL call and no exchange launch per iteration; GV / pipe-PR fold their
+ * K1 reduction in the next K1, so it overlaps the SpMV). Needs z-slab-like
+ * ranks (send rows = a prefix and a suffix of the rank's rows), the CSR
+ * engine and <= 8 ranks; NCCL groups exchange CUDA IPC handles once.
+ * Bit-identical to the default transport. */
+enum { CGVK_GROUP_P2P = 1 };
+int cgvk_group_create_ex(cgvk_comm comm, int nlocal, const cgvk_matrix* As, const cgvk_variant_config* cfg,
+                         int precond, const double* const* b, const double* const* x0, int flags,
+                         cgvk_solver* out);
+/* CGVK_GROUP_P2P or 0 for a group member; -1 otherwise. */
+int cgvk_group_transport(cgvk_solver s);
 /* n_iters step() calls on every local rank (graph replays incl. exchanges). */
 int cgvk_group_step(const cgvk_solver* solvers, int nlocal, int n_iters);
 /* ||b - A x|| over all ranks. */

@@ -204,6 +204,9 @@ def _load() -> C.CDLL:
         "cgvk_comm_create_local": (I, [I, I, pp]),
         "cgvk_comm_destroy": (I, [P]),
         "cgvk_group_create": (I, [P, I, P, C.POINTER(_Config), I, P, P, P]),
+        "cgvk_group_create_ex": (I, [P, I, P, C.POINTER(_Config), I, P, P, I, P]),
+        "cgvk_group_transport": (I, [P]),
+        "cgvk_rank_local_columns": (I, [I64, I, P, I, P, P, P, C.POINTER(I64)]),
         "cgvk_group_step": (I, [P, I, I]),
         "cgvk_group_true_residual": (I, [P, I, C.POINTER(D)]),
         "cgvk_host_unregister": (I, [P]),
@@ -722,9 +725,21 @@ def halo_plan(n: int, lo, rank: int, row_ptr, col_idx) -> dict:
     return {k: a[: int(s)] for k, a, s in zip(names, arrs, sizes)}
 
 
+def rank_local_columns(n: int, lo, rank: int, row_ptr, col_idx):
+    """The device's rank-local numbering of `rank`'s rows (host only):
+    (local column indices, hbase) — own columns first, the lower then upper
+    halo from hbase (own rows rounded up to 32 when there is a halo)."""
+    lo, rp, ci = _i64(lo), _i64(row_ptr), _i64(col_idx)
+    out = np.empty(max(ci.shape[0], 1), np.int64)
+    hb = C.c_int64()
+    _check(_lib.cgvk_rank_local_columns(int(n), lo.shape[0] - 1, _ptr(lo), int(rank), _ptr(rp),
+                                        _ptr(ci) if ci.size else None, _ptr(out), C.byref(hb)))
+    return out[: ci.shape[0]], int(hb.value)
+
+
 class RankMatrix(DeviceMatrix):
     """Rows [lo[rank], lo[rank+1]) of a global n x n matrix, local numbering
-    [own | lower halo | upper halo] (cgvk_matrix_create_rank)."""
+    [own | pad | lower halo | upper halo] (cgvk_matrix_create_rank)."""
 
     def __init__(self, n: int, lo, rank: int, row_ptr, col_idx, values, device: int = 0):
         lo, rp, ci, va = _i64(lo), _i64(row_ptr), _i64(col_idx), _f64(values)
@@ -773,8 +788,10 @@ class Comm:
 class Group:
     """initialize() of one solve over the ranks this process drives."""
 
+    P2P = 1  # CGVK_GROUP_P2P: halos and rank totals through peer memory inside the kernels
+
     def __init__(self, comm: Comm, mats: list, config: VariantConfig, precond: Precond, bs: list,
-                 x0s: list):
+                 x0s: list, p2p: bool = False):
         self.comm, self.mats = comm, mats
         bs = [_f64(b) for b in bs]
         x0s = [_f64(x) for x in x0s]
@@ -784,8 +801,10 @@ class Group:
         xp = (C.c_void_p * nl)(*[_ptr(x) if x.size else None for x in x0s])
         out = (C.c_void_p * nl)()
         c = config._to_c()
-        _check(_lib.cgvk_group_create(comm._h, nl, hs, C.byref(c), int(precond), bp, xp, out))
+        _check(_lib.cgvk_group_create_ex(comm._h, nl, hs, C.byref(c), int(precond), bp, xp,
+                                         self.P2P if p2p else 0, out))
         self._handles = out
+        self.transport = "p2p" if _lib.cgvk_group_transport(out[0]) == self.P2P else comm.kind
         self.solvers = [Solver(config, m, precond, None, None, _handle=C.c_void_p(out[i]))
                         for i, m in enumerate(mats)]
 

@@ -110,9 +110,48 @@ cudaStream_t pool_stream() {
     return streams[dev];
 }
 
+// Plain (cudaMalloc) allocations: the vectors of a multi-process peer-memory
+// group must be IPC-shareable, which stream-ordered pool memory is not
+// (cgvk_group.inc). Set per thread while such a group allocates.
+bool& plain_alloc_mode() {
+    static thread_local bool on = false;
+    return on;
+}
+std::mutex& plain_mu() {
+    static std::mutex mu;
+    return mu;
+}
+std::vector<void*>& plain_set() {
+    static std::vector<void*> v;
+    return v;
+}
+int dalloc_plain(void** p, size_t bytes) {
+    const cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        return set_err(CGVK_ENOMEM, "device allocation (%zu bytes): %s", bytes, cudaGetErrorString(e));
+    }
+    std::lock_guard<std::mutex> lock(plain_mu());
+    plain_set().push_back(*p);
+    return CGVK_OK;
+}
+// true if p was a plain allocation (now freed)
+bool plain_release(void* p) {
+    {
+        std::lock_guard<std::mutex> lock(plain_mu());
+        auto& v = plain_set();
+        auto it = std::find(v.begin(), v.end(), p);
+        if (it == v.end()) return false;
+        v.erase(it);
+    }
+    cudaFree(p);
+    return true;
+}
+
 template <class T>
 int dalloc(T** p, size_t count) {
     if (count == 0) count = 1;
+    if (plain_alloc_mode()) return dalloc_plain(reinterpret_cast<void**>(p), sizeof(T) * count);
     cudaStream_t st = pool_stream();
     cudaError_t e = cudaMallocAsync((void**)p, sizeof(T) * count, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -125,7 +164,9 @@ int dalloc(T** p, size_t count) {
 }
 
 void dfree(void* p) {
-    if (p) cudaFreeAsync(p, pool_stream());
+    if (!p) return;
+    if (plain_release(p)) return;
+    cudaFreeAsync(p, pool_stream());
 }
 
 }  // namespace
@@ -141,7 +182,8 @@ struct cgvk_matrix_s {
     // row partition (rank-local matrices; a plain matrix is rank 0 of 1)
     int nranks = 1, rank = 0;
     int64_t gn = 0, glo = 0;        // global size, first global row
-    int64_t nlow = 0, nup = 0;      // halo columns: [n, n+nlow) lower, [n+nlow, ncols) upper
+    int64_t nlow = 0, nup = 0;      // halo columns: [hbase, hbase+nlow) lower, [hbase+nlow, ncols) upper
+    int64_t hbase = 0;              // first halo column: n rounded up to 32 (no cache line holds own rows and halo)
     int64_t nsend_lo = 0, nsend_hi = 0;
     int* send_lo = nullptr;         // local rows the lower neighbour's halo reads (sorted)
     int* send_hi = nullptr;         // local rows the upper neighbour's halo reads (sorted)
@@ -457,6 +499,7 @@ int matrix_create(int64_t n, int64_t ncols, const int64_t* row_ptr, const int64_
     a->device = device;
     a->n = n;
     a->ncols = ncols;
+    a->hbase = n;
     a->nnz = nnz;
     a->ntiles = (int)((n + kBlock - 1) / kBlock);
     a->order = env_int("CGVK_ORDER", 0) ? 1 : 0;
@@ -786,6 +829,7 @@ using FinalizeFn = void (*)(Params, const double*, int);
 // One pipelined kernel: function, stage configuration, grid, dynamic smem.
 struct KLaunch {
     StreamFn fn = nullptr;
+    StreamFn fn_peer = nullptr;  // the peer-memory rank form of fn (null: none)
     StageCfg S{};
     int grid = 1;
     int threads = kThreads;
@@ -822,6 +866,7 @@ struct cgvk_solver_s {
     double *rank_tot = nullptr, *all_tot = nullptr;
     double *sbuf_lo = nullptr, *sbuf_hi = nullptr, *rbuf_lo = nullptr, *rbuf_hi = nullptr;
     FinalizeFn fin1 = nullptr, fin2 = nullptr;
+    unsigned int* p2p_err = nullptr;  // peer-memory rank: the window's give-up flag (cgvk_group.inc)
 };
 
 namespace {
@@ -904,14 +949,20 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
     if constexpr (Op::CSR) {
         if (a->band_h >= 0) return make_band<Op, Prev>(a, L);
     }
+    constexpr int kMinb = Op::CSR ? CGVK_SPMV_MIN_CTAS : CGVK_K1_MIN_CTAS;
     L->fn = k_stream<Op, Prev>;
+    // the peer form's SpMV gathers may call out to the halo receive buffers:
+    // 2 CTAs' register budget (3 spill)
+    L->fn_peer = k_stream<Op, Prev, (Op::CSR && kMinb > 2 ? 2 : kMinb), true>;
     // register-capped build of an Op that has one (GV / pipe-PR K1: 72
     // registers, 3 CTAs/SM): only when the working set fits L2 and the
     // virtual CTAs outnumber two CTAs per SM (measured P64 GV 18.4 -> 17.5 us,
     // pipe-PR 19.4 -> 18.8; P2D, whose 256 tiles fit either grid, and P128 /
     // V256 are slower with it)
     if constexpr (MaxnregOf<Op>::value > 0)
-        if ((a->l2pol == 3 && a->G > 2 * a->sms) || env_int("CGVK_K1_NR", 0)) L->fn = k_stream_nr<Op, Prev>;
+        if ((a->l2pol == 3 && a->G > 2 * a->sms) || env_int("CGVK_K1_NR", 0)) {
+            L->fn = k_stream_nr<Op, Prev>;  // (the peer form keeps its registers: it spills under the cap)
+        }
     L->threads = kThreads;
     StageCfg S{};
     S.nvec = Op::NV;
@@ -934,6 +985,7 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
         // long rows: a 2-stage ring fills the SM -> one CTA with the full
         // register file (see k_stream's MINB)
         L->fn = k_stream<Op, Prev, 1>;
+        L->fn_peer = k_stream<Op, Prev, 1, true>;
         ctas = 1;
     }
     const int budget = kSmemPerSM / ctas - 2048;
@@ -948,6 +1000,7 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
     if (L->smem > (size_t)kSmemPerSM - 1024)
         return set_err(CGVK_EINVAL, "pipeline stage (%d bytes) exceeds shared memory", S.stage_bytes);
     TRY(raise_smem((const void*)L->fn, L->smem));
+    if (L->fn_peer) TRY(raise_smem((const void*)L->fn_peer, L->smem));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L->fn, kThreads, L->smem));
     if (occ < 1) return set_err(CGVK_ECUDA, "pipeline kernel does not fit on an SM");
@@ -972,7 +1025,8 @@ int pick_pair(cgvk_matrix a, cgvk_solver s) {
     s->k2c = s->k2;
     s->k2c.S.chain = CH_ON | CH_FOLD | CH_ODD;
     s->kt = KLaunch{};
-    s->kt.fn = k_chain_tail<Op2>;
+    s->kt.fn = k_chain_tail<Op1, Op2>;
+    s->kt.fn_peer = k_chain_tail<Op1, Op2, true>;
     s->kt.grid = 1;
     s->kt.threads = 32;
     s->kt.smem = 0;
@@ -1017,7 +1071,11 @@ int ref_allocated(int v, bool prec) {
 // may start its prologue (barrier init, matrix prefetch) while the previous
 // kernel drains, and synchronises with griddepcontrol.wait before reading its
 // results. CGVK_PDL=0 turns it off (for A/B measurements).
-cudaError_t launch(cgvk_solver s, const KLaunch& L) {
+cudaError_t launch_with(cudaStream_t st, const KLaunch& L, const Params& P);
+
+cudaError_t launch(cgvk_solver s, const KLaunch& L) { return launch_with(s->stream, L, s->P); }
+
+cudaError_t launch_with(cudaStream_t st, const KLaunch& L, const Params& P) {
     // measured (profiles/r01): PDL gains 3-5 % on every variant; HS's kernels
     // signal their dependents late (PdlLate), else HS loses ~10 % to it
     static const int pdl_env = env_int("CGVK_PDL", -1);
@@ -1026,13 +1084,13 @@ cudaError_t launch(cgvk_solver s, const KLaunch& L) {
     cfg.gridDim = dim3(L.grid);
     cfg.blockDim = dim3(L.threads);
     cfg.dynamicSmemBytes = L.smem;
-    cfg.stream = s->stream;
+    cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, L.fn, s->P, L.S);
+    return cudaLaunchKernelEx(&cfg, L.fn, P, L.S);
 }
 
 // The chained schedule is the default for graphs; CGVK_CHAIN=0 captures the
@@ -1079,7 +1137,10 @@ int capture(cgvk_solver s, int iters, cudaGraphExec_t* exec) {
 
 int refresh_mirror(cgvk_solver s) {
     CK(cudaMemcpyAsync(&s->mirror, s->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s->stream));
+    unsigned int err = 0;
+    if (s->p2p_err) CK(cudaMemcpyAsync(&err, s->p2p_err, sizeof err, cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
+    if (err) return set_err(CGVK_ECUDA, "peer-memory exchange: a wait for a neighbour gave up");
     s->mirror_fresh = true;
     return CGVK_OK;
 }

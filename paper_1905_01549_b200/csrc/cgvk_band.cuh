@@ -133,7 +133,7 @@ __device__ __forceinline__ void band_body(const Params& P, const StageCfg& S) {
     pdl_wait();
     pdl_trigger();
     const int chain = S.chain;
-    if (chain) chain_prologue<Prev>(P, chain, H, (chain & CH_ODD) ? P.ctrl : P.ctrl_b);
+    if (chain) chain_prologue<Op, Prev>(P, chain, H, (chain & CH_ODD) ? P.ctrl : P.ctrl_b);
     Op op;
     if (!(chain ? op.enter(with_ctrl(P, &H->cs)) : op.enter(P))) return;  // uniform over the grid
 

@@ -54,13 +54,46 @@ struct __align__(16) Ctrl {
     int hist_cap;
     unsigned int count[2];  // last-CTA arrival counters
     int init_stage;         // initialize(): 0, or the check that settled the status (1 nu0, 2 mu0)
-    unsigned int spare_[3];
+    // peer-memory exchange of a row-partitioned solve (cgvk_p2p.cuh): the
+    // kernel sequence number (+1 per chained K1 / K2, identical on every
+    // rank), and a GV / pipe-PR K1 reduction left to the next K1 (its stamp)
+    unsigned int hseq;
+    unsigned int defer;
+    unsigned int dstamp;
     // chained schedule (cgvk_stream.cuh chain_prologue): the folded totals of
     // the kernel that wrote this copy, for its successor's scalar tail
     double tot[kMaxDots];
     double pad_[2];
 };
 static_assert(sizeof(Ctrl) == 256, "the control block is two 128-byte lines");
+
+// Peer-memory exchange plan of one rank of a row-partitioned solve
+// (cgvk_p2p.cuh): the rank's chained kernels push their boundary rows into
+// the neighbours' receive buffers and their rank totals into every rank's
+// table as stamped 8-byte words; consumers check the stamps as they read.
+constexpr int kP2pSlots = 4;    // halo-exchanged vectors per variant (physical slots)
+constexpr int kP2pRanks = 8;    // ranks of one NVSwitch box
+constexpr int kP2pTotSlots = 4; // rank-total tables in flight (by stamp & 3)
+
+struct PeerPlan {
+    int on;                 // 1: the chained kernels of this rank exchange through peer memory
+    int nranks, rank;
+    int psel;               // HS: physical slots 1 / 2 = p0 / p1, p_old chosen by ctrl->pcur
+    int tlo, hi_first;      // boundary tiles: [0, tlo) hold rows sent to the lower neighbour,
+                            // [hi_first, ntiles) rows sent to the upper
+    int nlo, hi0;           // send rows [0, nlo) -> lower neighbour, [hi0, n) -> upper
+    int hbase;              // first halo column (local numbering)
+    int rx_stride;          // receive entries per parity: nlow + nup
+    int lo_off, lo_stride;  // lower neighbour: where my rows land in its buffer (its nlow), its stride
+    int hi_stride;          // upper neighbour's stride (my rows land at its 0)
+    int push;               // physical slots this rank's vectors feed (bit q)
+    double* hv[kP2pSlots];                  // this rank's halo-exchanged vectors (physical slots)
+    unsigned long long* rx[kP2pSlots];      // mine: [2 parities][rx_stride] entries of 2 words
+    unsigned long long* rx_lo[kP2pSlots];   // the lower neighbour's receive buffers (null: none)
+    unsigned long long* rx_hi[kP2pSlots];   // the upper neighbour's
+    unsigned int* err;      // set when a wait gives up
+    double* xtot_peer[kP2pRanks];  // every rank's total tables
+};
 
 struct Params {
     int n, ntiles;
@@ -97,6 +130,7 @@ struct Params {
     int l2pol;  // TMA L2 policy: 0 evict_first everything, 1 only the matrix, 2 none
     int dist;          // rank of a row-partitioned solve: reducing kernels stop at the
     double* rank_tot;  // rank-local totals [kMaxDots]; k_finalize folds all ranks
+    const PeerPlan* pp;  // chained rank kernels exchanging through peer memory (device copy; null: off)
 };
 
 // Balanced contiguous partition: part k of `parts` covers [lo(k), lo(k+1)).

@@ -1,0 +1,201 @@
+// Peer-memory exchange of a row-partitioned solve (north star
+// (3)): NVLink P2P stores from the producing kernel and stamped reads in the
+// consuming kernel — no NCCL call, no exchange or finalize launch, and no
+// memory fence inside the iteration.
+//
+// A rank's chained kernels (cgvk_stream.cuh, CSR engine, z-slab partitions:
+// a rank sends a row prefix to its lower and a row suffix to its upper
+// neighbour) carry a kernel sequence number `hseq` in the control block —
+// +1 per K1 / K2, identical on every rank because every rank runs the same
+// schedule on bit-identical scalars. Everything exchanged travels as "LL"
+// words (NCCL's low-latency idea): 32 data bits + the 32-bit stamp (the
+// producer's hseq) in one 8-byte store, so a reader that sees the stamp it
+// expects in a word has that word's data — no fence on either side.
+//
+//  * halo: a kernel that updates a halo-exchanged vector pushes its boundary
+//    rows into the neighbour's receive buffer (two words per double, parity
+//    buffer (stamp >> 1) & 1). The consumer's SpMV gathers a halo column
+//    (j >= hbase) from that buffer, spinning until the stamp is the one it
+//    expects (its own hseq minus the slot's distance). Only boundary rows
+//    read the halo, so the interior SpMV never waits: it overlaps the
+//    exchange by construction.
+//  * rank totals: the reducing kernel's last CTA writes its rank-local total
+//    into table (stamp & 3) of every rank; the successor's prologue (warp 0)
+//    polls the words and folds the totals in rank order from 0.0 — the
+//    oracle's ORC_DOT_PART order, so every rank runs the scalar tail on
+//    identical bits. GV's and pipe-PR's K1 reductions are not waited for by
+//    K2 (their SpMV needs no scalar): K2 takes the go-ahead (dist_mark) and
+//    the NEXT K1 folds them — Table 1's max(C_gr, T_mv + C_mv).
+//  * buffer reuse: a producer writes a halo buffer parity again two
+//    iterations later, after folding a reduction that the consumer published
+//    only after it had finished reading it (every variant reduces at least
+//    once per iteration, in a kernel after the consumer in stream order), so
+//    no ack or back-pressure flag is needed.
+//
+// Every wait is bounded: a wait that gives up sets pp.err (the host reports
+// CGVK_ECUDA) and the kernel proceeds, so a broken peer never hangs the GPU.
+#pragma once
+
+#include "cgvk_device.cuh"
+
+namespace cgvk {
+
+// Memory scope of the exchange: system (peers on other GPUs over NVLink). An
+// A/B build may use -DCGVK_P2P_SCOPE=gpu for in-process ranks on one device.
+#ifndef CGVK_P2P_SCOPE
+#define CGVK_P2P_SCOPE sys
+#endif
+#define CGVK_STR2(x) #x
+#define CGVK_STR(x) CGVK_STR2(x)
+#define CGVK_SCOPE_S CGVK_STR(CGVK_P2P_SCOPE)
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed." CGVK_SCOPE_S ".global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void ld_relaxed_v2u64(const unsigned long long* p, unsigned long long& a,
+                                                 unsigned long long& b) {
+    asm volatile("ld.relaxed." CGVK_SCOPE_S ".global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+
+__device__ __forceinline__ void st_relaxed_v2u64(unsigned long long* p, unsigned long long a, unsigned long long b) {
+    asm volatile("st.relaxed." CGVK_SCOPE_S ".global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+
+constexpr long long kP2pSpinNs = 2000000000ll;  // give up after ~2 s
+
+__device__ __forceinline__ long long gtimer_ns() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// LL words: stamp in the high half, 32 data bits in the low half.
+__device__ __forceinline__ unsigned long long ll_word(unsigned int stamp, unsigned int data) {
+    return ((unsigned long long)stamp << 32) | data;
+}
+
+// ------------------------------------------------------------ rank totals
+// Table of rank q: [kP2pTotSlots][kP2pRanks][kLLWords] words.
+constexpr int kLLWords = 2 * kMaxDots;
+
+__device__ __forceinline__ unsigned long long* ll_table(double* base) {
+    return reinterpret_cast<unsigned long long*>(base);
+}
+
+// Warp 0 (all lanes): the totals stamped `stamp`, summed in rank order from
+// 0.0 into lane 0's tot[]. scratch: >= kP2pRanks * kLLWords 32-bit words of
+// shared memory.
+template <int ND>
+__device__ __noinline__ void p2p_fold_totals(const PeerPlan* P2, unsigned int stamp, double* tot,
+                                             unsigned int* scratch) {
+    const PeerPlan& pp = *P2;
+    const int lane = threadIdx.x & 31;
+    const unsigned long long* tab =
+        ll_table(pp.xtot_peer[pp.rank]) + (size_t)(stamp & (kP2pTotSlots - 1)) * kP2pRanks * kLLWords;
+    const int nw = pp.nranks * kLLWords;
+    long long t0 = 0;
+    for (int spin = 0;; ++spin) {
+        bool ok = true;
+        for (int q = lane; q < nw; q += 32) {
+            if ((q % kLLWords) >= 2 * ND) continue;
+            const unsigned long long w = ld_relaxed_u64(tab + q);
+            if ((unsigned int)(w >> 32) == stamp) scratch[q] = (unsigned int)w;
+            else ok = false;
+        }
+        if (__all_sync(0xffffffffu, ok)) break;
+        if (spin == 0) t0 = gtimer_ns();
+        else if ((spin & 255) == 0 && gtimer_ns() - t0 > kP2pSpinNs) {
+            if (lane == 0) atomicExch(pp.err, 1u);
+            break;
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll
+        for (int d = 0; d < kMaxDots; ++d) tot[d] = 0.0;
+        for (int r = 0; r < pp.nranks; ++r) {
+#pragma unroll
+            for (int d = 0; d < ND; ++d) {
+                const unsigned int* w = scratch + r * kLLWords + 2 * d;
+                tot[d] = ADD(tot[d], __hiloint2double((int)w[1], (int)w[0]));
+            }
+        }
+    }
+    __syncwarp();
+}
+
+// One thread (the reducing kernel's last CTA): this rank's total into every
+// rank's table (stamp & 3).
+template <int ND>
+__device__ __noinline__ void p2p_publish_totals(const PeerPlan* P2, unsigned int stamp, const double* tot) {
+    const PeerPlan& pp = *P2;
+    const size_t off = ((size_t)(stamp & (kP2pTotSlots - 1)) * kP2pRanks + pp.rank) * kLLWords;
+    for (int r = 0; r < pp.nranks; ++r) {
+        unsigned long long* dst = ll_table(pp.xtot_peer[r]) + off;
+#pragma unroll
+        for (int d = 0; d < ND; ++d)
+            st_relaxed_v2u64(dst + 2 * d, ll_word(stamp, (unsigned int)__double2loint(tot[d])),
+                             ll_word(stamp, (unsigned int)__double2hiint(tot[d])));
+    }
+}
+
+// ------------------------------------------------------------------- halo
+
+__device__ __forceinline__ int ll_parity(unsigned int stamp) { return (stamp >> 1) & 1; }
+
+// physical slot of HS's p_old (the other p buffer is p_new)
+__device__ __forceinline__ int p2p_pold(int pcur) { return pcur ? 2 : 1; }
+
+// A launch's push mask: physical slots, kPushPnew = HS's p_new (by pcur).
+constexpr unsigned int kPushPnew = 1u << 4;
+__device__ __forceinline__ unsigned int p2p_push_mask(unsigned int m, int pcur) {
+    if (m & kPushPnew) m = (m & ~kPushPnew) | (1u << (3 - p2p_pold(pcur)));
+    return m;
+}
+
+// The thread's row i of every vector in `mask` (physical slots) into the
+// neighbours' receive buffers, stamped h — the value the thread itself just
+// stored (re-read from L2). Rows outside the send prefix / suffix: nothing.
+__device__ __noinline__ void p2p_push_row(const PeerPlan* P2, unsigned int mask, int i, int n, unsigned int h) {
+    const PeerPlan& pp = *P2;
+    const bool lo = i < pp.nlo, hi = i >= pp.hi0 && i < n;
+    if (!lo && !hi) return;
+    const int par = ll_parity(h);
+    for (int q = 0; q < kP2pSlots; ++q) {
+        if (!((mask >> q) & 1)) continue;
+        const double v = __ldcg(pp.hv[q] + i);
+        const unsigned long long w0 = ll_word(h, (unsigned int)__double2loint(v));
+        const unsigned long long w1 = ll_word(h, (unsigned int)__double2hiint(v));
+        if (lo && pp.rx_lo[q])
+            st_relaxed_v2u64(pp.rx_lo[q] + 2 * ((size_t)par * pp.lo_stride + pp.lo_off + i), w0, w1);
+        if (hi && pp.rx_hi[q])
+            st_relaxed_v2u64(pp.rx_hi[q] + 2 * ((size_t)par * pp.hi_stride + (i - pp.hi0)), w0, w1);
+    }
+}
+
+// Halo column e = j - hbase of the vector `g` (one of pp.hv) as this kernel
+// (sequence number h) expects it: spin until both words carry the stamp.
+__device__ __noinline__ double p2p_halo_wait(const PeerPlan* P2, const double* g, int e, unsigned int h,
+                                             int pcur) {
+    const PeerPlan& pp = *P2;
+    int q = 0;
+    while (q < kP2pSlots - 1 && pp.hv[q] != g) ++q;
+    const unsigned int want = h - ((pp.psel && q == p2p_pold(pcur)) ? 2u : 1u);
+    const unsigned long long* w = pp.rx[q] + 2 * ((size_t)ll_parity(want) * pp.rx_stride + e);
+    long long t0 = gtimer_ns();
+    for (int spin = 0;; ++spin) {
+        unsigned long long a, b;
+        ld_relaxed_v2u64(w, a, b);
+        if ((unsigned int)(a >> 32) == want && (unsigned int)(b >> 32) == want)
+            return __hiloint2double((int)(unsigned int)b, (int)(unsigned int)a);
+        if ((spin & 255) == 255 && gtimer_ns() - t0 > kP2pSpinNs) {
+            atomicExch(pp.err, 1u);
+            return 0.0;
+        }
+    }
+}
+
+}  // namespace cgvk

@@ -23,6 +23,7 @@
 #pragma once
 
 #include "cgvk_device.cuh"
+#include "cgvk_p2p.cuh"
 
 #include <type_traits>
 
@@ -104,6 +105,7 @@ struct StageCfg {
     int ring;       // band engine: window ring tiles (2H + nstage)
     int pf;         // band engine: L2 prefetch distance (tiles)
     int chain;      // chained schedule: CH_* bits (0: last-CTA finish, in place)
+    unsigned int p2p_push;  // peer ranks: physical halo slots this launch pushes (kPushPnew: HS's p_new)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -423,6 +425,25 @@ struct StagedIn {
     }
 };
 
+// Peer-memory ranks (cgvk_p2p.cuh): halo columns (j >= hb) come from the
+// stamped receive buffers, the rest as in StagedIn.
+struct PeerIn {
+    const double* sv;
+    const PeerPlan* pp;
+    int hb;
+    unsigned int h;
+    int pcur;
+    __device__ __forceinline__ double operator()(int v) const { return sv[v * kBlock]; }
+    __device__ __forceinline__ double gather(int, int j, const double* __restrict__ g) const {
+        return j < hb ? __ldg(g + j) : p2p_halo_wait(pp, g, j - hb, h, pcur);
+    }
+    __device__ __forceinline__ double gather_p(int j, const double* __restrict__ rt, const double* __restrict__ po,
+                                               double beta) const {
+        if (j < hb) return ADD(__ldg(rt + j), MUL(beta, __ldg(po + j)));
+        return ADD(p2p_halo_wait(pp, rt, j - hb, h, pcur), MUL(beta, p2p_halo_wait(pp, po, j - hb, h, pcur)));
+    }
+};
+
 // Optional Op trait for the band engine: `static constexpr bool BAND_XF` — the
 // window holds band_xf(source 0, source 1) instead of the NG raw sources.
 template <class T, class = void>
@@ -613,8 +634,15 @@ constexpr int kCtrlHead = offsetof(Ctrl, tot) / 16;
 // copy, which would queue behind the producer's matrix prefetch in the TMA
 // unit; thread 0 runs the predecessor's finish on it; CTA 0 writes the
 // advanced state to `out`.
-template <class Prev>
-__device__ __forceinline__ void chain_prologue(const Params& P, int chain, PipeHeader* H, Ctrl* out) {
+//
+// Peer-memory ranks (P.pp.on, cgvk_p2p.cuh): the predecessor's totals are the
+// rank-ordered sum of every rank's published total (waited for by stamp); a
+// K2 whose predecessor has a dist_mark (GV / pipe-PR) takes the go-ahead and
+// leaves the K1 reduction to the next K1 (`defer`), which folds it first with
+// its own type (Self); `incr` advances the kernel sequence number.
+template <class Self, class Prev, bool PEER = false>
+__device__ __forceinline__ void chain_prologue(const Params& P, int chain, PipeHeader* H, Ctrl* out,
+                                               bool incr = true) {
     const int t = threadIdx.x;
     if (t < 32) {
         constexpr int kWords = sizeof(Ctrl) / 16;
@@ -622,8 +650,8 @@ __device__ __forceinline__ void chain_prologue(const Params& P, int chain, PipeH
         if (t < kWords) reinterpret_cast<uint4*>(&H->cs)[t] = __ldcg(in + t);
         __syncwarp();
     }
-    if (t == 0) {
-        if (chain & CH_FOLD) {
+    if constexpr (!PEER) {
+        if (t == 0 && (chain & CH_FOLD)) {
             Params Q = with_ctrl(P, &H->cs);
             if (blockIdx.x != 0) Q.hist = nullptr;  // side effects once
             Prev prev;
@@ -637,18 +665,69 @@ __device__ __forceinline__ void chain_prologue(const Params& P, int chain, PipeH
                 }
             }
         }
+    } else if (t < 32) {
+        // warp 0: every lane evaluates the (read-only) enter() decisions on
+        // the shared copy, the warp polls the exchanged totals together,
+        // lane 0 runs finish(); __syncwarp between lane 0's writes and the
+        // next reads
+        unsigned int* scratch = reinterpret_cast<unsigned int*>(H->red);
+        if (chain & CH_FOLD) {
+            Params Q = with_ctrl(P, &H->cs);
+            if (blockIdx.x != 0) Q.hist = nullptr;
+            if constexpr (HasDistMark<Self>::value) {
+                if (H->cs.defer) {  // the K1 reduction one iteration back (GV / pipe-PR)
+                    Self self;
+                    const bool go = self.enter(Q) && self.sync() == 2;
+                    double tot[kMaxDots];
+                    if (go) p2p_fold_totals<Self::ND>(P.pp, H->cs.dstamp, tot, scratch);
+                    if (t == 0) {
+                        if (go) self.finish(Q, &H->cs, tot);
+                        H->cs.defer = 0;
+                    }
+                    __syncwarp();
+                }
+            }
+            Prev prev;
+            if (prev.enter(Q)) {
+                const int m = prev.sync();
+                if (m == 2) {
+                    bool deferred = false;
+                    if constexpr (HasDistMark<Prev>::value) {
+                        if (chain & CH_ODD) {  // K2: take the go-ahead, the next K1 folds
+                            if (t == 0) {
+                                prev.dist_mark(Q, &H->cs);
+                                H->cs.defer = 1;
+                                H->cs.dstamp = H->cs.hseq;
+                            }
+                            deferred = true;
+                        }
+                    }
+                    if (!deferred) {
+                        double tot[kMaxDots];
+                        p2p_fold_totals<Prev::ND>(P.pp, H->cs.hseq, tot, scratch);
+                        if (t == 0) prev.finish(Q, &H->cs, tot);
+                    }
+                } else if (m == 1) {
+                    const double none[kMaxDots] = {};
+                    if (t == 0) prev.finish(Q, &H->cs, none);
+                }
+            }
+            __syncwarp();
+        }
+        if (t == 0 && incr) H->cs.hseq += 1;
     }
     __syncthreads();
     if (blockIdx.x == 0 && t < kCtrlHead)
         reinterpret_cast<uint4*>(out)[t] = reinterpret_cast<const uint4*>(&H->cs)[t];
 }
 
-// The chained graph's last node: the final K2's scalar tail.
-template <class Prev>
+// The chained graph's last node: the final K2's scalar tail (and, on
+// peer-memory ranks, a GV / pipe-PR K1 reduction K2 deferred).
+template <class Op1, class Op2, bool PEER = false>
 __global__ void __launch_bounds__(32) k_chain_tail(Params P, StageCfg) {
     __shared__ __align__(128) PipeHeader H;
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    chain_prologue<Prev>(P, CH_ON | CH_FOLD, &H, P.ctrl);
+    chain_prologue<Op1, Op2, PEER>(P, CH_ON | CH_FOLD, &H, P.ctrl, /*incr=*/false);
 }
 
 // Programmatic dependent launch: wait for the preceding kernel's results /
@@ -801,12 +880,14 @@ __device__ __forceinline__ uint64_t staged_policy(const Op& op, const Params& P,
 #ifndef CGVK_K1_MIN_CTAS
 #define CGVK_K1_MIN_CTAS 1  // register budget of the update kernels (resident CTAs)
 #endif
-template <class Op, class Prev>
+template <class Op, class Prev, bool PEER>
 __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S);
 
-template <class Op, class Prev, int MINB = (Op::CSR ? CGVK_SPMV_MIN_CTAS : CGVK_K1_MIN_CTAS)>
+// PEER: the peer-memory rank form (cgvk_p2p.cuh), a separate instantiation so
+// the single-GPU kernels carry none of its code or registers.
+template <class Op, class Prev, int MINB = (Op::CSR ? CGVK_SPMV_MIN_CTAS : CGVK_K1_MIN_CTAS), bool PEER = false>
 __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S) {
-    stream_body<Op, Prev>(P, S);
+    stream_body<Op, Prev, PEER>(P, S);
 }
 
 // The same kernel under an explicit register cap (__maxnreg__ cannot be
@@ -820,12 +901,12 @@ template <class T>
 struct MaxnregOf<T, std::void_t<decltype(T::MAXNREG)>> {
     static constexpr int value = T::MAXNREG;
 };
-template <class Op, class Prev>
+template <class Op, class Prev, bool PEER = false>
 __global__ void __maxnreg__(MaxnregOf<Op>::value > 0 ? MaxnregOf<Op>::value : 255) k_stream_nr(Params P, StageCfg S) {
-    stream_body<Op, Prev>(P, S);
+    stream_body<Op, Prev, PEER>(P, S);
 }
 
-template <class Op, class Prev>
+template <class Op, class Prev, bool PEER>
 __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PipeHeader* H = reinterpret_cast<PipeHeader*>(smem_raw);
@@ -911,11 +992,24 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
     if (!PdlLate<Op>::value) pdl_trigger();
     const int chain = S.chain;
     if (chain) {
-        chain_prologue<Prev>(P, chain, H, (chain & CH_ODD) ? P.ctrl : P.ctrl_b);
+        chain_prologue<Op, Prev, PEER>(P, chain, H, (chain & CH_ODD) ? P.ctrl : P.ctrl_b);
         tl_mark(Op::CSR, 5);
     }
     Op op;
     if (!(chain ? op.enter(with_ctrl(P, &H->cs)) : op.enter(P))) {  // uniform over the grid
+        if (PEER && threadIdx.x < kConsumers) {
+            // peer ranks: the neighbours still get this kernel's stamp on the
+            // (unchanged) boundary rows, as a single-GPU solve would read them
+            // (HS: both p buffers — the next p_old is this kernel's p_old)
+            const unsigned int mask = (S.p2p_push & kPushPnew) ? 6u : p2p_push_mask(S.p2p_push, H->cs.pcur);
+            const int tlo = P.pp->tlo, hif = P.pp->hi_first;
+            CGVK_FOR_VB(vb, P.order, blockIdx.x, Gv, Gp) {
+                CGVK_FOR_TILE(tile, P.order, vb, ntiles, Gv) {
+                    if (mask && (tile < tlo || tile >= hif))
+                        p2p_push_row(P.pp, mask, tile * kBlock + (int)threadIdx.x, P.n, H->cs.hseq);
+                }
+            }
+        }
         if (producer) {  // drain the prefetch before the CTA exits
             for (int q = 0; q < max(npre, nearly); ++q) {
                 if (q >= nearly) mbar_arrive(&H->full[q]);
@@ -983,7 +1077,17 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
     const int t = threadIdx.x;
     double acc[Op::ND > 0 ? Op::ND : 1];
     int j = 0;
+    // peer ranks (cgvk_p2p.cuh): after a boundary tile, its rows of the pushed
+    // vectors go to the neighbours (out of line: the common path only compares
+    // the tile); halo columns are gathered from the receive buffers (PeerIn)
+    const PeerPlan* const pp = P.pp;
+    const int p2p_tlo = PEER ? __ldg(&pp->tlo) : 0, p2p_hif = PEER ? __ldg(&pp->hi_first) : 0x7fffffff;
+    const int p2p_hb = PEER ? __ldg(&pp->hbase) : 0x7fffffff;
+    const unsigned int p2p_h = PEER ? H->cs.hseq : 0u;
+    const int p2p_pc = PEER ? H->cs.pcur : 0;
+    const unsigned int p2p_mask = PEER ? p2p_push_mask(S.p2p_push, p2p_pc) : 0u;
     auto consume_tile = [&](int slot, int tile) {
+        const bool pb = PEER && p2p_mask && (tile < p2p_tlo || tile >= p2p_hif);
         StageView V = stage_view(stages, S, slot);
         const int i = tile * kBlock + t;
         if (i < P.n) {
@@ -999,10 +1103,12 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
                     R.ci = V.ci + (b - H->k0c[slot]);
                 }
             }
-            op.row(P, i, StagedIn{V.vec + t}, R, acc);
+            if constexpr (PEER) op.row(P, i, PeerIn{V.vec + t, pp, p2p_hb, p2p_h, p2p_pc}, R, acc);
+            else op.row(P, i, StagedIn{V.vec + t}, R, acc);
         }
         __syncwarp();
         if ((t & 31) == 0) mbar_arrive(&H->empty[slot]);
+        if (pb) p2p_push_row(pp, p2p_mask, i, P.n, p2p_h);
     };
     double* const part = P.part;
     auto close_vb = [&](int vb) {
@@ -1087,8 +1193,12 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
     if (t == 0) *counter = 0u;
     if (chain) {  // the totals; the next kernel runs the scalar tail
         if (t == 0) {
+            if constexpr (PEER) {
+                p2p_publish_totals<Op::ND>(P.pp, H->cs.hseq, tot);
+            } else {
 #pragma unroll
-            for (int d = 0; d < Op::ND; ++d) ((chain & CH_ODD) ? P.ctrl : P.ctrl_b)->tot[d] = tot[d];
+                for (int d = 0; d < Op::ND; ++d) ((chain & CH_ODD) ? P.ctrl : P.ctrl_b)->tot[d] = tot[d];
+            }
         }
         tl_mark(Op::CSR, 6);
         return;

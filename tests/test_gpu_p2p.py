@@ -1,0 +1,146 @@
+"""Peer-memory exchange of a row-partitioned solve (CGVK_GROUP_P2P,
+csrc/cgvk_p2p.cuh): the chained kernels push boundary rows into the
+neighbours' halo regions and rank totals into every rank's table with
+stamps, and wait on the stamps inside the kernel — no exchange launch, no
+finalize launch. On one GPU the ranks run in this process (their peers'
+memory is this device's); every wait is then already satisfied in stream
+order, so the test exercises the data path and the stamp protocol, not the
+overlap. Every rank's state must be bit-identical to the oracle restatement
+with partitioned dots (ORC_DOT_PART), as the copy transport is."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1905_01549_b200 import cgvk, problems as pb
+from paper_1905_01549_b200.cgvk import Precond, Variant, Vec
+
+from helpers import ALL_VARIANTS
+from test_gpu_group import compare
+
+pytestmark = pytest.mark.gpu
+
+PROBLEMS = {
+    "poisson3d_12_slabs": (lambda: pb.poisson3d(12), 144),
+    "poisson3d_16_slabs": (lambda: pb.poisson3d(16), 256),
+}
+_cache = {}
+
+
+def problem(name):
+    if name not in _cache:
+        make, align = PROBLEMS[name]
+        _cache[name] = (pb.make_problem(name, make()), align)
+    return _cache[name]
+
+
+def make_group(P, align, nranks, variant, precond, cfg_kwargs=None, p2p=True):
+    A = P.A
+    lo = cgvk.partition_rows(A.n, nranks, align)
+    mats = [cgvk.RankMatrix(A.n, lo, r, *cgvk.local_rows(A, lo, r)) for r in range(nranks)]
+    comm = cgvk.Comm(nranks)
+    cfg = cgvk.VariantConfig.make(variant)
+    for k, v in (cfg_kwargs or {}).items():
+        setattr(cfg, k, v)
+    g = cgvk.Group(comm, mats, cfg, precond, [P.b[lo[r]:lo[r + 1]] for r in range(nranks)],
+                   [P.x0[lo[r]:lo[r + 1]] for r in range(nranks)], p2p=p2p)
+    return g, lo, mats, comm, cfg
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 4])
+@pytest.mark.parametrize("precond", [Precond.IDENTITY, Precond.JACOBI])
+@pytest.mark.parametrize("variant", ALL_VARIANTS)
+def test_p2p_bit_exact_vs_partitioned_oracle(variant, precond, nranks):
+    P, align = problem("poisson3d_12_slabs")
+    g, lo, mats, comm, cfg = make_group(P, align, nranks, variant, precond)
+    assert g.transport == "p2p"
+    block, gmax, order = mats[0].reduction_config()
+    o = O.Restatement(P.A, int(variant), int(precond), P.b, P.x0, dot=("part", block, gmax, lo, order))
+    tag = f"p2p/{variant.name}/{precond.name}/P{nranks}"
+    compare(g, o, tag + " init")
+    for k in range(1, 16):
+        if o.state()["state"] != 0:
+            break
+        g.step(1)
+        g.sync()
+        o.step()
+        if k % 5 == 0 or o.state()["state"] != 0:
+            compare(g, o, f"{tag} k={k}")
+    g.close()
+
+
+@pytest.mark.parametrize("variant", ALL_VARIANTS)
+def test_p2p_eight_ranks_batched_graphs(variant):
+    """8 ranks (one NVSwitch box), graph-replayed batches of 8 and 1
+    iterations (the chained graphs with their tails): bit-equal to single
+    steps of the copy transport and to the partitioned oracle."""
+    P, align = problem("poisson3d_16_slabs")
+    g, lo, mats, comm, cfg = make_group(P, align, 8, variant, Precond.JACOBI)
+    h, *_ = make_group(P, align, 8, variant, Precond.JACOBI, p2p=False)
+    block, gmax, order = mats[0].reduction_config()
+    o = O.Restatement(P.A, int(variant), 1, P.b, P.x0, dot=("part", block, gmax, lo, order))
+    done = 0
+    for k in (8, 1, 8, 3, 8):
+        g.step(k)
+        h.step(k)
+        g.sync()
+        h.sync()
+        for _ in range(k):
+            if o.state()["state"] == 0:
+                o.step()
+        done += k
+        compare(g, o, f"p2p8/{variant.name} after {done}")
+    for w in (Vec.X, Vec.R):
+        assert np.array_equal(g.vector(w).view(np.int64), h.vector(w).view(np.int64))
+    np.testing.assert_array_equal(g.solvers[0].history(), h.solvers[0].history())
+    g.close()
+    h.close()
+
+
+@pytest.mark.parametrize("kw", [{"recompute_w": False}, {"nu_expression": cgvk.NuExpression.EXPANDED},
+                                {"unsimplified_mu": True}])
+@pytest.mark.parametrize("variant", [Variant.PIPE_PR, Variant.GV])
+def test_p2p_ablations(variant, kw):
+    if variant == Variant.GV and "recompute_w" in kw:
+        pytest.skip("recompute_w is a pipe-PR flag")
+    P, align = problem("poisson3d_12_slabs")
+    try:
+        g, lo, mats, comm, cfg = make_group(P, align, 3, variant, Precond.JACOBI, kw)
+    except cgvk.InvalidArgument:
+        pytest.skip("configuration not valid for this variant")
+    block, gmax, order = mats[0].reduction_config()
+    o = O.Restatement(P.A, int(variant), 1, P.b, P.x0, dot=("part", block, gmax, lo, order),
+                      nu_expr=int(cfg.nu_expression), recompute_w=cfg.recompute_w,
+                      unsimplified_mu=cfg.unsimplified_mu)
+    for _ in range(10):
+        g.step(1)
+        g.sync()
+        o.step()
+    compare(g, o, f"p2p ablation {variant.name} {kw}")
+    g.close()
+
+
+def test_p2p_true_residual_and_tolerance_stop():
+    """A solve to ||r|| <= 1e-8 ||b|| through the peer-memory iteration: the
+    stop and the true residual equal the copy transport's."""
+    P, align = problem("poisson3d_16_slabs")
+    out = []
+    for p2p in (True, False):
+        g, *_ = make_group(P, align, 4, Variant.PIPE_PR, Precond.JACOBI, p2p=p2p)
+        for s in g.solvers:
+            s.set_tolerance(1e-8)
+        g.step(400)
+        g.sync()
+        st = g.solvers[0]._status()[0]
+        out.append((st.k, st.state, g.true_residual(), g.vector(Vec.X)))
+        g.close()
+    assert out[0][:3] == out[1][:3]
+    assert out[0][1] == 3  # converged
+    assert np.array_equal(out[0][3], out[1][3])
+
+
+def test_p2p_rejects_scattered_send_rows():
+    """A random-band partition sends scattered rows (not a prefix / suffix):
+    the peer-memory transport refuses it loudly instead of falling back."""
+    R = pb.make_problem("rs", pb.random_spd(3000, 13, 300, 7))
+    with pytest.raises(cgvk.InvalidArgument, match="prefix"):
+        make_group(R, 1, 2, Variant.HS, Precond.JACOBI)

@@ -138,3 +138,110 @@ def test_gloo_distributed_spmv_and_dot(world):
     for rank, y, tot in res:
         assert np.array_equal(y.view(np.int64), y_ref.view(np.int64))
         assert tot == want
+
+
+def _worker_lib(rank, world, port, q):
+    """The product's host logic on each process (libcgvk, no GPU): partition,
+    halo plan and the device's local numbering (cgvk_rank_local_columns,
+    exactly what cgvk_matrix_create_rank uploads); the halo moves as the
+    peer-memory transport moves it (a rank's send rows are a prefix / suffix
+    of its rows, landing at the neighbour's hbase + offset)."""
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        P = pb.make_problem("p3", pb.poisson3d(12))
+        A = P.A
+        lo = cgvk.partition_rows(A.n, world, 144)
+        rp, ci, va = cgvk.local_rows(A, lo, rank)
+        h = cgvk.halo_plan(A.n, lo, rank, rp, ci)
+        loc, hb = cgvk.rank_local_columns(A.n, lo, rank, rp, ci)
+        m = int(lo[rank + 1] - lo[rank])
+        nl, nu = len(h["lower"]), len(h["upper"])
+        # z-slabs: send rows are exactly a prefix and a suffix (peer-memory eligible)
+        assert np.array_equal(h["send_lo"], np.arange(len(h["send_lo"])))
+        assert np.array_equal(h["send_hi"], np.arange(m - len(h["send_hi"]), m))
+        assert hb == ((m + 31) // 32 * 32 if nl + nu else m)
+        x = P.x_star[lo[rank]:lo[rank + 1]]
+        xloc = np.full(hb + nl + nu, np.nan)  # the pad is never read
+        xloc[:m] = x
+        sizes = torch.tensor([len(h["send_lo"]), len(h["send_hi"]), nl, nu], dtype=torch.int64)
+        allsz = [torch.zeros(4, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(allsz, sizes)
+        if rank > 0:  # the lower neighbour's suffix is my lower halo, and I am its upper halo
+            assert int(allsz[rank - 1][1]) == nl and int(allsz[rank - 1][3]) == len(h["send_lo"])
+        reqs = []
+        if rank > 0:
+            reqs.append(dist.isend(torch.from_numpy(x[h["send_lo"]].copy()), rank - 1))
+            buf_lo = torch.zeros(nl, dtype=torch.float64)
+            reqs.append(dist.irecv(buf_lo, rank - 1))
+        if rank + 1 < world:
+            reqs.append(dist.isend(torch.from_numpy(x[h["send_hi"]].copy()), rank + 1))
+            buf_hi = torch.zeros(nu, dtype=torch.float64)
+            reqs.append(dist.irecv(buf_hi, rank + 1))
+        for rq in reqs:
+            rq.wait()
+        if rank > 0:
+            xloc[hb:hb + nl] = buf_lo.numpy()
+        if rank + 1 < world:
+            xloc[hb + nl:] = buf_hi.numpy()
+        y = OP.local_spmv(rp, loc, va, xloc)
+        assert not np.isnan(y).any()  # no row read the pad
+        part = O.dot(y, y, ("tree", 256, 1776, 0))
+        parts = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, torch.tensor([part], dtype=torch.float64))
+        tot = 0.0
+        for t in parts:
+            tot = tot + float(t.item())
+        ys = [torch.zeros(int(lo[r + 1] - lo[r]), dtype=torch.float64) for r in range(world)]
+        dist.all_gather(ys, torch.from_numpy(y))
+        q.put((rank, np.concatenate([t.numpy() for t in ys]), tot))
+    except BaseException as e:  # report instead of leaving the parent waiting
+        q.put((rank, None, repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_library_partition_halo_and_local_numbering(world):
+    """world_size 2 / 3 gloo processes driving libcgvk's partition, halo plan
+    and rank-local numbering: the distributed SpMV equals the global
+    reference spmv bit-for-bit and the rank-ordered dot equals ORC_DOT_PART."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_lib, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, y, tot in res:
+        assert y is not None, f"rank {rank}: {tot}"
+    P = pb.make_problem("p3", pb.poisson3d(12))
+    y_ref = O.spmv(P.A, P.x_star)
+    lo = OP.partition_rows(P.A.n, world, 144)
+    want = O.dot(y_ref, y_ref, ("part", 256, 1776, lo, 0))
+    for rank, y, tot in res:
+        assert np.array_equal(y.view(np.int64), y_ref.view(np.int64))
+        assert tot == want
+
+
+@pytest.mark.parametrize("nparts", [2, 3, 8])
+def test_rank_local_numbering_matches_restatement(nparts):
+    """cgvk_rank_local_columns == oracle/partition.py's [own | lower | upper]
+    numbering with the halo moved to hbase (own rows rounded up to 32)."""
+    A = pb.poisson3d(16)
+    lo = cgvk.partition_rows(A.n, nparts, 256)
+    for r in range(nparts):
+        rp, ci, va = cgvk.local_rows(A, lo, r)
+        loc, hb = cgvk.rank_local_columns(A.n, lo, r, rp, ci)
+        _, want, _, _ = OP.local_matrix(A, lo, r)
+        m = int(lo[r + 1] - lo[r])
+        assert hb == (m + 31) // 32 * 32
+        assert np.array_equal(np.where(want >= m, want - m + hb, want), loc)
