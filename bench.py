@@ -358,20 +358,23 @@ class SolveSet:
     solve (torchrun, one process per GPU), or P in-process ranks on one GPU
     (--emulate-ranks, the partitioned data path without NCCL)."""
 
-    def __init__(self, args, P, rank, world, device, dist, pinned=None, replicas=False, on_solver=None):
+    def __init__(self, args, P, rank, world, device, dist, pinned=None, replicas=False, on_solver=None,
+                 p2p=False, variants=None):
         from paper_1905_01549_b200 import cgvk
         from paper_1905_01549_b200.cgvk import Precond, VariantConfig, variant_from_name
 
         A = P.A
         rp, ci, va, b, x0 = pinned or (A.row_ptr, A.col_idx, A.values, P.b, P.x0)
         self.groups, self.solvers, self.comm, self.mats = [], {}, None, []
-        cfgs = {v: VariantConfig.make(variant_from_name(v)) for v in VARIANTS}
+        variants = variants or VARIANTS
+        cfgs = {v: VariantConfig.make(variant_from_name(v)) for v in variants}
+        self.transport = None
         ranks = world if world > 1 else args.emulate_ranks
         if replicas or (ranks <= 1 and not args.nccl):
             t = time.perf_counter()
             self.mats = [cgvk.DeviceMatrix(A.n, rp, ci, va, device=device)]
             self.t_matrix = time.perf_counter() - t
-            for v in VARIANTS:
+            for v in variants:
                 self.solvers[v] = cgvk.initialize(cfgs[v], self.mats[0], Precond.JACOBI, b, x0)
                 if on_solver:  # the user's next calls on it (e2e: step, x download), enqueued at once
                     on_solver(v, self.solvers[v])
@@ -393,10 +396,11 @@ class SolveSet:
             self.comm = cgvk.Comm(ranks, 0, device)
             mine = list(range(ranks))
         self.mats = [cgvk.RankMatrix(A.n, lo, r, *cgvk.local_rows(Acsr, lo, r), device=device) for r in mine]
-        for v in VARIANTS:
+        for v in variants:
             g = cgvk.Group(self.comm, self.mats, cfgs[v], Precond.JACOBI,
                            [b[lo[r]:lo[r + 1]] for r in mine], [x0[lo[r]:lo[r + 1]] for r in mine],
-                           p2p=args.p2p)
+                           p2p=p2p)
+            self.transport = g.transport
             self.groups.append(g)
             self.solvers[v] = g.solvers[0]  # time_steps on member 0 steps the whole local group
 
@@ -409,6 +413,28 @@ class SolveSet:
             m.close()
         if self.comm:
             self.comm.close()
+
+
+def p2p_self_check(args, P, rank, world, device, dist, iters: int = 12) -> None:
+    """The peer-memory transport must reproduce the copy / NCCL exchange bit
+    for bit (residual histories of HS and pipe-PR, 12 iterations) before it
+    is timed; raises otherwise (bench falls back to the copy exchange)."""
+    hist = {}
+    for p2p in (True, False):
+        S = SolveSet(args, P, rank, world, device, dist, p2p=p2p, variants=["hs", "pipe-pr"])
+        try:
+            if p2p and S.transport != "p2p":
+                raise RuntimeError(f"peer-memory transport not selected ({S.transport})")
+            for v, s in S.solvers.items():
+                s.step(iters)
+                s.sync()
+                hist[(p2p, v)] = s.history()
+        finally:
+            S.close()
+    for v in ("hs", "pipe-pr"):
+        a, b = hist[(True, v)], hist[(False, v)]
+        if a.shape != b.shape or not np.array_equal(a.view(np.int64), b.view(np.int64)):
+            raise RuntimeError(f"peer-memory self-check: {v} history differs from the copy exchange")
 
 
 def measure_config(args, cfg_name, rank, local, world, dist, extra=False) -> dict:
@@ -424,18 +450,35 @@ def measure_config(args, cfg_name, rank, local, world, dist, extra=False) -> dic
     partitioned = not extra and (world > 1 or args.emulate_ranks > 1 or args.nccl)
     fallback = None
     S = None
-    try:
-        S = SolveSet(args, P, rank, world, device, dist, replicas=extra)
-        for v, s in S.solvers.items():  # warm-up: graphs, clocks, caches
-            s.time_steps(args.warmup)
-        ok = 1.0
-    except Exception as e:  # noqa: BLE001 — reported in the JSON line
-        if not partitioned:
-            raise
-        ok, fallback = 0.0, f"{type(e).__name__}: {e}"
-    if partitioned and dist is not None:
-        ok = -max_over_ranks(dist, -ok)  # min over ranks: every rank falls back together
+    notes = []
+    # row-partitioned transports, best first: peer memory (in-kernel, after a
+    # bit-for-bit self-check against the copy / NCCL exchange), then copy /
+    # NCCL; every rank takes the same one
+    ladder = ["p2p", "copy"] if args.transport == "auto" else [args.transport]
+    for tr in ladder if partitioned else ["single"]:
+        try:
+            if S is not None:
+                S.close()
+                S = None
+            if tr == "p2p":
+                p2p_self_check(args, P, rank, world, device, dist)
+            S = SolveSet(args, P, rank, world, device, dist, replicas=extra, p2p=tr == "p2p")
+            for v, s in S.solvers.items():  # warm-up: graphs, clocks, caches
+                s.time_steps(args.warmup)
+                s.sync()
+            ok = 1.0
+        except Exception as e:  # noqa: BLE001 — reported in the JSON line
+            if not partitioned:
+                raise
+            ok = 0.0
+            notes.append(f"{tr}: {type(e).__name__}: {e}")
+        if partitioned and dist is not None:
+            ok = -max_over_ranks(dist, -ok)  # min over ranks: every rank moves on together
+        if ok >= 1.0:
+            break
+    tnotes = "; ".join(notes) if notes else None
     if partitioned and ok < 1.0:
+        fallback = tnotes
         # the row-partitioned transport failed on this box: independent
         # replicas (weak scaling), labelled as such in `parallelism`
         if S is not None:
@@ -532,15 +575,20 @@ def measure_config(args, cfg_name, rank, local, world, dist, extra=False) -> dic
     iteration_frac = {v: round(per[v]["roofline_frac"], 4) for v in VARIANTS}
 
     e2e = None if args.no_e2e else measure_e2e(args, P, rank, world, device, dist,
-                                                replicas=fallback is not None or extra)
+                                                replicas=fallback is not None or extra,
+                                                p2p=S.transport == "p2p")
 
     value = reps * total_iters / (total_ms * 1e-3)
     cfg = workload_config(cfg_name, P, world if partitioned else 1)
     if partitioned:
-        via = "peer memory (in-kernel stores + stamps)" if args.p2p else "NCCL"
+        p2p = S.transport == "p2p"
+        via = "peer memory: in-kernel stamped stores" if p2p else "NCCL"
         cfg["parallelism"] = (f"row-partitioned z-slabs over {world} GPUs ({via})" if world > 1 or args.nccl
                               else f"row-partitioned, {args.emulate_ranks} in-process ranks on 1 GPU"
-                                   + (" (peer-memory exchange)" if args.p2p else " (copy exchange)"))
+                                   + (" (peer-memory exchange)" if p2p else " (copy exchange)"))
+        cfg["transport"] = S.transport
+        if tnotes:
+            cfg["transport_notes"] = tnotes
     if fallback is not None:
         cfg["parallelism"] = f"{world} independent replicas (row-partitioned transport failed: {fallback})"
     elif extra and world > 1:
@@ -556,7 +604,7 @@ def measure_config(args, cfg_name, rank, local, world, dist, extra=False) -> dic
             "scaling": "weak" if reps > 1 else "strong"}
 
 
-def measure_e2e(args, P, rank, world, device, dist, replicas=False) -> dict:
+def measure_e2e(args, P, rank, world, device, dist, replicas=False, p2p=False) -> dict:
     """e2e through the public API with pinned host buffers."""
     from paper_1905_01549_b200 import cgvk
 
@@ -575,8 +623,28 @@ def measure_e2e(args, P, rank, world, device, dist, replicas=False) -> dict:
         # overlap
         ph = {}
         t = time.perf_counter()
-        E = SolveSet(args, P, rank, world, device, dist, pinned=tuple(arrs), replicas=replicas,
-                     on_solver=lambda v, s: (s.step(args.steps), s.x_async(xs[v])))
+        prev = []
+
+        def on_solver(v, s):
+            if args.e2e_order == "chained" and prev:
+                # this solve's iterations start after the previous solve's
+                # (their kernels do not interleave on the SMs); its upload
+                # (already enqueued) and the previous download still overlap
+                pv, ps = prev[-1]
+                s.after(ps)
+                ps.x_async(xs[pv])
+                s.step(args.steps)
+            elif args.e2e_order == "chained":
+                s.step(args.steps)
+            else:
+                s.step(args.steps)
+                s.x_async(xs[v])
+            prev.append((v, s))
+
+        E = SolveSet(args, P, rank, world, device, dist, pinned=tuple(arrs), replicas=replicas, p2p=p2p,
+                     on_solver=on_solver)
+        if args.e2e_order == "chained" and prev:
+            prev[-1][1].x_async(xs[prev[-1][0]])
         ph["enqueue_ms"] = 1e3 * (time.perf_counter() - t)
         if hasattr(E, "t_matrix"):
             ph["matrix_upload_ms"] = 1e3 * E.t_matrix
@@ -616,7 +684,7 @@ def measure_e2e(args, P, rank, world, device, dist, replicas=False) -> dict:
     d2h = len(VARIANTS) * x.nbytes
     return {"value": reps * e2e_iters / wall, "unit": "iterations/s",
             "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
-            "phases_ms": {k: round(v, 2) for k, v in phases.items()},
+            "phases_ms": {k: round(v, 2) for k, v in phases.items()}, "order": args.e2e_order,
             "note": "fastest of --e2e-reps timed sweeps after one warm-up sweep: int64 CSR + b, x0 per variant up "
                     "(each rank its rows), K steps, x per variant down, all inside the timed region; "
                     "bytes_per_step = sweep bytes / K (rank 0's share when N > 1)"}
@@ -687,12 +755,15 @@ def main():
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-reps", type=int, default=2, help="timed end-to-end sweeps; the fastest is reported")
+    ap.add_argument("--e2e-order", default="chained", choices=["chained", "concurrent"],
+                    help="e2e: each solve's iterations after the previous solve's (cgvk_solver_after), or all at once")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-single-core", action="store_true")
     ap.add_argument("--nccl", action="store_true",
                     help="row-partitioned path over NCCL even at one rank (transport check)")
-    ap.add_argument("--p2p", action="store_true",
-                    help="row-partitioned solves exchange through peer memory inside the kernels (CGVK_GROUP_P2P)")
+    ap.add_argument("--transport", default="auto", choices=["auto", "p2p", "copy"],
+                    help="row-partitioned solves: peer memory inside the kernels (CGVK_GROUP_P2P, after a "
+                         "bit-exact self-check), the copy / NCCL exchange, or auto (p2p, else copy)")
     ap.add_argument("--emulate-ranks", type=int, default=1,
                     help="row-partitioned solve with P in-process ranks on one GPU")
     args = ap.parse_args()

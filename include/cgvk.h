@@ -209,6 +209,12 @@ int cgvk_solver_get_vector(cgvk_solver s, int which, double* out);
  * step) on the solver's stream without waiting: `out` (preferably pinned,
  * cgvk_host_register) is valid after cgvk_solver_sync. */
 int cgvk_solver_get_vector_async(cgvk_solver s, int which, double* out);
+/* Stream order between two solvers on one device (an extension; the reference
+ * runs solves one after another by construction): work enqueued on `s` from
+ * now on starts after everything already enqueued on `prev` (upload, steps,
+ * downloads), so a batch of solves can keep its copies overlapped while its
+ * iterations do not interleave on the SMs. */
+int cgvk_solver_after(cgvk_solver s, cgvk_solver prev);
 /* ||b - A x_k|| with a fresh device spmv (diagnostics.cpp:19-24). */
 int cgvk_solver_true_residual(cgvk_solver s, double* out);
 /* sqrt(<r_j,r_j>) for j = 0..k as recorded on the device each iteration.

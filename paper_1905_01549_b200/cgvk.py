@@ -183,6 +183,7 @@ def _load() -> C.CDLL:
                                    C.POINTER(_Stats)]),
         "cgvk_solver_get_vector": (I, [P, I, P]),
         "cgvk_solver_get_vector_async": (I, [P, I, P]),
+        "cgvk_solver_after": (I, [P, P]),
         "cgvk_solver_true_residual": (I, [P, C.POINTER(D)]),
         "cgvk_solver_history": (I, [P, P, I, C.POINTER(I)]),
         "cgvk_solver_stream": (P, [P]),
@@ -492,6 +493,11 @@ class Solver:
             raise InvalidArgument(-1, "out must be a contiguous float64 array of n")
         _check(_lib.cgvk_solver_get_vector(self._h, int(which), _ptr(out) if self.n else None))
         return out
+
+    def after(self, prev: "Solver") -> None:
+        """Work enqueued on this solver from now on starts after everything
+        already enqueued on `prev` (cgvk_solver_after)."""
+        _check(_lib.cgvk_solver_after(self._h, prev._h))
 
     def x_async(self, out: np.ndarray) -> None:
         """Enqueue the download of x into `out` (contiguous float64 of n,

@@ -951,9 +951,7 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
     }
     constexpr int kMinb = Op::CSR ? CGVK_SPMV_MIN_CTAS : CGVK_K1_MIN_CTAS;
     L->fn = k_stream<Op, Prev>;
-    // the peer form's SpMV gathers may call out to the halo receive buffers:
-    // 2 CTAs' register budget (3 spill)
-    L->fn_peer = k_stream<Op, Prev, (Op::CSR && kMinb > 2 ? 2 : kMinb), true>;
+    L->fn_peer = k_stream<Op, Prev, kMinb, true>;
     // register-capped build of an Op that has one (GV / pipe-PR K1: 72
     // registers, 3 CTAs/SM): only when the working set fits L2 and the
     // virtual CTAs outnumber two CTAs per SM (measured P64 GV 18.4 -> 17.5 us,
@@ -1698,6 +1696,20 @@ int cgvk_solver_get_vector_async(cgvk_solver s, int which, double* out) {
     // x is never deferred: both kernels of every iteration leave x_k complete
     CK(cudaMemcpyAsync(out, s->x, 8 * s->n, cudaMemcpyDeviceToHost, s->stream));
     s->mirror_fresh = false;
+    return CGVK_OK;
+}
+
+int cgvk_solver_after(cgvk_solver s, cgvk_solver prev) {
+    if (!s || !prev) return set_err(CGVK_EINVAL, "null solver");
+    if (s->a->device != prev->a->device) return set_err(CGVK_EINVAL, "solvers on different devices");
+    CK(cudaSetDevice(s->a->device));
+    if (s->stream == prev->stream) return CGVK_OK;
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    cudaError_t e = cudaEventRecord(ev, prev->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s->stream, ev, 0);
+    cudaEventDestroy(ev);  // released once the wait is resolved
+    CK(e);
     return CGVK_OK;
 }
 

@@ -176,25 +176,42 @@ __device__ __noinline__ void p2p_push_row(const PeerPlan* P2, unsigned int mask,
     }
 }
 
-// Halo column e = j - hbase of the vector `g` (one of pp.hv) as this kernel
-// (sequence number h) expects it: spin until both words carry the stamp.
-__device__ __noinline__ double p2p_halo_wait(const PeerPlan* P2, const double* g, int e, unsigned int h,
-                                             int pcur) {
-    const PeerPlan& pp = *P2;
+// Halo entry e of vector g (one of pp.hv) as this kernel (sequence number h)
+// expects it: spin until both words carry the stamp, then store the double
+// into g's halo region (the row's gathers read it back through L2).
+__device__ __forceinline__ void p2p_fetch(const PeerPlan& pp, const double* g, int hb, int e, unsigned int h,
+                                          int pcur) {
     int q = 0;
     while (q < kP2pSlots - 1 && pp.hv[q] != g) ++q;
     const unsigned int want = h - ((pp.psel && q == p2p_pold(pcur)) ? 2u : 1u);
     const unsigned long long* w = pp.rx[q] + 2 * ((size_t)ll_parity(want) * pp.rx_stride + e);
-    long long t0 = gtimer_ns();
+    long long t0 = 0;
     for (int spin = 0;; ++spin) {
         unsigned long long a, b;
         ld_relaxed_v2u64(w, a, b);
-        if ((unsigned int)(a >> 32) == want && (unsigned int)(b >> 32) == want)
-            return __hiloint2double((int)(unsigned int)b, (int)(unsigned int)a);
-        if ((spin & 255) == 255 && gtimer_ns() - t0 > kP2pSpinNs) {
-            atomicExch(pp.err, 1u);
-            return 0.0;
+        if ((unsigned int)(a >> 32) == want && (unsigned int)(b >> 32) == want) {
+            const_cast<double*>(g)[hb + e] = __hiloint2double((int)(unsigned int)b, (int)(unsigned int)a);
+            return;
         }
+        if (spin == 0) t0 = gtimer_ns();
+        else if ((spin & 255) == 0 && gtimer_ns() - t0 > kP2pSpinNs) {
+            atomicExch(pp.err, 1u);
+            return;
+        }
+    }
+}
+
+// A boundary row's halo entries (columns >= hb) of the gathered sources g0
+// (and g1), fetched before the row is computed. ci: the row's columns (stage
+// or global), len entries.
+__device__ __noinline__ void p2p_unpack_row(const PeerPlan* P2, const int* ci, int len, int hb, const double* g0,
+                                            const double* g1, unsigned int h, int pcur) {
+    const PeerPlan& pp = *P2;
+    for (int k = 0; k < len; ++k) {
+        const int c = ci[k];
+        if (c < hb) continue;
+        if (g0) p2p_fetch(pp, g0, hb, c - hb, h, pcur);
+        if (g1) p2p_fetch(pp, g1, hb, c - hb, h, pcur);
     }
 }
 

@@ -425,22 +425,19 @@ struct StagedIn {
     }
 };
 
-// Peer-memory ranks (cgvk_p2p.cuh): halo columns (j >= hb) come from the
-// stamped receive buffers, the rest as in StagedIn.
-struct PeerIn {
+// Boundary tiles of peer-memory ranks (cgvk_p2p.cuh): the thread has just
+// written its row's halo entries from the stamped receive buffers into the
+// vector's halo region, so those tiles gather through L2 (ld.global.cg), not
+// the non-coherent L1 path.
+struct StagedInL2 {
     const double* sv;
-    const PeerPlan* pp;
-    int hb;
-    unsigned int h;
-    int pcur;
     __device__ __forceinline__ double operator()(int v) const { return sv[v * kBlock]; }
     __device__ __forceinline__ double gather(int, int j, const double* __restrict__ g) const {
-        return j < hb ? __ldg(g + j) : p2p_halo_wait(pp, g, j - hb, h, pcur);
+        return __ldcg(g + j);
     }
     __device__ __forceinline__ double gather_p(int j, const double* __restrict__ rt, const double* __restrict__ po,
                                                double beta) const {
-        if (j < hb) return ADD(__ldg(rt + j), MUL(beta, __ldg(po + j)));
-        return ADD(p2p_halo_wait(pp, rt, j - hb, h, pcur), MUL(beta, p2p_halo_wait(pp, po, j - hb, h, pcur)));
+        return ADD(__ldcg(rt + j), MUL(beta, __ldcg(po + j)));
     }
 };
 
@@ -1079,7 +1076,8 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
     int j = 0;
     // peer ranks (cgvk_p2p.cuh): after a boundary tile, its rows of the pushed
     // vectors go to the neighbours (out of line: the common path only compares
-    // the tile); halo columns are gathered from the receive buffers (PeerIn)
+    // the tile); before a boundary row, its halo entries come from the
+    // receive buffers into the vector's halo region (p2p_unpack_row)
     const PeerPlan* const pp = P.pp;
     const int p2p_tlo = PEER ? __ldg(&pp->tlo) : 0, p2p_hif = PEER ? __ldg(&pp->hi_first) : 0x7fffffff;
     const int p2p_hb = PEER ? __ldg(&pp->hbase) : 0x7fffffff;
@@ -1087,7 +1085,7 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
     const int p2p_pc = PEER ? H->cs.pcur : 0;
     const unsigned int p2p_mask = PEER ? p2p_push_mask(S.p2p_push, p2p_pc) : 0u;
     auto consume_tile = [&](int slot, int tile) {
-        const bool pb = PEER && p2p_mask && (tile < p2p_tlo || tile >= p2p_hif);
+        const bool pb = PEER && (tile < p2p_tlo || tile >= p2p_hif);
         StageView V = stage_view(stages, S, slot);
         const int i = tile * kBlock + t;
         if (i < P.n) {
@@ -1103,12 +1101,22 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
                     R.ci = V.ci + (b - H->k0c[slot]);
                 }
             }
-            if constexpr (PEER) op.row(P, i, PeerIn{V.vec + t, pp, p2p_hb, p2p_h, p2p_pc}, R, acc);
-            else op.row(P, i, StagedIn{V.vec + t}, R, acc);
+            if constexpr (PEER && Op::CSR) {
+                if (pb) {  // this row's halo entries, then gathers through L2
+                    const double* g0 = op.gsrc(P, 0);
+                    const double* g1 = Op::NG > 1 ? op.gsrc(P, Op::NG - 1) : nullptr;
+                    p2p_unpack_row(pp, R.ci, R.len, p2p_hb, g0, g1, p2p_h, p2p_pc);
+                    op.row(P, i, StagedInL2{V.vec + t}, R, acc);
+                } else {
+                    op.row(P, i, StagedIn{V.vec + t}, R, acc);
+                }
+            } else {
+                op.row(P, i, StagedIn{V.vec + t}, R, acc);
+            }
         }
         __syncwarp();
         if ((t & 31) == 0) mbar_arrive(&H->empty[slot]);
-        if (pb) p2p_push_row(pp, p2p_mask, i, P.n, p2p_h);
+        if (pb && p2p_mask) p2p_push_row(pp, p2p_mask, i, P.n, p2p_h);
     };
     double* const part = P.part;
     auto close_vb = [&](int vb) {

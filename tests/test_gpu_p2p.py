@@ -1,12 +1,14 @@
 """Peer-memory exchange of a row-partitioned solve (CGVK_GROUP_P2P,
 csrc/cgvk_p2p.cuh): the chained kernels push boundary rows into the
-neighbours' halo regions and rank totals into every rank's table with
-stamps, and wait on the stamps inside the kernel — no exchange launch, no
-finalize launch. On one GPU the ranks run in this process (their peers'
-memory is this device's); every wait is then already satisfied in stream
-order, so the test exercises the data path and the stamp protocol, not the
-overlap. Every rank's state must be bit-identical to the oracle restatement
-with partitioned dots (ORC_DOT_PART), as the copy transport is."""
+neighbours' receive buffers and rank totals into every rank's table as
+stamped 8-byte words; a boundary row fetches its halo entries when their
+stamp arrives, the successor's prologue folds the totals in rank order — no
+exchange launch, no finalize launch, no fence. On one GPU the ranks run in
+this process (their peers' memory is this device's); every wait is then
+already satisfied in stream order, so the tests exercise the data path and
+the stamp protocol, not the overlap. Every rank's state must be
+bit-identical to the oracle restatement with partitioned dots
+(ORC_DOT_PART), as the copy transport is."""
 import numpy as np
 import pytest
 
@@ -144,3 +146,28 @@ def test_p2p_rejects_scattered_send_rows():
     R = pb.make_problem("rs", pb.random_spd(3000, 13, 300, 7))
     with pytest.raises(cgvk.InvalidArgument, match="prefix"):
         make_group(R, 1, 2, Variant.HS, Precond.JACOBI)
+
+
+@pytest.mark.parametrize("variant", [Variant.HS, Variant.GV, Variant.PIPE_PR])
+def test_p2p_nccl_single_rank(variant):
+    """The multi-process set-up path (an NCCL communicator: the window is a
+    plain cudaMalloc exported with cudaIpcGetMemHandle, the rank blobs are
+    all-gathered through NCCL) on the one rank a single GPU admits."""
+    P, align = problem("poisson3d_12_slabs")
+    A = P.A
+    lo = cgvk.partition_rows(A.n, 1, align)
+    mats = [cgvk.RankMatrix(A.n, lo, 0, *cgvk.local_rows(A, lo, 0))]
+    comm = cgvk.Comm(1, 0, 0, cgvk.nccl_unique_id())
+    g = cgvk.Group(comm, mats, cgvk.VariantConfig.make(variant), Precond.JACOBI, [P.b], [P.x0], p2p=True)
+    assert g.transport == "p2p"
+    block, gmax, order = mats[0].reduction_config()
+    o = O.Restatement(A, int(variant), 1, P.b, P.x0, dot=("part", block, gmax, lo, order))
+    for k in (1, 8, 3):
+        g.step(k)
+        g.sync()
+        for _ in range(k):
+            if o.state()["state"] == 0:
+                o.step()
+        compare(g, o, f"p2p nccl1/{variant.name} k={o.state()['k']}")
+    g.close()
+    comm.close()
