@@ -86,10 +86,15 @@ def test_batched_steps_match_single_steps(variant, precond, devmats):
 HISTORY_CASES = [("poisson2d_33", Precond.IDENTITY), ("poisson2d_33", Precond.JACOBI),
                  ("poisson3d_20", Precond.IDENTITY), ("poisson3d_20", Precond.JACOBI),
                  ("varcoef_16", Precond.JACOBI)]
-# GV re-associates the residual recurrences so that its true residual carries
-# the reduction-order difference forward: its measured CPU
-# tree-vs-sequential floor on these cases is up to 8.7e-10, so its bound is 1e-9.
-GV_RTOL = 1e-9
+# The bar is the north star's 1e-10, or — where it is larger — the reorder
+# floor of the case: the distance between the oracle run in the device's
+# reduction order and the reference's sequential order, measured here on the
+# CPU for the same inputs (GV re-associates the residual recurrences, so its
+# true residual carries the reduction-order difference forward: up
+# to 8.7e-10 on these cases). The GPU's updated-residual history must equal
+# that tree-order oracle bit for bit, so its distance from the reference IS
+# the floor.
+FLOOR_MARGIN = 1.0 + 1e-6
 
 
 @pytest.fixture(scope="module")
@@ -117,10 +122,22 @@ def test_residual_history_vs_reference(variant, case, history_mats):
         cgvk.step(s)
         upd.append(np.sqrt(s.scalars()["rr"]))
         true.append(s.true_residual())
-    rtol = GV_RTOL if variant == Variant.GV else RESIDUAL_RTOL
-    np.testing.assert_allclose(upd, upd_ref, rtol=rtol, atol=0)
-    np.testing.assert_allclose(true, true_ref, rtol=rtol, atol=0)
-    np.testing.assert_allclose(s.history(), upd_ref, rtol=rtol, atol=0)
+    tree = O.Restatement(P.A, int(variant), int(precond), P.b, P.x0, dot=tree_dot(A))
+    t_taken, upd_tree, true_tree = tree.solve(P.b, 50, 0.0, true_cap=51)
+    assert t_taken == taken
+    assert same_bits(s.history(), upd_tree)  # the device IS the tree-order oracle
+
+    def rel(a, b):
+        a, b = np.asarray(a), np.asarray(b)
+        return float(np.max(np.abs(a - b) / np.abs(b)))
+
+    rtol_u = max(RESIDUAL_RTOL, rel(upd_tree, upd_ref) * FLOOR_MARGIN)
+    rtol_t = max(RESIDUAL_RTOL, rel(true_tree, true_ref) * FLOOR_MARGIN)
+    if variant != Variant.GV:  # the floor exceeds the north star only for GV
+        assert rtol_u == RESIDUAL_RTOL and rtol_t == RESIDUAL_RTOL, (rtol_u, rtol_t)
+    np.testing.assert_allclose(upd, upd_ref, rtol=rtol_u, atol=0)
+    np.testing.assert_allclose(true, true_ref, rtol=rtol_t, atol=0)
+    np.testing.assert_allclose(s.history(), upd_ref, rtol=rtol_u, atol=0)
 
 
 # Medium size: 50^3 = 125,000 rows = 489 tiles > the CSR engine's 444 canonical
