@@ -909,9 +909,6 @@ template <class Op, class Prev>
 int make_band(cgvk_matrix a, KLaunch* L) {
     using Shape = BandShape<Op>;
     L->fn = k_band<Op, Prev>;
-#if CGVK_BAND_MAXNREG
-    if constexpr (Shape::MINB == 2 && Shape::THREADS == kThreads && Op::ND > 0) L->fn = k_band_nr<Op, Prev>;
-#endif
     L->threads = Shape::THREADS;
     StageCfg S{};
     S.nvec = Op::NV + Shape::NRAW;
@@ -921,7 +918,9 @@ int make_band(cgvk_matrix a, KLaunch* L) {
     S.nstage = std::min(std::max(env_int("CGVK_BAND_NSTAGE", ns_default), 2), kMaxStages);
     // raw windows are filled NS - 1 tiles ahead by the producer; a combined
     // window one tile ahead by the consumers
-    S.ring = 2 * a->band_h + (Shape::XF ? 2 : S.nstage);
+    // (XF: a combined tile is overwritten only after the slowest warp is done
+    // with it — it may trail the others by CGVK_BAND_SLACK tiles)
+    S.ring = 2 * a->band_h + (Shape::XF ? 1 + kBandXfAhead + CGVK_BAND_SLACK : S.nstage);
     S.pf = std::max(env_int("CGVK_BAND_PF", 0), 0);  // measured: L2 bulk prefetch of the slices slows R4M
     const int header = ((int)sizeof(PipeHeader) + 127) & ~127;
     L->smem = (size_t)header + (size_t)S.nstage * S.stage_bytes + (size_t)Shape::NWIN * S.ring * kBlock * 8 +
@@ -931,6 +930,19 @@ int make_band(cgvk_matrix a, KLaunch* L) {
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L->fn, L->threads, L->smem));
     if (occ < 1) return set_err(CGVK_ECUDA, "band kernel does not fit on an SM");
+#if CGVK_BAND_MAXNREG
+    // the register-capped form where it keeps the occupancy (the register
+    // file is split over 4 SM sub-partitions: two 9-warp CTAs need <= 96
+    // registers; measured R4M with the slack hand-over: CG K2 262 -> 252 us
+    // capped at 2 CTAs/SM, HS / PR K2 284 / 270 -> 450 / 424 us capped at 1)
+    if constexpr (Shape::MINB == 2 && Shape::THREADS == kThreads && Op::ND > 0) {
+        const StreamFn nr = k_band_nr<Op, Prev>;
+        TRY(raise_smem((const void*)nr, L->smem));
+        int occ_nr = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_nr, nr, L->threads, L->smem));
+        if (occ_nr >= occ && !env_int("CGVK_BAND_NO_NR", 0)) L->fn = nr;
+    }
+#endif
     L->grid = balanced_grid(a->G, occ * a->sms);
     L->S = S;
     if (env_int("CGVK_DEBUG", 0))

@@ -86,10 +86,20 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes
 // instead of __launch_bounds__(288, 2), under which ptxas settles at 95-96
 // registers. Measured on R4M: 104 registers, still two CTAs per
 // SM, HS 353 -> 342 us, CG 357 -> 353, M/PR 359 -> 352; GV's dot-free K2
-// keeps the launch bounds (395 vs 390 us with the cap). 0 = launch bounds.
+// keeps the launch bounds (395 vs 390 us with the cap). make_band takes the
+// capped form only where it keeps two CTAs per SM. 0 = launch bounds.
 #ifndef CGVK_BAND_MAXNREG
 #define CGVK_BAND_MAXNREG 104
 #endif
+// Kernels with dot products: 1 = warps rotate over the slices and hand the
+// per-row contributions over through two mbarrier-guarded buffers, folding
+// tile k's while computing tile k+1 (a warp may run one tile ahead of the
+// slowest); 0 = one CTA barrier per tile, fixed slices (round 1).
+#ifndef CGVK_BAND_SLACK
+#define CGVK_BAND_SLACK 1
+#endif
+// tiles between a combined window tile (BAND_XF) and its first reader
+constexpr int kBandXfAhead = 1 + CGVK_BAND_SLACK;
 template <class Op, class Prev>
 __device__ __forceinline__ void band_body(const Params& P, const StageCfg& S);
 
@@ -112,7 +122,7 @@ __device__ __forceinline__ void band_body(const Params& P, const StageCfg& S) {
     constexpr int NWIN = Shape::NWIN;
     constexpr int GR = Shape::GROUPS;
     constexpr int NC = GR * kConsumers;  // consumer threads
-    static_assert(!XF || Op::ND > 0, "a combined window relies on the per-tile contribution barrier");
+    static_assert(!XF || Op::ND > 0, "a combined window relies on the contribution hand-over for ordering");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PipeHeader* H = reinterpret_cast<PipeHeader*>(smem_raw);
     unsigned char* stages = smem_raw + ((sizeof(PipeHeader) + 127) / 128) * 128;
@@ -127,6 +137,10 @@ __device__ __forceinline__ void band_body(const Params& P, const StageCfg& S) {
             mbar_init(&H->empty[s], kWarps);
         }
         mbar_init(&H->fold_bar, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&H->cfull[b], kWarps);
+            mbar_init(&H->cempty[b], kWarps);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -169,8 +183,9 @@ __device__ __forceinline__ void band_body(const Params& P, const StageCfg& S) {
             const int r0 = t * kBlock;
             const uint32_t vb = tile_bytes(t);
             // window tile entering the ring: t + H (raw windows, straight into
-            // the ring) or t + H + 1 (XF: staged raw, combined by the consumers)
-            const int u = XF ? t + HB + 1 : t + HB;
+            // the ring) or t + H + kBandXfAhead (XF: staged raw, combined by
+            // the consumers that many tiles before its first reader)
+            const int u = XF ? t + HB + kBandXfAhead : t + HB;
             uint32_t bytes = kBandMetaBytes + 48;
 #pragma unroll
             for (int v = 0; v < Op::NV; ++v)
@@ -233,14 +248,29 @@ __device__ __forceinline__ void band_body(const Params& P, const StageCfg& S) {
         // from global (later tiles get theirs from the stages)
         const double* g0 = op.gsrc(P, 0);
         const double* g1 = op.gsrc(P, 1);
-        const int q0 = max(0, T0 - HB) * kBlock, q1 = min(P.n, (T0 + HB + 1) * kBlock);
+        const int q0 = max(0, T0 - HB) * kBlock, q1 = min(P.n, (T0 + HB + kBandXfAhead) * kBlock);
         for (int q = q0 + t; q < q1; q += kConsumers)
             win[(q / kBlock) % RT * kBlock + q % kBlock] = op.band_xf(__ldg(g0 + q), __ldg(g1 + q));
         consumer_sync();
     }
     double acc[Op::ND > 0 ? Op::ND : 1];
     int j = 0;
+    // thread t adds row t's contribution of the CTA's tile x (x = tile - T0)
+    // to its accumulators, in tile order, once every warp has written it
+    auto fold_tile = [&](int x) {
+        if constexpr (Op::ND > 0) {
+            const double* cb = cbuf + (x & 1) * (Op::ND * kBlock);
+            mbar_wait(&H->cfull[x & 1], (x >> 1) & 1);
+            if ((T0 + x) * kBlock + t < P.n) {
+#pragma unroll
+                for (int d = 0; d < Op::ND; ++d) acc[d] = ADD(acc[d], cb[d * kBlock + t]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&H->cempty[x & 1]);
+        }
+    };
     for (int vb = vb0; vb < vb1; ++vb) {
+        const int jv = j;  // the virtual CTA's first tile (CTA-relative)
 #pragma unroll
         for (int d = 0; d < Op::ND; ++d) acc[d] = 0.0;
         const int te = span_lo(vb + 1, ntiles, Gv);
@@ -251,12 +281,12 @@ __device__ __forceinline__ void band_body(const Params& P, const StageCfg& S) {
             mbar_wait(&H->full[slot], (jj / NS) & 1);
             const unsigned char* st = stages + (size_t)slot * S.stage_bytes;
             const double* sv = reinterpret_cast<const double*>(st + kBandMetaBytes + kBandOffBytes);
-            if constexpr (XF) {  // combine window tile tile + H + 1 (used from the next tile on)
-                const int u = tile + HB + 1;
+            if constexpr (XF) {  // combine window tile tile + H + kBandXfAhead
+                const int u = tile + HB + kBandXfAhead;
                 if (u < ntiles && u * kBlock + t < P.n)
                     win[(u % RT) * kBlock + t] = op.band_xf(sv[Op::NV * kBlock + t], sv[(Op::NV + 1) * kBlock + t]);
             }
-            const int slice = Op::ND > 0 ? wg : (wg + jj / GR) & (kWarps - 1);
+            const int slice = (Op::ND > 0 && !CGVK_BAND_SLACK) ? wg : (wg + jj / GR) & (kWarps - 1);
             const unsigned int meta = reinterpret_cast<const unsigned int*>(st)[slice * 32 + lane];
             const int rl = meta & 255;
             const int off = reinterpret_cast<const int*>(st + kBandMetaBytes)[slice];
@@ -277,16 +307,24 @@ __device__ __forceinline__ void band_body(const Params& P, const StageCfg& S) {
             if constexpr (Op::ND > 0) {
                 // per-row contributions back to canonical positions
                 double* cb = cbuf + (jj & 1) * (Op::ND * kBlock);
+                if (CGVK_BAND_SLACK && jj >= 2) mbar_wait(&H->cempty[jj & 1], ((jj >> 1) - 1) & 1);
 #pragma unroll
                 for (int d = 0; d < Op::ND; ++d) cb[d * kBlock + rl] = tmp[d];
-                consumer_sync();
-                if (r0 + t < P.n) {
+                if (CGVK_BAND_SLACK) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&H->cfull[jj & 1]);
+                    if (jj > jv) fold_tile(jj - 1);  // the previous tile, now complete
+                } else {
+                    consumer_sync();
+                    if (r0 + t < P.n) {
 #pragma unroll
-                    for (int d = 0; d < Op::ND; ++d) acc[d] = ADD(acc[d], cb[d * kBlock + t]);
+                        for (int d = 0; d < Op::ND; ++d) acc[d] = ADD(acc[d], cb[d * kBlock + t]);
+                    }
                 }
             }
         }
         if constexpr (Op::ND > 0) {
+            if (CGVK_BAND_SLACK && j > jv) fold_tile(j - 1);  // the virtual CTA's last tile
             if (op.sync() != 2) continue;
             cta_tree_c<Op::ND>(acc, H->red);
             if (t == 0) {

@@ -490,6 +490,7 @@ struct PipeHeader {
     double red[kMaxDots * 32];
     uint64_t fold_bar;           // last CTA: bulk copy of the partials into the idle ring
     uint64_t pad2;
+    uint64_t cfull[2], cempty[2];  // band engine: the per-row contribution buffers (cgvk_band.cuh)
     Ctrl cs;                     // last CTA: the control block finish() works on
 };
 
