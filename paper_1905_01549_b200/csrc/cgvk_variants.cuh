@@ -64,6 +64,24 @@ __device__ __forceinline__ bool step_wanted(const Ctrl* c) {
 
 #define SV(v) in(v)
 
+// Outputs that the next kernel does not read: streaming stores (L2
+// evict-first), so they leave L2 to the vectors it does read — when the
+// working set exceeds L2 (l2pol != 3; a problem that fits keeps everything).
+// Measured P128: GV 92.7 -> 88.2 us, pipe-PR 84.2 -> 80.7 us;
+// V256 neutral. CGVK_K1_STCS=0: plain stores (A/B).
+#ifndef CGVK_K1_STCS
+#define CGVK_K1_STCS 1
+#endif
+__device__ __forceinline__ void st_far(const Params& P, double* p, double v) {
+#if CGVK_K1_STCS
+    if (P.l2pol != 3) {
+        __stcs(p, v);
+        return;
+    }
+#endif
+    *p = v;
+}
+
 // =====================================================================  HS
 // src/variants.cpp:189-205, paper Alg. 1. V = 3+1 (K1) + 4+3 (K2) vectors.
 
@@ -87,7 +105,8 @@ struct HsK1 {
     template <class In, class RR>
     __device__ void row(const Params& P, int i, const In& in, const RR&, double* acc) const {
         const double r = SUB(SV(0), MUL(alpha, SV(1)));
-        P.r[i] = r;
+        if (PREC) st_far(P, P.r + i, r);  // K2 reads r~ (without Jacobi it gathers r)
+        else P.r[i] = r;
         double rt = r;
         if constexpr (PREC) {  // r~ = M r stored for K2 (its gather and own-row read)
             rt = MUL(SV(2), r);
@@ -160,7 +179,7 @@ struct HsK2 {
     template <class In>
     __device__ void apply(const Params& P, int i, const In& in, double sum, double* acc) const {
         const double po = SV(0);
-        P.x[i] = ADD(SV(2), MUL(alpha, po));
+        st_far(P, P.x + i, ADD(SV(2), MUL(alpha, po)));
         if (mode != MODE_FULL) return;
         const double pi = ADD(SV(1), MUL(beta, po));
         pnew[i] = pi;
@@ -232,11 +251,16 @@ struct CgK1 {
         if (F) {
             p = ADD(PREC ? MUL(SV(5), r) : r, MUL(beta, p));
             s = ADD(SV(4), MUL(beta, s));
-            P.p0[i] = p;
-            P.s[i] = s;
+            if (P.unsimplified_mu) {  // K2 reads them
+                P.p0[i] = p;
+                P.s[i] = s;
+            } else {
+                st_far(P, P.p0 + i, p);
+                st_far(P, P.s + i, s);
+            }
         }
         if (S) {
-            P.x[i] = ADD(SV(2), MUL(alpha, p));
+            st_far(P, P.x + i, ADD(SV(2), MUL(alpha, p)));
             const double rn = SUB(r, MUL(alpha, s));
             P.r[i] = rn;
             if constexpr (PREC) P.rt[i] = MUL(SV(5), rn);  // r~ = M r for K2's gather
@@ -369,7 +393,7 @@ struct PrK1 {
     template <class In, class RR>
     __device__ void row(const Params& P, int i, const In& in, const RR&, double* acc) const {
         const double s = SV(3), p = SV(1);
-        P.x[i] = ADD(SV(0), MUL(alpha, p));
+        st_far(P, P.x + i, ADD(SV(0), MUL(alpha, p)));
         const double r = SUB(SV(2), MUL(alpha, s));
         P.r[i] = r;
         double rt = r;
@@ -521,24 +545,28 @@ struct GvK1 {
             if constexpr (PREC) st = ADD(MUL(SV(9), w), MUL(beta, st));
             else st = s;
             u = ADD(SV(4), MUL(beta, u));
-            P.p0[i] = p;
-            P.s[i] = s;
-            if constexpr (PREC) P.st[i] = st;
-            P.u[i] = u;
+            st_far(P, P.p0 + i, p);
+            st_far(P, P.s + i, s);
+            if constexpr (PREC) st_far(P, P.st + i, st);
+            st_far(P, P.u + i, u);
         }
         if (S) {
-            P.x[i] = ADD(SV(5), MUL(alpha, p));
+            st_far(P, P.x + i, ADD(SV(5), MUL(alpha, p)));
             const double r = SUB(SV(6), MUL(alpha, s));
-            P.r[i] = r;
+            st_far(P, P.r + i, r);
             if constexpr (PREC) {
                 rt = SUB(rt, MUL(alpha, st));
-                P.rt[i] = rt;
+                st_far(P, P.rt + i, rt);
             } else {
                 rt = r;
             }
             w = SUB(w, MUL(alpha, u));
-            P.w[i] = w;
-            if constexpr (PREC) P.wt[i] = MUL(SV(9), w);  // w~ = M w for K2's gather
+            if constexpr (PREC) {
+                st_far(P, P.w + i, w);
+                P.wt[i] = MUL(SV(9), w);  // w~ = M w for K2's gather
+            } else {
+                P.w[i] = w;
+            }
             acc[0] = ADD(acc[0], MUL(rt, r));
             acc[1] = ADD(acc[1], MUL(rt, w));
             acc[2] = ADD(acc[2], MUL(r, r));
@@ -671,9 +699,10 @@ struct PprK1 {
     template <class In, class RR>
     __device__ void row(const Params& P, int i, const In& in, const RR&, double* acc) const {
         const double p_old = SV(1), s_old = SV(3), w_old = SV(4), u = SV(5);
-        P.x[i] = ADD(SV(0), MUL(alpha, p_old));
+        st_far(P, P.x + i, ADD(SV(0), MUL(alpha, p_old)));
         const double r = SUB(SV(2), MUL(alpha, s_old));
-        P.r[i] = r;
+        if (PREC) st_far(P, P.r + i, r);  // (without Jacobi K2 gathers r)
+        else P.r[i] = r;
         double rt = r, st_old = s_old;
         if constexpr (PREC) {
             st_old = SV(6);
@@ -696,11 +725,12 @@ struct PprK1 {
                 st = ADD(wtn, MUL(beta, st_old));
                 P.st[i] = st;
             }
-            P.p0[i] = p;
-            P.s[i] = s;
+            st_far(P, P.p0 + i, p);
+            if (PREC) st_far(P, P.s + i, s);  // (without Jacobi K2 gathers s)
+            else P.s[i] = s;
             if (!recw) {
-                P.w[i] = wn;
-                if constexpr (PREC) P.wt[i] = wtn;
+                st_far(P, P.w + i, wn);
+                if constexpr (PREC) st_far(P, P.wt + i, wtn);
             }
             acc[0] = ADD(acc[0], MUL(p, s));
             if (want_delta) acc[1] = ADD(acc[1], MUL(rt, s));
