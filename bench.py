@@ -420,17 +420,29 @@ def p2p_self_check(args, P, rank, world, device, dist, iters: int = 12) -> None:
     for bit (residual histories of HS and pipe-PR, 12 iterations) before it
     is timed; raises otherwise (bench falls back to the copy exchange)."""
     hist = {}
+    fail = None
     for p2p in (True, False):
+        # group creation is collective (a failed set-up fails on every rank);
+        # a rank whose solve gives up keeps taking part, and the verdict is
+        # agreed over the ranks before anyone moves on
         S = SolveSet(args, P, rank, world, device, dist, p2p=p2p, variants=["hs", "pipe-pr"])
         try:
             if p2p and S.transport != "p2p":
-                raise RuntimeError(f"peer-memory transport not selected ({S.transport})")
+                fail = fail or f"peer-memory transport not selected ({S.transport})"
             for v, s in S.solvers.items():
                 s.step(iters)
-                s.sync()
-                hist[(p2p, v)] = s.history()
+                try:
+                    s.sync()
+                    hist[(p2p, v)] = s.history()
+                except Exception as e:  # noqa: BLE001
+                    fail = fail or f"{v}: {type(e).__name__}: {e}"
         finally:
             S.close()
+    ok = 0.0 if fail else 1.0
+    if dist is not None:
+        ok = -max_over_ranks(dist, -ok)
+    if ok < 1.0:
+        raise RuntimeError(fail or "peer-memory self-check failed on another rank")
     for v in ("hs", "pipe-pr"):
         a, b = hist[(True, v)], hist[(False, v)]
         if a.shape != b.shape or not np.array_equal(a.view(np.int64), b.view(np.int64)):
