@@ -353,6 +353,9 @@ def load_traffic() -> dict:
 ALIGN = {"p2d": 256, "p64": 64 * 64, "p128": 128 * 128, "v256": 256 * 256, "r4m": 1}
 
 
+_COMMS = {}  # communicators of this process, by (kind, ranks / world, rank, device)
+
+
 class SolveSet:
     """One solver per variant: single-GPU, one NCCL rank of a row-partitioned
     solve (torchrun, one process per GPU), or P in-process ranks on one GPU
@@ -385,16 +388,23 @@ class SolveSet:
             raise RuntimeError("CGVK_BENCH_FAIL_PARTITION set")
         lo = cgvk.partition_rows(A.n, ranks, ALIGN[args.config])
         Acsr = type(A)(A.n, rp, ci, va)
+        # the communicator is process set-up (like the CUDA context): created
+        # once, shared by every solve of the run, outside the timed regions
         if world > 1 or args.nccl:  # NCCL: this process drives rank `rank`
-            nid = cgvk.nccl_unique_id() if rank == 0 else None
-            obj = [nid]
-            if dist is not None:
-                dist.broadcast_object_list(obj, src=0)
-            self.comm = cgvk.Comm(world, rank, device, obj[0])
+            key = ("nccl", world, rank, device)
+            if key not in _COMMS:
+                nid = cgvk.nccl_unique_id() if rank == 0 else None
+                obj = [nid]
+                if dist is not None:
+                    dist.broadcast_object_list(obj, src=0)
+                _COMMS[key] = cgvk.Comm(world, rank, device, obj[0])
             mine = [rank]
         else:
-            self.comm = cgvk.Comm(ranks, 0, device)
+            key = ("local", ranks, device)
+            if key not in _COMMS:
+                _COMMS[key] = cgvk.Comm(ranks, 0, device)
             mine = list(range(ranks))
+        self.comm = _COMMS[key]
         self.mats = [cgvk.RankMatrix(A.n, lo, r, *cgvk.local_rows(Acsr, lo, r), device=device) for r in mine]
         for v in variants:
             g = cgvk.Group(self.comm, self.mats, cfgs[v], Precond.JACOBI,
@@ -411,8 +421,6 @@ class SolveSet:
             s.close()
         for m in self.mats:
             m.close()
-        if self.comm:
-            self.comm.close()
 
 
 def p2p_self_check(args, P, rank, world, device, dist, iters: int = 12) -> None:

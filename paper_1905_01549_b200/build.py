@@ -54,7 +54,7 @@ def build_cuda(force: bool = False) -> str:
     deps = [os.path.join(CSRC, f) for f in CUDA_DEPS] + [os.path.join(INCLUDE, "cgvk.h")]
     if force or _stale(out, deps):
         _run([NVCC, *ARCH, *NVFLAGS, "-I", INCLUDE, "-shared", "-o", out,
-              *[os.path.join(CSRC, f) for f in CUDA_SOURCES], "-lcudart"])
+              *[os.path.join(CSRC, f) for f in CUDA_SOURCES], "-lcudart", "-lpthread"])
     return out
 
 
