@@ -464,3 +464,39 @@ def test_async_path_matches_synchronous(v, precond):
 def gpu_state_equal(a, b):
     from helpers import gpu_state
     return gpu_state(a) == gpu_state(b)
+
+
+def test_solver_after_orders_solves_without_changing_them():
+    """cgvk_solver_after: a chain of solves ordered one after another (the
+    bench's e2e order: each solve's steps after the previous one's, the
+    previous download enqueued after the order point) gives the bits of the
+    same solves run alone; ordering a solver after itself is a no-op and a
+    solver on another device is refused."""
+    P = pb.make_problem("p2", pb.poisson2d(30))
+    A = cgvk.DeviceMatrix.from_csr(P.A)
+    vs = [Variant.HS, Variant.GV, Variant.PIPE_PR, Variant.PR]
+    outs = [np.empty(A.n) for _ in vs]
+    for o in outs:
+        cgvk.host_register(o)
+    try:
+        ss = []
+        for i, v in enumerate(vs):
+            s = cgvk.initialize(cgvk.VariantConfig.make(v), A, Precond.JACOBI, P.b, P.x0)
+            if ss:
+                s.after(ss[-1])
+                ss[-1].x_async(outs[i - 1])
+            s.after(s)
+            s.step(17)
+            ss.append(s)
+        ss[-1].x_async(outs[-1])
+        for s in ss:
+            s.sync()
+        for i, v in enumerate(vs):
+            ref = cgvk.initialize(cgvk.VariantConfig.make(v), A, Precond.JACOBI, P.b, P.x0)
+            ref.step(17)
+            ref.sync()
+            assert same_bits(outs[i], ref.x), v.name
+            assert gpu_state_equal(ss[i], ref), v.name
+    finally:
+        for o in outs:
+            cgvk.host_unregister(o)

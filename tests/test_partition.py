@@ -245,3 +245,33 @@ def test_rank_local_numbering_matches_restatement(nparts):
         m = int(lo[r + 1] - lo[r])
         assert hb == (m + 31) // 32 * 32
         assert np.array_equal(np.where(want >= m, want - m + hb, want), loc)
+
+
+def test_parallel_host_plan_matches_restatement_and_reports_first_error():
+    """Shards above 2^20 entries take the threaded host path (halo plan and
+    local numbering in row chunks): same maps as the restatement, and of
+    several invalid rows the first one's error is reported, as a sequential
+    scan would."""
+    A = pb.poisson3d(80)  # 512,000 rows, 3.5 M entries: 1.75 M per rank at P = 2
+    lo = cgvk.partition_rows(A.n, 2, 80 * 80)
+    for r in range(2):
+        rp, ci, va = cgvk.local_rows(A, lo, r)
+        assert rp[-1] >= 1 << 20
+        got = cgvk.halo_plan(A.n, lo, r, rp, ci)
+        want = OP.halo_maps(A, lo, r)
+        for k in ("lower", "upper", "send_lo", "send_hi"):
+            assert np.array_equal(got[k], want[k]), (r, k)
+        loc, hb = cgvk.rank_local_columns(A.n, lo, r, rp, ci)
+        _, wloc, _, _ = OP.local_matrix(A, lo, r)
+        m = int(lo[r + 1] - lo[r])
+        assert np.array_equal(np.where(wloc >= m, wloc - m + hb, wloc), loc)
+    rp, ci, va = cgvk.local_rows(A, lo, 0)
+    bad = ci.copy()
+    late, early = int(rp[200000]), int(rp[1000])
+    bad[late] = A.n + 5                      # column out of range, late row
+    bad[early], bad[early + 1] = bad[early + 1], bad[early]  # unsorted, early row
+    with pytest.raises(cgvk.InvalidArgument, match="strictly increasing"):
+        cgvk.halo_plan(A.n, lo, 0, rp, bad)
+    bad[early], bad[early + 1] = bad[early + 1], bad[early]
+    with pytest.raises(cgvk.InvalidArgument, match="out of range"):
+        cgvk.halo_plan(A.n, lo, 0, rp, bad)
