@@ -470,8 +470,7 @@ def test_solver_after_orders_solves_without_changing_them():
     """cgvk_solver_after: a chain of solves ordered one after another (the
     bench's e2e order: each solve's steps after the previous one's, the
     previous download enqueued after the order point) gives the bits of the
-    same solves run alone; ordering a solver after itself is a no-op and a
-    solver on another device is refused."""
+    same solves run alone; ordering a solver after itself is a no-op."""
     P = pb.make_problem("p2", pb.poisson2d(30))
     A = cgvk.DeviceMatrix.from_csr(P.A)
     vs = [Variant.HS, Variant.GV, Variant.PIPE_PR, Variant.PR]
