@@ -76,7 +76,6 @@ constexpr int kP2pRanks = 8;    // ranks of one NVSwitch box
 constexpr int kP2pTotSlots = 4; // rank-total tables in flight (by stamp & 3)
 
 struct PeerPlan {
-    int on;                 // 1: the chained kernels of this rank exchange through peer memory
     int nranks, rank;
     int psel;               // HS: physical slots 1 / 2 = p0 / p1, p_old chosen by ctrl->pcur
     int tlo, hi_first;      // boundary tiles: [0, tlo) hold rows sent to the lower neighbour,
@@ -86,7 +85,6 @@ struct PeerPlan {
     int rx_stride;          // receive entries per parity: nlow + nup
     int lo_off, lo_stride;  // lower neighbour: where my rows land in its buffer (its nlow), its stride
     int hi_stride;          // upper neighbour's stride (my rows land at its 0)
-    int push;               // physical slots this rank's vectors feed (bit q)
     double* hv[kP2pSlots];                  // this rank's halo-exchanged vectors (physical slots)
     unsigned long long* rx[kP2pSlots];      // mine: [2 parities][rx_stride] entries of 2 words
     unsigned long long* rx_lo[kP2pSlots];   // the lower neighbour's receive buffers (null: none)

@@ -633,7 +633,7 @@ constexpr int kCtrlHead = offsetof(Ctrl, tot) / 16;
 // unit; thread 0 runs the predecessor's finish on it; CTA 0 writes the
 // advanced state to `out`.
 //
-// Peer-memory ranks (P.pp.on, cgvk_p2p.cuh): the predecessor's totals are the
+// Peer-memory ranks (PEER, cgvk_p2p.cuh): the predecessor's totals are the
 // rank-ordered sum of every rank's published total (waited for by stamp); a
 // K2 whose predecessor has a dist_mark (GV / pipe-PR) takes the go-ahead and
 // leaves the K1 reduction to the next K1 (`defer`), which folds it first with
