@@ -416,3 +416,53 @@ def ref_run(A, variant: int, precond: int, b, x0, x_star, max_iter: int, stop_ki
     k = min(nrec.value, rec_cap)
     return {"iters_to_1e5": it.value, "min_log10_err": mle.value, "final_state": fs.value,
             "n_records": nrec.value, "k": rk[:k], "err": re[:k], "true": rt[:k], "upd": ru[:k]}
+
+
+# ------------------------------------------------ extended precision (extprec.c)
+# The reference tests' MPFR oracles (proj/tests/oracles.hpp: exact_dot,
+# exact_dot_ratio, HighPrecCg) restated in binary128; TEST INFRASTRUCTURE.
+EXTPREC_PATH = os.path.join(HERE, "_build", "libextprec.so")
+_xp = None
+
+
+def _extprec():
+    global _xp
+    if _xp is None:
+        L = C.CDLL(EXTPREC_PATH)
+        P, I64, D = C.c_void_p, C.c_int64, C.c_double
+        L.xp_dot.restype = D
+        L.xp_dot.argtypes = [I64, P, P]
+        L.xp_abs_dot.restype = D
+        L.xp_abs_dot.argtypes = [I64, P, P]
+        L.xp_ratio.restype = D
+        L.xp_ratio.argtypes = [I64, P, P, P, P]
+        L.xp_cg.restype = C.c_int
+        L.xp_cg.argtypes = [I64, P, P, P, P, P, P, C.c_int, P]
+        _xp = L
+    return _xp
+
+
+def exact_dot(x, y) -> float:
+    x, y = _f64(x), _f64(y)
+    return _extprec().xp_dot(x.shape[0], _p(x), _p(y))
+
+
+def abs_dot(x, y) -> float:
+    x, y = _f64(x), _f64(y)
+    return _extprec().xp_abs_dot(x.shape[0], _p(x), _p(y))
+
+
+def exact_ratio(a, b, c, d) -> float:
+    a, b, c, d = _f64(a), _f64(b), _f64(c), _f64(d)
+    return _extprec().xp_ratio(a.shape[0], _p(a), _p(b), _p(c), _p(d))
+
+
+def high_prec_cg(A, b, x0, steps: int, inv_diag=None):
+    """x_1 .. x_steps of PCG carried in binary128 (rows of the result)."""
+    rp, ci, va = _i64(A.row_ptr), _i64(A.col_idx), _f64(A.values)
+    b, x0 = _f64(b), _f64(x0)
+    d = None if inv_diag is None else _f64(inv_diag)
+    xs = np.zeros((steps, A.n))
+    k = _extprec().xp_cg(A.n, _p(rp), _p(ci), _p(va), _p(d) if d is not None else None, _p(b), _p(x0),
+                         steps, _p(xs))
+    return xs[:k]
