@@ -90,6 +90,9 @@ struct PeerPlan {
     unsigned long long* rx_lo[kP2pSlots];   // the lower neighbour's receive buffers (null: none)
     unsigned long long* rx_hi[kP2pSlots];   // the upper neighbour's
     unsigned int* err;      // set when a wait gives up
+    long long delay_ns;     // experiments (CGVK_P2P_DELAY_NS): a published total counts as
+                            // arrived only this long after its publication (an injected
+                            // link latency; 0: off)
     double* xtot_peer[kP2pRanks];  // every rank's total tables
 };
 

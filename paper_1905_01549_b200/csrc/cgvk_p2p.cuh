@@ -78,8 +78,10 @@ __device__ __forceinline__ unsigned long long ll_word(unsigned int stamp, unsign
 }
 
 // ------------------------------------------------------------ rank totals
-// Table of rank q: [kP2pTotSlots][kP2pRanks][kLLWords] words.
-constexpr int kLLWords = 2 * kMaxDots;
+// Table of rank q: [kP2pTotSlots][kP2pRanks][kLLWords] words: the totals,
+// then (latency injection only) the publication time.
+constexpr int kLLTime = 2 * kMaxDots;
+constexpr int kLLWords = kLLTime + 2;
 
 __device__ __forceinline__ unsigned long long* ll_table(double* base) {
     return reinterpret_cast<unsigned long long*>(base);
@@ -96,11 +98,13 @@ __device__ __noinline__ void p2p_fold_totals(const PeerPlan* P2, unsigned int st
     const unsigned long long* tab =
         ll_table(pp.xtot_peer[pp.rank]) + (size_t)(stamp & (kP2pTotSlots - 1)) * kP2pRanks * kLLWords;
     const int nw = pp.nranks * kLLWords;
+    const bool timed = pp.delay_ns > 0;
     long long t0 = 0;
     for (int spin = 0;; ++spin) {
         bool ok = true;
         for (int q = lane; q < nw; q += 32) {
-            if ((q % kLLWords) >= 2 * ND) continue;
+            const int wi = q % kLLWords;
+            if (wi >= 2 * ND && (wi < kLLTime || !timed)) continue;
             const unsigned long long w = ld_relaxed_u64(tab + q);
             if ((unsigned int)(w >> 32) == stamp) scratch[q] = (unsigned int)w;
             else ok = false;
@@ -110,6 +114,17 @@ __device__ __noinline__ void p2p_fold_totals(const PeerPlan* P2, unsigned int st
         else if ((spin & 255) == 0 && gtimer_ns() - t0 > kP2pSpinNs) {
             if (lane == 0) atomicExch(pp.err, 1u);
             break;
+        }
+    }
+    __syncwarp();
+    if (timed && lane == 0) {  // an injected link latency: arrival = publication + delay
+        long long tmax = 0;
+        for (int r = 0; r < pp.nranks; ++r) {
+            const unsigned int* w = scratch + r * kLLWords + kLLTime;
+            const long long tp = (long long)(((unsigned long long)w[1] << 32) | w[0]);
+            tmax = tp > tmax ? tp : tmax;
+        }
+        while (gtimer_ns() < tmax + pp.delay_ns) {
         }
     }
     __syncwarp();
@@ -133,12 +148,15 @@ template <int ND>
 __device__ __noinline__ void p2p_publish_totals(const PeerPlan* P2, unsigned int stamp, const double* tot) {
     const PeerPlan& pp = *P2;
     const size_t off = ((size_t)(stamp & (kP2pTotSlots - 1)) * kP2pRanks + pp.rank) * kLLWords;
+    const unsigned long long tp = pp.delay_ns > 0 ? (unsigned long long)gtimer_ns() : 0ull;
     for (int r = 0; r < pp.nranks; ++r) {
         unsigned long long* dst = ll_table(pp.xtot_peer[r]) + off;
 #pragma unroll
         for (int d = 0; d < ND; ++d)
             st_relaxed_v2u64(dst + 2 * d, ll_word(stamp, (unsigned int)__double2loint(tot[d])),
                              ll_word(stamp, (unsigned int)__double2hiint(tot[d])));
+        if (pp.delay_ns > 0)
+            st_relaxed_v2u64(dst + kLLTime, ll_word(stamp, (unsigned int)tp), ll_word(stamp, (unsigned int)(tp >> 32)));
     }
 }
 
