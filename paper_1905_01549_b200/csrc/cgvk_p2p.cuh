@@ -124,7 +124,12 @@ __device__ __noinline__ void p2p_fold_totals(const PeerPlan* P2, unsigned int st
             const long long tp = (long long)(((unsigned long long)w[1] << 32) | w[0]);
             tmax = tp > tmax ? tp : tmax;
         }
+        const long long t1 = gtimer_ns();
         while (gtimer_ns() < tmax + pp.delay_ns) {
+            if (gtimer_ns() - t1 > kP2pSpinNs) {  // bounded like every wait
+                atomicExch(pp.err, 1u);
+                break;
+            }
         }
     }
     __syncwarp();

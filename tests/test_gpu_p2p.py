@@ -171,3 +171,35 @@ def test_p2p_nccl_single_rank(variant):
         compare(g, o, f"p2p nccl1/{variant.name} k={o.state()['k']}")
     g.close()
     comm.close()
+
+
+def test_p2p_wait_that_gives_up_is_reported(monkeypatch):
+    """A rank whose wait gives up (here: an injected link latency longer than
+    the 2 s bound) finishes its kernels and reports CGVK_ECUDA at the next
+    sync instead of hanging the GPU."""
+    monkeypatch.setenv("CGVK_P2P_DELAY_NS", str(int(2.1e9)))  # (an int: < 2^31 ns)
+    P, align = problem("poisson3d_12_slabs")
+    g, *_ = make_group(P, align, 1, Variant.HS, Precond.JACOBI)
+    monkeypatch.delenv("CGVK_P2P_DELAY_NS")
+    g.step(1)
+    with pytest.raises(cgvk.CgvkError, match="gave up"):
+        g.sync()
+    g.close()
+
+
+@pytest.mark.parametrize("kind", ["local", "nccl"])
+def test_communicator_released_before_its_groups(kind):
+    """The caller may release the communicator before the groups made over
+    it (interpreter shutdown does, in any order): the groups keep it alive."""
+    P, align = problem("poisson3d_12_slabs")
+    A = P.A
+    lo = cgvk.partition_rows(A.n, 1, align)
+    mats = [cgvk.RankMatrix(A.n, lo, 0, *cgvk.local_rows(A, lo, 0))]
+    comm = cgvk.Comm(1, 0, 0, cgvk.nccl_unique_id()) if kind == "nccl" else cgvk.Comm(1)
+    g = cgvk.Group(comm, mats, cgvk.VariantConfig.make(Variant.PIPE_PR), Precond.JACOBI, [P.b], [P.x0],
+                   p2p=True)
+    comm.close()
+    g.step(3)
+    g.sync()
+    assert g.solvers[0].k == 3
+    g.close()
