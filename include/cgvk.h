@@ -17,8 +17,11 @@
  *
  * Threading: a matrix handle is immutable after creation and may be shared by
  * solvers on the same device (the reference borrows A read-only,
- * inc/variants.hpp:103-104). A solver handle is single-owner
- * (inc/variants.hpp:95-97) and owns its stream, graphs and device buffers.
+ * inc/variants.hpp:103-104): as there, a matrix must outlive the solvers
+ * that use it. A solver handle is single-owner (inc/variants.hpp:95-97) and
+ * owns its stream, graphs and device buffers. A communicator (row-partitioned
+ * solves) is kept alive by the groups made over it, so it may be destroyed
+ * before them.
  */
 #ifndef CGVK_H
 #define CGVK_H
