@@ -60,8 +60,19 @@ __device__ __forceinline__ void ld_relaxed_v2u64(const unsigned long long* p, un
     asm volatile("ld.relaxed." CGVK_SCOPE_S ".global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
 
+// A/B of the LL store form (CGVK_P2P_ST: 0 relaxed at the exchange scope,
+// 1 volatile, 2 weak)
+#ifndef CGVK_P2P_ST
+#define CGVK_P2P_ST 0
+#endif
 __device__ __forceinline__ void st_relaxed_v2u64(unsigned long long* p, unsigned long long a, unsigned long long b) {
+#if CGVK_P2P_ST == 1
+    asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+#elif CGVK_P2P_ST == 2
+    asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+#else
     asm volatile("st.relaxed." CGVK_SCOPE_S ".global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+#endif
 }
 
 constexpr long long kP2pSpinNs = 2000000000ll;  // give up after ~2 s
@@ -95,10 +106,15 @@ __device__ __noinline__ void p2p_fold_totals(const PeerPlan* P2, unsigned int st
                                              unsigned int* scratch) {
     const PeerPlan& pp = *P2;
     const int lane = threadIdx.x & 31;
-    const unsigned long long* tab =
-        ll_table(pp.xtot_peer[pp.rank]) + (size_t)(stamp & (kP2pTotSlots - 1)) * kP2pRanks * kLLWords;
-    const int nw = pp.nranks * kLLWords;
-    const bool timed = pp.delay_ns > 0;
+    // the plan's fields in one round of independent loads (lane r: rank r's
+    // table pointer; ours is picked by a shuffle)
+    const int nranks = __ldg(&pp.nranks), rank = __ldg(&pp.rank);
+    const long long delay = __ldg(&pp.delay_ns);
+    const unsigned long long mytab = lane < kP2pRanks ? __ldg((const unsigned long long*)&pp.xtot_peer[lane]) : 0ull;
+    const unsigned long long* tab = ll_table((double*)__shfl_sync(0xffffffffu, mytab, rank)) +
+                                    (size_t)(stamp & (kP2pTotSlots - 1)) * kP2pRanks * kLLWords;
+    const int nw = nranks * kLLWords;
+    const bool timed = delay > 0;
     long long t0 = 0;
     for (int spin = 0;; ++spin) {
         bool ok = true;
@@ -112,22 +128,22 @@ __device__ __noinline__ void p2p_fold_totals(const PeerPlan* P2, unsigned int st
         if (__all_sync(0xffffffffu, ok)) break;
         if (spin == 0) t0 = gtimer_ns();
         else if ((spin & 255) == 0 && gtimer_ns() - t0 > kP2pSpinNs) {
-            if (lane == 0) atomicExch(pp.err, 1u);
+            if (lane == 0) atomicExch(P2->err, 1u);
             break;
         }
     }
     __syncwarp();
     if (timed && lane == 0) {  // an injected link latency: arrival = publication + delay
         long long tmax = 0;
-        for (int r = 0; r < pp.nranks; ++r) {
+        for (int r = 0; r < nranks; ++r) {
             const unsigned int* w = scratch + r * kLLWords + kLLTime;
             const long long tp = (long long)(((unsigned long long)w[1] << 32) | w[0]);
             tmax = tp > tmax ? tp : tmax;
         }
         const long long t1 = gtimer_ns();
-        while (gtimer_ns() < tmax + pp.delay_ns) {
+        while (gtimer_ns() < tmax + delay) {
             if (gtimer_ns() - t1 > kP2pSpinNs) {  // bounded like every wait
-                atomicExch(pp.err, 1u);
+                atomicExch(P2->err, 1u);
                 break;
             }
         }
@@ -136,7 +152,7 @@ __device__ __noinline__ void p2p_fold_totals(const PeerPlan* P2, unsigned int st
     if (lane == 0) {
 #pragma unroll
         for (int d = 0; d < kMaxDots; ++d) tot[d] = 0.0;
-        for (int r = 0; r < pp.nranks; ++r) {
+        for (int r = 0; r < nranks; ++r) {
 #pragma unroll
             for (int d = 0; d < ND; ++d) {
                 const unsigned int* w = scratch + r * kLLWords + 2 * d;
@@ -152,15 +168,24 @@ __device__ __noinline__ void p2p_fold_totals(const PeerPlan* P2, unsigned int st
 template <int ND>
 __device__ __noinline__ void p2p_publish_totals(const PeerPlan* P2, unsigned int stamp, const double* tot) {
     const PeerPlan& pp = *P2;
-    const size_t off = ((size_t)(stamp & (kP2pTotSlots - 1)) * kP2pRanks + pp.rank) * kLLWords;
-    const unsigned long long tp = pp.delay_ns > 0 ? (unsigned long long)gtimer_ns() : 0ull;
-    for (int r = 0; r < pp.nranks; ++r) {
-        unsigned long long* dst = ll_table(pp.xtot_peer[r]) + off;
+    // every plan field in one round of independent loads (a chain of
+    // dependent loads here sits on the critical path of the kernel's end)
+    const int nranks = __ldg(&pp.nranks), rank = __ldg(&pp.rank);
+    const long long delay = __ldg(&pp.delay_ns);
+    unsigned long long ptab[kP2pRanks];
+#pragma unroll
+    for (int r = 0; r < kP2pRanks; ++r) ptab[r] = __ldg((const unsigned long long*)&pp.xtot_peer[r]);
+    const size_t off = ((size_t)(stamp & (kP2pTotSlots - 1)) * kP2pRanks + rank) * kLLWords;
+    const unsigned long long tp = delay > 0 ? (unsigned long long)gtimer_ns() : 0ull;
+#pragma unroll
+    for (int r = 0; r < kP2pRanks; ++r) {
+        if (r >= nranks) break;
+        unsigned long long* dst = ll_table((double*)ptab[r]) + off;
 #pragma unroll
         for (int d = 0; d < ND; ++d)
             st_relaxed_v2u64(dst + 2 * d, ll_word(stamp, (unsigned int)__double2loint(tot[d])),
                              ll_word(stamp, (unsigned int)__double2hiint(tot[d])));
-        if (pp.delay_ns > 0)
+        if (delay > 0)
             st_relaxed_v2u64(dst + kLLTime, ll_word(stamp, (unsigned int)tp), ll_word(stamp, (unsigned int)(tp >> 32)));
     }
 }
@@ -182,20 +207,31 @@ __device__ __forceinline__ unsigned int p2p_push_mask(unsigned int m, int pcur) 
 // The thread's row i of every vector in `mask` (physical slots) into the
 // neighbours' receive buffers, stamped h — the value the thread itself just
 // stored (re-read from L2). Rows outside the send prefix / suffix: nothing.
+__device__ __forceinline__ const void* ldg_ptr(const void* const* p) {
+    return (const void*)__ldg((const unsigned long long*)p);
+}
+
 __device__ __noinline__ void p2p_push_row(const PeerPlan* P2, unsigned int mask, int i, int n, unsigned int h) {
     const PeerPlan& pp = *P2;
-    const bool lo = i < pp.nlo, hi = i >= pp.hi0 && i < n;
+    // plan fields through the read-only path, all issued before the stores
+    // (plain loads would be re-issued after every store: the compiler cannot
+    // rule out that a remote store aliases the plan)
+    const int nlo = __ldg(&pp.nlo), hi0 = __ldg(&pp.hi0);
+    const bool lo = i < nlo, hi = i >= hi0 && i < n;
     if (!lo && !hi) return;
+    const int lo_stride = __ldg(&pp.lo_stride), lo_off = __ldg(&pp.lo_off), hi_stride = __ldg(&pp.hi_stride);
     const int par = ll_parity(h);
+#pragma unroll
     for (int q = 0; q < kP2pSlots; ++q) {
         if (!((mask >> q) & 1)) continue;
-        const double v = __ldcg(pp.hv[q] + i);
+        const double* hv = (const double*)ldg_ptr((const void* const*)&pp.hv[q]);
+        auto* rlo = (unsigned long long*)ldg_ptr((const void* const*)&pp.rx_lo[q]);
+        auto* rhi = (unsigned long long*)ldg_ptr((const void* const*)&pp.rx_hi[q]);
+        const double v = __ldcg(hv + i);
         const unsigned long long w0 = ll_word(h, (unsigned int)__double2loint(v));
         const unsigned long long w1 = ll_word(h, (unsigned int)__double2hiint(v));
-        if (lo && pp.rx_lo[q])
-            st_relaxed_v2u64(pp.rx_lo[q] + 2 * ((size_t)par * pp.lo_stride + pp.lo_off + i), w0, w1);
-        if (hi && pp.rx_hi[q])
-            st_relaxed_v2u64(pp.rx_hi[q] + 2 * ((size_t)par * pp.hi_stride + (i - pp.hi0)), w0, w1);
+        if (lo && rlo) st_relaxed_v2u64(rlo + 2 * ((size_t)par * lo_stride + lo_off + i), w0, w1);
+        if (hi && rhi) st_relaxed_v2u64(rhi + 2 * ((size_t)par * hi_stride + (i - hi0)), w0, w1);
     }
 }
 
@@ -205,9 +241,10 @@ __device__ __noinline__ void p2p_push_row(const PeerPlan* P2, unsigned int mask,
 __device__ __forceinline__ void p2p_fetch(const PeerPlan& pp, const double* g, int hb, int e, unsigned int h,
                                           int pcur) {
     int q = 0;
-    while (q < kP2pSlots - 1 && pp.hv[q] != g) ++q;
-    const unsigned int want = h - ((pp.psel && q == p2p_pold(pcur)) ? 2u : 1u);
-    const unsigned long long* w = pp.rx[q] + 2 * ((size_t)ll_parity(want) * pp.rx_stride + e);
+    while (q < kP2pSlots - 1 && ldg_ptr((const void* const*)&pp.hv[q]) != (const void*)g) ++q;
+    const unsigned int want = h - ((__ldg(&pp.psel) && q == p2p_pold(pcur)) ? 2u : 1u);
+    const auto* rx = (const unsigned long long*)ldg_ptr((const void* const*)&pp.rx[q]);
+    const unsigned long long* w = rx + 2 * ((size_t)ll_parity(want) * __ldg(&pp.rx_stride) + e);
     long long t0 = 0;
     for (int spin = 0;; ++spin) {
         unsigned long long a, b;

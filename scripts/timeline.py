@@ -10,20 +10,32 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1905_01549_b200 import cgvk, problems as pb  # noqa: E402
 
-cfg = sys.argv[1] if len(sys.argv) > 1 else "p64"
+args = [a for a in sys.argv[1:] if a != "--p2p"]
+p2p = "--p2p" in sys.argv  # a one-rank peer-memory group instead of the single-GPU solver
+cfg = args[0] if args else "p64"
 P = pb.config_problem(cfg)
 A = cgvk.DeviceMatrix.from_csr(P.A)
 lib = cgvk._lib
 lib.cgvk_debug_timeline.argtypes = [C.c_void_p]
-for v in sys.argv[2:] or ["pr", "hs", "gv"]:
-    s = cgvk.initialize(cgvk.VariantConfig.make(cgvk.variant_from_name(v)), A, cgvk.Precond.JACOBI, P.b, P.x0)
+if p2p:
+    plane = {"p2d": 256, "p64": 4096, "p128": 16384, "v256": 65536}[cfg]
+    lo = cgvk.partition_rows(P.A.n, 1, plane)
+    mats = [cgvk.RankMatrix(P.A.n, lo, 0, *cgvk.local_rows(P.A, lo, 0))]
+    comm = cgvk.Comm(1)
+for v in args[1:] or ["pr", "hs", "gv"]:
+    cfgv = cgvk.VariantConfig.make(cgvk.variant_from_name(v))
+    if p2p:
+        g = cgvk.Group(comm, mats, cfgv, cgvk.Precond.JACOBI, [P.b], [P.x0], p2p=True)
+        s = g.solvers[0]
+    else:
+        s = cgvk.initialize(cfgv, A, cgvk.Precond.JACOBI, P.b, P.x0)
     s.time_steps(20)
     buf = np.zeros((2, 1024, 8), np.uint64)
     lib.cgvk_debug_timeline(buf.ctypes.data)  # read-and-clear
     s.step(1)
     s.sync()
     assert lib.cgvk_debug_timeline(buf.ctypes.data) == 0
-    print(f"== {cfg} {v}")
+    print(f"== {cfg} {v}" + (" (one-rank peer-memory group)" if p2p else ""))
     t0 = None
     for k, name in ((0, "K1 update"), (1, "K2 spmv")):
         b = buf[k].astype(np.int64)
@@ -42,4 +54,4 @@ for v in sys.argv[2:] or ["pr", "hs", "gv"]:
         if os.environ.get("CGVK_CHAIN", "1") != "0" and (b[:, 5] > 0).all():
             pro = b[:, 5] - t0
             print(f"      chain prologue done {pro.min()/1e3:6.2f}..{pro.max()/1e3:6.2f}")
-    s.close()
+    (g if p2p else s).close()
