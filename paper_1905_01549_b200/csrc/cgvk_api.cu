@@ -210,6 +210,7 @@ struct cgvk_matrix_s {
     double* out = nullptr;
     int* flags = nullptr;
     double* tmp[4] = {nullptr, nullptr, nullptr, nullptr};
+    struct SpmvEngine* spmv_eng = nullptr;  // the L1 SpMV through the solver's engines (built on first use)
 
     Params base() const {
         Params P{};
@@ -232,6 +233,11 @@ struct cgvk_matrix_s {
 
 int matrix_create(int64_t n, int64_t ncols, const int64_t* row_ptr, const int64_t* col_idx,
                   const double* values, int device, int flags, bool check_sorted, cgvk_matrix* out);
+// The L1 SpMV through the solver's engines (defined with the launch machinery below).
+struct SpmvEngine;
+int spmv_engine(cgvk_matrix a, int nrhs, const double* x1, const double* x2, double* y1, double* y2);
+int spmv_engine_launch(cgvk_matrix a, int nrhs, const double* x1, const double* x2, double* y1, double* y2);
+void free_spmv_engine(SpmvEngine* e);
 
 namespace {
 
@@ -295,7 +301,7 @@ int run_dots(cgvk_matrix a, cudaStream_t stream, double* part, unsigned int* cou
 
 int ensure_tmp(cgvk_matrix a, int count) {
     for (int q = 0; q < count; ++q)
-        if (!a->tmp[q]) TRY(dalloc(&a->tmp[q], a->n));
+        if (!a->tmp[q]) TRY(dalloc(&a->tmp[q], a->n + 32));  // (+32: bulk copies of the last tile)
     return CGVK_OK;
 }
 
@@ -641,6 +647,7 @@ int cgvk_matrix_destroy(cgvk_matrix a) {
     dfree(a->out);
     dfree(a->flags);
     for (double* t : a->tmp) dfree(t);
+    free_spmv_engine(a->spmv_eng);
     if (a->stream) cudaStreamDestroy(a->stream);
     delete a;
     return CGVK_OK;
@@ -675,6 +682,7 @@ int cgvk_spmv(cgvk_matrix a, const double* x, double* y) {
     std::lock_guard<std::mutex> lock(a->mu);
     CK(cudaSetDevice(a->device));
     if (a->n == 0) return CGVK_OK;
+    if (a->ncols == a->n) return spmv_engine(a, 1, x, nullptr, y, nullptr);
     TRY(ensure_tmp(a, 2));
     CK(cudaMemcpyAsync(a->tmp[0], x, 8 * a->n, cudaMemcpyHostToDevice, a->stream));
     k_spmv<<<a->G, kBlock, 0, a->stream>>>(a->base(), a->tmp[0], nullptr, a->tmp[1], 0);
@@ -689,6 +697,7 @@ int cgvk_block_spmv(cgvk_matrix a, const double* x1, const double* x2, double* y
     std::lock_guard<std::mutex> lock(a->mu);
     CK(cudaSetDevice(a->device));
     if (a->n == 0) return CGVK_OK;
+    if (a->ncols == a->n) return spmv_engine(a, 2, x1, x2, y1, y2);
     TRY(ensure_tmp(a, 4));
     CK(cudaMemcpyAsync(a->tmp[0], x1, 8 * a->n, cudaMemcpyHostToDevice, a->stream));
     CK(cudaMemcpyAsync(a->tmp[1], x2, 8 * a->n, cudaMemcpyHostToDevice, a->stream));
@@ -765,11 +774,17 @@ int cgvk_time_ops(cgvk_matrix a, int reps, double* ms) {
     D.part = a->part;
     D.counter = a->counter;
     D.out = a->out;
+    const bool eng = a->ncols == a->n;  // the engines' SpMV (cgvk_spmv's), else the generic kernels
+    int erc = CGVK_OK;
     auto op = [&](int which) {
         switch (which) {
-            case CGVK_TIME_SPMV: k_spmv<<<a->G, kBlock, 0, a->stream>>>(P, a->tmp[0], nullptr, a->tmp[2], 0); break;
+            case CGVK_TIME_SPMV:
+                if (eng) erc = spmv_engine_launch(a, 1, a->tmp[0], nullptr, a->tmp[2], nullptr);
+                else k_spmv<<<a->G, kBlock, 0, a->stream>>>(P, a->tmp[0], nullptr, a->tmp[2], 0);
+                break;
             case CGVK_TIME_BLOCK_SPMV:
-                k_block_spmv<<<a->G, kBlock, 0, a->stream>>>(P, a->tmp[0], a->tmp[1], a->tmp[2], a->tmp[3]);
+                if (eng) erc = spmv_engine_launch(a, 2, a->tmp[0], a->tmp[1], a->tmp[2], a->tmp[3]);
+                else k_block_spmv<<<a->G, kBlock, 0, a->stream>>>(P, a->tmp[0], a->tmp[1], a->tmp[2], a->tmp[3]);
                 break;
             case CGVK_TIME_DOT: k_dots<1><<<a->G, kBlock, 0, a->stream>>>(D); break;
             default: k_scale<<<grid_elem(n), 256, 0, a->stream>>>(n, nullptr, a->tmp[0], a->tmp[2]); break;
@@ -784,6 +799,7 @@ int cgvk_time_ops(cgvk_matrix a, int reps, double* ms) {
         for (int r = 0; r < reps; ++r) op(which);
         CK(cudaEventRecord(e1, a->stream));
         CK(cudaEventSynchronize(e1));
+        TRY(erc);
         float f = 0.f;
         CK(cudaEventElapsedTime(&f, e0, e1));
         ms[which] = f / reps;
@@ -1102,6 +1118,51 @@ cudaError_t launch_with(cudaStream_t st, const KLaunch& L, const Params& P) {
     cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, L.fn, P, L.S);
 }
+
+}  // namespace
+
+// The L1 SpMV of the C ABI through the solver's engines (the CSR tile
+// pipeline or the band engine, whichever the matrix uses): SpmvOp<1> / <2>.
+struct SpmvEngine {
+    KLaunch L[2];  // 1 and 2 right-hand sides
+};
+
+void free_spmv_engine(SpmvEngine* e) { delete e; }
+
+// a->mu held
+int spmv_engine_launch(cgvk_matrix a, int nrhs, const double* x1, const double* x2, double* y1, double* y2) {
+    if (!a->spmv_eng) {
+        auto* e = new SpmvEngine;
+        int rc = make_launch<SpmvOp<1>, SpmvOp<1>>(a, &e->L[0]);
+        if (rc == CGVK_OK) rc = make_launch<SpmvOp<2>, SpmvOp<2>>(a, &e->L[1]);
+        if (rc != CGVK_OK) {
+            delete e;
+            return rc;
+        }
+        a->spmv_eng = e;
+    }
+    Params P = a->base();
+    P.w = const_cast<double*>(x1);
+    P.u = const_cast<double*>(x2);
+    P.t = y1;
+    P.s = y2;
+    CK(launch_with(a->stream, a->spmv_eng->L[nrhs - 1], P));
+    return CGVK_OK;
+}
+
+// host vectors in and out (cgvk_spmv / cgvk_block_spmv); a->mu held
+int spmv_engine(cgvk_matrix a, int nrhs, const double* x1, const double* x2, double* y1, double* y2) {
+    TRY(ensure_tmp(a, 4));
+    CK(cudaMemcpyAsync(a->tmp[0], x1, 8 * a->n, cudaMemcpyHostToDevice, a->stream));
+    if (nrhs == 2) CK(cudaMemcpyAsync(a->tmp[1], x2, 8 * a->n, cudaMemcpyHostToDevice, a->stream));
+    TRY(spmv_engine_launch(a, nrhs, a->tmp[0], a->tmp[1], a->tmp[2], a->tmp[3]));
+    CK(cudaMemcpyAsync(y1, a->tmp[2], 8 * a->n, cudaMemcpyDeviceToHost, a->stream));
+    if (nrhs == 2) CK(cudaMemcpyAsync(y2, a->tmp[3], 8 * a->n, cudaMemcpyDeviceToHost, a->stream));
+    CK(cudaStreamSynchronize(a->stream));
+    return CGVK_OK;
+}
+
+namespace {
 
 // The chained schedule is the default for graphs; CGVK_CHAIN=0 captures the
 // last-CTA schedule instead (A/B). Row-partitioned ranks never chain (their

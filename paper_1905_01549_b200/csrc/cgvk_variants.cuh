@@ -821,6 +821,38 @@ struct PprK2 {
     __device__ void finish(const Params&, Ctrl* c, const double*) const { c->mode2 = MODE_SKIP; }
 };
 
+// ============================================================  L1 SpMV
+// y = A x (NRHS 1) or (y1, y2) = (A x1, A x2) in one pass (NRHS 2) through
+// the solver's engines, for the C ABI's cgvk_spmv / cgvk_block_spmv
+// (src/sparse_matrix.cpp:109-143): x1, x2 in P.w, P.u; y1, y2 in P.t, P.s.
+// Rows summed in CSR order, as every SpMV here.
+template <int NRHS>
+struct SpmvOp {
+    static constexpr int NV = 0, ND = 0;
+    static constexpr bool CSR = true;
+    static constexpr int NG = NRHS;
+    __device__ bool enter(const Params&) { return true; }
+    __device__ const double* vec(const Params&, int) const { return nullptr; }
+    __device__ const double* gsrc(const Params& P, int k) const { return k ? P.u : P.w; }
+    __device__ int sync() const { return 0; }
+    __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
+    template <class In, class RR>
+    __device__ void row(const Params& P, int i, const In& in, const RR& R, double*) const {
+        const double* __restrict__ x1 = P.w;
+        if constexpr (NRHS == 2) {
+            const double* __restrict__ x2 = P.u;
+            double y1, y2;
+            row_dot2(R, [&](int j) { return in.gather(0, j, x1); }, [&](int j) { return in.gather(1, j, x2); }, y1,
+                     y2);
+            P.t[i] = y1;
+            P.s[i] = y2;
+        } else {
+            P.t[i] = row_dot(R, [&](int j) { return in.gather(0, j, x1); });
+        }
+    }
+    __device__ void finish(const Params&, Ctrl*, const double*) const {}
+};
+
 #undef SV
 
 }  // namespace cgvk
