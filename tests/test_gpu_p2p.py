@@ -203,3 +203,23 @@ def test_communicator_released_before_its_groups(kind):
     g.sync()
     assert g.solvers[0].k == 3
     g.close()
+
+
+@pytest.mark.parametrize("cfg,nranks", [("p64", 8), ("p128", 2)])
+@pytest.mark.parametrize("variant", [Variant.HS, Variant.PR, Variant.GV, Variant.PIPE_PR])
+def test_p2p_baseline_shards_equal_copy_transport(cfg, nranks, variant):
+    """BASELINE-size shards (P64 over 8 ranks: 16 boundary tiles per side of a
+    128-tile rank; P128 over 2: 64 of 4096): 24 iterations through the peer
+    transport give the copy transport's bits — histories and x."""
+    P = pb.config_problem(cfg)
+    plane = {"p64": 64 * 64, "p128": 128 * 128}[cfg]
+    out = []
+    for p2p in (True, False):
+        g, *_ = make_group(P, plane, nranks, variant, Precond.JACOBI, p2p=p2p)
+        assert g.transport == ("p2p" if p2p else "local")
+        g.step(24)
+        g.sync()
+        out.append((g.solvers[0].history(), g.vector(Vec.X)))
+        g.close()
+    assert np.array_equal(out[0][0].view(np.int64), out[1][0].view(np.int64))
+    assert np.array_equal(out[0][1].view(np.int64), out[1][1].view(np.int64))
