@@ -1141,6 +1141,7 @@ int spmv_engine_launch(cgvk_matrix a, int nrhs, const double* x1, const double* 
         }
         a->spmv_eng = e;
     }
+    if (nrhs == 0) return CGVK_OK;  // (build only)
     Params P = a->base();
     P.w = const_cast<double*>(x1);
     P.u = const_cast<double*>(x2);
@@ -1365,6 +1366,24 @@ int solver_init(cgvk_solver s, const double* b, const double* x0) {
     CK(cudaMemcpyAsync(s->b, b, 8 * n, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(s->x, x0, 8 * n, cudaMemcpyHostToDevice, st));
     TRY(order_uploads(s, true));
+    // y = A x through the engines' SpMV for a plain matrix (the generic kernel
+    // for a rank-local one)
+    const bool eng = a->ncols == a->n;
+    if (eng) {
+        std::lock_guard<std::mutex> lock(a->mu);
+        TRY(spmv_engine_launch(a, 0, nullptr, nullptr, nullptr, nullptr));  // (builds it; launches nothing)
+    }
+    auto spmv = [&](const double* src, double* dst) -> int {
+        if (eng) {
+            Params Q = P;
+            Q.w = const_cast<double*>(src);
+            Q.t = dst;
+            CK(launch_with(st, a->spmv_eng->L[0], Q));
+        } else {
+            k_spmv<<<G, kBlock, 0, st>>>(P, src, nullptr, dst, 0);
+        }
+        return CGVK_OK;
+    };
     // r0 = b - A x0
     k_spmv<<<G, kBlock, 0, st>>>(P, s->x, s->b, s->r, 0);
     if (stores_rt) k_scale<<<eg, 256, 0, st>>>((int)n, d, s->r, s->rt);
@@ -1378,7 +1397,7 @@ int solver_init(cgvk_solver s, const double* b, const double* x0) {
     k_init_nu<<<1, 1, 0, st>>>(s->ctrl, s->dout, s->hist, prec ? 1 : 0);
     // p0 = r~0; s0 = A p0; mu0; alpha0
     k_scale<<<eg, 256, 0, st>>>((int)n, nullptr, rtv, s->p0);
-    k_spmv<<<G, kBlock, 0, st>>>(P, s->p0, nullptr, s->s, 0);
+    TRY(spmv(s->p0, s->s));
     {
         const double* xs[1] = {s->p0};
         const double* ys[1] = {s->s};
@@ -1409,14 +1428,14 @@ int solver_init(cgvk_solver s, const double* b, const double* x0) {
             TRY(scalar_dots(v == CGVK_PR || expr != CGVK_NU_MEURANT || s->cfg.track_delta));
             break;
         case CGVK_GV:
-            k_spmv<<<G, kBlock, 0, st>>>(P, rtv, nullptr, s->w, 0);
-            k_spmv<<<G, kBlock, 0, st>>>(P, stv, nullptr, s->u, 0);
+            TRY(spmv(rtv, s->w));
+            TRY(spmv(stv, s->u));
             e.spmv = 2;
             break;
         default:  // pipelined PR
-            k_spmv<<<G, kBlock, 0, st>>>(P, rtv, nullptr, s->w, 0);
+            TRY(spmv(rtv, s->w));
             if (prec && !s->cfg.recompute_w) k_scale<<<eg, 256, 0, st>>>((int)n, d, s->w, s->wt);
-            k_spmv<<<G, kBlock, 0, st>>>(P, stv, nullptr, s->u, 0);
+            TRY(spmv(stv, s->u));
             e.spmv = 2;
             e.prec = prec ? 2 : 0;  // w~ = M w, u~ = M u
             TRY(scalar_dots(expr != CGVK_NU_MEURANT || s->cfg.track_delta));
