@@ -1124,7 +1124,7 @@ cudaError_t launch_with(cudaStream_t st, const KLaunch& L, const Params& P) {
 // The L1 SpMV of the C ABI through the solver's engines (the CSR tile
 // pipeline or the band engine, whichever the matrix uses): SpmvOp<1> / <2>.
 struct SpmvEngine {
-    KLaunch L[2];  // 1 and 2 right-hand sides
+    KLaunch L[3];  // 1 and 2 right-hand sides; the residual form b - A x
 };
 
 void free_spmv_engine(SpmvEngine* e) { delete e; }
@@ -1135,6 +1135,7 @@ int spmv_engine_launch(cgvk_matrix a, int nrhs, const double* x1, const double* 
         auto* e = new SpmvEngine;
         int rc = make_launch<SpmvOp<1>, SpmvOp<1>>(a, &e->L[0]);
         if (rc == CGVK_OK) rc = make_launch<SpmvOp<2>, SpmvOp<2>>(a, &e->L[1]);
+        if (rc == CGVK_OK) rc = make_launch<SpmvOp<1, true>, SpmvOp<1, true>>(a, &e->L[2]);
         if (rc != CGVK_OK) {
             delete e;
             return rc;
@@ -1373,19 +1374,20 @@ int solver_init(cgvk_solver s, const double* b, const double* x0) {
         std::lock_guard<std::mutex> lock(a->mu);
         TRY(spmv_engine_launch(a, 0, nullptr, nullptr, nullptr, nullptr));  // (builds it; launches nothing)
     }
-    auto spmv = [&](const double* src, double* dst) -> int {
+    auto spmv = [&](const double* src, const double* bvec, double* dst) -> int {
         if (eng) {
             Params Q = P;
             Q.w = const_cast<double*>(src);
+            Q.u = const_cast<double*>(bvec);
             Q.t = dst;
-            CK(launch_with(st, a->spmv_eng->L[0], Q));
+            CK(launch_with(st, a->spmv_eng->L[bvec ? 2 : 0], Q));
         } else {
-            k_spmv<<<G, kBlock, 0, st>>>(P, src, nullptr, dst, 0);
+            k_spmv<<<G, kBlock, 0, st>>>(P, src, bvec, dst, 0);
         }
         return CGVK_OK;
     };
     // r0 = b - A x0
-    k_spmv<<<G, kBlock, 0, st>>>(P, s->x, s->b, s->r, 0);
+    TRY(spmv(s->x, s->b, s->r));
     if (stores_rt) k_scale<<<eg, 256, 0, st>>>((int)n, d, s->r, s->rt);
     const double* rtv = stores_rt ? s->rt : s->r;
     {
@@ -1397,7 +1399,7 @@ int solver_init(cgvk_solver s, const double* b, const double* x0) {
     k_init_nu<<<1, 1, 0, st>>>(s->ctrl, s->dout, s->hist, prec ? 1 : 0);
     // p0 = r~0; s0 = A p0; mu0; alpha0
     k_scale<<<eg, 256, 0, st>>>((int)n, nullptr, rtv, s->p0);
-    TRY(spmv(s->p0, s->s));
+    TRY(spmv(s->p0, nullptr, s->s));
     {
         const double* xs[1] = {s->p0};
         const double* ys[1] = {s->s};
@@ -1428,14 +1430,14 @@ int solver_init(cgvk_solver s, const double* b, const double* x0) {
             TRY(scalar_dots(v == CGVK_PR || expr != CGVK_NU_MEURANT || s->cfg.track_delta));
             break;
         case CGVK_GV:
-            TRY(spmv(rtv, s->w));
-            TRY(spmv(stv, s->u));
+            TRY(spmv(rtv, nullptr, s->w));
+            TRY(spmv(stv, nullptr, s->u));
             e.spmv = 2;
             break;
         default:  // pipelined PR
-            TRY(spmv(rtv, s->w));
+            TRY(spmv(rtv, nullptr, s->w));
             if (prec && !s->cfg.recompute_w) k_scale<<<eg, 256, 0, st>>>((int)n, d, s->w, s->wt);
-            TRY(spmv(stv, s->u));
+            TRY(spmv(stv, nullptr, s->u));
             e.spmv = 2;
             e.prec = prec ? 2 : 0;  // w~ = M w, u~ = M u
             TRY(scalar_dots(expr != CGVK_NU_MEURANT || s->cfg.track_delta));
@@ -1813,7 +1815,15 @@ int cgvk_solver_true_residual(cgvk_solver s, double* out) {
         return CGVK_OK;
     }
     Params P = s->a->base();
-    k_spmv<<<s->a->G, kBlock, 0, s->stream>>>(P, s->x, s->b, s->tmp, 0);
+    if (s->a->spmv_eng) {  // the engines' residual form (built by initialize for a plain matrix)
+        Params Q = P;
+        Q.w = s->x;
+        Q.u = s->b;
+        Q.t = s->tmp;
+        CK(launch_with(s->stream, s->a->spmv_eng->L[2], Q));
+    } else {
+        k_spmv<<<s->a->G, kBlock, 0, s->stream>>>(P, s->x, s->b, s->tmp, 0);
+    }
     CK(cudaGetLastError());
     const double* xs[1] = {s->tmp};
     double h[1];

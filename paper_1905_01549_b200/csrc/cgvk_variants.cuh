@@ -825,8 +825,9 @@ struct PprK2 {
 // y = A x (NRHS 1) or (y1, y2) = (A x1, A x2) in one pass (NRHS 2) through
 // the solver's engines, for the C ABI's cgvk_spmv / cgvk_block_spmv
 // (src/sparse_matrix.cpp:109-143): x1, x2 in P.w, P.u; y1, y2 in P.t, P.s.
+// RESID: y = b - A x with b in P.u (initialize()'s r0, src/variants.cpp:376).
 // Rows summed in CSR order, as every SpMV here.
-template <int NRHS>
+template <int NRHS, bool RESID = false>
 struct SpmvOp {
     static constexpr int NV = 0, ND = 0;
     static constexpr bool CSR = true;
@@ -847,7 +848,8 @@ struct SpmvOp {
             P.t[i] = y1;
             P.s[i] = y2;
         } else {
-            P.t[i] = row_dot(R, [&](int j) { return in.gather(0, j, x1); });
+            const double y = row_dot(R, [&](int j) { return in.gather(0, j, x1); });
+            P.t[i] = RESID ? SUB(P.u[i], y) : y;
         }
     }
     __device__ void finish(const Params&, Ctrl*, const double*) const {}
