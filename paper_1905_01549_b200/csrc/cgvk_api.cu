@@ -1048,15 +1048,18 @@ int pick_pair(cgvk_matrix a, cgvk_solver s) {
     s->k1c0.S.chain = CH_ON;
     s->k1c = s->k1;
     s->k1c.S.chain = CH_ON | CH_FOLD;
+    s->k1c.S.gprev = s->k2.S.gvirt;
     s->k2c = s->k2;
     s->k2c.S.chain = CH_ON | CH_FOLD | CH_ODD;
+    s->k2c.S.gprev = s->k1.S.gvirt;
     s->kt = KLaunch{};
     s->kt.fn = k_chain_tail<Op1, Op2>;
     s->kt.fn_peer = k_chain_tail<Op1, Op2, true>;
     s->kt.grid = 1;
-    s->kt.threads = 32;
+    s->kt.threads = kConsumers;
     s->kt.smem = 0;
     s->kt.S = s->k2.S;
+    s->kt.S.gprev = s->k2.S.gvirt;
     s->fin1 = k_finalize<Op1>;
     s->fin2 = k_finalize<Op2>;
     return CGVK_OK;
@@ -1594,7 +1597,7 @@ int solver_alloc(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, cud
     const int64_t nv = a->ncols + 32;
     if ((rc = dalloc(&s->x, nv)) || (rc = dalloc(&s->r, nv)) || (rc = dalloc(&s->p0, nv)) ||
         (rc = dalloc(&s->s, nv)) || (rc = dalloc(&s->b, nv)) || (rc = dalloc(&s->tmp, nv)) ||
-        (rc = dalloc(&s->part, kMaxDots * (size_t)a->gmax + 4)) ||
+        (rc = dalloc(&s->part, 2 * kMaxDots * (size_t)a->gmax + 4)) ||
         (rc = dalloc(&s->hist, s->hist_cap)) ||
         (rc = dalloc(&s->dout, 8)) || (rc = dalloc(&s->counter, 4)) || (rc = dalloc(&s->ctrl, 2)))
         return bail(rc);
@@ -1633,6 +1636,7 @@ int solver_alloc(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, cud
     P.st = s->st;
     P.wt = s->wt;
     P.part = s->part;
+    P.part_b = s->part + kMaxDots * (size_t)a->gmax;
     P.hist = s->hist;
     P.ctrl = s->ctrl;
     P.ctrl_b = s->ctrl + 1;

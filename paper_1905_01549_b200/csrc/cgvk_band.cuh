@@ -147,7 +147,8 @@ __device__ __forceinline__ void band_body(const Params& P, const StageCfg& S) {
     pdl_wait();
     pdl_trigger();
     const int chain = S.chain;
-    if (chain) chain_prologue<Op, Prev>(P, chain, H, (chain & CH_ODD) ? P.ctrl : P.ctrl_b);
+    if (chain) chain_prologue<Op, Prev>(P, chain, H, (chain & CH_ODD) ? P.ctrl : P.ctrl_b, S.gprev);
+    double* const partw = (chain && !(chain & CH_ODD)) ? P.part_b : P.part;
     Op op;
     if (!(chain ? op.enter(with_ctrl(P, &H->cs)) : op.enter(P))) return;  // uniform over the grid
 
@@ -329,12 +330,13 @@ __device__ __forceinline__ void band_body(const Params& P, const StageCfg& S) {
             cta_tree_c<Op::ND>(acc, H->red);
             if (t == 0) {
 #pragma unroll
-                for (int d = 0; d < Op::ND; ++d) P.part[d * Gv + vb] = acc[d];
+                for (int d = 0; d < Op::ND; ++d) partw[d * Gv + vb] = acc[d];
             }
         }
     }
     const int mode = op.sync();
-    if (mode == 0 || (chain && mode == 1)) return;  // chained: the next kernel finishes
+    // chained: the next kernel finishes (and folds the partials)
+    if (mode == 0 || chain) return;
     unsigned int* counter = op.counter(P);
     if constexpr (GR > 1) {  // no dots: arrive, the last CTA finishes
         static_assert(GR == 1 || Op::ND == 0, "consumer groups only without dot products");
@@ -363,13 +365,6 @@ __device__ __forceinline__ void band_body(const Params& P, const StageCfg& S) {
         }
     }
     if (t == 0) *counter = 0u;
-    if (chain) {  // the totals; the next kernel runs the scalar tail
-        if (t == 0) {
-#pragma unroll
-            for (int d = 0; d < Op::ND; ++d) ((chain & CH_ODD) ? P.ctrl : P.ctrl_b)->tot[d] = tot[d];
-        }
-        return;
-    }
     if (P.dist && mode == 2) {
         if (t == 0) {
 #pragma unroll

@@ -60,8 +60,8 @@ struct __align__(16) Ctrl {
     unsigned int hseq;
     unsigned int defer;
     unsigned int dstamp;
-    // chained schedule (cgvk_stream.cuh chain_prologue): the folded totals of
-    // the kernel that wrote this copy, for its successor's scalar tail
+    // spare (the chained schedule's successor folds the partials itself,
+    // cgvk_stream.cuh chain_prologue); CTA 0 copies the words before it forward
     double tot[kMaxDots];
     double pad_[2];
 };
@@ -121,6 +121,7 @@ struct Params {
     const unsigned short* __restrict__ band_ci;   // column - (tile - band_h) * 256
     int band_h;                                   // window half-width in tiles
     double* part;  // [kMaxDots][G] CTA partials
+    double* part_b;  // chained schedule: K1's partials (K2 writes `part`)
     double* hist;  // rr per iteration (null: not recorded by this CTA)
     Ctrl* ctrl;
     // chained schedule (cgvk_stream.cuh chain_prologue): the second control

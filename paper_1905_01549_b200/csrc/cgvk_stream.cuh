@@ -105,6 +105,7 @@ struct StageCfg {
     int ring;       // band engine: window ring tiles (2H + nstage)
     int pf;         // band engine: L2 prefetch distance (tiles)
     int chain;      // chained schedule: CH_* bits (0: last-CTA finish, in place)
+    int gprev;      // chained schedule: the predecessor's Gv (its partials)
     unsigned int p2p_push;  // peer ranks: physical halo slots this launch pushes (kPushPnew: HS's p_new)
 };
 
@@ -600,19 +601,22 @@ __device__ __forceinline__ void finish_last(const Op& op, const Params& P, PipeH
 // ------------------------------------------------------ chained schedule
 //
 // The last-CTA schedule ends every reducing kernel with a chain of round
-// trips on its critical path: the fold, then a load of the control block, the
-// scalar tail, the write-back, the kernel's end — and only then may the next
-// kernel read a scalar. In the chained schedule the last CTA stops at the
-// folded totals (Ctrl::tot of the copy its kernel writes); every CTA of the
-// NEXT kernel brings that copy in with one bulk copy right after
-// griddepcontrol.wait and runs the predecessor's finish on it — the same
-// scalar code on the same bits in every CTA. A kernel whose finish needs no
-// dots (sync() == 1) does not arrive at all. The control block is double-
-// buffered: K1 reads `ctrl` and CTA 0 writes the advanced state to `ctrl_b`;
-// K2 reads `ctrl_b` and writes `ctrl` (no kernel reads the copy it writes).
-// A graph of chained iterations ends with k_chain_tail (one CTA), which
-// finishes the last K2 and leaves `ctrl` complete, as the last-CTA schedule
-// does.
+// trips on its critical path: a fence and the arrival atomic, the fold of
+// all partials, a load of the control block, the scalar tail, the
+// write-back, the kernel's end — and only then may the next kernel read a
+// scalar. In the chained schedule a reducing kernel's CTAs stop at their
+// partials; every CTA of the NEXT kernel, right after griddepcontrol.wait,
+// loads the control block and the partials together, folds them in the
+// canonical order and runs the predecessor's finish — the same scalar code
+// on the same bits in every CTA (measured: P64 61.1 k -> 66.9 k it/s, P2D
+// 86.7 k -> 96.4 k against the last CTA folding into the control block). A
+// kernel whose finish needs no dots (sync() == 1) does not arrive at all.
+// Control block and partials are double-buffered: K1 reads `ctrl` / `part`
+// and writes `ctrl_b` (CTA 0) / `part_b`; K2 the other way round (no kernel
+// reads the copy it writes). A graph of chained iterations ends with
+// k_chain_tail (one CTA), which finishes the last K2 and leaves `ctrl`
+// complete, as the last-CTA schedule does. Peer-memory ranks keep a last CTA
+// per rank: it publishes the rank total (cgvk_p2p.cuh).
 constexpr int CH_ON = 1;    // chained: totals only, the successor finishes
 constexpr int CH_FOLD = 2;  // run the predecessor's finish first
 constexpr int CH_ODD = 4;   // the iteration's second kernel (K2)
@@ -623,15 +627,25 @@ __device__ __forceinline__ Params with_ctrl(const Params& P, Ctrl* c) {
     return Q;
 }
 
+constexpr int kSuccFoldMax = 2 * kConsumers;  // predecessor partials per register pass
+
 // Words of the control block CTA 0 copies forward (the totals are written by
 // the kernel's last CTA).
 constexpr int kCtrlHead = offsetof(Ctrl, tot) / 16;
 
-// All threads of the CTA. Warp 0 loads the control block (with the
-// predecessor's totals) into H->cs — one coalesced 256-byte load, not a bulk
-// copy, which would queue behind the producer's matrix prefetch in the TMA
-// unit; thread 0 runs the predecessor's finish on it; CTA 0 writes the
-// advanced state to `out`.
+// All threads of the CTA. Warp 0 loads the control block into H->cs — one
+// coalesced 256-byte load, not a bulk copy, which would queue behind the
+// producer's matrix prefetch in the TMA unit; thread 0 runs the
+// predecessor's finish on it; CTA 0 writes the advanced state to `out`.
+//
+// Single GPU: the predecessor's CTAs only wrote their
+// partials (no arrival counter, no fence, no last CTA — griddepcontrol.wait
+// already orders them before this kernel); the consumer warps of EVERY CTA
+// fold them here in the canonical order (fold_partials + cta_tree_c: the
+// same bits the last CTA produced), their loads issued together with the
+// control-block load. `gprev` = the predecessor's virtual CTAs. The partial
+// buffers are double-buffered like the control block (K1 writes `part_b`,
+// K2 `part`), so a slow CTA still folding never sees its successor's writes.
 //
 // Peer-memory ranks (PEER, cgvk_p2p.cuh): the predecessor's totals are the
 // rank-ordered sum of every rank's published total (waited for by stamp); a
@@ -639,31 +653,61 @@ constexpr int kCtrlHead = offsetof(Ctrl, tot) / 16;
 // leaves the K1 reduction to the next K1 (`defer`), which folds it first with
 // its own type (Self); `incr` advances the kernel sequence number.
 template <class Self, class Prev, bool PEER = false>
-__device__ __forceinline__ void chain_prologue(const Params& P, int chain, PipeHeader* H, Ctrl* out,
+__device__ __forceinline__ void chain_prologue(const Params& P, int chain, PipeHeader* H, Ctrl* out, int gprev,
                                                bool incr = true) {
     const int t = threadIdx.x;
-    if (t < 32) {
-        constexpr int kWords = sizeof(Ctrl) / 16;
-        const uint4* in = reinterpret_cast<const uint4*>((chain & CH_ODD) ? P.ctrl_b : P.ctrl);
-        if (t < kWords) reinterpret_cast<uint4*>(&H->cs)[t] = __ldcg(in + t);
-        __syncwarp();
-    }
     if constexpr (!PEER) {
-        if (t == 0 && (chain & CH_FOLD)) {
-            Params Q = with_ctrl(P, &H->cs);
-            if (blockIdx.x != 0) Q.hist = nullptr;  // side effects once
-            Prev prev;
-            if (prev.enter(Q)) {
-                const int m = prev.sync();
-                if (m == 2) {
-                    prev.finish(Q, &H->cs, H->cs.tot);
-                } else if (m == 1) {
-                    const double none[kMaxDots] = {};
-                    prev.finish(Q, &H->cs, none);
+        if (t < kConsumers) {
+            constexpr int ND = Prev::ND > 0 ? Prev::ND : 1;
+            constexpr int U = kSuccFoldMax / kConsumers;
+            const bool fold = Prev::ND > 0 && (chain & CH_FOLD);
+            const double* pin = (chain & CH_ODD) ? P.part_b : P.part;
+            double v[U][ND];
+            auto load = [&](int q0) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int q = q0 + t + u * kConsumers;
+#pragma unroll
+                    for (int d = 0; d < ND; ++d) v[u][d] = q < gprev ? __ldcg(pin + d * gprev + q) : 0.0;
                 }
+            };
+            if (fold) load(0);  // issued before the control block arrives
+            if (t < 32) {
+                constexpr int kWords = sizeof(Ctrl) / 16;
+                const uint4* in = reinterpret_cast<const uint4*>((chain & CH_ODD) ? P.ctrl_b : P.ctrl);
+                if (t < kWords) reinterpret_cast<uint4*>(&H->cs)[t] = __ldcg(in + t);
+            }
+            consumer_sync();
+            if (chain & CH_FOLD) {
+                Params Q = with_ctrl(P, &H->cs);
+                if (blockIdx.x != 0) Q.hist = nullptr;  // side effects once
+                Prev prev;
+                const bool go = prev.enter(Q);  // read-only on the shared copy: uniform
+                const int m = go ? prev.sync() : 0;
+                double tot[ND];
+#pragma unroll
+                for (int d = 0; d < ND; ++d) tot[d] = 0.0;
+                if (Prev::ND > 0 && m == 2) {
+                    // thread t: q = t, t + 256, ... in order (fold_partials' order)
+                    for (int q0 = 0; q0 < gprev; q0 += kSuccFoldMax) {
+                        if (q0 > 0) load(q0);
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            if (q0 + t + u * kConsumers < gprev) {
+#pragma unroll
+                                for (int d = 0; d < ND; ++d) tot[d] = ADD(tot[d], v[u][d]);
+                            }
+                        }
+                    }
+                    cta_tree_c<ND>(tot, H->red);
+                }
+                if (t == 0 && go && m != 0) prev.finish(Q, &H->cs, tot);
             }
         }
     } else if (t < 32) {
+        constexpr int kWords = sizeof(Ctrl) / 16;
+        if (t < kWords) reinterpret_cast<uint4*>(&H->cs)[t] = __ldcg(reinterpret_cast<const uint4*>((chain & CH_ODD) ? P.ctrl_b : P.ctrl) + t);
+        __syncwarp();
         // warp 0: every lane evaluates the (read-only) enter() decisions on
         // the shared copy, the warp polls the exchanged totals together,
         // lane 0 runs finish(); __syncwarp between lane 0's writes and the
@@ -721,11 +765,12 @@ __device__ __forceinline__ void chain_prologue(const Params& P, int chain, PipeH
 
 // The chained graph's last node: the final K2's scalar tail (and, on
 // peer-memory ranks, a GV / pipe-PR K1 reduction K2 deferred).
+// Launched with kConsumers threads (the successor fold's canonical tree).
 template <class Op1, class Op2, bool PEER = false>
-__global__ void __launch_bounds__(32) k_chain_tail(Params P, StageCfg) {
+__global__ void __launch_bounds__(kConsumers) k_chain_tail(Params P, StageCfg S) {
     __shared__ __align__(128) PipeHeader H;
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    chain_prologue<Op1, Op2, PEER>(P, CH_ON | CH_FOLD, &H, P.ctrl, /*incr=*/false);
+    chain_prologue<Op1, Op2, PEER>(P, CH_ON | CH_FOLD, &H, P.ctrl, S.gprev, /*incr=*/false);
 }
 
 // Programmatic dependent launch: wait for the preceding kernel's results /
@@ -990,7 +1035,7 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
     if (!PdlLate<Op>::value) pdl_trigger();
     const int chain = S.chain;
     if (chain) {
-        chain_prologue<Op, Prev, PEER>(P, chain, H, (chain & CH_ODD) ? P.ctrl : P.ctrl_b);
+        chain_prologue<Op, Prev, PEER>(P, chain, H, (chain & CH_ODD) ? P.ctrl : P.ctrl_b, S.gprev);
         tl_mark(Op::CSR, 5);
     }
     Op op;
@@ -1119,7 +1164,7 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
         if ((t & 31) == 0) mbar_arrive(&H->empty[slot]);
         if (pb && p2p_mask) p2p_push_row(pp, p2p_mask, i, P.n, p2p_h);
     };
-    double* const part = P.part;
+    double* const part = (!PEER && chain && !(chain & CH_ODD)) ? P.part_b : P.part;
     auto close_vb = [&](int vb) {
         if constexpr (Op::ND > 0) {
             if (op.sync() != 2) return;
@@ -1184,7 +1229,8 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
     if (PdlLate<Op>::value) pdl_trigger();
     tl_mark(Op::CSR, 3);
     const int mode = op.sync();
-    if (mode == 0 || (chain && mode == 1)) return;  // chained: the next kernel finishes
+    // chained: the next kernel finishes (single GPU: and folds the partials)
+    if (mode == 0 || (chain && (mode == 1 || !PEER))) return;
     unsigned int* counter = op.counter(P);
     const bool is_last = arrive_last_c(counter, &H->last_flag);
     tl_mark(Op::CSR, 4);
@@ -1200,15 +1246,8 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
         }
     }
     if (t == 0) *counter = 0u;
-    if (chain) {  // the totals; the next kernel runs the scalar tail
-        if (t == 0) {
-            if constexpr (PEER) {
-                p2p_publish_totals<Op::ND>(P.pp, H->cs.hseq, tot);
-            } else {
-#pragma unroll
-                for (int d = 0; d < Op::ND; ++d) ((chain & CH_ODD) ? P.ctrl : P.ctrl_b)->tot[d] = tot[d];
-            }
-        }
+    if (PEER && chain) {  // the rank total; the next kernel folds the ranks and runs the scalar tail
+        if (t == 0) p2p_publish_totals<Op::ND>(P.pp, H->cs.hseq, tot);
         tl_mark(Op::CSR, 6);
         return;
     }
