@@ -97,9 +97,11 @@ struct HsK1 {
         alpha = P.ctrl->sc[SA];
         return true;
     }
-    // (no early_vec: measured P128 HS 68.0 -> 69.1 us with it — the K1 burst
-    // delays the chained prologue's control-block load)
-    __device__ const double* vec(const Params& P, int v) const { return v == 0 ? P.r : v == 1 ? P.s : P.d; }
+    // early_vec: the first stages issued right after the wait. Measured with
+    // the successor fold: P64 HS 14.8 -> 14.5 us, P2D 10.7 ->
+    // 10.5, P128 neutral (before it, with the last-CTA fold: P128 68.0 -> 69.1)
+    __device__ const double* vec(const Params& P, int v) const { return early_vec(P, v); }
+    __device__ static const double* early_vec(const Params& P, int v) { return v == 0 ? P.r : v == 1 ? P.s : P.d; }
     __device__ int sync() const { return 2; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[0]; }
     template <class In, class RR>
@@ -531,7 +533,8 @@ struct GvK1 {
         }
     }
     // (no early_vec: measured P64 GV 18.9 -> 20.9 us with it — ten streams
-    // per stage issued at once delay the chained prologue)
+    // per stage issued at once delay the chained prologue; with the successor
+    // fold 15.6 -> 16.3 us)
     __device__ int sync() const { return S ? 2 : 1; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[0]; }
     template <class In, class RR>
@@ -689,7 +692,8 @@ struct PprK1 {
             default: return recw ? nullptr : P.wt;
         }
     }
-    // (no early_vec: measured P64 pipe-PR 21.1 -> 22.9 us with it)
+    // (no early_vec: measured P64 pipe-PR 21.1 -> 22.9 us with it; with the
+    // successor fold 17.0 -> 17.4, P128 80.7 -> 85.5)
     __device__ int sync() const { return 2; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[0]; }
     // row-partitioned: the block SpMV's go-ahead, set by K1 (see GvK1)
