@@ -555,7 +555,10 @@ def measure_config(args, cfg_name, rank, local, world, dist, extra=False) -> dic
             # event-timed pair; the raw per-launch times are kept.
             t_it = per[v]["ms"] / max(per[v]["iters"], 1)
             f1 = k1 / (k1 + k2) if k1 + k2 > 0 else 0.5
-            for name, b, raw, f in ((names[0], b1, k1 / it, f1), (names[1], b2, k2 / it, 1.0 - f1)):
+            rows = ((names[0], b1, k1 / it, f1), (names[1], b2, k2 / it, 1.0 - f1))
+            if s.launches_per_iter() == 1:  # one kernel per iteration (PR / M on an L2-resident problem)
+                rows = ((names[0].replace("_k1", "_f"), b1 + b2, k1 / it, 1.0),)
+            for name, b, raw, f in rows:
                 ms = t_it * f
                 kernels.append({"variant": v, "kernel": name, "ms_per_launch": ms,
                                 "ms_per_launch_unfused": raw, "bytes_per_launch": b,

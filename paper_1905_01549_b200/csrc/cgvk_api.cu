@@ -871,6 +871,13 @@ struct cgvk_solver_s {
     int k_target = 0;
     KLaunch k1, k2;
     KLaunch k1c0, k1c, k2c, kt;  // chained schedule (graphs): see chain_prologue
+    // One kernel per iteration (PrF, cgvk_variants.cuh: PR / M on a problem
+    // that fits L2): k1 = k2 = that kernel, even and odd launches alternate
+    // the control-block / partial copies, kt_odd closes a graph with an odd
+    // number of them; s2 / g2 are the second buffers of s and r~ (or r).
+    bool fused = false;
+    KLaunch kt_odd;
+    double *s2 = nullptr, *g2 = nullptr;
     cudaGraphExec_t g1 = nullptr, g8 = nullptr;  // 1- and gn-iteration graphs
     int gn = 8;
     Params P{};
@@ -974,12 +981,12 @@ int make_band(cgvk_matrix a, KLaunch* L) {
 // per SM the stage budget targets.
 template <class Op, class Prev>
 int make_launch(cgvk_matrix a, KLaunch* L) {
-    if constexpr (Op::CSR) {
+    if constexpr (Op::CSR && !NoBand<Op>::value) {
         if (a->band_h >= 0) return make_band<Op, Prev>(a, L);
     }
     constexpr int kMinb = Op::CSR ? CGVK_SPMV_MIN_CTAS : CGVK_K1_MIN_CTAS;
     L->fn = k_stream<Op, Prev>;
-    L->fn_peer = k_stream<Op, Prev, kMinb, true>;
+    if constexpr (!NoBand<Op>::value) L->fn_peer = k_stream<Op, Prev, kMinb, true>;
     // register-capped build of an Op that has one (GV / pipe-PR K1: 72
     // registers, 3 CTAs/SM): only when the working set fits L2 and the
     // virtual CTAs outnumber two CTAs per SM (measured P64 GV 18.4 -> 17.5 us,
@@ -991,7 +998,7 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
         }
     L->threads = kThreads;
     StageCfg S{};
-    S.nvec = Op::NV;
+    S.nvec = Op::NV + XvOf<Op>::value;
     S.cap = Op::CSR ? a->cap : 0;
     const int header = ((int)sizeof(PipeHeader) + 127) & ~127;
     if (Op::CSR) {  // two stages must fit one CTA: tiles beyond the capacity go direct
@@ -1011,7 +1018,7 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
         // long rows: a 2-stage ring fills the SM -> one CTA with the full
         // register file (see k_stream's MINB)
         L->fn = k_stream<Op, Prev, 1>;
-        L->fn_peer = k_stream<Op, Prev, 1, true>;
+        if constexpr (!NoBand<Op>::value) L->fn_peer = k_stream<Op, Prev, 1, true>;
         ctas = 1;
     }
     const int budget = kSmemPerSM / ctas - 2048;
@@ -1065,8 +1072,35 @@ int pick_pair(cgvk_matrix a, cgvk_solver s) {
     return CGVK_OK;
 }
 
+// One kernel per iteration, chained with itself: even launches read `ctrl` /
+// `part` and write the _b copies, odd launches (CH_ODD) the reverse.
+template <class Op>
+int pick_fused(cgvk_matrix a, cgvk_solver s) {
+    TRY((make_launch<Op, Op>(a, &s->k1)));
+    s->k2 = s->k1;
+    s->k1c0 = s->k1;
+    s->k1c0.S.chain = CH_ON;
+    s->k1c = s->k1;
+    s->k1c.S.chain = CH_ON | CH_FOLD;
+    s->k1c.S.gprev = s->k1.S.gvirt;
+    s->k2c = s->k1c;
+    s->k2c.S.chain = CH_ON | CH_FOLD | CH_ODD;
+    s->kt = KLaunch{};
+    s->kt.fn = k_chain_tail<Op, Op>;
+    s->kt.grid = 1;
+    s->kt.threads = kConsumers;
+    s->kt.smem = 0;
+    s->kt.S = s->k1.S;
+    s->kt.S.gprev = s->k1.S.gvirt;
+    s->kt_odd = s->kt;
+    s->kt_odd.S.chain = CH_ODD;
+    s->fin1 = s->fin2 = k_finalize<Op>;
+    return CGVK_OK;
+}
+
 template <bool PREC>
 int pick_kernels(cgvk_matrix a, int v, cgvk_solver s) {
+    if (s->fused) return pick_fused<PrF<PREC>>(a, s);
     switch (v) {
         case CGVK_HS: return pick_pair<HsK1<PREC>, HsK2<PREC>>(a, s);
         case CGVK_CG_CG: return pick_pair<CgK1<PREC>, CgK2<PREC>>(a, s);
@@ -1188,15 +1222,21 @@ int capture(cgvk_solver s, int iters, cudaGraphExec_t* exec) {
     CK(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
     cudaError_t e = cudaSuccess;
     if (use_chain()) {
-        for (int i = 0; i < iters && e == cudaSuccess; ++i) {
-            e = launch(s, i ? s->k1c : s->k1c0);
-            if (e == cudaSuccess) e = launch(s, s->k2c);
+        if (s->fused) {
+            for (int i = 0; i < iters && e == cudaSuccess; ++i)
+                e = launch(s, i == 0 ? s->k1c0 : (i & 1) ? s->k2c : s->k1c);
+            if (e == cudaSuccess) e = launch(s, (iters & 1) ? s->kt_odd : s->kt);
+        } else {
+            for (int i = 0; i < iters && e == cudaSuccess; ++i) {
+                e = launch(s, i ? s->k1c : s->k1c0);
+                if (e == cudaSuccess) e = launch(s, s->k2c);
+            }
+            if (e == cudaSuccess) e = launch(s, s->kt);
         }
-        if (e == cudaSuccess) e = launch(s, s->kt);
     } else {
         for (int i = 0; i < iters && e == cudaSuccess; ++i) {
             e = launch(s, s->k1);
-            if (e == cudaSuccess) e = launch(s, s->k2);
+            if (e == cudaSuccess && !s->fused) e = launch(s, s->k2);
         }
     }
     cudaGraph_t g = nullptr;
@@ -1512,21 +1552,21 @@ int vector_device(cgvk_solver s, int which, double* scratch, const double** out)
         return set_err(CGVK_EINVAL, "vector %d was not allocated: initialize() stopped at mu0", which);
     switch (which) {
         case CGVK_VEC_X: src = s->x; break;
-        case CGVK_VEC_R: src = s->r; break;
-        case CGVK_VEC_P: src = (v == CGVK_HS && c.pcur) ? s->p1 : s->p0; break;
-        case CGVK_VEC_S: src = s->s; break;
-        case CGVK_VEC_W: src = s->w; break;
-        case CGVK_VEC_U: src = s->u; break;
+        case CGVK_VEC_R: src = (s->fused && !prec && c.pcur) ? s->g2 : s->r; break;
+        case CGVK_VEC_P: src = ((v == CGVK_HS || s->fused) && c.pcur) ? s->p1 : s->p0; break;
+        case CGVK_VEC_S: src = (s->fused && c.pcur) ? s->s2 : s->s; break;
+        case CGVK_VEC_W: src = s->fused ? nullptr : s->w; break;  // (fused: w / u hold second buffers)
+        case CGVK_VEC_U: src = s->fused ? nullptr : s->u; break;
         case CGVK_VEC_T: src = s->t; break;
         case CGVK_VEC_R_TILDE:
             if (!prec) break;
-            if (s->rt) src = s->rt;
+            if (s->rt) src = (s->fused && c.pcur) ? s->g2 : s->rt;
             else scale_src = s->r;
             break;
         case CGVK_VEC_S_TILDE:
             if (!prec || v == CGVK_HS || v == CGVK_CG_CG) break;
             if (s->st) src = s->st;
-            else scale_src = s->s;
+            else scale_src = (s->fused && c.pcur) ? s->s2 : s->s;
             break;
         case CGVK_VEC_W_TILDE:
             if (!prec || !(v == CGVK_GV || pipe)) break;
@@ -1567,7 +1607,7 @@ extern "C" {
 // Allocate a solver's device state for matrix `a`, choose its kernels; uses
 // `stream` when given (a local group shares one), else creates its own.
 int solver_alloc(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, cudaStream_t stream,
-                 cgvk_solver* out) {
+                 cgvk_solver* out, bool allow_fuse = false) {
     *out = nullptr;
     if (!a) return set_err(CGVK_EINVAL, "null matrix");
     TRY(cgvk_variant_config_validate(cfg));
@@ -1601,6 +1641,15 @@ int solver_alloc(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, cud
         (rc = dalloc(&s->hist, s->hist_cap)) ||
         (rc = dalloc(&s->dout, 8)) || (rc = dalloc(&s->counter, 4)) || (rc = dalloc(&s->ctrl, 2)))
         return bail(rc);
+    // PR / M on a problem that fits L2 (CSR engine, chained graphs): one kernel
+    // per iteration (PrF); CGVK_FUSE=0 keeps the two-kernel schedule
+    s->fused = allow_fuse && (v == CGVK_M || v == CGVK_PR) && a->band_h < 0 && a->l2pol == 3 && a->nranks <= 1 &&
+               use_chain() && env_int("CGVK_FUSE", 1) != 0;
+    if (s->fused) {  // second buffers of p, s and r~ (or r)
+        if ((rc = dalloc(&s->p1, nv)) || (rc = dalloc(&s->w, nv)) || (rc = dalloc(&s->u, nv))) return bail(rc);
+        s->s2 = s->w;
+        s->g2 = s->u;
+    }
     if (v == CGVK_HS && (rc = dalloc(&s->p1, nv))) return bail(rc);
     if ((v == CGVK_CG_CG || v == CGVK_GV || pipe) && (rc = dalloc(&s->w, nv))) return bail(rc);
     if ((v == CGVK_GV || pipe) && (rc = dalloc(&s->u, nv))) return bail(rc);
@@ -1662,7 +1711,7 @@ int cgvk_solver_create(cgvk_matrix a, const cgvk_variant_config* cfg, int precon
     if (a && a->nranks > 1)
         return set_err(CGVK_EINVAL, "a rank-local matrix needs cgvk_group_create");
     cgvk_solver s = nullptr;
-    TRY(solver_alloc(a, cfg, precond, nullptr, &s));
+    TRY(solver_alloc(a, cfg, precond, nullptr, &s, /*allow_fuse=*/true));
     int rc;
     auto bail = [&](int code) {
         free_solver(s);
@@ -1856,14 +1905,14 @@ void* cgvk_solver_stream(cgvk_solver s) { return s ? (void*)s->stream : nullptr;
 
 int cgvk_solver_launches_per_iter(cgvk_solver s) {
     if (!s) return 0;
-    return s->group ? group_launches_per_iter(s) : 2;
+    return s->group ? group_launches_per_iter(s) : s->fused ? 1 : 2;
 }
 
 long long cgvk_solver_launches(cgvk_solver s, int n_iters) {
     if (!s || n_iters <= 0) return 0;
     if (s->group) return 1 + (long long)group_launches_per_iter(s) * n_iters;
     const long long graphs = n_iters / s->gn + n_iters % s->gn;
-    return 1 + 2LL * n_iters + (use_chain() ? graphs : 0);
+    return 1 + (s->fused ? 1LL : 2LL) * n_iters + (use_chain() ? graphs : 0);
 }
 
 int cgvk_solver_time_steps(cgvk_solver s, int n_iters, double* ms, int* iters) {
@@ -1904,7 +1953,7 @@ int cgvk_solver_profile(cgvk_solver s, int n_iters, double* k1_ms, double* k2_ms
         CK(cudaEventRecord(ev[3 * i], s->stream));
         CK(launch(s, s->k1));
         CK(cudaEventRecord(ev[3 * i + 1], s->stream));
-        CK(launch(s, s->k2));
+        if (!s->fused) CK(launch(s, s->k2));  // (one kernel per iteration: k2_ms = 0)
         CK(cudaEventRecord(ev[3 * i + 2], s->stream));
     }
     CK(cudaGetLastError());

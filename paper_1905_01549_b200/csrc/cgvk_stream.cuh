@@ -86,6 +86,49 @@ struct HasEarlyVec<T, std::void_t<decltype(T::early_vec(std::declval<const Param
     static constexpr bool value = true;
 };
 
+// `static constexpr bool NO_BAND = true`: an Op of the CSR engine only (no
+// band-engine or peer-memory instantiation).
+template <class T, class = void>
+struct NoBand {
+    static constexpr bool value = false;
+};
+template <class T>
+struct NoBand<T, std::void_t<decltype(T::NO_BAND)>> {
+    static constexpr bool value = T::NO_BAND;
+};
+// One-kernel iterations (PrF, cgvk_variants.cuh). `early_vec(P, v, b)`: the
+// staged vectors as a function of P and the buffer-set bit b = ctrl->pcur as
+// this launch will see it — the producer works it out from the incoming
+// control block itself (the predecessor toggles it iff it stepped), so the
+// first stages' vectors are issued right after the wait, not after the
+// chained prologue. `XV`: extra per-stage vector slots written by the
+// consumers (never by bulk copies). `SPLIT`: the row is consumed in two
+// parts with a consumer barrier in between — row_a stores the tile's new
+// gather operand into the stage, row_b gathers in-tile columns from there.
+template <class T, class = void>
+struct HasEarlyPcur {
+    static constexpr bool value = false;
+};
+template <class T>
+struct HasEarlyPcur<T, std::void_t<decltype(T::early_vec(std::declval<const Params&>(), 0, false))>> {
+    static constexpr bool value = true;
+};
+template <class T, class = void>
+struct XvOf {
+    static constexpr int value = 0;
+};
+template <class T>
+struct XvOf<T, std::void_t<decltype(T::XV)>> {
+    static constexpr int value = T::XV;
+};
+template <class T, class = void>
+struct SplitOf {
+    static constexpr bool value = false;
+};
+template <class T>
+struct SplitOf<T, std::void_t<decltype(T::SPLIT)>> {
+    static constexpr bool value = T::SPLIT;
+};
 // Optional per-Op ring-depth hint: `static constexpr int STAGES`.
 template <class T, class = void>
 struct StagesOf {
@@ -770,7 +813,9 @@ template <class Op1, class Op2, bool PEER = false>
 __global__ void __launch_bounds__(kConsumers) k_chain_tail(Params P, StageCfg S) {
     __shared__ __align__(128) PipeHeader H;
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    chain_prologue<Op1, Op2, PEER>(P, CH_ON | CH_FOLD, &H, P.ctrl, S.gprev, /*incr=*/false);
+    // (S.chain & CH_ODD: the last kernel was an even one — a one-kernel
+    // iteration schedule after an odd number of launches — and wrote ctrl_b)
+    chain_prologue<Op1, Op2, PEER>(P, CH_ON | CH_FOLD | (S.chain & CH_ODD), &H, P.ctrl, S.gprev, /*incr=*/false);
 }
 
 // Programmatic dependent launch: wait for the preceding kernel's results /
@@ -978,7 +1023,8 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
     const int nrev = rev ? ((int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / Gp + 1 : 0) : 0;
     const bool rr2 = Rr2Of<Op>::value && !Op::CSR && P.order == 0 && (int)blockIdx.x + Gp < Gv &&
                      (int)blockIdx.x + 2 * Gp >= Gv;
-    constexpr bool kEarly = HasEarlyVec<Op>::value && CGVK_EARLY > 0;
+    constexpr bool kEarlyP = HasEarlyPcur<Op>::value && CGVK_EARLY > 0;
+    constexpr bool kEarly = (HasEarlyVec<Op>::value || kEarlyP) && CGVK_EARLY > 0;
     int early_tile[kMaxStages];
     int nearly = 0;  // stages whose vectors are issued right after the wait
     if (producer && (Op::CSR || kEarly)) {
@@ -1015,6 +1061,17 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
     if constexpr (kEarly) {
         if (producer) {
             const uint64_t vpol = P.l2pol == 0 ? (Op::CSR ? pol : evict_first_policy()) : 0;
+            bool pb = false;  // kEarlyP: ctrl->pcur as this launch's enter() will see it
+            if constexpr (kEarlyP) {
+                const Ctrl* cin = (S.chain & CH_ODD) ? P.ctrl_b : P.ctrl;
+                pb = __ldcg(&cin->pcur) != 0;
+                if ((S.chain & CH_FOLD) && __ldcg(&cin->state) == ST_RUNNING && __ldcg(&cin->k) < __ldcg(&cin->k_limit))
+                    pb = !pb;  // the predecessor stepped: its finish (run in the prologue) flips the set
+            }
+            auto evec = [&](int v) -> const double* {
+                if constexpr (kEarlyP) return Op::early_vec(P, v, pb);
+                else return Op::early_vec(P, v);
+            };
             for (int q = 0; q < nearly; ++q) {
                 StageView V = stage_view(stages, S, q);
                 const int r0 = early_tile[q] * kBlock;
@@ -1022,12 +1079,14 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
                 uint32_t bytes = 0;
 #pragma unroll
                 for (int v = 0; v < Op::NV; ++v)
-                    if (Op::early_vec(P, v)) bytes += vec_bytes;
+                    if (evec(v)) bytes += vec_bytes;
                 mbar_expect_tx(&H->full[q], bytes);  // + the stage's arrival
 #pragma unroll
                 for (int v = 0; v < Op::NV; ++v) {
-                    const double* src = Op::early_vec(P, v);
-                    if (src) bulk_g2s(V.vec + v * kBlock, src + r0, vec_bytes, &H->full[q], staged_policy(Op{}, P, src, vpol));
+                    const double* src = evec(v);
+                    uint64_t vp = vpol;
+                    if constexpr (!kEarlyP) vp = staged_policy(Op{}, P, src, vpol);
+                    if (src) bulk_g2s(V.vec + v * kBlock, src + r0, vec_bytes, &H->full[q], vp);
                 }
             }
         }
@@ -1134,7 +1193,27 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
         const bool pb = PEER && (tile < p2p_tlo || tile >= p2p_hif);
         StageView V = stage_view(stages, S, slot);
         const int i = tile * kBlock + t;
-        if (i < P.n) {
+        if constexpr (SplitOf<Op>::value) {
+            // both parts around ONE convergent consumer barrier (bar.sync is
+            // warp-aligned: rows past n of the last tile take it too)
+            const bool live = i < P.n;
+            RowRef R{nullptr, nullptr, 0};
+            typename Op::Mid mid{};
+            if (live) {
+                const int b = V.rp[t];
+                R.len = V.rp[t + 1] - b;
+                if (H->direct[slot]) {
+                    R.va = P.va + b;
+                    R.ci = P.ci + b;
+                } else {
+                    R.va = V.va + (b - H->k0a[slot]);
+                    R.ci = V.ci + (b - H->k0c[slot]);
+                }
+                op.row_a(P, i, StagedIn{V.vec + t}, mid);
+            }
+            consumer_sync();
+            if (live) op.row_b(P, i, tile * kBlock, V.vec, StagedIn{V.vec + t}, R, mid, acc);
+        } else if (i < P.n) {
             RowRef R{nullptr, nullptr, 0};
             if (Op::CSR) {
                 const int b = V.rp[t];

@@ -45,6 +45,20 @@ namespace cgvk {
 #ifndef CGVK_PPR_LATE
 #define CGVK_PPR_LATE 2  // pipe-PR K1 (1) / K2 (2) signal their dependents after their tiles
 #endif
+#ifndef CGVK_PRF_LATE
+#define CGVK_PRF_LATE 0  // the one-kernel PR / M iteration signals its dependent after its tiles
+#endif
+#ifndef CGVK_PRF_SPLIT
+#define CGVK_PRF_SPLIT 0  // in-tile columns gathered from the stage (a consumer barrier per tile)
+#endif
+#ifndef CGVK_PRF_EARLY
+#define CGVK_PRF_EARLY 1  // first stages' vectors issued right after the wait
+#endif
+#if CGVK_PRF_EARLY
+#define CGVK_PRF_EVEC early_vec
+#else
+#define CGVK_PRF_EVEC evec_off
+#endif
 #ifndef CGVK_GV_K1_CTAS
 #define CGVK_GV_K1_CTAS 3  // stage ring sized for this many resident CTAs (registers allow 2)
 #endif
@@ -491,6 +505,159 @@ struct PrK2 {
         }
         if (finalize_alpha(c)) return;
         check_tolerance(c);
+    }
+};
+
+// ---------------------------------------------------- PR / M, one kernel
+// The same step (src/variants.cpp:237-265) as ONE launch per iteration, for
+// problems whose working set fits L2 (launch- and latency-bound: each kernel
+// boundary costs 3-5 us of drain, dependency release, scalar prologue and
+// pipeline fill against a ~3 us tile pass). PR has one global reduction per
+// iteration, so one boundary is all it needs: the K1 -> K2 boundary only
+// carries p to the rows that gather it, and p_j = r~_j + beta p_j with
+// r~_j = r~_j - alpha (d_j s_j) is re-formed at every gathered column from the
+// previous iteration's r~, s, p (the expression, operand order and rounding
+// of PrK1::row, so the same bits) — as HsK2 forms its p on the fly. The
+// vectors other rows gather (p, s and r~, or r without a preconditioner) are
+// double-buffered: a launch reads the set chosen by ctrl->pcur and writes the
+// other one (second buffers: P.p1, P.w = s, P.u = r~ | r); x (and r with
+// Jacobi) are updated in place. A breakdown of nu' (PrK1's `valid == false`)
+// copies p and s forward unchanged, so the state stays in one buffer set.
+// Dots, their canonical order and the scalar tail are PrK2's (PrK1's on that
+// breakdown). The launch chains with itself (chain_prologue<PrF, PrF>).
+// streams: A, x p r s [r~ d]
+template <bool PREC>
+struct PrF {
+    static constexpr int NV = PREC ? 6 : 4, ND = 6;
+    static constexpr int MAXNREG = CGVK_SPMV_MAXNREG;
+    static constexpr bool CSR = true;
+    static constexpr bool PDL_LATE = CGVK_PRF_LATE != 0;
+    static constexpr bool NO_BAND = true;
+    double alpha, beta, nup;
+    bool valid, want_delta, want_dhat;
+    const double *pc, *sc, *gc;  // this iteration's inputs: p, s and g = r~ (Jacobi) | r
+    double *pn, *sn, *gn;        // its outputs
+    __device__ bool enter(const Params& P) {
+        const Ctrl* c = P.ctrl;
+        if (!step_wanted(c)) return false;
+        alpha = c->sc[SA];
+        nup = predicted_nu(P.nu_expr, c->sc);
+        valid = isfinite(nup) && nup > 0.0;
+        beta = DIV(nup, c->sc[SNU]);
+        want_delta = P.nu_expr != 2 || P.track_delta;
+        want_dhat = P.nu_expr == 0;
+        double* const g0 = PREC ? P.rt : P.r;
+        const bool b = c->pcur != 0;
+        pc = b ? P.p1 : P.p0;
+        pn = b ? P.p0 : P.p1;
+        sc = b ? P.w : P.s;
+        sn = b ? P.s : P.w;
+        gc = b ? P.u : g0;
+        gn = b ? g0 : P.u;
+        return true;
+    }
+    __device__ const double* vec(const Params& P, int v) const { return CGVK_PRF_EVEC(P, v, pc == P.p1); }
+    // the streams given the buffer-set bit (cgvk_stream.cuh HasEarlyPcur)
+    __device__ static const double* CGVK_PRF_EVEC(const Params& P, int v, bool b) {
+        const double* const g = b ? P.u : (PREC ? P.rt : P.r);
+        switch (v) {
+            case 0: return P.x;
+            case 1: return b ? P.p1 : P.p0;
+            case 2: return PREC ? P.r : g;
+            case 3: return b ? P.w : P.s;
+            case 4: return g;
+            default: return P.d;
+        }
+    }
+    static constexpr int NG = PREC ? 4 : 3;
+    __device__ const double* gsrc(const Params& P, int k) const { return k == 0 ? pc : k == 1 ? sc : k == 2 ? gc : P.d; }
+    __device__ int sync() const { return 2; }
+    __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
+    // Two parts around a consumer barrier (cgvk_stream.cuh SplitOf): row_a =
+    // PrK1's row, its p also stored into the stage's extra vector slot; row_b
+    // = PrK2's row, gathering columns inside the tile from that slot and
+    // re-forming p at the others.
+    static constexpr bool SPLIT = CGVK_PRF_SPLIT != 0;
+    static constexpr int XV = SPLIT ? 1 : 0;
+    // (unsplit form: p re-formed at every gathered column)
+    template <class In, class RR>
+    __device__ void row(const Params& P, int i, const In& in, const RR& R, double* acc) const {
+        Mid m{0.0, 0.0, 0.0};
+        row_a(P, i, in, m);
+        row_b(P, i, 0, nullptr, in, R, m, acc);
+    }
+    struct Mid {
+        double r, rt, pi;
+    };
+    template <class In>
+    __device__ void row_a(const Params& P, int i, const In& in, Mid& m) const {
+        const double s = SV(3), p = SV(1);
+        P.x[i] = ADD(SV(0), MUL(alpha, p));
+        const double r = SUB(SV(2), MUL(alpha, s));
+        double rt = r;
+        if constexpr (PREC) {
+            P.r[i] = r;
+            rt = SUB(SV(4), MUL(alpha, MUL(SV(5), s)));
+        }
+        gn[i] = rt;
+        m.r = r;
+        m.rt = rt;
+        if (!valid) {  // PrK1's breakdown step: p, s unchanged
+            pn[i] = p;
+            sn[i] = s;
+            return;
+        }
+        m.pi = ADD(rt, MUL(beta, p));
+        pn[i] = m.pi;
+        if constexpr (SPLIT) const_cast<double*>(in.sv)[NV * kBlock] = m.pi;
+    }
+    template <class In, class RR>
+    __device__ void row_b(const Params& P, int i, int r0, const double* stage_vec, const In& in, const RR& R,
+                          const Mid& m, double* acc) const {
+        const double r = m.r, rt = m.rt;
+        if (!valid) {  // <r,r> for the record
+            acc[5] = ADD(acc[5], MUL(r, r));
+            return;
+        }
+        const double* __restrict__ pt = stage_vec + NV * kBlock;  // the tile's new p
+        const double* __restrict__ pg = pc;
+        const double* __restrict__ sg = sc;
+        const double* __restrict__ gg = gc;
+        const double* __restrict__ dg = P.d;
+        const double a = alpha, b = beta;
+        const double sum = row_dot(R, [=](int j) {
+            if constexpr (SPLIT) {
+                const unsigned int q = static_cast<unsigned int>(j - r0);
+                if (q < static_cast<unsigned int>(kBlock)) return pt[q];
+            }
+            const double sj = in.gather(1, j, sg);
+            const double gj = in.gather(2, j, gg);
+            const double rtj = SUB(gj, MUL(a, PREC ? MUL(in.gather(3, j, dg), sj) : sj));
+            return ADD(rtj, MUL(b, in.gather(0, j, pg)));
+        });
+        sn[i] = sum;
+        const double st = PREC ? MUL(SV(5), sum) : sum;
+        acc[0] = ADD(acc[0], MUL(m.pi, sum));
+        if (want_delta) acc[1] = ADD(acc[1], MUL(rt, sum));
+        if (want_dhat) acc[2] = ADD(acc[2], MUL(st, r));
+        acc[3] = ADD(acc[3], MUL(st, sum));
+        acc[4] = ADD(acc[4], MUL(rt, r));
+        acc[5] = ADD(acc[5], MUL(r, r));
+    }
+    __device__ void finish(const Params& P, Ctrl* c, const double* tot) const {
+        c->pcur ^= 1;
+        if (!valid) {
+            PrK1<PREC> k1;
+            k1.nup = nup;
+            const double t0[1] = {tot[5]};
+            k1.finish(P, c, t0);
+            return;
+        }
+        PrK2<PREC> k2;
+        k2.nup = nup;
+        k2.want_delta = want_delta;
+        k2.want_dhat = want_dhat;
+        k2.finish(P, c, tot);
     }
 };
 

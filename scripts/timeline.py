@@ -41,6 +41,8 @@ for v in args[1:] or ["pr", "hs", "gv"]:
         b = buf[k].astype(np.int64)
         live = b[:, 0] > 0
         b = b[live]
+        if not len(b):  # one kernel per iteration (PrF): only the SpMV slot is stamped
+            continue
         if t0 is None:
             t0 = b[:, 0].min()
         ent, wt, first, done, arr = (b[:, q] - t0 for q in range(5))
