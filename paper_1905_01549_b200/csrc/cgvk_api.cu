@@ -998,7 +998,7 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
         }
     L->threads = kThreads;
     StageCfg S{};
-    S.nvec = Op::NV + XvOf<Op>::value;
+    S.nvec = Op::NV;
     S.cap = Op::CSR ? a->cap : 0;
     const int header = ((int)sizeof(PipeHeader) + 127) & ~127;
     if (Op::CSR) {  // two stages must fit one CTA: tiles beyond the capacity go direct

@@ -101,10 +101,7 @@ struct NoBand<T, std::void_t<decltype(T::NO_BAND)>> {
 // this launch will see it — the producer works it out from the incoming
 // control block itself (the predecessor toggles it iff it stepped), so the
 // first stages' vectors are issued right after the wait, not after the
-// chained prologue. `XV`: extra per-stage vector slots written by the
-// consumers (never by bulk copies). `SPLIT`: the row is consumed in two
-// parts with a consumer barrier in between — row_a stores the tile's new
-// gather operand into the stage, row_b gathers in-tile columns from there.
+// chained prologue.
 template <class T, class = void>
 struct HasEarlyPcur {
     static constexpr bool value = false;
@@ -112,22 +109,6 @@ struct HasEarlyPcur {
 template <class T>
 struct HasEarlyPcur<T, std::void_t<decltype(T::early_vec(std::declval<const Params&>(), 0, false))>> {
     static constexpr bool value = true;
-};
-template <class T, class = void>
-struct XvOf {
-    static constexpr int value = 0;
-};
-template <class T>
-struct XvOf<T, std::void_t<decltype(T::XV)>> {
-    static constexpr int value = T::XV;
-};
-template <class T, class = void>
-struct SplitOf {
-    static constexpr bool value = false;
-};
-template <class T>
-struct SplitOf<T, std::void_t<decltype(T::SPLIT)>> {
-    static constexpr bool value = T::SPLIT;
 };
 // Optional per-Op ring-depth hint: `static constexpr int STAGES`.
 template <class T, class = void>
@@ -660,6 +641,22 @@ __device__ __forceinline__ void finish_last(const Op& op, const Params& P, PipeH
 // k_chain_tail (one CTA), which finishes the last K2 and leaves `ctrl`
 // complete, as the last-CTA schedule does. Peer-memory ranks keep a last CTA
 // per rank: it publishes the rank total (cgvk_p2p.cuh).
+#ifndef CGVK_TIMELINE
+#define CGVK_TIMELINE 0
+#endif
+#if CGVK_TIMELINE
+__device__ unsigned long long g_timeline[2][1024][8];
+#endif
+__device__ __forceinline__ void tl_mark(int kernel, int slot) {
+#if CGVK_TIMELINE
+    if (threadIdx.x == 0 && blockIdx.x < 1024) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_timeline[kernel][blockIdx.x][slot] = t;
+    }
+#endif
+}
+
 constexpr int CH_ON = 1;    // chained: totals only, the successor finishes
 constexpr int CH_FOLD = 2;  // run the predecessor's finish first
 constexpr int CH_ODD = 4;   // the iteration's second kernel (K2)
@@ -671,6 +668,19 @@ __device__ __forceinline__ Params with_ctrl(const Params& P, Ctrl* c) {
 }
 
 constexpr int kSuccFoldMax = 2 * kConsumers;  // predecessor partials per register pass
+// Every CTA of the successor reads the same partials (ND x Gv doubles: hot
+// lines in L2). CGVK_FOLD_L1=1 reads them through L1, so the CTAs resident on
+// one SM share one L2 read (the non-coherent path is safe here as it is for
+// the SpMV gathers: the buffers were written by the previous kernel).
+// Measured: P64 68.7 k -> 69.9 k it/s (pipe-PR 17.1 -> 16.4 us), P128 +0.3 %.
+#ifndef CGVK_FOLD_L1
+#define CGVK_FOLD_L1 1
+#endif
+#if CGVK_FOLD_L1
+#define CGVK_FOLD_LD __ldg
+#else
+#define CGVK_FOLD_LD __ldcg
+#endif
 
 // Words of the control block CTA 0 copies forward (the totals are written by
 // the kernel's last CTA).
@@ -711,7 +721,7 @@ __device__ __forceinline__ void chain_prologue(const Params& P, int chain, PipeH
                 for (int u = 0; u < U; ++u) {
                     const int q = q0 + t + u * kConsumers;
 #pragma unroll
-                    for (int d = 0; d < ND; ++d) v[u][d] = q < gprev ? __ldcg(pin + d * gprev + q) : 0.0;
+                    for (int d = 0; d < ND; ++d) v[u][d] = q < gprev ? CGVK_FOLD_LD(pin + d * gprev + q) : 0.0;
                 }
             };
             if (fold) load(0);  // issued before the control block arrives
@@ -721,6 +731,7 @@ __device__ __forceinline__ void chain_prologue(const Params& P, int chain, PipeH
                 if (t < kWords) reinterpret_cast<uint4*>(&H->cs)[t] = __ldcg(in + t);
             }
             consumer_sync();
+            tl_mark(Self::CSR, 7);
             if (chain & CH_FOLD) {
                 Params Q = with_ctrl(P, &H->cs);
                 if (blockIdx.x != 0) Q.hist = nullptr;  // side effects once
@@ -744,6 +755,7 @@ __device__ __forceinline__ void chain_prologue(const Params& P, int chain, PipeH
                     }
                     cta_tree_c<ND>(tot, H->red);
                 }
+                tl_mark(Self::CSR, 4);
                 if (t == 0 && go && m != 0) prev.finish(Q, &H->cs, tot);
             }
         }
@@ -886,22 +898,6 @@ __device__ __forceinline__ void stage_csr(const Params& P, const StageCfg& S, Pi
 // SM gets the registers to keep a whole chunk of gathers in flight.
 // CGVK_TIMELINE=1 (A/B builds only): per-CTA %globaltimer stamps of the
 // kernel's phases, read back with cgvk_debug_timeline.
-#ifndef CGVK_TIMELINE
-#define CGVK_TIMELINE 0
-#endif
-#if CGVK_TIMELINE
-__device__ unsigned long long g_timeline[2][1024][8];
-#endif
-__device__ __forceinline__ void tl_mark(int kernel, int slot) {
-#if CGVK_TIMELINE
-    if (threadIdx.x == 0 && blockIdx.x < 1024) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        g_timeline[kernel][blockIdx.x][slot] = t;
-    }
-#endif
-}
-
 // Prev: the other kernel of the iteration (chained schedule: its partials
 // are folded here, see chain_prologue).
 // Two virtual CTAs per physical CTA (order 0; the register-bound update
@@ -1193,27 +1189,7 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
         const bool pb = PEER && (tile < p2p_tlo || tile >= p2p_hif);
         StageView V = stage_view(stages, S, slot);
         const int i = tile * kBlock + t;
-        if constexpr (SplitOf<Op>::value) {
-            // both parts around ONE convergent consumer barrier (bar.sync is
-            // warp-aligned: rows past n of the last tile take it too)
-            const bool live = i < P.n;
-            RowRef R{nullptr, nullptr, 0};
-            typename Op::Mid mid{};
-            if (live) {
-                const int b = V.rp[t];
-                R.len = V.rp[t + 1] - b;
-                if (H->direct[slot]) {
-                    R.va = P.va + b;
-                    R.ci = P.ci + b;
-                } else {
-                    R.va = V.va + (b - H->k0a[slot]);
-                    R.ci = V.ci + (b - H->k0c[slot]);
-                }
-                op.row_a(P, i, StagedIn{V.vec + t}, mid);
-            }
-            consumer_sync();
-            if (live) op.row_b(P, i, tile * kBlock, V.vec, StagedIn{V.vec + t}, R, mid, acc);
-        } else if (i < P.n) {
+        if (i < P.n) {
             RowRef R{nullptr, nullptr, 0};
             if (Op::CSR) {
                 const int b = V.rp[t];

@@ -48,9 +48,6 @@ namespace cgvk {
 #ifndef CGVK_PRF_LATE
 #define CGVK_PRF_LATE 0  // the one-kernel PR / M iteration signals its dependent after its tiles
 #endif
-#ifndef CGVK_PRF_SPLIT
-#define CGVK_PRF_SPLIT 0  // in-tile columns gathered from the stage (a consumer barrier per tile)
-#endif
 #ifndef CGVK_PRF_EARLY
 #define CGVK_PRF_EARLY 1  // first stages' vectors issued right after the wait
 #endif
@@ -573,24 +570,9 @@ struct PrF {
     __device__ const double* gsrc(const Params& P, int k) const { return k == 0 ? pc : k == 1 ? sc : k == 2 ? gc : P.d; }
     __device__ int sync() const { return 2; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
-    // Two parts around a consumer barrier (cgvk_stream.cuh SplitOf): row_a =
-    // PrK1's row, its p also stored into the stage's extra vector slot; row_b
-    // = PrK2's row, gathering columns inside the tile from that slot and
-    // re-forming p at the others.
-    static constexpr bool SPLIT = CGVK_PRF_SPLIT != 0;
-    static constexpr int XV = SPLIT ? 1 : 0;
-    // (unsplit form: p re-formed at every gathered column)
     template <class In, class RR>
     __device__ void row(const Params& P, int i, const In& in, const RR& R, double* acc) const {
-        Mid m{0.0, 0.0, 0.0};
-        row_a(P, i, in, m);
-        row_b(P, i, 0, nullptr, in, R, m, acc);
-    }
-    struct Mid {
-        double r, rt, pi;
-    };
-    template <class In>
-    __device__ void row_a(const Params& P, int i, const In& in, Mid& m) const {
+        // PrK1's row
         const double s = SV(3), p = SV(1);
         P.x[i] = ADD(SV(0), MUL(alpha, p));
         const double r = SUB(SV(2), MUL(alpha, s));
@@ -600,36 +582,21 @@ struct PrF {
             rt = SUB(SV(4), MUL(alpha, MUL(SV(5), s)));
         }
         gn[i] = rt;
-        m.r = r;
-        m.rt = rt;
-        if (!valid) {  // PrK1's breakdown step: p, s unchanged
+        if (!valid) {  // its breakdown step: p, s unchanged, <r,r> for the record
             pn[i] = p;
             sn[i] = s;
-            return;
-        }
-        m.pi = ADD(rt, MUL(beta, p));
-        pn[i] = m.pi;
-        if constexpr (SPLIT) const_cast<double*>(in.sv)[NV * kBlock] = m.pi;
-    }
-    template <class In, class RR>
-    __device__ void row_b(const Params& P, int i, int r0, const double* stage_vec, const In& in, const RR& R,
-                          const Mid& m, double* acc) const {
-        const double r = m.r, rt = m.rt;
-        if (!valid) {  // <r,r> for the record
             acc[5] = ADD(acc[5], MUL(r, r));
             return;
         }
-        const double* __restrict__ pt = stage_vec + NV * kBlock;  // the tile's new p
+        const double pi = ADD(rt, MUL(beta, p));
+        pn[i] = pi;
+        // PrK2's row, p re-formed at every gathered column
         const double* __restrict__ pg = pc;
         const double* __restrict__ sg = sc;
         const double* __restrict__ gg = gc;
         const double* __restrict__ dg = P.d;
         const double a = alpha, b = beta;
         const double sum = row_dot(R, [=](int j) {
-            if constexpr (SPLIT) {
-                const unsigned int q = static_cast<unsigned int>(j - r0);
-                if (q < static_cast<unsigned int>(kBlock)) return pt[q];
-            }
             const double sj = in.gather(1, j, sg);
             const double gj = in.gather(2, j, gg);
             const double rtj = SUB(gj, MUL(a, PREC ? MUL(in.gather(3, j, dg), sj) : sj));
@@ -637,7 +604,7 @@ struct PrF {
         });
         sn[i] = sum;
         const double st = PREC ? MUL(SV(5), sum) : sum;
-        acc[0] = ADD(acc[0], MUL(m.pi, sum));
+        acc[0] = ADD(acc[0], MUL(pi, sum));
         if (want_delta) acc[1] = ADD(acc[1], MUL(rt, sum));
         if (want_dhat) acc[2] = ADD(acc[2], MUL(st, r));
         acc[3] = ADD(acc[3], MUL(st, sum));

@@ -32,7 +32,7 @@ for v in args[1:] or ["pr", "hs", "gv"]:
     s.time_steps(20)
     buf = np.zeros((2, 1024, 8), np.uint64)
     lib.cgvk_debug_timeline(buf.ctypes.data)  # read-and-clear
-    s.step(1)
+    s.step(int(os.environ.get("TL_STEPS", "1")))  # > 1: the last iteration's stamps (steady state)
     s.sync()
     assert lib.cgvk_debug_timeline(buf.ctypes.data) == 0
     print(f"== {cfg} {v}" + (" (one-rank peer-memory group)" if p2p else ""))
@@ -56,4 +56,8 @@ for v in args[1:] or ["pr", "hs", "gv"]:
         if os.environ.get("CGVK_CHAIN", "1") != "0" and (b[:, 5] > 0).all():
             pro = b[:, 5] - t0
             print(f"      chain prologue done {pro.min()/1e3:6.2f}..{pro.max()/1e3:6.2f}")
+            if (b[:, 7] > 0).all() and (b[:, 4] > 0).all():
+                c7, c4 = b[:, 7] - t0, b[:, 4] - t0
+                print(f"      control block in smem {c7.min()/1e3:6.2f}..{c7.max()/1e3:6.2f}  "
+                      f"partials folded {c4.min()/1e3:6.2f}..{c4.max()/1e3:6.2f}")
     (g if p2p else s).close()
