@@ -875,9 +875,10 @@ struct cgvk_solver_s {
     // that fits L2): k1 = k2 = that kernel, even and odd launches alternate
     // the control-block / partial copies, kt_odd closes a graph with an odd
     // number of them; s2 / g2 are the second buffers of s and r~ (or r).
-    bool fused = false;
+    int fused = 0;  // 0: two kernels per iteration; 1: PrF; 2: CgF
     KLaunch kt_odd;
-    double *s2 = nullptr, *g2 = nullptr;
+    double *s2 = nullptr, *g2 = nullptr;          // PrF
+    double *r2 = nullptr, *w2 = nullptr;          // CgF (s2 too)
     cudaGraphExec_t g1 = nullptr, g8 = nullptr;  // 1- and gn-iteration graphs
     int gn = 8;
     Params P{};
@@ -1100,7 +1101,8 @@ int pick_fused(cgvk_matrix a, cgvk_solver s) {
 
 template <bool PREC>
 int pick_kernels(cgvk_matrix a, int v, cgvk_solver s) {
-    if (s->fused) return pick_fused<PrF<PREC>>(a, s);
+    if (s->fused == 1) return pick_fused<PrF<PREC>>(a, s);
+    if (s->fused == 2) return pick_fused<CgF<PREC>>(a, s);
     switch (v) {
         case CGVK_HS: return pick_pair<HsK1<PREC>, HsK2<PREC>>(a, s);
         case CGVK_CG_CG: return pick_pair<CgK1<PREC>, CgK2<PREC>>(a, s);
@@ -1552,15 +1554,20 @@ int vector_device(cgvk_solver s, int which, double* scratch, const double** out)
         return set_err(CGVK_EINVAL, "vector %d was not allocated: initialize() stopped at mu0", which);
     switch (which) {
         case CGVK_VEC_X: src = s->x; break;
-        case CGVK_VEC_R: src = (s->fused && !prec && c.pcur) ? s->g2 : s->r; break;
-        case CGVK_VEC_P: src = ((v == CGVK_HS || s->fused) && c.pcur) ? s->p1 : s->p0; break;
+        // (one-kernel schedules: the current buffer set by ctrl->pcur; w / u / t
+        // may hold second buffers of a variant that does not allocate them)
+        case CGVK_VEC_R:
+            src = (s->fused == 1 && !prec && c.pcur) ? s->g2 : (s->fused == 2 && c.pcur) ? s->r2 : s->r;
+            break;
+        case CGVK_VEC_P: src = ((v == CGVK_HS || s->fused == 1) && c.pcur) ? s->p1 : s->p0; break;
         case CGVK_VEC_S: src = (s->fused && c.pcur) ? s->s2 : s->s; break;
-        case CGVK_VEC_W: src = s->fused ? nullptr : s->w; break;  // (fused: w / u hold second buffers)
+        case CGVK_VEC_W: src = s->fused == 1 ? nullptr : (s->fused == 2 && c.pcur) ? s->w2 : s->w; break;
         case CGVK_VEC_U: src = s->fused ? nullptr : s->u; break;
-        case CGVK_VEC_T: src = s->t; break;
+        case CGVK_VEC_T: src = s->fused ? nullptr : s->t; break;
         case CGVK_VEC_R_TILDE:
             if (!prec) break;
-            if (s->rt) src = (s->fused && c.pcur) ? s->g2 : s->rt;
+            if (s->fused == 2) scale_src = c.pcur ? s->r2 : s->r;  // (CgF never stores r~)
+            else if (s->rt) src = (s->fused && c.pcur) ? s->g2 : s->rt;
             else scale_src = s->r;
             break;
         case CGVK_VEC_S_TILDE:
@@ -1643,12 +1650,20 @@ int solver_alloc(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, cud
         return bail(rc);
     // PR / M on a problem that fits L2 (CSR engine, chained graphs): one kernel
     // per iteration (PrF); CGVK_FUSE=0 keeps the two-kernel schedule
-    s->fused = allow_fuse && (v == CGVK_M || v == CGVK_PR) && a->band_h < 0 && a->l2pol == 3 && a->nranks <= 1 &&
-               use_chain() && env_int("CGVK_FUSE", 1) != 0;
-    if (s->fused) {  // second buffers of p, s and r~ (or r)
+    // (CGVK_FUSE bit 0: PR / M, bit 1: CG-CG)
+    const bool small = allow_fuse && a->band_h < 0 && a->l2pol == 3 && a->nranks <= 1 && use_chain();
+    const int fuse_env = env_int("CGVK_FUSE", 3);
+    s->fused = !small ? 0 : ((v == CGVK_M || v == CGVK_PR) && (fuse_env & 1)) ? 1 : (v == CGVK_CG_CG && (fuse_env & 2)) ? 2 : 0;
+    if (s->fused == 1) {  // second buffers of p, s and r~ (or r)
         if ((rc = dalloc(&s->p1, nv)) || (rc = dalloc(&s->w, nv)) || (rc = dalloc(&s->u, nv))) return bail(rc);
         s->s2 = s->w;
         s->g2 = s->u;
+    }
+    if (s->fused == 2) {  // second buffers of r, s and w (Params u, t, p1)
+        if ((rc = dalloc(&s->u, nv)) || (rc = dalloc(&s->t, nv)) || (rc = dalloc(&s->p1, nv))) return bail(rc);
+        s->r2 = s->u;
+        s->s2 = s->t;
+        s->w2 = s->p1;
     }
     if (v == CGVK_HS && (rc = dalloc(&s->p1, nv))) return bail(rc);
     if ((v == CGVK_CG_CG || v == CGVK_GV || pipe) && (rc = dalloc(&s->w, nv))) return bail(rc);

@@ -1061,8 +1061,8 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
             if constexpr (kEarlyP) {
                 const Ctrl* cin = (S.chain & CH_ODD) ? P.ctrl_b : P.ctrl;
                 pb = __ldcg(&cin->pcur) != 0;
-                if ((S.chain & CH_FOLD) && __ldcg(&cin->state) == ST_RUNNING && __ldcg(&cin->k) < __ldcg(&cin->k_limit))
-                    pb = !pb;  // the predecessor stepped: its finish (run in the prologue) flips the set
+                if ((S.chain & CH_FOLD) && Prev::entered(cin))
+                    pb = !pb;  // the predecessor ran: its finish (in the prologue) flips the set
             }
             auto evec = [&](int v) -> const double* {
                 if constexpr (kEarlyP) return Op::early_vec(P, v, pb);

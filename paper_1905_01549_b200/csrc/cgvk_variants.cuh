@@ -359,6 +359,125 @@ struct CgK2 {
     }
 };
 
+// --------------------------------------------------- CG-CG, one kernel
+// The same step (src/variants.cpp:207-234) as ONE launch per iteration for
+// problems that fit L2 (see PrF below for the why). CG-CG has one global
+// reduction per iteration; the K1 -> K2 boundary only carries r~ to the rows
+// that gather it, and r~_j = d_j (r_j - alpha s_j) with s_j = w_j + beta s_j
+// (when the beta-recurrences of the previous step are owed) is re-formed at
+// every gathered column from the previous iteration's r, s, w with CgK1's
+// expressions, operand order and rounding. r, s and w are double-buffered (a
+// launch reads the set chosen by ctrl->pcur and writes the other; second
+// buffers: P.u = r, P.t = s, P.p1 = w); p and x are updated in place; r~ is
+// never stored (vector reads form d∘r). A form-only launch (materialize:
+// F && !S) copies r and w forward, so the state stays in one set.
+// streams: A, p s x r w [d]
+template <bool PREC>
+struct CgF {
+    static constexpr int NV = PREC ? 6 : 5, ND = 5;
+    static constexpr int MAXNREG = CGVK_SPMV_MAXNREG;
+    static constexpr bool CSR = true;
+    static constexpr bool PDL_LATE = false;
+    static constexpr bool NO_BAND = true;
+    static constexpr int STAGES = 2;
+    bool F, S, unsimp;
+    double alpha, beta;
+    const double *rc, *sc, *wc;  // this launch's inputs
+    double *rn, *sn, *wn;        // its outputs
+    __device__ bool enter(const Params& P) {
+        const Ctrl* c = P.ctrl;
+        F = c->form_pending != 0;
+        S = step_wanted(c);
+        unsimp = P.unsimplified_mu != 0;
+        alpha = c->sc[SA];
+        beta = c->sc[SB];
+        const bool b = c->pcur != 0;
+        rc = b ? P.u : P.r;
+        rn = b ? P.r : P.u;
+        sc = b ? P.t : P.s;
+        sn = b ? P.s : P.t;
+        wc = b ? P.p1 : P.w;
+        wn = b ? P.w : P.p1;
+        return F || S;
+    }
+    // whether a launch entered (and so flipped the buffer set), from the
+    // control block it read (cgvk_stream.cuh HasEarlyPcur)
+    __device__ static bool entered(const Ctrl* c) {
+        return __ldcg(&c->form_pending) != 0 ||
+               (__ldcg(&c->state) == ST_RUNNING && __ldcg(&c->k) < __ldcg(&c->k_limit));
+    }
+    __device__ const double* vec(const Params& P, int v) const { return early_vec(P, v, rc == P.u); }
+    __device__ static const double* early_vec(const Params& P, int v, bool b) {
+        switch (v) {
+            case 0: return P.p0;
+            case 1: return b ? P.t : P.s;
+            case 2: return P.x;
+            case 3: return b ? P.u : P.r;
+            case 4: return b ? P.p1 : P.w;
+            default: return P.d;
+        }
+    }
+    static constexpr int NG = PREC ? 4 : 3;
+    __device__ const double* gsrc(const Params& P, int k) const { return k == 0 ? rc : k == 1 ? sc : k == 2 ? wc : P.d; }
+    __device__ int sync() const { return S ? 2 : 1; }
+    __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
+    template <class In, class RR>
+    __device__ void row(const Params& P, int i, const In& in, const RR& R, double* acc) const {
+        // CgK1's row
+        double p = SV(0), s = SV(1);
+        const double r = SV(3);
+        if (F) {
+            p = ADD(PREC ? MUL(SV(5), r) : r, MUL(beta, p));
+            s = ADD(SV(4), MUL(beta, s));
+            P.p0[i] = p;
+        }
+        sn[i] = s;
+        if (!S) {  // form only: r, w unchanged
+            rn[i] = r;
+            wn[i] = SV(4);
+            return;
+        }
+        P.x[i] = ADD(SV(2), MUL(alpha, p));
+        const double ri = SUB(r, MUL(alpha, s));
+        rn[i] = ri;
+        const double rti = PREC ? MUL(SV(5), ri) : ri;
+        // CgK2's row, r~ re-formed at every gathered column
+        const double* __restrict__ rg = rc;
+        const double* __restrict__ sg = sc;
+        const double* __restrict__ wg = wc;
+        const double* __restrict__ dg = P.d;
+        const double a = alpha, b = beta;
+        const bool f = F;
+        const double w = row_dot(R, [=](int j) {
+            // (branch-free: w_j is loaded even when no recurrence is owed, so
+            // a chunk's loads all issue before its arithmetic)
+            const double s0 = in.gather(1, j, sg);
+            const double sf = ADD(in.gather(2, j, wg), MUL(b, s0));
+            const double sj = f ? sf : s0;
+            const double rj = SUB(in.gather(0, j, rg), MUL(a, sj));
+            return PREC ? MUL(in.gather(3, j, dg), rj) : rj;
+        });
+        wn[i] = w;
+        acc[0] = ADD(acc[0], MUL(rti, ri));
+        acc[1] = ADD(acc[1], MUL(rti, w));
+        acc[2] = ADD(acc[2], MUL(ri, ri));
+        if (unsimp) {
+            acc[3] = ADD(acc[3], MUL(rti, s));  // <r~_k, s_{k-1}>
+            acc[4] = ADD(acc[4], MUL(p, w));    // <p_{k-1}, w_k>
+        }
+    }
+    __device__ void finish(const Params& P, Ctrl* c, const double* tot) const {
+        c->pcur ^= 1;
+        if (!S) {
+            c->form_pending = 0;
+            return;
+        }
+        CgK2<PREC> k2;
+        k2.unsimp = unsimp;
+        k2.finish(P, c, tot);
+    }
+};
+
 // ===============================================================  PR / M
 // src/variants.cpp:237-265, paper Alg. 2 (M-CG with the Meurant nu').
 // K1: x, r, r~ (s~ = M s on the fly) and p; K2: s = A p with mu, delta,
@@ -552,6 +671,9 @@ struct PrF {
         gc = b ? P.u : g0;
         gn = b ? g0 : P.u;
         return true;
+    }
+    __device__ static bool entered(const Ctrl* c) {  // (cgvk_stream.cuh HasEarlyPcur)
+        return __ldcg(&c->state) == ST_RUNNING && __ldcg(&c->k) < __ldcg(&c->k_limit);
     }
     __device__ const double* vec(const Params& P, int v) const { return CGVK_PRF_EVEC(P, v, pc == P.p1); }
     // the streams given the buffer-set bit (cgvk_stream.cuh HasEarlyPcur)

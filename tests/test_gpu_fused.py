@@ -1,10 +1,13 @@
-"""PR / M as one kernel per iteration (PrF, csrc/cgvk_variants.cuh) — the
+"""PR / M and CG-CG as one kernel per iteration (PrF / CgF,
+csrc/cgvk_variants.cuh) — the
 schedule libcgvk picks for problems whose working set fits L2 — against the
 two-kernel schedule (CGVK_FUSE=0) and the tree-order oracle: the same bits
 in every state vector and scalar, whatever the step batching (1-iteration
 and 8-iteration graphs alternate the buffer sets and control-block copies),
-through breakdown, the tolerance stop and the ablation flags. The step is
-src/variants.cpp:237-265 in both schedules."""
+through breakdown, the tolerance stop and the ablation flags; for CG-CG also
+the deferred beta-recurrences (a vector read between steps materialises them
+with a form-only launch, the next launch is step-only). The steps are
+src/variants.cpp:207-234 and :237-265 in both schedules."""
 import os
 
 import numpy as np
@@ -17,7 +20,7 @@ from helpers import gpu_state, gpu_vectors, lockstep, same_bits
 
 pytestmark = pytest.mark.gpu
 
-PR_LIKE = [Variant.M, Variant.PR]
+PR_LIKE = [Variant.M, Variant.PR, Variant.CG_CG]
 PRECS = [Precond.IDENTITY, Precond.JACOBI]
 
 
@@ -96,12 +99,13 @@ def test_two_kernel_schedule_still_bit_exact(v):
     s.close()
 
 
-@pytest.mark.parametrize("kw", [{"recompute_nu": False}, {"track_delta": True}, {"nu_expression": 0},
-                                {"nu_expression": 2}])
-def test_ablation_flags(kw):
+@pytest.mark.parametrize("v,kw", [(Variant.PR, {"recompute_nu": False}), (Variant.PR, {"track_delta": True}),
+                                  (Variant.PR, {"nu_expression": 0}), (Variant.PR, {"nu_expression": 2}),
+                                  (Variant.CG_CG, {"unsimplified_mu": True})])
+def test_ablation_flags(v, kw):
     A, b, x0 = small_problem()
     Ad = cgvk.DeviceMatrix.from_csr(A)
-    cfg = cgvk.VariantConfig.make(Variant.PR)
+    cfg = cgvk.VariantConfig.make(v)
     for k_, v_ in kw.items():
         setattr(cfg, k_, v_)
     try:
@@ -116,6 +120,8 @@ def test_ablation_flags(kw):
         f.step(n)
         t.step(n)
         states_equal(f, t, f"{kw} after +{n}")
+    s_, _ = lockstep(A, Ad, v, Precond.JACOBI, b, x0, 6, cfg_kwargs=kw)
+    s_.close()
     f.close()
     t.close()
 
