@@ -875,10 +875,12 @@ struct cgvk_solver_s {
     // that fits L2): k1 = k2 = that kernel, even and odd launches alternate
     // the control-block / partial copies, kt_odd closes a graph with an odd
     // number of them; s2 / g2 are the second buffers of s and r~ (or r).
-    int fused = 0;  // 0: two kernels per iteration; 1: PrF; 2: CgF
+    int fused = 0;  // 0: two kernels per iteration; 1: PrF; 2: CgF; 3: GvF
     KLaunch kt_odd;
     double *s2 = nullptr, *g2 = nullptr;          // PrF
     double *r2 = nullptr, *w2 = nullptr;          // CgF (s2 too)
+    double *u2 = nullptr, *t2 = nullptr;          // GvF (w2 too; owned: b0 / b1 / b2)
+    double *b0 = nullptr, *b1 = nullptr, *b2 = nullptr;
     cudaGraphExec_t g1 = nullptr, g8 = nullptr;  // 1- and gn-iteration graphs
     int gn = 8;
     Params P{};
@@ -985,7 +987,7 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
     if constexpr (Op::CSR && !NoBand<Op>::value) {
         if (a->band_h >= 0) return make_band<Op, Prev>(a, L);
     }
-    constexpr int kMinb = Op::CSR ? CGVK_SPMV_MIN_CTAS : CGVK_K1_MIN_CTAS;
+    constexpr int kMinb = MinbOf<Op>::value;
     L->fn = k_stream<Op, Prev>;
     if constexpr (!NoBand<Op>::value) L->fn_peer = k_stream<Op, Prev, kMinb, true>;
     // register-capped build of an Op that has one (GV / pipe-PR K1: 72
@@ -1103,6 +1105,7 @@ template <bool PREC>
 int pick_kernels(cgvk_matrix a, int v, cgvk_solver s) {
     if (s->fused == 1) return pick_fused<PrF<PREC>>(a, s);
     if (s->fused == 2) return pick_fused<CgF<PREC>>(a, s);
+    if (s->fused == 3) return pick_fused<GvF<PREC>>(a, s);
     switch (v) {
         case CGVK_HS: return pick_pair<HsK1<PREC>, HsK2<PREC>>(a, s);
         case CGVK_CG_CG: return pick_pair<CgK1<PREC>, CgK2<PREC>>(a, s);
@@ -1510,7 +1513,7 @@ void free_solver(cgvk_solver s) {
     if (s->g1) cudaGraphExecDestroy(s->g1);
     if (s->g8) cudaGraphExecDestroy(s->g8);
     for (double* p : {s->x, s->r, s->p0, s->p1, s->s, s->w, s->u, s->t, s->rt, s->st, s->wt, s->wpred, s->b,
-                      s->tmp, s->part, s->hist, s->dout, s->rank_tot, s->all_tot, s->sbuf_lo, s->sbuf_hi,
+                      s->b0, s->b1, s->b2, s->tmp, s->part, s->hist, s->dout, s->rank_tot, s->all_tot, s->sbuf_lo, s->sbuf_hi,
                       s->rbuf_lo, s->rbuf_hi})
         dfree(p);
     dfree(s->counter);
@@ -1560,26 +1563,26 @@ int vector_device(cgvk_solver s, int which, double* scratch, const double** out)
             src = (s->fused == 1 && !prec && c.pcur) ? s->g2 : (s->fused == 2 && c.pcur) ? s->r2 : s->r;
             break;
         case CGVK_VEC_P: src = ((v == CGVK_HS || s->fused == 1) && c.pcur) ? s->p1 : s->p0; break;
-        case CGVK_VEC_S: src = (s->fused && c.pcur) ? s->s2 : s->s; break;
-        case CGVK_VEC_W: src = s->fused == 1 ? nullptr : (s->fused == 2 && c.pcur) ? s->w2 : s->w; break;
-        case CGVK_VEC_U: src = s->fused ? nullptr : s->u; break;
-        case CGVK_VEC_T: src = s->fused ? nullptr : s->t; break;
+        case CGVK_VEC_S: src = ((s->fused == 1 || s->fused == 2) && c.pcur) ? s->s2 : s->s; break;
+        case CGVK_VEC_W: src = s->fused == 1 ? nullptr : (s->fused >= 2 && c.pcur) ? s->w2 : s->w; break;
+        case CGVK_VEC_U: src = s->fused == 3 ? (c.pcur ? s->u2 : s->u) : s->fused ? nullptr : s->u; break;
+        case CGVK_VEC_T: src = s->fused == 3 ? (c.pcur ? s->t2 : s->t) : s->fused ? nullptr : s->t; break;
         case CGVK_VEC_R_TILDE:
             if (!prec) break;
             if (s->fused == 2) scale_src = c.pcur ? s->r2 : s->r;  // (CgF never stores r~)
-            else if (s->rt) src = (s->fused && c.pcur) ? s->g2 : s->rt;
+            else if (s->rt) src = (s->fused == 1 && c.pcur) ? s->g2 : s->rt;
             else scale_src = s->r;
             break;
         case CGVK_VEC_S_TILDE:
             if (!prec || v == CGVK_HS || v == CGVK_CG_CG) break;
             if (s->st) src = s->st;
-            else scale_src = (s->fused && c.pcur) ? s->s2 : s->s;
+            else scale_src = (s->fused == 1 && c.pcur) ? s->s2 : s->s;
             break;
         case CGVK_VEC_W_TILDE:
             if (!prec || !(v == CGVK_GV || pipe)) break;
             if (v == CGVK_GV) {
                 if (c.k == 0) zeros = true;  // resized, never applied before step 1
-                else scale_src = s->w;
+                else scale_src = (s->fused == 3 && c.pcur) ? s->w2 : s->w;
             } else if (!s->cfg.recompute_w || c.wt_stored) {
                 src = s->wt;
             } else {
@@ -1650,14 +1653,26 @@ int solver_alloc(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, cud
         return bail(rc);
     // PR / M on a problem that fits L2 (CSR engine, chained graphs): one kernel
     // per iteration (PrF); CGVK_FUSE=0 keeps the two-kernel schedule
-    // (CGVK_FUSE bit 0: PR / M, bit 1: CG-CG)
+    // (CGVK_FUSE bit 0: PR / M, bit 1: CG-CG, bit 2: GV)
     const bool small = allow_fuse && a->band_h < 0 && a->l2pol == 3 && a->nranks <= 1 && use_chain();
-    const int fuse_env = env_int("CGVK_FUSE", 3);
-    s->fused = !small ? 0 : ((v == CGVK_M || v == CGVK_PR) && (fuse_env & 1)) ? 1 : (v == CGVK_CG_CG && (fuse_env & 2)) ? 2 : 0;
+    const int fuse_env = env_int("CGVK_FUSE", 7);
+    s->fused = !small                                            ? 0
+               : ((v == CGVK_M || v == CGVK_PR) && (fuse_env & 1)) ? 1
+               : (v == CGVK_CG_CG && (fuse_env & 2))               ? 2
+               // (GvF runs 2 CTAs per SM: only while every CTA has one tile — measured
+               // P2D 10.7 -> 7.1 us, but P64, 1024 tiles on 222 CTAs, 15.6 -> 18.2 us)
+               : (v == CGVK_GV && (fuse_env & 4) && (a->ntiles <= 2 * a->sms || (fuse_env & 8))) ? 3
+                                                                   : 0;
     if (s->fused == 1) {  // second buffers of p, s and r~ (or r)
         if ((rc = dalloc(&s->p1, nv)) || (rc = dalloc(&s->w, nv)) || (rc = dalloc(&s->u, nv))) return bail(rc);
         s->s2 = s->w;
         s->g2 = s->u;
+    }
+    if (s->fused == 3) {  // second buffers of w, u and t
+        if ((rc = dalloc(&s->b0, nv)) || (rc = dalloc(&s->b1, nv)) || (rc = dalloc(&s->b2, nv))) return bail(rc);
+        s->w2 = s->b0;
+        s->u2 = s->b1;
+        s->t2 = s->b2;
     }
     if (s->fused == 2) {  // second buffers of r, s and w (Params u, t, p1)
         if ((rc = dalloc(&s->u, nv)) || (rc = dalloc(&s->t, nv)) || (rc = dalloc(&s->p1, nv))) return bail(rc);
@@ -1678,7 +1693,8 @@ int solver_alloc(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, cud
     } else if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess) {
         return bail(set_err(CGVK_ECUDA, "stream create failed"));
     }
-    for (double* p : {s->x, s->r, s->p0, s->p1, s->s, s->w, s->u, s->t, s->rt, s->st, s->wt, s->tmp})
+    for (double* p : {s->x, s->r, s->p0, s->p1, s->s, s->w, s->u, s->t, s->rt, s->st, s->wt, s->tmp, s->b0, s->b1,
+                      s->b2})
         if (p && cudaMemsetAsync(p, 0, 8 * (n ? n : 1), s->stream) != cudaSuccess)
             return bail(set_err(CGVK_ECUDA, "memset failed"));
     if (cudaMemsetAsync(s->counter, 0, 4 * sizeof(unsigned int), s->stream) != cudaSuccess)
@@ -1699,6 +1715,9 @@ int solver_alloc(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, cud
     P.rt = s->rt;
     P.st = s->st;
     P.wt = s->wt;
+    P.b0 = s->b0;
+    P.b1 = s->b1;
+    P.b2 = s->b2;
     P.part = s->part;
     P.part_b = s->part + kMaxDots * (size_t)a->gmax;
     P.hist = s->hist;

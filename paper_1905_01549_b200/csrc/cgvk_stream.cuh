@@ -110,6 +110,19 @@ template <class T>
 struct HasEarlyPcur<T, std::void_t<decltype(T::early_vec(std::declval<const Params&>(), 0, false))>> {
     static constexpr bool value = true;
 };
+#ifndef CGVK_K1_MIN_CTAS
+#define CGVK_K1_MIN_CTAS 1  // register budget of the update kernels (resident CTAs)
+#endif
+// Optional `static constexpr int MINB`: resident CTAs per SM the register
+// budget of the Op's kernel is sized for (__launch_bounds__).
+template <class T, class = void>
+struct MinbOf {
+    static constexpr int value = T::CSR ? CGVK_SPMV_MIN_CTAS : CGVK_K1_MIN_CTAS;
+};
+template <class T>
+struct MinbOf<T, std::void_t<decltype(T::MINB)>> {
+    static constexpr int value = T::MINB;
+};
 // Optional per-Op ring-depth hint: `static constexpr int STAGES`.
 template <class T, class = void>
 struct StagesOf {
@@ -961,15 +974,12 @@ __device__ __forceinline__ uint64_t staged_policy(const Op& op, const Params& P,
     return vpol;
 }
 
-#ifndef CGVK_K1_MIN_CTAS
-#define CGVK_K1_MIN_CTAS 1  // register budget of the update kernels (resident CTAs)
-#endif
 template <class Op, class Prev, bool PEER>
 __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S);
 
 // PEER: the peer-memory rank form (cgvk_p2p.cuh), a separate instantiation so
 // the single-GPU kernels carry none of its code or registers.
-template <class Op, class Prev, int MINB = (Op::CSR ? CGVK_SPMV_MIN_CTAS : CGVK_K1_MIN_CTAS), bool PEER = false>
+template <class Op, class Prev, int MINB = MinbOf<Op>::value, bool PEER = false>
 __global__ void __launch_bounds__(kThreads, MINB) k_stream(Params P, StageCfg S) {
     stream_body<Op, Prev, PEER>(P, S);
 }

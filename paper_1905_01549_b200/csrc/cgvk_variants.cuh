@@ -904,6 +904,133 @@ struct GvK2 {
     __device__ void finish(const Params&, Ctrl* c, const double*) const { c->mode2 = MODE_SKIP; }
 };
 
+// ------------------------------------------------------ GV, one kernel
+// The same step (src/variants.cpp:267-298) as ONE launch per iteration for a
+// single-GPU problem that fits L2 (see PrF above for the why; a row-
+// partitioned solve keeps two kernels — there K1's reduction overlaps K2).
+// The K1 -> K2 boundary only carries w~ to the rows that gather it, and
+// w~_j = d_j (w_j - alpha u_j) with u_j = t_j + beta u_j (when the
+// beta-recurrences are owed) is re-formed at every gathered column from the
+// previous iteration's w, u, t with GvK1's expressions and rounding. w, u and
+// t are double-buffered (second buffers P.b0 / b1 / b2, set chosen by
+// ctrl->pcur); everything else is updated in place; w~ is never stored. The
+// SpMV runs before the step's checks are known, as in the reference.
+// streams: A, p s u w t x r [s~ r~ d]
+template <bool PREC>
+struct GvF {
+    static constexpr int NV = PREC ? 10 : 7, ND = 5;
+    static constexpr int MAXNREG = CGVK_SPMV_MAXNREG;
+    static constexpr bool CSR = true;
+    static constexpr bool PDL_LATE = false;
+    static constexpr bool NO_BAND = true;
+    static constexpr int STAGES = 2;
+    static constexpr int MINB = 2;       // GvK1's register appetite
+    static constexpr int SMEM_CTAS = 2;
+    bool F, S, unsimp;
+    double alpha, beta;
+    const double *wc, *uc, *tc;
+    double *wn, *un, *tn;
+    __device__ bool enter(const Params& P) {
+        const Ctrl* c = P.ctrl;
+        F = c->form_pending != 0;
+        S = step_wanted(c);
+        alpha = c->sc[SA];
+        beta = c->sc[SB];
+        unsimp = P.unsimplified_mu != 0;
+        const bool b = c->pcur != 0;
+        wc = b ? P.b0 : P.w;
+        wn = b ? P.w : P.b0;
+        uc = b ? P.b1 : P.u;
+        un = b ? P.u : P.b1;
+        tc = b ? P.b2 : P.t;
+        tn = b ? P.t : P.b2;
+        return F || S;
+    }
+    __device__ static bool entered(const Ctrl* c) { return CgF<PREC>::entered(c); }
+    __device__ const double* vec(const Params& P, int v) const { return early_vec(P, v, wc == P.b0); }
+    __device__ static const double* early_vec(const Params& P, int v, bool b) {
+        switch (v) {
+            case 0: return P.p0;
+            case 1: return P.s;
+            case 2: return b ? P.b1 : P.u;
+            case 3: return b ? P.b0 : P.w;
+            case 4: return b ? P.b2 : P.t;
+            case 5: return P.x;
+            case 6: return P.r;
+            case 7: return P.st;
+            case 8: return P.rt;
+            default: return P.d;
+        }
+    }
+    static constexpr int NG = PREC ? 4 : 3;
+    __device__ const double* gsrc(const Params& P, int k) const { return k == 0 ? wc : k == 1 ? uc : k == 2 ? tc : P.d; }
+    __device__ int sync() const { return S ? 2 : 1; }
+    __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
+    template <class In, class RR>
+    __device__ void row(const Params& P, int i, const In& in, const RR& R, double* acc) const {
+        // GvK1's row
+        double p = SV(0), s = SV(1), u = SV(2), w = SV(3);
+        double st = PREC ? SV(7) : s;
+        double rt = PREC ? SV(8) : SV(6);
+        if (F) {
+            p = ADD(rt, MUL(beta, p));
+            s = ADD(w, MUL(beta, s));
+            if constexpr (PREC) st = ADD(MUL(SV(9), w), MUL(beta, st));
+            else st = s;
+            u = ADD(SV(4), MUL(beta, u));
+            P.p0[i] = p;
+            P.s[i] = s;
+            if constexpr (PREC) P.st[i] = st;
+        }
+        un[i] = u;
+        if (!S) {  // form only: w, t unchanged
+            wn[i] = w;
+            tn[i] = SV(4);
+            return;
+        }
+        P.x[i] = ADD(SV(5), MUL(alpha, p));
+        const double r = SUB(SV(6), MUL(alpha, s));
+        P.r[i] = r;
+        if constexpr (PREC) {
+            rt = SUB(rt, MUL(alpha, st));
+            P.rt[i] = rt;
+        } else {
+            rt = r;
+        }
+        w = SUB(w, MUL(alpha, u));
+        wn[i] = w;
+        acc[0] = ADD(acc[0], MUL(rt, r));
+        acc[1] = ADD(acc[1], MUL(rt, w));
+        acc[2] = ADD(acc[2], MUL(r, r));
+        if (unsimp) {
+            acc[3] = ADD(acc[3], MUL(rt, s));  // <r~_k, s_{k-1}>
+            acc[4] = ADD(acc[4], MUL(p, w));   // <p_{k-1}, w_k>
+        }
+        // GvK2's row, w~ re-formed at every gathered column (branch-free)
+        const double* __restrict__ wg = wc;
+        const double* __restrict__ ug = uc;
+        const double* __restrict__ tg = tc;
+        const double* __restrict__ dg = P.d;
+        const double a = alpha, b = beta;
+        const bool f = F;
+        tn[i] = row_dot(R, [=](int j) {
+            const double u0 = in.gather(1, j, ug);
+            const double uf = ADD(in.gather(2, j, tg), MUL(b, u0));
+            const double uj = f ? uf : u0;
+            const double wj = SUB(in.gather(0, j, wg), MUL(a, uj));
+            return PREC ? MUL(in.gather(3, j, dg), wj) : wj;
+        });
+    }
+    __device__ void finish(const Params& P, Ctrl* c, const double* tot) const {
+        c->pcur ^= 1;
+        GvK1<PREC> k1;
+        k1.S = S;
+        k1.unsimp = unsimp;
+        k1.finish(P, c, tot);
+        c->mode2 = MODE_SKIP;  // (GvK2's finish: the SpMV is done)
+    }
+};
+
 // ===============================================================  pipe-PR
 // src/variants.cpp:303-350, paper Alg. 3 and the §2.2.1 schedule
 // (PAPER.md:384-401): every dot of step k is computed in K1 from the updated

@@ -1,13 +1,13 @@
-"""PR / M and CG-CG as one kernel per iteration (PrF / CgF,
+"""PR / M, CG-CG and GV as one kernel per iteration (PrF / CgF / GvF,
 csrc/cgvk_variants.cuh) — the
 schedule libcgvk picks for problems whose working set fits L2 — against the
 two-kernel schedule (CGVK_FUSE=0) and the tree-order oracle: the same bits
 in every state vector and scalar, whatever the step batching (1-iteration
 and 8-iteration graphs alternate the buffer sets and control-block copies),
-through breakdown, the tolerance stop and the ablation flags; for CG-CG also
+through breakdown, the tolerance stop and the ablation flags; for CG-CG / GV also
 the deferred beta-recurrences (a vector read between steps materialises them
 with a form-only launch, the next launch is step-only). The steps are
-src/variants.cpp:207-234 and :237-265 in both schedules."""
+src/variants.cpp:207-234, :237-265 and :267-298 in both schedules."""
 import os
 
 import numpy as np
@@ -20,7 +20,7 @@ from helpers import gpu_state, gpu_vectors, lockstep, same_bits
 
 pytestmark = pytest.mark.gpu
 
-PR_LIKE = [Variant.M, Variant.PR, Variant.CG_CG]
+PR_LIKE = [Variant.M, Variant.PR, Variant.CG_CG, Variant.GV]
 PRECS = [Precond.IDENTITY, Precond.JACOBI]
 
 
@@ -101,7 +101,8 @@ def test_two_kernel_schedule_still_bit_exact(v):
 
 @pytest.mark.parametrize("v,kw", [(Variant.PR, {"recompute_nu": False}), (Variant.PR, {"track_delta": True}),
                                   (Variant.PR, {"nu_expression": 0}), (Variant.PR, {"nu_expression": 2}),
-                                  (Variant.CG_CG, {"unsimplified_mu": True})])
+                                  (Variant.CG_CG, {"unsimplified_mu": True}),
+                                  (Variant.GV, {"unsimplified_mu": True})])
 def test_ablation_flags(v, kw):
     A, b, x0 = small_problem()
     Ad = cgvk.DeviceMatrix.from_csr(A)
