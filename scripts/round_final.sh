@@ -11,7 +11,7 @@ python bench.py --gpus 1 --steps 20 --warmup 5 > $OUT/bench_driver.json 2> $OUT/
 for c in p64 p2d; do
   python bench.py --config $c --per-config "" > $OUT/bench_$c.json 2> $OUT/bench_$c.err; echo "bench $c rc=$?"
 done
-for c in ${LAUNCH_CFGS:-p128 r4m p64 v256}; do
+for c in ${LAUNCH_CFGS:-p128 r4m p64 v256 p2d}; do
   CMD=(python bench.py --config $c --per-config "" --steps 3 --warmup 3 --no-e2e --no-cpu --no-clocks)
   "${CMD[@]}" > $OUT/plain_$c.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
@@ -34,3 +34,4 @@ full() {  # config, kernel regex, name
 full p128 'k_stream<cgvk::GvK1<\(bool\)1>' p128_gvk1
 full r4m 'k_band<cgvk::HsK2<\(bool\)1>' r4m_band_hsk2
 full r4m 'k_band<cgvk::PrK2<\(bool\)1>' r4m_band_prk2
+full p64 'k_stream<cgvk::PrF<\(bool\)1>' p64_prf

@@ -16,7 +16,8 @@ import sys
 
 # k_stream / k_band Op -> bench.py kernel name
 OPS = {"HsK1": "hs_k1", "HsK2": "hs_k2", "CgK1": "cg_k1", "CgK2": "cg_k2", "PrK1": "pr_k1",
-       "PrK2": "pr_k2", "GvK1": "gv_k1", "GvK2": "gv_k2", "PprK1": "ppr_k1", "PprK2": "ppr_k2"}
+       "PrK2": "pr_k2", "GvK1": "gv_k1", "GvK2": "gv_k2", "PprK1": "ppr_k1", "PprK2": "ppr_k2",
+       "PrF": "pr_f", "CgF": "cg_f", "GvF": "gv_f"}  # (one kernel per iteration)
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1,
          "msecond": 1e3, "ns": 1e-3, "us": 1, "ms": 1e3}
 
