@@ -245,7 +245,7 @@ int ensure_jacobi(cgvk_matrix a) {
     if (a->jacobi_state == 1) return CGVK_OK;
     if (a->jacobi_state == -1)
         return set_err(CGVK_EINVAL, "Jacobi preconditioner needs a positive diagonal");
-    if (!a->inv_diag) TRY(dalloc(&a->inv_diag, a->n + 32));
+    if (!a->inv_diag) TRY(dalloc(&a->inv_diag, a->ncols + 32));  // (+ halo columns: PrF on a rank gathers d there)
     CK(cudaMemsetAsync(a->flags, 0, sizeof(int), a->stream));
     if (a->n > 0)
         k_jacobi<<<grid_elem(a->n), 256, 0, a->stream>>>((int)a->n, a->rp, a->ci, a->va, a->inv_diag,
@@ -989,7 +989,10 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
     }
     constexpr int kMinb = MinbOf<Op>::value;
     L->fn = k_stream<Op, Prev>;
-    if constexpr (!NoBand<Op>::value) L->fn_peer = k_stream<Op, Prev, kMinb, true>;
+    // (the peer form of a one-kernel iteration spills under the 3-CTA register
+    // cap, and rank shards are small: budget for 2 CTAs)
+    constexpr int kMinbPeer = HasEarlyPcur<Op>::value ? 2 : kMinb;
+    if constexpr (!NoPeer<Op>::value) L->fn_peer = k_stream<Op, Prev, kMinbPeer, true>;
     // register-capped build of an Op that has one (GV / pipe-PR K1: 72
     // registers, 3 CTAs/SM): only when the working set fits L2 and the
     // virtual CTAs outnumber two CTAs per SM (measured P64 GV 18.4 -> 17.5 us,
@@ -1021,7 +1024,7 @@ int make_launch(cgvk_matrix a, KLaunch* L) {
         // long rows: a 2-stage ring fills the SM -> one CTA with the full
         // register file (see k_stream's MINB)
         L->fn = k_stream<Op, Prev, 1>;
-        if constexpr (!NoBand<Op>::value) L->fn_peer = k_stream<Op, Prev, 1, true>;
+        if constexpr (!NoPeer<Op>::value) L->fn_peer = k_stream<Op, Prev, 1, true>;
         ctas = 1;
     }
     const int budget = kSmemPerSM / ctas - 2048;
@@ -1090,6 +1093,7 @@ int pick_fused(cgvk_matrix a, cgvk_solver s) {
     s->k2c.S.chain = CH_ON | CH_FOLD | CH_ODD;
     s->kt = KLaunch{};
     s->kt.fn = k_chain_tail<Op, Op>;
+    if constexpr (!NoPeer<Op>::value) s->kt.fn_peer = k_chain_tail<Op, Op, true>;
     s->kt.grid = 1;
     s->kt.threads = kConsumers;
     s->kt.smem = 0;
@@ -1616,8 +1620,10 @@ extern "C" {
 
 // Allocate a solver's device state for matrix `a`, choose its kernels; uses
 // `stream` when given (a local group shares one), else creates its own.
+// allow_fuse: 1 = a single-GPU solver, 2 = a rank of a peer-memory group
+// (PrF only), 0 = two kernels per iteration.
 int solver_alloc(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, cudaStream_t stream,
-                 cgvk_solver* out, bool allow_fuse = false) {
+                 cgvk_solver* out, int allow_fuse = 0) {
     *out = nullptr;
     if (!a) return set_err(CGVK_EINVAL, "null matrix");
     TRY(cgvk_variant_config_validate(cfg));
@@ -1654,7 +1660,8 @@ int solver_alloc(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, cud
     // PR / M on a problem that fits L2 (CSR engine, chained graphs): one kernel
     // per iteration (PrF); CGVK_FUSE=0 keeps the two-kernel schedule
     // (CGVK_FUSE bit 0: PR / M, bit 1: CG-CG, bit 2: GV)
-    const bool small = allow_fuse && a->band_h < 0 && a->l2pol == 3 && a->nranks <= 1 && use_chain();
+    const bool small = allow_fuse && a->band_h < 0 && a->l2pol == 3 && use_chain() &&
+                       (allow_fuse == 2 ? (v == CGVK_M || v == CGVK_PR) : a->nranks <= 1);
     const int fuse_env = env_int("CGVK_FUSE", 7);
     s->fused = !small                                            ? 0
                : ((v == CGVK_M || v == CGVK_PR) && (fuse_env & 1)) ? 1
@@ -1745,7 +1752,7 @@ int cgvk_solver_create(cgvk_matrix a, const cgvk_variant_config* cfg, int precon
     if (a && a->nranks > 1)
         return set_err(CGVK_EINVAL, "a rank-local matrix needs cgvk_group_create");
     cgvk_solver s = nullptr;
-    TRY(solver_alloc(a, cfg, precond, nullptr, &s, /*allow_fuse=*/true));
+    TRY(solver_alloc(a, cfg, precond, nullptr, &s, /*allow_fuse=*/1));
     int rc;
     auto bail = [&](int code) {
         free_solver(s);

@@ -71,7 +71,7 @@ static_assert(sizeof(Ctrl) == 256, "the control block is two 128-byte lines");
 // (cgvk_p2p.cuh): the rank's chained kernels push their boundary rows into
 // the neighbours' receive buffers and their rank totals into every rank's
 // table as stamped 8-byte words; consumers check the stamps as they read.
-constexpr int kP2pSlots = 4;    // halo-exchanged vectors per variant (physical slots)
+constexpr int kP2pSlots = 6;    // halo-exchanged vectors per variant (physical slots; PrF: 2 sets of 3)
 constexpr int kP2pRanks = 8;    // ranks of one NVSwitch box
 constexpr int kP2pTotSlots = 4; // rank-total tables in flight (by stamp & 3)
 

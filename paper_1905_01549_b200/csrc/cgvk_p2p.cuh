@@ -197,10 +197,21 @@ __device__ __forceinline__ int ll_parity(unsigned int stamp) { return (stamp >> 
 // physical slot of HS's p_old (the other p buffer is p_new)
 __device__ __forceinline__ int p2p_pold(int pcur) { return pcur ? 2 : 1; }
 
-// A launch's push mask: physical slots, kPushPnew = HS's p_new (by pcur).
-constexpr unsigned int kPushPnew = 1u << 4;
+// A launch's push mask: physical slots, kPushPnew = HS's p_new (by pcur),
+// kPushFused = the buffer set a one-kernel iteration (PrF: slots p0 p1 s s2
+// g g2, sets {0, 2, 4} / {1, 3, 5}) writes — the other one than ctrl->pcur
+// names. A launch that does not step pushes the set its successor will read
+// (the current one), p2p_idle_mask.
+constexpr unsigned int kPushPnew = 1u << 8;
+constexpr unsigned int kPushFused = 1u << 9;
 __device__ __forceinline__ unsigned int p2p_push_mask(unsigned int m, int pcur) {
     if (m & kPushPnew) m = (m & ~kPushPnew) | (1u << (3 - p2p_pold(pcur)));
+    if (m & kPushFused) m = pcur ? 0x15u : 0x2au;
+    return m;
+}
+__device__ __forceinline__ unsigned int p2p_idle_mask(unsigned int m, int pcur) {
+    if (m & kPushPnew) return 6u;  // HS: both p buffers (the next p_old is this kernel's p_old)
+    if (m & kPushFused) return pcur ? 0x2au : 0x15u;
     return m;
 }
 
@@ -272,6 +283,48 @@ __device__ __noinline__ void p2p_unpack_row(const PeerPlan* P2, const int* ci, i
         if (c < hb) continue;
         if (g0) p2p_fetch(pp, g0, hb, c - hb, h, pcur);
         if (g1) p2p_fetch(pp, g1, hb, c - hb, h, pcur);
+    }
+}
+
+// The same for a one-kernel iteration (PrF): three exchanged sources, their
+// physical slots known from ctrl->pcur (no pointer search), pushed by the
+// previous launch (stamp h - 1); the three entries of a halo column are
+// polled together, so a boundary row costs one peer round trip per halo
+// column, not three chains of dependent plan loads.
+__device__ __noinline__ void p2p_unpack_row3(const PeerPlan* P2, const int* ci, int len, int hb, int pcur,
+                                             const double* g0, const double* g1, const double* g2, unsigned int h) {
+    const PeerPlan& pp = *P2;
+    const unsigned int want = h - 1u;
+    const int b = pcur ? 1 : 0;  // slots: p0 p1 | s s2 | g g2
+    const auto* r0 = (const unsigned long long*)ldg_ptr((const void* const*)&pp.rx[0 + b]);
+    const auto* r1 = (const unsigned long long*)ldg_ptr((const void* const*)&pp.rx[2 + b]);
+    const auto* r2 = (const unsigned long long*)ldg_ptr((const void* const*)&pp.rx[4 + b]);
+    const size_t base = (size_t)ll_parity(want) * __ldg(&pp.rx_stride);
+    for (int k = 0; k < len; ++k) {
+        const int c = ci[k];
+        if (c < hb) continue;
+        const size_t e = 2 * (base + (size_t)(c - hb));
+        long long t0 = 0;
+        for (int spin = 0;; ++spin) {
+            unsigned long long a0, b0, a1, b1, a2, b2;
+            ld_relaxed_v2u64(r0 + e, a0, b0);
+            ld_relaxed_v2u64(r1 + e, a1, b1);
+            ld_relaxed_v2u64(r2 + e, a2, b2);
+            const bool ok = (unsigned int)(a0 >> 32) == want && (unsigned int)(b0 >> 32) == want &&
+                            (unsigned int)(a1 >> 32) == want && (unsigned int)(b1 >> 32) == want &&
+                            (unsigned int)(a2 >> 32) == want && (unsigned int)(b2 >> 32) == want;
+            if (ok) {
+                const_cast<double*>(g0)[c] = __hiloint2double((int)(unsigned int)b0, (int)(unsigned int)a0);
+                const_cast<double*>(g1)[c] = __hiloint2double((int)(unsigned int)b1, (int)(unsigned int)a1);
+                const_cast<double*>(g2)[c] = __hiloint2double((int)(unsigned int)b2, (int)(unsigned int)a2);
+                break;
+            }
+            if (spin == 0) t0 = gtimer_ns();
+            else if ((spin & 255) == 0 && gtimer_ns() - t0 > kP2pSpinNs) {
+                atomicExch(pp.err, 1u);
+                break;
+            }
+        }
     }
 }
 

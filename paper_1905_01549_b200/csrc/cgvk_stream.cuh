@@ -87,7 +87,7 @@ struct HasEarlyVec<T, std::void_t<decltype(T::early_vec(std::declval<const Param
 };
 
 // `static constexpr bool NO_BAND = true`: an Op of the CSR engine only (no
-// band-engine or peer-memory instantiation).
+// band-engine instantiation); `NO_PEER = true`: no peer-memory rank form.
 template <class T, class = void>
 struct NoBand {
     static constexpr bool value = false;
@@ -122,6 +122,14 @@ struct MinbOf {
 template <class T>
 struct MinbOf<T, std::void_t<decltype(T::MINB)>> {
     static constexpr int value = T::MINB;
+};
+template <class T, class = void>
+struct NoPeer {
+    static constexpr bool value = false;
+};
+template <class T>
+struct NoPeer<T, std::void_t<decltype(T::NO_PEER)>> {
+    static constexpr bool value = T::NO_PEER;
 };
 // Optional per-Op ring-depth hint: `static constexpr int STAGES`.
 template <class T, class = void>
@@ -1109,7 +1117,7 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
             // peer ranks: the neighbours still get this kernel's stamp on the
             // (unchanged) boundary rows, as a single-GPU solve would read them
             // (HS: both p buffers — the next p_old is this kernel's p_old)
-            const unsigned int mask = (S.p2p_push & kPushPnew) ? 6u : p2p_push_mask(S.p2p_push, H->cs.pcur);
+            const unsigned int mask = p2p_idle_mask(S.p2p_push, H->cs.pcur);
             const int tlo = P.pp->tlo, hif = P.pp->hi_first;
             CGVK_FOR_VB(vb, P.order, blockIdx.x, Gv, Gp) {
                 CGVK_FOR_TILE(tile, P.order, vb, ntiles, Gv) {
@@ -1214,9 +1222,14 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
             }
             if constexpr (PEER && Op::CSR) {
                 if (pb) {  // this row's halo entries, then gathers through L2
-                    const double* g0 = op.gsrc(P, 0);
-                    const double* g1 = Op::NG > 1 ? op.gsrc(P, Op::NG - 1) : nullptr;
-                    p2p_unpack_row(pp, R.ci, R.len, p2p_hb, g0, g1, p2p_h, p2p_pc);
+                    if constexpr (HasEarlyPcur<Op>::value) {  // one-kernel iteration: three exchanged sources
+                        p2p_unpack_row3(pp, R.ci, R.len, p2p_hb, p2p_pc, op.gsrc(P, 0), op.gsrc(P, 1), op.gsrc(P, 2),
+                                        p2p_h);
+                    } else {
+                        const double* g0 = op.gsrc(P, 0);
+                        const double* g1 = Op::NG > 1 ? op.gsrc(P, Op::NG - 1) : nullptr;
+                        p2p_unpack_row(pp, R.ci, R.len, p2p_hb, g0, g1, p2p_h, p2p_pc);
+                    }
                     op.row(P, i, StagedInL2{V.vec + t}, R, acc);
                 } else {
                     op.row(P, i, StagedIn{V.vec + t}, R, acc);

@@ -379,6 +379,7 @@ struct CgF {
     static constexpr bool CSR = true;
     static constexpr bool PDL_LATE = false;
     static constexpr bool NO_BAND = true;
+    static constexpr bool NO_PEER = true;
     static constexpr int STAGES = 2;
     bool F, S, unsimp;
     double alpha, beta;
@@ -923,6 +924,7 @@ struct GvF {
     static constexpr bool CSR = true;
     static constexpr bool PDL_LATE = false;
     static constexpr bool NO_BAND = true;
+    static constexpr bool NO_PEER = true;
     static constexpr int STAGES = 2;
     static constexpr int MINB = 2;       // GvK1's register appetite
     static constexpr int SMEM_CTAS = 2;

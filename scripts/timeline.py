@@ -19,13 +19,15 @@ lib = cgvk._lib
 lib.cgvk_debug_timeline.argtypes = [C.c_void_p]
 if p2p:
     plane = {"p2d": 256, "p64": 4096, "p128": 16384, "v256": 65536}[cfg]
-    lo = cgvk.partition_rows(P.A.n, 1, plane)
-    mats = [cgvk.RankMatrix(P.A.n, lo, 0, *cgvk.local_rows(P.A, lo, 0))]
-    comm = cgvk.Comm(1)
+    nr = int(os.environ.get("TL_RANKS", "1"))  # in-process ranks (the stamps are the last rank's kernels)
+    lo = cgvk.partition_rows(P.A.n, nr, plane)
+    mats = [cgvk.RankMatrix(P.A.n, lo, r, *cgvk.local_rows(P.A, lo, r)) for r in range(nr)]
+    comm = cgvk.Comm(nr)
 for v in args[1:] or ["pr", "hs", "gv"]:
     cfgv = cgvk.VariantConfig.make(cgvk.variant_from_name(v))
     if p2p:
-        g = cgvk.Group(comm, mats, cfgv, cgvk.Precond.JACOBI, [P.b], [P.x0], p2p=True)
+        g = cgvk.Group(comm, mats, cfgv, cgvk.Precond.JACOBI, [P.b[lo[r]:lo[r + 1]] for r in range(nr)],
+                       [P.x0[lo[r]:lo[r + 1]] for r in range(nr)], p2p=True)
         s = g.solvers[0]
     else:
         s = cgvk.initialize(cfgv, A, cgvk.Precond.JACOBI, P.b, P.x0)

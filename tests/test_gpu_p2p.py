@@ -223,3 +223,38 @@ def test_p2p_baseline_shards_equal_copy_transport(cfg, nranks, variant):
         g.close()
     assert np.array_equal(out[0][0].view(np.int64), out[1][0].view(np.int64))
     assert np.array_equal(out[0][1].view(np.int64), out[1][1].view(np.int64))
+
+
+@pytest.mark.parametrize("nranks", [2, 8])
+@pytest.mark.parametrize("precond", [Precond.IDENTITY, Precond.JACOBI])
+@pytest.mark.parametrize("variant", [Variant.M, Variant.PR])
+def test_p2p_one_kernel_iteration(variant, precond, nranks, monkeypatch):
+    """PR / M ranks that fit L2 run ONE kernel per rank and iteration (PrF,
+    csrc/cgvk_variants.cuh: the previous iteration's r~, s, p pushed to the
+    neighbours, p re-formed at the halo columns too): bit-equal to the
+    two-kernel peer schedule (CGVK_FUSE_PEER=0) and the partitioned oracle,
+    through odd and even graph batches."""
+    P, align = problem("poisson3d_16_slabs")
+    g, lo, mats, comm, cfg = make_group(P, align, nranks, variant, precond)
+    monkeypatch.setenv("CGVK_FUSE_PEER", "0")
+    h, *_ = make_group(P, align, nranks, variant, precond)
+    monkeypatch.delenv("CGVK_FUSE_PEER")
+    assert g.transport == "p2p" and h.transport == "p2p"
+    assert g.solvers[0].launches_per_iter() == nranks and h.solvers[0].launches_per_iter() == 2 * nranks
+    block, gmax, order = mats[0].reduction_config()
+    o = O.Restatement(P.A, int(variant), int(precond), P.b, P.x0, dot=("part", block, gmax, lo, order))
+    done = 0
+    for k in (1, 1, 8, 3, 2, 9):
+        g.step(k)
+        h.step(k)
+        g.sync()
+        h.sync()
+        for _ in range(k):
+            if o.state()["state"] == 0:
+                o.step()
+        done += k
+        compare(g, o, f"p2p-one-kernel/{variant.name}/{precond.name}/P{nranks} after {done}")
+        for w in (Vec.X, Vec.R, Vec.P, Vec.S):
+            assert np.array_equal(g.vector(w).view(np.int64), h.vector(w).view(np.int64)), (w, done)
+    g.close()
+    h.close()
