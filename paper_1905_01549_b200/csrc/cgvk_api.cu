@@ -1661,7 +1661,10 @@ int solver_alloc(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, cud
     // per iteration (PrF); CGVK_FUSE=0 keeps the two-kernel schedule
     // (CGVK_FUSE bit 0: PR / M, bit 1: CG-CG, bit 2: GV)
     const bool small = allow_fuse && a->band_h < 0 && a->l2pol == 3 && use_chain() &&
-                       (allow_fuse == 2 ? (v == CGVK_M || v == CGVK_PR) : a->nranks <= 1);
+                       // (the peer form runs 2 CTAs per SM: while every CTA holds one tile — measured
+                       // per rank-iteration at P64: 128-tile shards 15.2 -> 14.0 us, 256 tiles 16.9 ->
+                       // 13.3, but 512 tiles 16.3 -> 17.0 and 1024 tiles 17.2 -> 19.8)
+                       (allow_fuse == 2 ? ((v == CGVK_M || v == CGVK_PR) && a->ntiles <= 2 * a->sms) : a->nranks <= 1);
     const int fuse_env = env_int("CGVK_FUSE", 7);
     s->fused = !small                                            ? 0
                : ((v == CGVK_M || v == CGVK_PR) && (fuse_env & 1)) ? 1
