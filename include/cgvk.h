@@ -229,7 +229,7 @@ int cgvk_solver_history(cgvk_solver s, double* out, int cap, int* len);
 /* The stream the solver enqueues on (cudaStream_t), for event timing. */
 void* cgvk_solver_stream(cgvk_solver s);
 /* Number of kernel launches one iteration makes (graph nodes / iteration):
- * 2, or 1 for PR / M, CG-CG and GV on single-GPU problems that fit L2 (the
+ * 2, or 1 for PR / M, CG-CG, GV and pipe-PR on single-GPU problems that fit L2 (the
  * one-kernel schedule, same bits; environment CGVK_FUSE=0 turns it off). */
 int cgvk_solver_launches_per_iter(cgvk_solver s);
 /* Kernel launches of one cgvk_solver_step(s, n_iters) call on this rank: the

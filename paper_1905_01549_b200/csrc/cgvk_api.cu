@@ -875,11 +875,12 @@ struct cgvk_solver_s {
     // that fits L2): k1 = k2 = that kernel, even and odd launches alternate
     // the control-block / partial copies, kt_odd closes a graph with an odd
     // number of them; s2 / g2 are the second buffers of s and r~ (or r).
-    int fused = 0;  // 0: two kernels per iteration; 1: PrF; 2: CgF; 3: GvF
+    int fused = 0;  // 0: two kernels per iteration; 1: PrF; 2: CgF; 3: GvF; 4: PprF
     KLaunch kt_odd;
     double *s2 = nullptr, *g2 = nullptr;          // PrF
     double *r2 = nullptr, *w2 = nullptr;          // CgF (s2 too)
     double *u2 = nullptr, *t2 = nullptr;          // GvF (w2 too; owned: b0 / b1 / b2)
+    double *a2 = nullptr;                         // PprF: s~ | s (g2 = r~ | r, w2, u2 too)
     double *b0 = nullptr, *b1 = nullptr, *b2 = nullptr;
     cudaGraphExec_t g1 = nullptr, g8 = nullptr;  // 1- and gn-iteration graphs
     int gn = 8;
@@ -1110,6 +1111,7 @@ int pick_kernels(cgvk_matrix a, int v, cgvk_solver s) {
     if (s->fused == 1) return pick_fused<PrF<PREC>>(a, s);
     if (s->fused == 2) return pick_fused<CgF<PREC>>(a, s);
     if (s->fused == 3) return pick_fused<GvF<PREC>>(a, s);
+    if (s->fused == 4) return pick_fused<PprF<PREC>>(a, s);
     switch (v) {
         case CGVK_HS: return pick_pair<HsK1<PREC>, HsK2<PREC>>(a, s);
         case CGVK_CG_CG: return pick_pair<CgK1<PREC>, CgK2<PREC>>(a, s);
@@ -1564,22 +1566,28 @@ int vector_device(cgvk_solver s, int which, double* scratch, const double** out)
         // (one-kernel schedules: the current buffer set by ctrl->pcur; w / u / t
         // may hold second buffers of a variant that does not allocate them)
         case CGVK_VEC_R:
-            src = (s->fused == 1 && !prec && c.pcur) ? s->g2 : (s->fused == 2 && c.pcur) ? s->r2 : s->r;
+            src = ((s->fused == 1 || s->fused == 4) && !prec && c.pcur) ? s->g2
+                  : (s->fused == 2 && c.pcur)                          ? s->r2
+                                                                       : s->r;
             break;
         case CGVK_VEC_P: src = ((v == CGVK_HS || s->fused == 1) && c.pcur) ? s->p1 : s->p0; break;
-        case CGVK_VEC_S: src = ((s->fused == 1 || s->fused == 2) && c.pcur) ? s->s2 : s->s; break;
+        case CGVK_VEC_S:
+            src = ((s->fused == 1 || s->fused == 2) && c.pcur) ? s->s2
+                  : (s->fused == 4 && !prec && c.pcur)         ? s->a2
+                                                               : s->s;
+            break;
         case CGVK_VEC_W: src = s->fused == 1 ? nullptr : (s->fused >= 2 && c.pcur) ? s->w2 : s->w; break;
-        case CGVK_VEC_U: src = s->fused == 3 ? (c.pcur ? s->u2 : s->u) : s->fused ? nullptr : s->u; break;
+        case CGVK_VEC_U: src = s->fused >= 3 ? (c.pcur ? s->u2 : s->u) : s->fused ? nullptr : s->u; break;
         case CGVK_VEC_T: src = s->fused == 3 ? (c.pcur ? s->t2 : s->t) : s->fused ? nullptr : s->t; break;
         case CGVK_VEC_R_TILDE:
             if (!prec) break;
             if (s->fused == 2) scale_src = c.pcur ? s->r2 : s->r;  // (CgF never stores r~)
-            else if (s->rt) src = (s->fused == 1 && c.pcur) ? s->g2 : s->rt;
+            else if (s->rt) src = ((s->fused == 1 || s->fused == 4) && c.pcur) ? s->g2 : s->rt;
             else scale_src = s->r;
             break;
         case CGVK_VEC_S_TILDE:
             if (!prec || v == CGVK_HS || v == CGVK_CG_CG) break;
-            if (s->st) src = s->st;
+            if (s->st) src = (s->fused == 4 && c.pcur) ? s->a2 : s->st;
             else scale_src = (s->fused == 1 && c.pcur) ? s->s2 : s->s;
             break;
         case CGVK_VEC_W_TILDE:
@@ -1590,12 +1598,12 @@ int vector_device(cgvk_solver s, int which, double* scratch, const double** out)
             } else if (!s->cfg.recompute_w || c.wt_stored) {
                 src = s->wt;
             } else {
-                scale_src = s->w;
+                scale_src = (s->fused == 4 && c.pcur) ? s->w2 : s->w;
             }
             break;
         case CGVK_VEC_U_TILDE:
             if (!prec || !pipe) break;
-            scale_src = s->u;
+            scale_src = (s->fused == 4 && c.pcur) ? s->u2 : s->u;
             break;
         default: break;
     }
@@ -1659,24 +1667,36 @@ int solver_alloc(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, cud
         return bail(rc);
     // PR / M on a problem that fits L2 (CSR engine, chained graphs): one kernel
     // per iteration (PrF); CGVK_FUSE=0 keeps the two-kernel schedule
-    // (CGVK_FUSE bit 0: PR / M, bit 1: CG-CG, bit 2: GV)
+    // (CGVK_FUSE bit 0: PR / M, bit 1: CG-CG, bit 2: GV, bit 4: pipe-PR; bit 3: GV / pipe-PR at any size)
     const bool small = allow_fuse && a->band_h < 0 && a->l2pol == 3 && use_chain() &&
                        // (the peer form runs 2 CTAs per SM: while every CTA holds one tile — measured
                        // per rank-iteration at P64: 128-tile shards 15.2 -> 14.0 us, 256 tiles 16.9 ->
                        // 13.3, but 512 tiles 16.3 -> 17.0 and 1024 tiles 17.2 -> 19.8)
                        (allow_fuse == 2 ? ((v == CGVK_M || v == CGVK_PR) && a->ntiles <= 2 * a->sms) : a->nranks <= 1);
-    const int fuse_env = env_int("CGVK_FUSE", 7);
+    const int fuse_env = env_int("CGVK_FUSE", 23);
+    const bool one_tile = a->ntiles <= 2 * a->sms || (fuse_env & 8);
     s->fused = !small                                            ? 0
                : ((v == CGVK_M || v == CGVK_PR) && (fuse_env & 1)) ? 1
                : (v == CGVK_CG_CG && (fuse_env & 2))               ? 2
                // (GvF runs 2 CTAs per SM: only while every CTA has one tile — measured
                // P2D 10.7 -> 7.1 us, but P64, 1024 tiles on 222 CTAs, 15.6 -> 18.2 us)
-               : (v == CGVK_GV && (fuse_env & 4) && (a->ntiles <= 2 * a->sms || (fuse_env & 8))) ? 3
+               : (v == CGVK_GV && (fuse_env & 4) && one_tile) ? 3
+               // (PprF: the same 2-CTA kernel shape; recompute_w on, as the paper's pipe-PR)
+               : (pipe && cfg->recompute_w && (fuse_env & 16) && one_tile) ? 4
                                                                    : 0;
     if (s->fused == 1) {  // second buffers of p, s and r~ (or r)
         if ((rc = dalloc(&s->p1, nv)) || (rc = dalloc(&s->w, nv)) || (rc = dalloc(&s->u, nv))) return bail(rc);
         s->s2 = s->w;
         s->g2 = s->u;
+    }
+    if (s->fused == 4) {  // second buffers of s~ | s, r~ | r, w and u
+        if ((rc = dalloc(&s->b0, nv)) || (rc = dalloc(&s->b1, nv)) || (rc = dalloc(&s->b2, nv)) ||
+            (rc = dalloc(&s->p1, nv)))
+            return bail(rc);
+        s->a2 = s->b0;
+        s->g2 = s->b1;
+        s->w2 = s->b2;
+        s->u2 = s->p1;
     }
     if (s->fused == 3) {  // second buffers of w, u and t
         if ((rc = dalloc(&s->b0, nv)) || (rc = dalloc(&s->b1, nv)) || (rc = dalloc(&s->b2, nv))) return bail(rc);

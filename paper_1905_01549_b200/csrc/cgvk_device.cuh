@@ -114,7 +114,7 @@ struct Params {
     double* st;
     double* wt;
     double* wpred;  // run() with probes: pipe-PR's predicted w'_k (src/variants.cpp:312), or null
-    double *b0, *b1, *b2;  // GvF (one kernel per iteration): second buffers of w, u, t
+    double *b0, *b1, *b2;  // one kernel per iteration: second buffers (GvF: w, u, t; PprF: s~ | s, r~ | r, w)
     // band engine (cgvk_band.cuh): SELL-C-sigma copy of A, null when unused
     const int* __restrict__ band_off;             // slice offsets (entries), ntiles*8+1
     const unsigned int* __restrict__ band_meta;   // per tile slot: len << 8 | tile-local row

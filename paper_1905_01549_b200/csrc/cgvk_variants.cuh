@@ -1210,6 +1210,164 @@ struct PprK2 {
     __device__ void finish(const Params&, Ctrl* c, const double*) const { c->mode2 = MODE_SKIP; }
 };
 
+// -------------------------------------------------- pipe-PR, one kernel
+// The same step (src/variants.cpp:303-350, recompute_w on) as ONE launch per
+// iteration for a single-GPU problem with at most one tile per resident CTA
+// (see PrF / GvF for the why; a row-partitioned solve keeps two kernels —
+// there K1's reduction overlaps the block SpMV). The K1 -> K2 boundary only
+// carries s~ and r~ to the rows that gather them; both are re-formed at every
+// gathered column from the previous iteration's s~, r~, w, u (and Jacobi's d)
+// with PprK1's expressions and rounding:
+//   r~_j = r~_j - alpha s~_j,   s~_j = (d_j w_j - alpha (d_j u_j)) + beta s~_j
+// (without a preconditioner s~ = s, r~ = r, d = 1). Those four vectors are
+// double-buffered (second buffers P.b0 = s~ | s, P.b1 = r~ | r, P.b2 = w,
+// P.p1 = u; set by ctrl->pcur); x, p (and r, s with Jacobi) are updated in
+// place. The block SpMV runs before the step's checks are known, as in the
+// reference. A breakdown of nu' keeps PprK1's partial update (w, w~ stored).
+// streams: A, x p r s w u [s~ r~ d]
+template <bool PREC>
+struct PprF {
+    static constexpr int NV = PREC ? 9 : 6, ND = 6;
+    static constexpr int MAXNREG = CGVK_SPMV_MAXNREG;
+    static constexpr bool CSR = true;
+    static constexpr bool PDL_LATE = false;
+    static constexpr bool NO_BAND = true;
+    static constexpr bool NO_PEER = true;
+    static constexpr int STAGES = 2;
+    static constexpr int MINB = 2;  // PprK1's register appetite
+    static constexpr int SMEM_CTAS = 2;
+    double alpha, beta, nup;
+    bool valid, want_delta, want_dhat;
+    const double *ac, *bc, *wc, *uc;  // inputs: a = s~ | s, b = r~ | r
+    double *an, *bn, *wn, *un;        // outputs
+    __device__ bool enter(const Params& P) {
+        const Ctrl* c = P.ctrl;
+        if (!step_wanted(c)) return false;
+        alpha = c->sc[SA];
+        nup = predicted_nu(P.nu_expr, c->sc);
+        valid = isfinite(nup) && nup > 0.0;
+        beta = DIV(nup, c->sc[SNU]);
+        want_delta = P.nu_expr != 2 || P.track_delta;
+        want_dhat = P.nu_expr == 0;
+        double* const a0 = PREC ? P.st : P.s;
+        double* const b0 = PREC ? P.rt : P.r;
+        const bool b = c->pcur != 0;
+        ac = b ? P.b0 : a0;
+        an = b ? a0 : P.b0;
+        bc = b ? P.b1 : b0;
+        bn = b ? b0 : P.b1;
+        wc = b ? P.b2 : P.w;
+        wn = b ? P.w : P.b2;
+        uc = b ? P.p1 : P.u;
+        un = b ? P.u : P.p1;
+        return true;
+    }
+    __device__ static bool entered(const Ctrl* c) { return PrF<PREC>::entered(c); }
+    __device__ const double* vec(const Params& P, int v) const { return early_vec(P, v, wc == P.b2); }
+    __device__ static const double* early_vec(const Params& P, int v, bool b) {
+        const double* const a = b ? P.b0 : (PREC ? P.st : P.s);
+        const double* const g = b ? P.b1 : (PREC ? P.rt : P.r);
+        switch (v) {
+            case 0: return P.x;
+            case 1: return P.p0;
+            case 2: return PREC ? P.r : g;
+            case 3: return PREC ? P.s : a;
+            case 4: return b ? P.b2 : P.w;
+            case 5: return b ? P.p1 : P.u;
+            case 6: return a;
+            case 7: return g;
+            default: return P.d;
+        }
+    }
+    static constexpr int NG = PREC ? 5 : 4;
+    __device__ const double* gsrc(const Params& P, int k) const {
+        return k == 0 ? ac : k == 1 ? bc : k == 2 ? wc : k == 3 ? uc : P.d;
+    }
+    __device__ int sync() const { return 2; }
+    __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
+    template <class In, class RR>
+    __device__ void row(const Params& P, int i, const In& in, const RR& R, double* acc) const {
+        // PprK1's row
+        const double p_old = SV(1), s_old = SV(3), w_old = SV(4), u = SV(5);
+        P.x[i] = ADD(SV(0), MUL(alpha, p_old));
+        const double r = SUB(SV(2), MUL(alpha, s_old));
+        double rt = r, st_old = s_old;
+        if constexpr (PREC) {
+            P.r[i] = r;
+            st_old = SV(6);
+            rt = SUB(SV(7), MUL(alpha, st_old));
+        }
+        bn[i] = rt;
+        const double wp = SUB(w_old, MUL(alpha, u));  // w'_k
+        if (P.wpred) P.wpred[i] = wp;                  // run()'s probes track the prediction
+        double wtp = wp;
+        if constexpr (PREC) {
+            const double d = SV(8);
+            wtp = SUB(MUL(d, w_old), MUL(alpha, MUL(d, u)));
+        }
+        acc[5] = ADD(acc[5], MUL(r, r));
+        if (!valid) {  // PprK1's breakdown step: w'_k (and w~'_k) stored, p, s, s~, u unchanged
+            wn[i] = wp;
+            if constexpr (PREC) P.wt[i] = wtp;
+            an[i] = st_old;
+            un[i] = u;
+            return;
+        }
+        const double p = ADD(rt, MUL(beta, p_old));
+        const double s = ADD(wp, MUL(beta, s_old));
+        double st = s;
+        if constexpr (PREC) {
+            st = ADD(wtp, MUL(beta, st_old));
+            P.s[i] = s;
+        }
+        an[i] = st;
+        P.p0[i] = p;
+        acc[0] = ADD(acc[0], MUL(p, s));
+        if (want_delta) acc[1] = ADD(acc[1], MUL(rt, s));
+        if (want_dhat) acc[2] = ADD(acc[2], MUL(st, r));
+        acc[3] = ADD(acc[3], MUL(st, s));
+        acc[4] = ADD(acc[4], MUL(rt, r));
+        // PprK2's row: (u, w) = A (s~, r~), both re-formed at every gathered column
+        const double* __restrict__ ag = ac;
+        const double* __restrict__ bg = bc;
+        const double* __restrict__ wg = wc;
+        const double* __restrict__ ug = uc;
+        const double* __restrict__ dg = P.d;
+        const double a = alpha, b = beta;
+        double un_, wn_;
+        row_dot2(
+            R,
+            [=](int j) {
+                const double so = in.gather(0, j, ag);
+                const double wj = in.gather(2, j, wg), uj = in.gather(3, j, ug);
+                double wt;
+                if constexpr (PREC) {
+                    const double dj = in.gather(4, j, dg);
+                    wt = SUB(MUL(dj, wj), MUL(a, MUL(dj, uj)));
+                } else {
+                    wt = SUB(wj, MUL(a, uj));
+                }
+                return ADD(wt, MUL(b, so));
+            },
+            [=](int j) { return SUB(in.gather(1, j, bg), MUL(a, in.gather(0, j, ag))); }, un_, wn_);
+        un[i] = un_;
+        wn[i] = wn_;
+    }
+    __device__ void finish(const Params& P, Ctrl* c, const double* tot) const {
+        c->pcur ^= 1;
+        PprK1<PREC> k1;
+        k1.alpha = alpha;
+        k1.beta = beta;
+        k1.nup = nup;
+        k1.valid = valid;
+        k1.want_delta = want_delta;
+        k1.want_dhat = want_dhat;
+        k1.recw = true;
+        k1.finish(P, c, tot);
+        c->mode2 = MODE_SKIP;  // (PprK2's finish: the block SpMV is done)
+    }
+};
+
 // ============================================================  L1 SpMV
 // y = A x (NRHS 1) or (y1, y2) = (A x1, A x2) in one pass (NRHS 2) through
 // the solver's engines, for the C ABI's cgvk_spmv / cgvk_block_spmv

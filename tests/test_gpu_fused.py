@@ -1,5 +1,5 @@
-"""PR / M, CG-CG and GV as one kernel per iteration (PrF / CgF / GvF,
-csrc/cgvk_variants.cuh) — the
+"""PR / M, CG-CG, GV and pipe-PR (-M) as one kernel per iteration (PrF / CgF /
+GvF / PprF, csrc/cgvk_variants.cuh) — the
 schedule libcgvk picks for problems whose working set fits L2 — against the
 two-kernel schedule (CGVK_FUSE=0) and the tree-order oracle: the same bits
 in every state vector and scalar, whatever the step batching (1-iteration
@@ -7,7 +7,7 @@ and 8-iteration graphs alternate the buffer sets and control-block copies),
 through breakdown, the tolerance stop and the ablation flags; for CG-CG / GV also
 the deferred beta-recurrences (a vector read between steps materialises them
 with a form-only launch, the next launch is step-only). The steps are
-src/variants.cpp:207-234, :237-265 and :267-298 in both schedules."""
+src/variants.cpp:207-234, :237-265, :267-298 and :303-350 in both schedules."""
 import os
 
 import numpy as np
@@ -20,7 +20,7 @@ from helpers import gpu_state, gpu_vectors, lockstep, same_bits
 
 pytestmark = pytest.mark.gpu
 
-PR_LIKE = [Variant.M, Variant.PR, Variant.CG_CG, Variant.GV]
+PR_LIKE = [Variant.M, Variant.PR, Variant.CG_CG, Variant.GV, Variant.PIPE_PR, Variant.PIPE_PR_M]
 PRECS = [Precond.IDENTITY, Precond.JACOBI]
 
 
@@ -54,6 +54,7 @@ def states_equal(a: cgvk.Solver, b: cgvk.Solver, where: str) -> None:
     va, vb = gpu_vectors(a), gpu_vectors(b)
     for w in va:
         assert same_bits(va[w], vb[w]), f"{where}: vector {w}"
+    assert same_bits(a.history(), b.history()), f"{where}: residual history"
 
 
 @pytest.mark.parametrize("v", PR_LIKE)
@@ -102,7 +103,9 @@ def test_two_kernel_schedule_still_bit_exact(v):
 @pytest.mark.parametrize("v,kw", [(Variant.PR, {"recompute_nu": False}), (Variant.PR, {"track_delta": True}),
                                   (Variant.PR, {"nu_expression": 0}), (Variant.PR, {"nu_expression": 2}),
                                   (Variant.CG_CG, {"unsimplified_mu": True}),
-                                  (Variant.GV, {"unsimplified_mu": True})])
+                                  (Variant.GV, {"unsimplified_mu": True}),
+                                  (Variant.PIPE_PR, {"recompute_nu": False}), (Variant.PIPE_PR, {"track_delta": True}),
+                                  (Variant.PIPE_PR, {"nu_expression": 0})])
 def test_ablation_flags(v, kw):
     A, b, x0 = small_problem()
     Ad = cgvk.DeviceMatrix.from_csr(A)
@@ -169,3 +172,15 @@ def test_breakdown_on_indefinite_matrix():
         assert f.status.state == t.status.state
         f.close()
         t.close()
+
+
+def test_pipe_pr_without_recompute_w_keeps_two_kernels():
+    """PprF is the paper's pipe-PR (recompute_w on); the stored-recurrence
+    ablation runs the two-kernel schedule."""
+    A, b, x0 = small_problem()
+    Ad = cgvk.DeviceMatrix.from_csr(A)
+    cfg = cgvk.VariantConfig.make(Variant.PIPE_PR)
+    cfg.recompute_w = False
+    s = cgvk.initialize(cfg, Ad, Precond.JACOBI, b, x0)
+    assert s.launches_per_iter() == 2
+    s.close()
