@@ -769,7 +769,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "p128"), choices=["p2d", "p64", "p128", "v256", "r4m"])
-    ap.add_argument("--per-config", default=os.environ.get("BENCH_PER_CONFIG", "v256,r4m"),
+    ap.add_argument("--per-config", default=os.environ.get("BENCH_PER_CONFIG", "v256,r4m,p64,p2d"),
                     help="further single-GPU configs measured after the headline one (own roofline, e2e, "
                          "clocks, single-core CPU baseline each); '' for none")
     ap.add_argument("--cpu-steps", type=int, default=10)

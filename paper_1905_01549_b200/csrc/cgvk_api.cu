@@ -862,6 +862,7 @@ struct cgvk_solver_s {
            *u = nullptr, *t = nullptr, *rt = nullptr, *st = nullptr, *wt = nullptr, *b = nullptr,
            *tmp = nullptr;
     double* wpred = nullptr;  // run() with probes on a pipelined PR variant
+    double* slab = nullptr;   // backs every vector above and part / hist / dout / counter / ctrl
     double *part = nullptr, *hist = nullptr, *dout = nullptr;
     unsigned int* counter = nullptr;
     int hist_cap = 0;
@@ -1518,12 +1519,8 @@ void free_solver(cgvk_solver s) {
     if (s->stream) cudaStreamSynchronize(s->stream);
     if (s->g1) cudaGraphExecDestroy(s->g1);
     if (s->g8) cudaGraphExecDestroy(s->g8);
-    for (double* p : {s->x, s->r, s->p0, s->p1, s->s, s->w, s->u, s->t, s->rt, s->st, s->wt, s->wpred, s->b,
-                      s->b0, s->b1, s->b2, s->tmp, s->part, s->hist, s->dout, s->rank_tot, s->all_tot, s->sbuf_lo, s->sbuf_hi,
-                      s->rbuf_lo, s->rbuf_hi})
+    for (double* p : {s->slab, s->wpred, s->rank_tot, s->all_tot, s->sbuf_lo, s->sbuf_hi, s->rbuf_lo, s->rbuf_hi})
         dfree(p);
-    dfree(s->counter);
-    dfree(s->ctrl);
     if (s->stream && s->owns_stream) cudaStreamDestroy(s->stream);
     delete s;
 }
@@ -1658,12 +1655,25 @@ int solver_alloc(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, cud
     s->hist_cap = CGVK_HISTORY_CAP;
     // + halo columns of a rank-local matrix; + 32: bulk copies of the last
     // tile round up to 16 bytes
-    const int64_t nv = a->ncols + 32;
-    if ((rc = dalloc(&s->x, nv)) || (rc = dalloc(&s->r, nv)) || (rc = dalloc(&s->p0, nv)) ||
-        (rc = dalloc(&s->s, nv)) || (rc = dalloc(&s->b, nv)) || (rc = dalloc(&s->tmp, nv)) ||
-        (rc = dalloc(&s->part, 2 * kMaxDots * (size_t)a->gmax + 4)) ||
-        (rc = dalloc(&s->hist, s->hist_cap)) ||
-        (rc = dalloc(&s->dout, 8)) || (rc = dalloc(&s->counter, 4)) || (rc = dalloc(&s->ctrl, 2)))
+    const int64_t nv = (a->ncols + 32 + 15) & ~(int64_t)15;
+    // One stream-ordered allocation for the solver's vectors and small arrays
+    // (each pool allocation is a host round trip: measured 0.17-0.22 ms of a
+    // 0.4 ms solver creation on P2D with ~20 separate ones): `want` records a
+    // 128-byte-aligned segment, `slab` backs them all.
+    struct Seg {
+        void** dst;
+        size_t doubles;
+    };
+    std::vector<Seg> segs;
+    auto want = [&segs](auto** p, size_t doubles) {
+        segs.push_back({reinterpret_cast<void**>(p), (doubles + 15) & ~(size_t)15});
+        return 0;
+    };
+    if ((rc = want(&s->x, nv)) || (rc = want(&s->r, nv)) || (rc = want(&s->p0, nv)) ||
+        (rc = want(&s->s, nv)) || (rc = want(&s->b, nv)) || (rc = want(&s->tmp, nv)) ||
+        (rc = want(&s->part, 2 * kMaxDots * (size_t)a->gmax + 4)) ||
+        (rc = want(&s->hist, s->hist_cap)) ||
+        (rc = want(&s->dout, 8)) || (rc = want(&s->counter, 2)) || (rc = want(&s->ctrl, 2 * sizeof(Ctrl) / 8)))
         return bail(rc);
     // PR / M on a problem that fits L2 (CSR engine, chained graphs): one kernel
     // per iteration (PrF); CGVK_FUSE=0 keeps the two-kernel schedule
@@ -1685,50 +1695,61 @@ int solver_alloc(cgvk_matrix a, const cgvk_variant_config* cfg, int precond, cud
                : (pipe && cfg->recompute_w && (fuse_env & 16) && one_tile) ? 4
                                                                    : 0;
     if (s->fused == 1) {  // second buffers of p, s and r~ (or r)
-        if ((rc = dalloc(&s->p1, nv)) || (rc = dalloc(&s->w, nv)) || (rc = dalloc(&s->u, nv))) return bail(rc);
-        s->s2 = s->w;
-        s->g2 = s->u;
+        if ((rc = want(&s->p1, nv)) || (rc = want(&s->w, nv)) || (rc = want(&s->u, nv))) return bail(rc);
     }
     if (s->fused == 4) {  // second buffers of s~ | s, r~ | r, w and u
-        if ((rc = dalloc(&s->b0, nv)) || (rc = dalloc(&s->b1, nv)) || (rc = dalloc(&s->b2, nv)) ||
-            (rc = dalloc(&s->p1, nv)))
+        if ((rc = want(&s->b0, nv)) || (rc = want(&s->b1, nv)) || (rc = want(&s->b2, nv)) ||
+            (rc = want(&s->p1, nv)))
             return bail(rc);
-        s->a2 = s->b0;
-        s->g2 = s->b1;
-        s->w2 = s->b2;
-        s->u2 = s->p1;
     }
     if (s->fused == 3) {  // second buffers of w, u and t
-        if ((rc = dalloc(&s->b0, nv)) || (rc = dalloc(&s->b1, nv)) || (rc = dalloc(&s->b2, nv))) return bail(rc);
-        s->w2 = s->b0;
-        s->u2 = s->b1;
-        s->t2 = s->b2;
+        if ((rc = want(&s->b0, nv)) || (rc = want(&s->b1, nv)) || (rc = want(&s->b2, nv))) return bail(rc);
     }
     if (s->fused == 2) {  // second buffers of r, s and w (Params u, t, p1)
-        if ((rc = dalloc(&s->u, nv)) || (rc = dalloc(&s->t, nv)) || (rc = dalloc(&s->p1, nv))) return bail(rc);
-        s->r2 = s->u;
-        s->s2 = s->t;
-        s->w2 = s->p1;
+        if ((rc = want(&s->u, nv)) || (rc = want(&s->t, nv)) || (rc = want(&s->p1, nv))) return bail(rc);
     }
-    if (v == CGVK_HS && (rc = dalloc(&s->p1, nv))) return bail(rc);
-    if ((v == CGVK_CG_CG || v == CGVK_GV || pipe) && (rc = dalloc(&s->w, nv))) return bail(rc);
-    if ((v == CGVK_GV || pipe) && (rc = dalloc(&s->u, nv))) return bail(rc);
-    if (v == CGVK_GV && (rc = dalloc(&s->t, nv))) return bail(rc);
-    if (s->prec && (rc = dalloc(&s->rt, nv))) return bail(rc);
-    if (s->prec && (v == CGVK_GV || pipe) && (rc = dalloc(&s->st, nv))) return bail(rc);
-    if (s->prec && (v == CGVK_GV || pipe) && (rc = dalloc(&s->wt, nv))) return bail(rc);
+    if (v == CGVK_HS && (rc = want(&s->p1, nv))) return bail(rc);
+    if ((v == CGVK_CG_CG || v == CGVK_GV || pipe) && (rc = want(&s->w, nv))) return bail(rc);
+    if ((v == CGVK_GV || pipe) && (rc = want(&s->u, nv))) return bail(rc);
+    if (v == CGVK_GV && (rc = want(&s->t, nv))) return bail(rc);
+    if (s->prec && (rc = want(&s->rt, nv))) return bail(rc);
+    if (s->prec && (v == CGVK_GV || pipe) && (rc = want(&s->st, nv))) return bail(rc);
+    if (s->prec && (v == CGVK_GV || pipe) && (rc = want(&s->wt, nv))) return bail(rc);
+    {
+        size_t total = 0;
+        for (const Seg& g : segs) total += g.doubles;
+        if ((rc = dalloc(&s->slab, total)) != CGVK_OK) return bail(rc);
+        double* at = s->slab;
+        for (const Seg& g : segs) {
+            *g.dst = at;
+            at += g.doubles;
+        }
+    }
+    // the one-kernel schedules' names for their second buffers
+    if (s->fused == 1) s->s2 = s->w, s->g2 = s->u;
+    if (s->fused == 2) s->r2 = s->u, s->s2 = s->t, s->w2 = s->p1;
+    if (s->fused == 3) s->w2 = s->b0, s->u2 = s->b1, s->t2 = s->b2;
+    if (s->fused == 4) s->a2 = s->b0, s->g2 = s->b1, s->w2 = s->b2, s->u2 = s->p1;
     if (stream) {
         s->stream = stream;
         s->owns_stream = false;
     } else if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess) {
         return bail(set_err(CGVK_ECUDA, "stream create failed"));
     }
-    for (double* p : {s->x, s->r, s->p0, s->p1, s->s, s->w, s->u, s->t, s->rt, s->st, s->wt, s->tmp, s->b0, s->b1,
-                      s->b2})
-        if (p && cudaMemsetAsync(p, 0, 8 * (n ? n : 1), s->stream) != cudaSuccess)
+    {   // zero everything but the residual history (1 MB, written before it is read): one memset
+        size_t lo = 0, hist_at = 0, total = 0;
+        for (const Seg& g : segs) {
+            if (g.dst == reinterpret_cast<void**>(&s->hist)) hist_at = total;
+            total += g.doubles;
+        }
+        const size_t hist_len = (size_t)(((size_t)s->hist_cap + 15) & ~(size_t)15);
+        (void)lo;
+        if (cudaMemsetAsync(s->slab, 0, 8 * hist_at, s->stream) != cudaSuccess ||
+            (total > hist_at + hist_len &&
+             cudaMemsetAsync(s->slab + hist_at + hist_len, 0, 8 * (total - hist_at - hist_len), s->stream) !=
+                 cudaSuccess))
             return bail(set_err(CGVK_ECUDA, "memset failed"));
-    if (cudaMemsetAsync(s->counter, 0, 4 * sizeof(unsigned int), s->stream) != cudaSuccess)
-        return bail(set_err(CGVK_ECUDA, "memset failed"));
+    }
     s->allocated = ref_allocated(v, s->prec);
 
     Params& P = s->P;

@@ -702,6 +702,15 @@ constexpr int kSuccFoldMax = 2 * kConsumers;  // predecessor partials per regist
 #else
 #define CGVK_FOLD_LD __ldcg
 #endif
+// The control block itself (256 bytes every CTA reads): CGVK_CTRL_L1=1 the same way.
+#ifndef CGVK_CTRL_L1
+#define CGVK_CTRL_L1 0
+#endif
+#if CGVK_CTRL_L1
+#define CGVK_CTRL_LD __ldg
+#else
+#define CGVK_CTRL_LD __ldcg
+#endif
 
 // Words of the control block CTA 0 copies forward (the totals are written by
 // the kernel's last CTA).
@@ -749,7 +758,7 @@ __device__ __forceinline__ void chain_prologue(const Params& P, int chain, PipeH
             if (t < 32) {
                 constexpr int kWords = sizeof(Ctrl) / 16;
                 const uint4* in = reinterpret_cast<const uint4*>((chain & CH_ODD) ? P.ctrl_b : P.ctrl);
-                if (t < kWords) reinterpret_cast<uint4*>(&H->cs)[t] = __ldcg(in + t);
+                if (t < kWords) reinterpret_cast<uint4*>(&H->cs)[t] = CGVK_CTRL_LD(in + t);
             }
             consumer_sync();
             tl_mark(Self::CSR, 7);
