@@ -883,7 +883,7 @@ struct cgvk_solver_s {
     double *u2 = nullptr, *t2 = nullptr;          // GvF (w2 too; owned: b0 / b1 / b2)
     double *a2 = nullptr;                         // PprF: s~ | s (g2 = r~ | r, w2, u2 too)
     double *b0 = nullptr, *b1 = nullptr, *b2 = nullptr;
-    cudaGraphExec_t g1 = nullptr, g8 = nullptr;  // 1- and gn-iteration graphs
+    cudaGraphExec_t g8 = nullptr;  // the gn-iteration graph (a remainder goes out as plain launches)
     int gn = 8;
     Params P{};
     int allocated = 0;
@@ -1263,6 +1263,26 @@ int capture(cgvk_solver s, int iters, cudaGraphExec_t* exec) {
     return CGVK_OK;
 }
 
+// One iteration outside a graph: the kernels a 1-iteration graph would hold,
+// launched on the solver's stream (step(n)'s remainder n % gn — a second
+// graph per solver cost 0.06 ms of every solver creation to capture and
+// instantiate, more than the launches it saves a short solve).
+int launch_one(cgvk_solver s) {
+    if (!use_chain()) {
+        CK(launch(s, s->k1));
+        if (!s->fused) CK(launch(s, s->k2));
+        return CGVK_OK;
+    }
+    CK(launch(s, s->k1c0));
+    if (s->fused) {
+        CK(launch(s, s->kt_odd));
+    } else {
+        CK(launch(s, s->k2c));
+        CK(launch(s, s->kt));
+    }
+    return CGVK_OK;
+}
+
 int refresh_mirror(cgvk_solver s) {
     CK(cudaMemcpyAsync(&s->mirror, s->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s->stream));
     unsigned int err = 0;
@@ -1517,7 +1537,6 @@ void free_solver(cgvk_solver s) {
     if (!s) return;
     if (s->a) cudaSetDevice(s->a->device);
     if (s->stream) cudaStreamSynchronize(s->stream);
-    if (s->g1) cudaGraphExecDestroy(s->g1);
     if (s->g8) cudaGraphExecDestroy(s->g8);
     for (double* p : {s->slab, s->wpred, s->rank_tot, s->all_tot, s->sbuf_lo, s->sbuf_hi, s->rbuf_lo, s->rbuf_hi})
         dfree(p);
@@ -1821,8 +1840,7 @@ int cgvk_solver_create(cgvk_matrix a, const cgvk_variant_config* cfg, int precon
     if ((rc = solver_init(s, b, x0)) != CGVK_OK) return bail(rc);
     pt.mark("initialize");
     s->gn = graph_iters();
-    if ((rc = capture(s, 1, &s->g1)) != CGVK_OK || (rc = capture(s, s->gn, &s->g8)) != CGVK_OK)
-        return bail(rc);
+    if ((rc = capture(s, s->gn, &s->g8)) != CGVK_OK) return bail(rc);
     pt.mark("graphs");
     if (env_int("CGVK_SYNC_CREATE", 0) && (rc = refresh_mirror(s)) != CGVK_OK) return bail(rc);
     *out = s;
@@ -1856,7 +1874,7 @@ int cgvk_solver_step(cgvk_solver s, int n_iters) {
     s->k_target += n_iters;
     k_set_limit<<<1, 1, 0, s->stream>>>(s->ctrl, s->k_target);
     for (int i = 0; i < n_iters / s->gn; ++i) CK(cudaGraphLaunch(s->g8, s->stream));
-    for (int i = 0; i < n_iters % s->gn; ++i) CK(cudaGraphLaunch(s->g1, s->stream));
+    for (int i = 0; i < n_iters % s->gn; ++i) TRY(launch_one(s));
     CK(cudaGetLastError());
     s->mirror_fresh = false;
     return CGVK_OK;
