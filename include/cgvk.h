@@ -233,9 +233,9 @@ void* cgvk_solver_stream(cgvk_solver s);
  * one-kernel schedule, same bits; environment CGVK_FUSE=0 turns it off). */
 int cgvk_solver_launches_per_iter(cgvk_solver s);
 /* Kernel launches of one cgvk_solver_step(s, n_iters) call on this rank: the
- * limit-setting kernel, the captured kernels of every replayed graph
- * (including the closing tail kernel of each chained graph); NCCL's own
- * kernels not counted. */
+ * limit-setting kernel, the captured kernels of every replayed graph and the
+ * plain launches of the remainder (including the closing tail kernel of each
+ * chained run); NCCL's own kernels not counted. */
 long long cgvk_solver_launches(cgvk_solver s, int n_iters);
 /* Device-timed step(): CUDA events on the solver's stream around the enqueue
  * of n_iters graph-replayed iterations; synchronises. *iters = iterations

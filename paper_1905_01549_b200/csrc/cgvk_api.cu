@@ -1263,21 +1263,28 @@ int capture(cgvk_solver s, int iters, cudaGraphExec_t* exec) {
     return CGVK_OK;
 }
 
-// One iteration outside a graph: the kernels a 1-iteration graph would hold,
-// launched on the solver's stream (step(n)'s remainder n % gn — a second
-// graph per solver cost 0.06 ms of every solver creation to capture and
-// instantiate, more than the launches it saves a short solve).
-int launch_one(cgvk_solver s) {
+// `iters` iterations outside a graph: the kernels a graph of that length
+// would hold — one chained run with one closing tail — launched on the
+// solver's stream (step(n)'s remainder n % gn: a second graph per solver cost
+// 0.06 ms of every solver creation to capture and instantiate, more than the
+// launches it saves a short solve).
+int launch_chain(cgvk_solver s, int iters) {
+    if (iters <= 0) return CGVK_OK;
     if (!use_chain()) {
-        CK(launch(s, s->k1));
-        if (!s->fused) CK(launch(s, s->k2));
+        for (int i = 0; i < iters; ++i) {
+            CK(launch(s, s->k1));
+            if (!s->fused) CK(launch(s, s->k2));
+        }
         return CGVK_OK;
     }
-    CK(launch(s, s->k1c0));
     if (s->fused) {
-        CK(launch(s, s->kt_odd));
+        for (int i = 0; i < iters; ++i) CK(launch(s, i == 0 ? s->k1c0 : (i & 1) ? s->k2c : s->k1c));
+        CK(launch(s, (iters & 1) ? s->kt_odd : s->kt));
     } else {
-        CK(launch(s, s->k2c));
+        for (int i = 0; i < iters; ++i) {
+            CK(launch(s, i ? s->k1c : s->k1c0));
+            CK(launch(s, s->k2c));
+        }
         CK(launch(s, s->kt));
     }
     return CGVK_OK;
@@ -1874,7 +1881,7 @@ int cgvk_solver_step(cgvk_solver s, int n_iters) {
     s->k_target += n_iters;
     k_set_limit<<<1, 1, 0, s->stream>>>(s->ctrl, s->k_target);
     for (int i = 0; i < n_iters / s->gn; ++i) CK(cudaGraphLaunch(s->g8, s->stream));
-    for (int i = 0; i < n_iters % s->gn; ++i) TRY(launch_one(s));
+    TRY(launch_chain(s, n_iters % s->gn));
     CK(cudaGetLastError());
     s->mirror_fresh = false;
     return CGVK_OK;
@@ -2014,7 +2021,7 @@ int cgvk_solver_launches_per_iter(cgvk_solver s) {
 long long cgvk_solver_launches(cgvk_solver s, int n_iters) {
     if (!s || n_iters <= 0) return 0;
     if (s->group) return 1 + (long long)group_launches_per_iter(s) * n_iters;
-    const long long graphs = n_iters / s->gn + n_iters % s->gn;
+    const long long graphs = n_iters / s->gn + (n_iters % s->gn ? 1 : 0);  // chained runs (one tail each)
     return 1 + (s->fused ? 1LL : 2LL) * n_iters + (use_chain() ? graphs : 0);
 }
 
