@@ -575,6 +575,18 @@ __device__ __forceinline__ void fold_last(const double* part, int Gv, int t, Pip
     // dots [0, nb) by one bulk copy; up to two more from registers, their loads
     // issued before the bulk wait so both take one L2 latency together
     constexpr int kRegDots = 2;
+    if (Gv <= kConsumers) {
+        // small grids (rank shards): one partial per thread and dot, all loads
+        // in flight together — one L2 round trip, no proxy fence, no barrier
+        double v[ND];
+#pragma unroll
+        for (int d = 0; d < ND; ++d) v[d] = t < Gv ? __ldcg(part + (size_t)d * Gv + t) : 0.0;
+        if (t < Gv) {
+#pragma unroll
+            for (int d = 0; d < ND; ++d) tot[d] = ADD(tot[d], v[d]);
+        }
+        return;
+    }
     const size_t per_dot = (size_t)Gv * 8;
     const int nb = (int)min((size_t)ND, ring_bytes / per_dot);
     if (ND - nb > kRegDots || Gv > kConsumers * kFoldMax) {
@@ -694,6 +706,9 @@ constexpr int kSuccFoldMax = 2 * kConsumers;  // predecessor partials per regist
 // one SM share one L2 read (the non-coherent path is safe here as it is for
 // the SpMV gathers: the buffers were written by the previous kernel).
 // Measured: P64 68.7 k -> 69.9 k it/s (pipe-PR 17.1 -> 16.4 us), P128 +0.3 %.
+#ifndef CGVK_P2P_PLAN_PF
+#define CGVK_P2P_PLAN_PF 1  // peer ranks: prefetch the exchange plan into L1 before the dependency wait
+#endif
 #ifndef CGVK_FOLD_L1
 #define CGVK_FOLD_L1 1
 #endif
@@ -1077,6 +1092,13 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
         }
         if (Op::CSR) npre = q;
         if (kEarly) nearly = min(q, CGVK_EARLY);
+    }
+    if constexpr (PEER && CGVK_P2P_PLAN_PF) {
+        // the exchange plan is immutable: its three lines into L1 while the
+        // previous kernel drains, so the prologue's fold, the boundary rows
+        // and the last CTA's publication read it at L1 latency
+        if (threadIdx.x < (sizeof(PeerPlan) + 127) / 128)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(P.pp) + 128 * threadIdx.x));
     }
     tl_mark(Op::CSR, 0);
     pdl_wait();
