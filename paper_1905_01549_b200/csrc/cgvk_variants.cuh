@@ -3,11 +3,14 @@
 // Appendix A), each an "Op" run by the TMA-staged pipeline of
 // cgvk_stream.cuh.
 //
-// Each iteration is exactly two launches, K1 then K2, captured in a CUDA
-// graph. Global reductions are folded by the last-arriving CTA of the kernel
-// that produces the operands, which also runs the scalar recurrences and the
-// breakdown/convergence checks of src/variants.cpp:128-187 on the device, so
-// the host never synchronises inside the loop. Every vector value is bit-
+// Each iteration is two launches, K1 then K2, captured in a CUDA graph — or,
+// for problems that fit L2, ONE launch doing both halves (PrF, CgF, GvF, PprF
+// below: the SpMV operand re-formed at every gathered column, same bits).
+// Global reductions are folded by the next kernel's prologue (chained graphs)
+// or the last-arriving CTA of the kernel that produces the operands, which
+// also runs the scalar recurrences and the breakdown/convergence checks of
+// src/variants.cpp:128-187 on the device, so the host never synchronises
+// inside the loop. Every vector value is bit-
 // identical to the reference's (no FMA; the Jacobi products d∘v that the
 // reference stores are recomputed on the fly from the same operands); dots
 // follow the canonical tree of cgvk_device.cuh.
