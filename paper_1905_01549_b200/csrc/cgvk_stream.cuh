@@ -222,22 +222,27 @@ __device__ __forceinline__ uint64_t matrix_policy(int l2pol) {
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
 
 // Canonical CTA tree over the 256 consumer threads (same order as cta_tree).
+// `mask` (uniform over the CTA): the dots in use — the others are skipped
+// (their v[] is left as it is; nobody reads it).
 template <int ND>
-__device__ __forceinline__ void cta_tree_c(double (&v)[ND], double* sm) {
+__device__ __forceinline__ void cta_tree_c(double (&v)[ND], double* sm, unsigned int mask = ~0u) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int d = 0; d < ND; ++d) {
+        if (!((mask >> d) & 1u)) continue;
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) v[d] = ADD(v[d], __shfl_down_sync(0xffffffffu, v[d], off));
     }
     if (lane == 0) {
 #pragma unroll
-        for (int d = 0; d < ND; ++d) sm[d * 32 + warp] = v[d];
+        for (int d = 0; d < ND; ++d)
+            if ((mask >> d) & 1u) sm[d * 32 + warp] = v[d];
     }
     consumer_sync();
     if (warp == 0) {
 #pragma unroll
         for (int d = 0; d < ND; ++d) {
+            if (!((mask >> d) & 1u)) continue;
             double y = lane < kWarps ? sm[d * 32 + lane] : 0.0;
 #pragma unroll
             for (int off = kWarps / 2; off >= 1; off >>= 1) y = ADD(y, __shfl_down_sync(0xffffffffu, y, off));
@@ -246,6 +251,24 @@ __device__ __forceinline__ void cta_tree_c(double (&v)[ND], double* sm) {
     }
     consumer_sync();
 }
+
+// Optional Op member `static unsigned int dmask(const Params&)`: the dot
+// products this configuration uses, as a function of the solver's flags
+// alone (CG-CG / GV: two of their five only with unsimplified_mu). A
+// single-GPU chained kernel skips the others' trees and partial stores, its
+// successor their loads and fold (measured per dot: 0.06 us per tree, 0.14 us
+// in the successor's prologue; CG-CG P2D 7.3 -> 6.9 us, P64 12.7 -> 12.3, GV
+// P64 15.0 -> 14.6). The PR family, which would skip one dot of six, measured
+// slower with the predicates (P2D PR 7.5 -> 7.8, pipe-PR 7.8 -> 8.3 us) and
+// declares no mask.
+template <class T, class = void>
+struct DmaskOf {
+    __device__ static unsigned int get(const Params&) { return ~0u; }
+};
+template <class T>
+struct DmaskOf<T, std::void_t<decltype(T::dmask(std::declval<const Params&>()))>> {
+    __device__ static unsigned int get(const Params& P) { return T::dmask(P); }
+};
 
 __device__ __forceinline__ bool arrive_last_c(unsigned int* counter, int* flag) {
     consumer_sync();
@@ -760,13 +783,15 @@ __device__ __forceinline__ void chain_prologue(const Params& P, int chain, PipeH
             constexpr int U = kSuccFoldMax / kConsumers;
             const bool fold = Prev::ND > 0 && (chain & CH_FOLD);
             const double* pin = (chain & CH_ODD) ? P.part_b : P.part;
+            const unsigned int dm = DmaskOf<Prev>::get(P);  // the predecessor's dots in use
             double v[U][ND];
             auto load = [&](int q0) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int q = q0 + t + u * kConsumers;
 #pragma unroll
-                    for (int d = 0; d < ND; ++d) v[u][d] = q < gprev ? CGVK_FOLD_LD(pin + d * gprev + q) : 0.0;
+                    for (int d = 0; d < ND; ++d)
+                        v[u][d] = (q < gprev && ((dm >> d) & 1u)) ? CGVK_FOLD_LD(pin + d * gprev + q) : 0.0;
                 }
             };
             if (fold) load(0);  // issued before the control block arrives
@@ -798,7 +823,7 @@ __device__ __forceinline__ void chain_prologue(const Params& P, int chain, PipeH
                             }
                         }
                     }
-                    cta_tree_c<ND>(tot, H->red);
+                    cta_tree_c<ND>(tot, H->red, dm);
                 }
                 tl_mark(Self::CSR, 4);
                 if (t == 0 && go && m != 0) prev.finish(Q, &H->cs, tot);
@@ -1274,13 +1299,17 @@ __device__ __forceinline__ void stream_body(const Params& P, const StageCfg& S) 
         if (pb && p2p_mask) p2p_push_row(pp, p2p_mask, i, P.n, p2p_h);
     };
     double* const part = (!PEER && chain && !(chain & CH_ODD)) ? P.part_b : P.part;
+    // (single-GPU chained kernels: only the dots in use — the successor folds
+    // exactly those; every other schedule folds all ND partial arrays)
+    const unsigned int dm = (!PEER && chain) ? DmaskOf<Op>::get(P) : ~0u;
     auto close_vb = [&](int vb) {
         if constexpr (Op::ND > 0) {
             if (op.sync() != 2) return;
-            cta_tree_c<Op::ND>(acc, H->red);
+            cta_tree_c<Op::ND>(acc, H->red, dm);
             if (t == 0) {
 #pragma unroll
-                for (int d = 0; d < Op::ND; ++d) part[d * Gv + vb] = acc[d];
+                for (int d = 0; d < Op::ND; ++d)
+                    if ((dm >> d) & 1u) part[d * Gv + vb] = acc[d];
             }
         }
     };

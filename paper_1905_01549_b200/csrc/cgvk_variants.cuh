@@ -310,6 +310,8 @@ struct CgK2 {
     }
     static constexpr int NG = 1;  // gathered: r~
     __device__ const double* gsrc(const Params& P, int) const { return PREC ? P.rt : P.r; }
+    // dots: <r~,r> <r~,w> <r,r> [+ two with unsimplified_mu]
+    __device__ static unsigned int dmask(const Params& P) { return P.unsimplified_mu ? 0x1fu : 0x07u; }
     __device__ int sync() const { return 2; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
     static constexpr bool PAIR = true;
@@ -423,6 +425,8 @@ struct CgF {
     }
     static constexpr int NG = PREC ? 4 : 3;
     __device__ const double* gsrc(const Params& P, int k) const { return k == 0 ? rc : k == 1 ? sc : k == 2 ? wc : P.d; }
+    // dots: <r~,r> <r~,w> <r,r> [+ two with unsimplified_mu]
+    __device__ static unsigned int dmask(const Params& P) { return P.unsimplified_mu ? 0x1fu : 0x07u; }
     __device__ int sync() const { return S ? 2 : 1; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
     template <class In, class RR>
@@ -795,6 +799,8 @@ struct GvK1 {
     // (no early_vec: measured P64 GV 18.9 -> 20.9 us with it — ten streams
     // per stage issued at once delay the chained prologue; with the successor
     // fold 15.6 -> 16.3 us)
+    // dots: <r~,r> <r~,w> <r,r> [+ two with unsimplified_mu]
+    __device__ static unsigned int dmask(const Params& P) { return P.unsimplified_mu ? 0x1fu : 0x07u; }
     __device__ int sync() const { return S ? 2 : 1; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[0]; }
     template <class In, class RR>
@@ -969,6 +975,8 @@ struct GvF {
     }
     static constexpr int NG = PREC ? 4 : 3;
     __device__ const double* gsrc(const Params& P, int k) const { return k == 0 ? wc : k == 1 ? uc : k == 2 ? tc : P.d; }
+    // dots: <r~,r> <r~,w> <r,r> [+ two with unsimplified_mu]
+    __device__ static unsigned int dmask(const Params& P) { return P.unsimplified_mu ? 0x1fu : 0x07u; }
     __device__ int sync() const { return S ? 2 : 1; }
     __device__ unsigned int* counter(const Params& P) const { return &P.ctrl->count[1]; }
     template <class In, class RR>
