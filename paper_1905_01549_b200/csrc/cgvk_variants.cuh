@@ -51,6 +51,9 @@ namespace cgvk {
 #ifndef CGVK_PRF_LATE
 #define CGVK_PRF_LATE 0  // the one-kernel PR / M iteration signals its dependent after its tiles
 #endif
+#ifndef CGVK_F_LATE
+#define CGVK_F_LATE 0  // CgF (1) / GvF (2) / PprF (4) signal their dependent after their tiles
+#endif
 #ifndef CGVK_PRF_EARLY
 #define CGVK_PRF_EARLY 1  // first stages' vectors issued right after the wait
 #endif
@@ -382,7 +385,7 @@ struct CgF {
     static constexpr int NV = PREC ? 6 : 5, ND = 5;
     static constexpr int MAXNREG = CGVK_SPMV_MAXNREG;
     static constexpr bool CSR = true;
-    static constexpr bool PDL_LATE = false;
+    static constexpr bool PDL_LATE = (CGVK_F_LATE & 1) != 0;
     static constexpr bool NO_BAND = true;
     static constexpr bool NO_PEER = true;
     static constexpr int STAGES = 2;
@@ -931,7 +934,7 @@ struct GvF {
     static constexpr int NV = PREC ? 10 : 7, ND = 5;
     static constexpr int MAXNREG = CGVK_SPMV_MAXNREG;
     static constexpr bool CSR = true;
-    static constexpr bool PDL_LATE = false;
+    static constexpr bool PDL_LATE = (CGVK_F_LATE & 2) != 0;
     static constexpr bool NO_BAND = true;
     static constexpr bool NO_PEER = true;
     static constexpr int STAGES = 2;
@@ -1241,7 +1244,7 @@ struct PprF {
     static constexpr int NV = PREC ? 9 : 6, ND = 6;
     static constexpr int MAXNREG = CGVK_SPMV_MAXNREG;
     static constexpr bool CSR = true;
-    static constexpr bool PDL_LATE = false;
+    static constexpr bool PDL_LATE = (CGVK_F_LATE & 4) != 0;
     static constexpr bool NO_BAND = true;
     static constexpr bool NO_PEER = true;
     static constexpr int STAGES = 2;
