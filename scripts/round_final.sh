@@ -18,7 +18,8 @@ for c in ${LAUNCH_CFGS:-p128 r4m p64 v256 p2d}; do
       -k 'regex:k_stream|k_band' --csv --log-file $OUT/launches_$c.csv "${CMD[@]}" > $OUT/ncu_l_$c.log 2>&1
   echo "launches $c rc=$?"
 done
-full() {  # config, kernel regex, name
+full() {  # config, kernel regex, name   (ONLY_FULL=name: just that capture)
+  [ -n "${ONLY_FULL:-}" ] && [ "${ONLY_FULL}" != "$3" ] && return
   local CMD=(python bench.py --config $1 --per-config "" --steps 3 --warmup 3 --no-e2e --no-cpu --no-clocks)
   "${CMD[@]}" > $OUT/plain_full_$3.log 2>&1 && \
   ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
@@ -32,6 +33,6 @@ full() {  # config, kernel regex, name
   rm -f $OUT/full_$3.ncu-rep
 }
 full p128 'k_stream<cgvk::GvK1<\(bool\)1>' p128_gvk1
-full r4m 'k_band<cgvk::HsK2<\(bool\)1>' r4m_band_hsk2
-full r4m 'k_band<cgvk::PrK2<\(bool\)1>' r4m_band_prk2
+full r4m 'k_band(_nr)?<cgvk::HsK2<\(bool\)1>' r4m_band_hsk2
+full r4m 'k_band(_nr)?<cgvk::PrK2<\(bool\)1>' r4m_band_prk2
 full p64 'k_stream<cgvk::PrF<\(bool\)1>' p64_prf
