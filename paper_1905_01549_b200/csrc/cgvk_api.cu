@@ -1260,6 +1260,8 @@ int capture(cgvk_solver s, int iters, cudaGraphExec_t* exec) {
     CK(e);
     CK(e_end);
     CK(cudaGraphInstantiate(exec, g, 0));
+    // upload now (stream-ordered, off the first step()'s critical path)
+    if (env_int("CGVK_GRAPH_UPLOAD", 1)) CK(cudaGraphUpload(*exec, s->stream));
     return CGVK_OK;
 }
 
